@@ -1,0 +1,207 @@
+/*
+ * bae_b200.h -- C ABI of the B200-native bundle-adjustment hot path.
+ *
+ * This is the drop-in boundary for the reference library's BA/LM entry points
+ * (traceopt, /root/reference/proj/include/traceopt). The reference is a
+ * header-only C++ API with no FFI of its own; each entry point below names the
+ * reference function it replaces. Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary and no exceptions escape it: the reference
+ * exception classes (errors.hpp:10-69) map to the BAE_ERR_* return codes, and
+ * the offending position/observation is available from bae_last_error_index().
+ *
+ * Threading: a handle is used from one host thread at a time (the reference
+ * runs one orchestrating caller thread). Independent handles
+ * may be used concurrently.
+ *
+ * Layouts (all host buffers, row-major, FP64 unless noted):
+ *   pose   : 7 doubles [tx, ty, tz, qx, qy, qz, qw], world->camera
+ *            (trace.hpp:318-326 write_pose). Quaternions are taken as-is
+ *            (read_pose uses QuatRotation::from_unit, trace.hpp:329-333).
+ *   point  : 3 doubles [x, y, z]
+ *   intr   : 3 doubles [f, k1, k2] (BalIntrinsics, camera.hpp:23-25)
+ *   pixel  : 2 doubles per observation
+ *   indices: int32 camera / point index per observation (problems.hpp:19-23)
+ */
+#ifndef BAE_B200_H_
+#define BAE_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes (errors.hpp:10-69 + device-side failures). */
+#define BAE_OK 0
+#define BAE_ERR_INVALID_ARGUMENT 1    /* std::invalid_argument                    */
+#define BAE_ERR_INDEX 2               /* IndexError(position)  problems.hpp:105-110 */
+#define BAE_ERR_CHEIRALITY 3          /* CheiralityError(observation) camera.hpp:51 */
+#define BAE_ERR_NOT_SPD 4             /* NotSpdError(pivot)                        */
+#define BAE_ERR_NUMERICAL_BREAKDOWN 5 /* NumericalBreakdownError                   */
+#define BAE_ERR_UNSUPPORTED 6         /* UnsupportedOperationError                 */
+#define BAE_ERR_CUDA 7                /* CUDA runtime failure (no device, OOM ...) */
+#define BAE_ERR_NCCL 8                /* NCCL failure                              */
+
+/* LmConfig::solver (lm.hpp:20). */
+#define BAE_SOLVER_CHOLESKY 0
+#define BAE_SOLVER_PCG 1
+
+/* TerminationReason (lm.hpp:21). */
+#define BAE_TERM_PLATEAU 0
+#define BAE_TERM_MAX_ITERS 1
+#define BAE_TERM_SOLVER_FAILURE 2
+
+/* = LmConfig (lm.hpp:23-38); defaults from bae_lm_config_default(). */
+typedef struct bae_lm_config {
+  double initial_damping; /* 1e-6  */
+  double damping_min;     /* 1e-16 */
+  double damping_max;     /* 1e16  */
+  double damping_up;      /* 2.0   */
+  double damping_down;    /* 0.5   */
+  double clamp_min;       /* 1e-6  */
+  double clamp_max;       /* 1e32  */
+  double plateau_rel_tol; /* 1e-6  */
+  double pcg_tol;         /* 1e-8  (relative, on the reduced camera system) */
+  int64_t pcg_max_iters;  /* 0: max(250, 2 * num_cameras)                     */
+  int32_t max_iterations; /* 10    */
+  int32_t plateau_patience; /* 3   */
+  int32_t solver;         /* BAE_SOLVER_*; the reference default is cholesky  */
+  int32_t use_caches;     /* 1 (symbolic reuse; the GPU path always caches)   */
+} bae_lm_config;
+
+/* ⊇ LmIterationRecord (lm.hpp:62-69); entry 0 is the initial state. */
+typedef struct bae_iter_record {
+  int32_t iteration;
+  int32_t accepted;
+  double cost;       /* accepted-history cost after this iteration */
+  double mse;        /* cost / residual rows (lm.hpp:214)          */
+  double lambda;     /* damping used by this iteration's solve     */
+  double cum_time_s; /* wall seconds since the loop started        */
+  int64_t pcg_iters; /* inner iterations of this step (extension)  */
+  double grad_norm;  /* ||J^T r|| at the linearisation point (ext) */
+  double trial_cost; /* cost of the tentative step (inf = rejected by cheirality) */
+} bae_iter_record;
+
+/* = LmReport (lm.hpp:71-77) minus the trajectory vector. */
+typedef struct bae_lm_report {
+  double final_cost;
+  double final_mse;
+  int32_t iterations;
+  int32_t reason; /* BAE_TERM_* */
+  int32_t accepted_steps;
+  int32_t rejected_steps;
+  double final_lambda;
+  double solve_seconds;   /* wall time of the LM loop (lm.hpp:222-232) */
+  int64_t total_pcg_iters;
+} bae_lm_report;
+
+/* Creation options (no reference counterpart; NULL = defaults). */
+typedef struct bae_create_options {
+  int32_t device;      /* CUDA ordinal, default 0                                  */
+  int32_t tile_obs;    /* observations per tile (0 = auto)                        */
+  int32_t jacobian;    /* 0 = recompute blocks in every pass, 1 = store J in HBM  */
+  int32_t rank;        /* distributed: this rank (default 0)                      */
+  int32_t world;       /* distributed: number of ranks (default 1)                */
+  int32_t reserved;
+  const void* nccl_id; /* distributed: 128-byte ncclUniqueId from rank 0           */
+} bae_create_options;
+
+typedef struct bae_problem bae_problem;
+
+/* ---- library -------------------------------------------------------------- */
+const char* bae_version(void);
+void bae_lm_config_default(bae_lm_config* cfg);
+void bae_create_options_default(bae_create_options* opt);
+/* Message / index of the last failure on this host thread (any entry point). */
+const char* bae_last_error(void);
+int64_t bae_last_error_index(void);
+/* 128-byte NCCL unique id for bae_create_options.nccl_id (rank 0 creates it). */
+int bae_nccl_unique_id(void* out128);
+
+/* ---- problem (make_ba_problem, problems.hpp:87-136) ------------------------- */
+/* Validates like the reference (intrinsics count, empty observations,
+ * IndexError with the observation position, camera index checked first) and
+ * evaluates the initial residual, so a point on the camera plane fails here
+ * with BAE_ERR_CHEIRALITY and the lowest offending observation, exactly as the
+ * reference's eager forward at graph construction does (trace.hpp:464-474). */
+int bae_create_ba(const double* poses7, int32_t num_cameras, const double* points3,
+                  int32_t num_points, const double* bal_intrinsics3, const int32_t* cam_idx,
+                  const int32_t* pt_idx, const double* pixels2, int64_t num_observations,
+                  const bae_create_options* opts, bae_problem** out);
+void bae_destroy(bae_problem* p);
+
+int32_t bae_num_poses(const bae_problem* p);    /* TracedProblem::num_poses   */
+int32_t bae_num_points(const bae_problem* p);   /* TracedProblem::num_points  */
+int64_t bae_residual_rows(const bae_problem* p);/* TracedProblem::residual_rows */
+
+/* TracedProblem::set_parameters (problems.hpp:61-64). */
+int bae_set_parameters(bae_problem* p, const double* poses7, const double* points3);
+int bae_get_parameters(bae_problem* p, double* poses7, double* points3);
+/* TracedProblem::evaluate (problems.hpp:66) + squared_norm (lm.hpp:81-85).
+ * residuals2 (nullable) receives r = projection - pixel in observation order. */
+int bae_evaluate(bae_problem* p, double* residuals2, double* cost);
+/* TracedProblem::jacobian (problems.hpp:68, trace.hpp:553-806): the two BSR
+ * halves of JacobianPair. One block per row, so row_ptr = 0..N; col arrays are
+ * the gather indices. Any output pointer may be NULL. */
+int bae_jacobian(bae_problem* p, double* jpose_2x6, double* jpoint_2x3,
+                 int64_t* pose_row_ptr, int32_t* pose_col, int64_t* point_row_ptr,
+                 int32_t* point_col);
+/* transpose_symbolic (bsr.hpp:140-160) of one Jacobian half, which = 0 pose /
+ * 1 point: row_ptr (num_cols+1), col_idx (N, observation ids ascending within
+ * each row), src_block (N). This is the camera / point segmentation the
+ * device reductions use. */
+int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t* col_idx,
+                       int64_t* src_block);
+/* Damped normal-equation pieces for parity (assemble.hpp:61-101): per-camera
+ * 6x6 H_cc and 6-vector g_c = J_c^T r, per-point 3x3 H_pp and g_p, undamped,
+ * at the current parameters. Any output may be NULL. */
+int bae_block_diagonals(bae_problem* p, double* hcc36, double* gc6, double* hpp9, double* gp3);
+
+/* ---- optimizer (optimize, lm.hpp:205-255) ----------------------------------- */
+/* traj receives min(iterations+1, traj_cap) records; poses_out / points_out
+ * (nullable) receive the optimised parameters, which the handle also keeps
+ * (lm.hpp:250-252). */
+int bae_optimize(bae_problem* p, const double* init_poses7, const double* init_points3,
+                 const bae_lm_config* cfg, bae_iter_record* traj, int32_t traj_cap,
+                 bae_lm_report* report, double* poses_out, double* points_out);
+
+/* ---- reduced-camera-system solve, one damping value (assemble + pcg) -------- */
+/* Linearises at the current parameters, damps with lambda and solves with the
+ * implicit-Schur PCG; delta receives [6C pose tangents | 3P point deltas] in
+ * the reference's column order (lm.hpp:159-173). */
+int bae_solve_step(bae_problem* p, double lambda, const bae_lm_config* cfg, double* delta,
+                   int64_t* pcg_iters, double* rel_residual);
+
+/* ---- plateau rule, exposed for host-logic tests (lm.hpp:89-108) -------------- */
+int bae_stop_on_plateau(const double* history, int64_t n, const bae_lm_config* cfg,
+                        int32_t* stop);
+
+/* ---- synthetic BAL-shaped scene (io/synthetic.hpp conventions) - */
+/* Deterministic from the seed. Writes the parsed BAL-equivalent problem:
+ * initial poses7 / points3 / intrinsics3 / observations (camera-major), and the
+ * ground truth (true_poses7, true_points3; nullable). num_observations must be
+ * >= 2 * num_points and <= num_points * min(num_cameras, 16). */
+int bae_synth_bal_shaped(int32_t num_cameras, int32_t num_points, int64_t num_observations,
+                         uint64_t seed, double pixel_sigma, double pose_sigma,
+                         double point_sigma, double* poses7, double* points3,
+                         double* intrinsics3, int32_t* cam_idx, int32_t* pt_idx,
+                         double* pixels2, double* true_poses7, double* true_points3);
+
+/* ---- measurement hooks (bench.py) ------------------------------------------ */
+/* Device-timed (CUDA events on the solver stream) averages over `reps`
+ * launches: kind 0 = linearisation (fused residual + Jacobian + block
+ * reductions), 1 = one implicit Schur S*x product (one PCG iteration's
+ * operator), 2 = one full PCG iteration, 3 = fused residual+Jacobian to HBM
+ * (stored J). ms receives the mean milliseconds per launch. */
+int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms);
+/* Number of kernel launches issued by this handle since creation. */
+int64_t bae_launch_count(const bae_problem* p);
+/* Static sizes the roofline arithmetic needs: [N, P, C, tiles, tile-camera
+ * entries, max obs per tile]. */
+int bae_problem_stats(const bae_problem* p, int64_t* out6);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BAE_B200_H_ */

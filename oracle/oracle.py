@@ -1,0 +1,349 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes wrapper of the CPU restatement of the
+reference hot path (oracle/bae_oracle.cpp -> oracle/liboracle_bae.so).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU arms may import this,
+and only as the checker / CPU baseline. See bae_oracle.cpp's header for what
+pins it (reference unit-test KATs + the reference RNG golden stream)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle_bae.so")
+
+# share the struct layouts with the product binding (plain C structs of the header)
+sys.path.insert(0, os.path.dirname(_HERE))
+from paper_2409_12190_b200._lib import IterRecordC, LmConfigC, LmReportC  # noqa: E402
+
+D = ctypes.POINTER(ctypes.c_double)
+I32 = ctypes.POINTER(ctypes.c_int32)
+I64 = ctypes.POINTER(ctypes.c_int64)
+VP = ctypes.c_void_p
+
+_SIG = {
+    "or_last_error": (ctypes.c_char_p, []),
+    "or_last_error_index": (ctypes.c_int64, []),
+    "or_set_threads": (None, [ctypes.c_int]),
+    "or_symbolic_count": (ctypes.c_int64, []),
+    "or_rng_new": (VP, [ctypes.c_uint64]),
+    "or_rng_free": (None, [VP]),
+    "or_rng_uniform": (ctypes.c_double, [VP]),
+    "or_rng_uniform_range": (ctypes.c_double, [VP, ctypes.c_double, ctypes.c_double]),
+    "or_rng_normal": (ctypes.c_double, [VP]),
+    "or_rng_index": (ctypes.c_uint64, [VP, ctypes.c_uint64]),
+    "or_se3_exp": (ctypes.c_int, [D, D]),
+    "or_se3_log": (ctypes.c_int, [D, D]),
+    "or_se3_compose": (ctypes.c_int, [D, D, D]),
+    "or_se3_retract": (ctypes.c_int, [D, D, D]),
+    "or_quat_make": (ctypes.c_int, [D, D]),
+    "or_quat_matrix": (None, [D, D]),
+    "or_bal_project": (ctypes.c_int, [D, D, D, D]),
+    "or_pinhole_project": (ctypes.c_int, [D, D, D, D]),
+    "or_bal_project_cam": (ctypes.c_int, [D, D, D]),
+    "or_pinhole_project_cam": (ctypes.c_int, [D, D, D]),
+    "or_bal_camera_pose": (ctypes.c_int, [D, D, D]),
+    "or_make_random_ba": (ctypes.c_int, [VP, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, D, D, D, I32,
+                                         I32, D, I64]),
+    "or_synth_ba": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, D,
+                                   D, D, I32, I32, D, D]),
+    "or_ba_problem_new": (VP, [ctypes.c_int, ctypes.c_int, D, ctypes.c_int, D, D, ctypes.c_int64, I32, I32, D,
+                               ctypes.POINTER(ctypes.c_int)]),
+    "or_scalar_problem_new": (VP, [ctypes.c_int, D]),
+    "or_problem_free": (None, [VP]),
+    "or_problem_evaluate": (ctypes.c_int, [VP, D, D, D, D]),
+    "or_problem_jacobian": (ctypes.c_int, [VP, D, D, I64, I32, I64, I32]),
+    "or_transpose_plan": (ctypes.c_int, [VP, ctypes.c_int, I64, I32, I64]),
+    "or_normal_size": (ctypes.c_int, [VP, I64, I64]),
+    "or_normal_dense": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_double, ctypes.c_double, D, D]),
+    "or_solve_step": (ctypes.c_int, [VP, ctypes.c_double, ctypes.POINTER(LmConfigC), D, I64]),
+    "or_lm_begin": (ctypes.c_int, [VP, D, D, ctypes.c_double]),
+    "or_lm_step": (ctypes.c_int, [VP, ctypes.POINTER(LmConfigC), ctypes.POINTER(ctypes.c_int)]),
+    "or_lm_state": (ctypes.c_int, [VP, D, D, D, ctypes.POINTER(ctypes.c_int), D, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_int)]),
+    "or_optimize": (ctypes.c_int, [VP, D, D, ctypes.POINTER(LmConfigC), ctypes.POINTER(IterRecordC), ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(LmReportC), D, D]),
+    "or_stop_on_plateau": (ctypes.c_int, [D, ctypes.c_int64, ctypes.POINTER(LmConfigC), ctypes.POINTER(ctypes.c_int)]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `make -C oracle`")
+        L = ctypes.CDLL(LIB_PATH)
+        for n, (r, a) in _SIG.items():
+            f = getattr(L, n)
+            f.restype = r
+            f.argtypes = a
+        _lib = L
+    return _lib
+
+
+class OracleError(Exception):
+    def __init__(self, code, msg, index):
+        super().__init__(f"[{code}] {msg} (index {index})")
+        self.code, self.msg, self.index = code, msg, index
+
+
+def _chk(code):
+    if code != 0:
+        L = lib()
+        raise OracleError(code, (L.or_last_error() or b"").decode(), int(L.or_last_error_index()))
+
+
+def p(a, t=ctypes.c_double):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def set_threads(n: int):
+    lib().or_set_threads(int(n))
+
+
+class Rng:
+    def __init__(self, seed):
+        self.h = lib().or_rng_new(int(seed))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().or_rng_free(self.h)
+
+    def uniform(self, lo=None, hi=None):
+        if lo is None:
+            return lib().or_rng_uniform(self.h)
+        return lib().or_rng_uniform_range(self.h, lo, hi)
+
+    def normal(self):
+        return lib().or_rng_normal(self.h)
+
+    def index(self, n):
+        return int(lib().or_rng_index(self.h, int(n)))
+
+
+def make_random_ba(rng: Rng, C: int, P: int, pinhole: bool, keep: float = 0.8):
+    """tests/oracles.hpp:26-61."""
+    kw = 4 if pinhole else 3
+    poses = np.empty((C, 7))
+    pts = np.empty((P, 3))
+    intr = np.empty((C, kw))
+    ci = np.empty(C * P, np.int32)
+    pi = np.empty(C * P, np.int32)
+    px = np.empty((C * P, 2))
+    n = ctypes.c_int64()
+    _chk(lib().or_make_random_ba(rng.h, C, P, 1 if pinhole else 0, keep, p(poses), p(pts), p(intr),
+                                 p(ci, ctypes.c_int32), p(pi, ctypes.c_int32), p(px), ctypes.byref(n)))
+    N = n.value
+    return dict(poses=poses, points=pts, intrinsics=intr, cam_idx=ci[:N].copy(), pt_idx=pi[:N].copy(),
+                pixels=px[:N].copy(), pinhole=pinhole)
+
+
+def synth_ba(C, P, pix_sigma, pose_sigma, seed):
+    """io/synthetic.hpp:46-91 (dense visibility), poses via BalCamera::pose."""
+    N = C * P
+    poses = np.empty((C, 7))
+    intr = np.empty((C, 3))
+    pts = np.empty((P, 3))
+    ci = np.empty(N, np.int32)
+    pi = np.empty(N, np.int32)
+    px = np.empty((N, 2))
+    tp = np.empty((C, 7))
+    _chk(lib().or_synth_ba(C, P, pix_sigma, pose_sigma, seed, p(poses), p(intr), p(pts), p(ci, ctypes.c_int32),
+                           p(pi, ctypes.c_int32), p(px), p(tp)))
+    return dict(poses=poses, points=pts, intrinsics=intr, cam_idx=ci, pt_idx=pi, pixels=px, true_poses=tp,
+                pinhole=False)
+
+
+class Problem:
+    """make_ba_problem restated (problems.hpp:87-136) + LM driver."""
+
+    def __init__(self, poses, points, intrinsics, cam_idx, pt_idx, pixels, pinhole=False):
+        self.poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 7)
+        self.points = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        self.kw = 4 if pinhole else 3
+        intr = np.ascontiguousarray(intrinsics, dtype=np.float64).reshape(-1, self.kw)
+        ci = np.ascontiguousarray(cam_idx, dtype=np.int32)
+        pi = np.ascontiguousarray(pt_idx, dtype=np.int32)
+        px = np.ascontiguousarray(pixels, dtype=np.float64).reshape(-1, 2)
+        self.C, self.P, self.N = self.poses.shape[0], self.points.shape[0], ci.shape[0]
+        err = ctypes.c_int()
+        self.h = lib().or_ba_problem_new(1 if pinhole else 0, self.C, p(self.poses), self.P, p(self.points), p(intr),
+                                         self.N, p(ci, ctypes.c_int32), p(pi, ctypes.c_int32), p(px),
+                                         ctypes.byref(err))
+        _chk(err.value)
+
+    @classmethod
+    def from_dict(cls, d):
+        return cls(d["poses"], d["points"], d["intrinsics"], d["cam_idx"], d["pt_idx"], d["pixels"],
+                   d.get("pinhole", False))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().or_problem_free(self.h)
+
+    def evaluate(self, poses=None, points=None):
+        r = np.empty(2 * self.N)
+        c = ctypes.c_double()
+        p7 = None if poses is None else np.ascontiguousarray(poses, dtype=np.float64)
+        p3 = None if points is None else np.ascontiguousarray(points, dtype=np.float64)
+        _chk(lib().or_problem_evaluate(self.h, p(p7), p(p3), p(r), ctypes.byref(c)))
+        return r, c.value
+
+    def jacobian(self):
+        N = self.N
+        jp = np.empty((N, 2, 6))
+        jl = np.empty((N, 2, 3))
+        prp = np.empty(N + 1, np.int64)
+        lrp = np.empty(N + 1, np.int64)
+        pc = np.empty(N, np.int32)
+        lc = np.empty(N, np.int32)
+        _chk(lib().or_problem_jacobian(self.h, p(jp), p(jl), p(prp, ctypes.c_int64), p(pc, ctypes.c_int32),
+                                       p(lrp, ctypes.c_int64), p(lc, ctypes.c_int32)))
+        return dict(j_pose=jp, j_point=jl, pose_row_ptr=prp, pose_col=pc, point_row_ptr=lrp, point_col=lc)
+
+    def transpose_plan(self, which):
+        cols = self.C if which == 0 else self.P
+        rp = np.empty(cols + 1, np.int64)
+        ci = np.empty(self.N, np.int32)
+        sb = np.empty(self.N, np.int64)
+        _chk(lib().or_transpose_plan(self.h, which, p(rp, ctypes.c_int64), p(ci, ctypes.c_int32),
+                                     p(sb, ctypes.c_int64)))
+        return rp, ci, sb
+
+    def normal_dense(self, lmbda, cmin=1e-6, cmax=1e32):
+        n = ctypes.c_int64()
+        nnz = ctypes.c_int64()
+        _chk(lib().or_normal_size(self.h, ctypes.byref(n), ctypes.byref(nnz)))
+        A = np.empty((n.value, n.value))
+        b = np.empty(n.value)
+        _chk(lib().or_normal_dense(self.h, lmbda, cmin, cmax, p(A), p(b)))
+        return A, b
+
+    def solve_step(self, lmbda, config):
+        n = 6 * self.C + 3 * self.P
+        x = np.empty(n)
+        it = ctypes.c_int64()
+        cfg = config.to_c()
+        _chk(lib().or_solve_step(self.h, lmbda, ctypes.byref(cfg), p(x), ctypes.byref(it)))
+        return x, it.value
+
+    def optimize(self, config, poses=None, points=None):
+        cfg = config.to_c()
+        cap = int(config.max_iterations) + 1
+        recs = (IterRecordC * cap)()
+        n = ctypes.c_int()
+        rep = LmReportC()
+        p7 = np.ascontiguousarray(self.poses if poses is None else poses, dtype=np.float64)
+        p3 = np.ascontiguousarray(self.points if points is None else points, dtype=np.float64)
+        o7 = np.empty_like(p7)
+        o3 = np.empty_like(p3)
+        _chk(lib().or_optimize(self.h, p(p7), p(p3), ctypes.byref(cfg), recs, cap, ctypes.byref(n),
+                               ctypes.byref(rep), p(o7), p(o3)))
+        traj = [dict(iteration=r.iteration, accepted=bool(r.accepted), cost=r.cost, mse=r.mse, lmbda=r.lmbda,
+                     cum_time_s=r.cum_time_s, pcg_iters=r.pcg_iters, grad_norm=r.grad_norm, trial_cost=r.trial_cost)
+                for r in recs[:min(cap, n.value)]]
+        return dict(final_cost=rep.final_cost, final_mse=rep.final_mse, iterations=rep.iterations,
+                    reason=rep.reason, trajectory=traj, poses=o7, points=o3, solve_seconds=rep.solve_seconds,
+                    accepted_steps=rep.accepted_steps, rejected_steps=rep.rejected_steps)
+
+
+class ScalarProblem:
+    """Points-only LM KAT models (test_optim.cpp:15-32): kind 0 r = theta,
+    1 r = theta^2 - 2, 2 r = theta^2 + 1."""
+
+    def __init__(self, kind, theta):
+        th = np.ascontiguousarray(theta, dtype=np.float64)
+        self.h = lib().or_scalar_problem_new(kind, p(th))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().or_problem_free(self.h)
+
+    def begin(self, theta, lmbda):
+        th = np.ascontiguousarray(theta, dtype=np.float64).reshape(1, 3)
+        _chk(lib().or_lm_begin(self.h, None, p(th), lmbda))
+
+    def step(self, config):
+        cfg = config.to_c()
+        acc = ctypes.c_int()
+        _chk(lib().or_lm_step(self.h, ctypes.byref(cfg), ctypes.byref(acc)))
+        return bool(acc.value)
+
+    def state(self):
+        pts = np.empty((1, 3))
+        lam = ctypes.c_double()
+        cnt = (ctypes.c_int * 3)()
+        hist = np.empty(4096)
+        nh = ctypes.c_int()
+        _chk(lib().or_lm_state(self.h, None, p(pts), ctypes.byref(lam), cnt, p(hist), 4096, ctypes.byref(nh)))
+        return dict(points=pts, lmbda=lam.value, iterations=cnt[0], accepted=cnt[1], rejected=cnt[2],
+                    history=hist[:nh.value].copy())
+
+    def optimize(self, config, theta):
+        cfg = config.to_c()
+        cap = int(config.max_iterations) + 1
+        recs = (IterRecordC * cap)()
+        n = ctypes.c_int()
+        rep = LmReportC()
+        th = np.ascontiguousarray(theta, dtype=np.float64).reshape(1, 3)
+        o3 = np.empty((1, 3))
+        _chk(lib().or_optimize(self.h, None, p(th), ctypes.byref(cfg), recs, cap, ctypes.byref(n), ctypes.byref(rep),
+                               None, p(o3)))
+        return dict(final_cost=rep.final_cost, iterations=rep.iterations, reason=rep.reason,
+                    trajectory=[dict(cost=r.cost, accepted=bool(r.accepted)) for r in recs[:min(cap, n.value)]],
+                    points=o3)
+
+
+def stop_on_plateau(history, config):
+    h = np.ascontiguousarray(history, dtype=np.float64)
+    cfg = config.to_c()
+    s = ctypes.c_int()
+    _chk(lib().or_stop_on_plateau(p(h), h.size, ctypes.byref(cfg), ctypes.byref(s)))
+    return bool(s.value)
+
+
+def se3_exp(tau):
+    out = np.empty(7)
+    _chk(lib().or_se3_exp(p(np.ascontiguousarray(tau, dtype=np.float64)), p(out)))
+    return out
+
+
+def se3_retract(pose, tau):
+    out = np.empty(7)
+    _chk(lib().or_se3_retract(p(np.ascontiguousarray(pose, dtype=np.float64)),
+                              p(np.ascontiguousarray(tau, dtype=np.float64)), p(out)))
+    return out
+
+
+def se3_compose(a, b):
+    out = np.empty(7)
+    _chk(lib().or_se3_compose(p(np.ascontiguousarray(a, dtype=np.float64)), p(np.ascontiguousarray(b, dtype=np.float64)),
+                              p(out)))
+    return out
+
+
+def quat_matrix(q):
+    out = np.empty(9)
+    lib().or_quat_matrix(p(np.ascontiguousarray(q, dtype=np.float64)), p(out))
+    return out.reshape(3, 3)
+
+
+def bal_project(pose, point, k3):
+    out = np.empty(2)
+    _chk(lib().or_bal_project(p(np.ascontiguousarray(pose, dtype=np.float64)),
+                              p(np.ascontiguousarray(point, dtype=np.float64)),
+                              p(np.ascontiguousarray(k3, dtype=np.float64)), p(out)))
+    return out
+
+
+def pinhole_project(pose, point, k4):
+    out = np.empty(2)
+    _chk(lib().or_pinhole_project(p(np.ascontiguousarray(pose, dtype=np.float64)),
+                                  p(np.ascontiguousarray(point, dtype=np.float64)),
+                                  p(np.ascontiguousarray(k4, dtype=np.float64)), p(out)))
+    return out

@@ -1,0 +1,11 @@
+"""B200-native bundle adjustment: the BA / LM hot path of arXiv 2409.12190
+(reference: traceopt) as FP64 sm_100a kernels behind a C ABI
+(include/bae_b200.h). See DESIGN.md."""
+from .api import (CheiralityError, DeviceError, IndexError, JacobianPair, LmConfig, LmIterationRecord, LmReport,
+                  NotSpdError, NumericalBreakdownError, SolverChoice, TerminationReason, TracedProblem,
+                  UnsupportedOperationError, make_ba_problem, optimize, stop_on_plateau, write_csv)
+from . import synthetic
+
+__all__ = ["CheiralityError", "DeviceError", "IndexError", "JacobianPair", "LmConfig", "LmIterationRecord", "LmReport",
+           "NotSpdError", "NumericalBreakdownError", "SolverChoice", "TerminationReason", "TracedProblem",
+           "UnsupportedOperationError", "make_ba_problem", "optimize", "stop_on_plateau", "write_csv", "synthetic"]

@@ -1,0 +1,371 @@
+"""Python mirror of the reference's BA / LM API over the C ABI.
+
+Names, argument meaning and error behaviour follow traceopt
+(/root/reference/proj/include/traceopt):
+
+* ``make_ba_problem(poses, points, intrinsics, observations)`` -- problems.hpp:87-136
+* ``TracedProblem.{set_parameters, evaluate, jacobian, residual_rows, num_poses, num_points}``
+  -- problems.hpp:36-82
+* ``LmConfig`` / ``LmIterationRecord`` / ``LmReport`` / ``TerminationReason`` / ``SolverChoice``
+  -- lm.hpp:20-77
+* ``optimize(model, init_poses, init_points, config, final_state=None)`` -- lm.hpp:205-255
+* ``stop_on_plateau(history, config)`` -- lm.hpp:104-108
+* exceptions ``IndexError`` (with ``position``), ``CheiralityError`` (``observation``),
+  ``NotSpdError``, ``NumericalBreakdownError``, ``UnsupportedOperationError`` -- errors.hpp:10-57;
+  ``std::invalid_argument`` maps to ``ValueError``.
+
+Arrays: poses (C, 7) = [tx, ty, tz, qx, qy, qz, qw] world->camera, points (P, 3),
+BAL intrinsics (C, 3) = [f, k1, k2], observations = (cam_idx (N,), pt_idx (N,), pixels (N, 2)).
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes
+import dataclasses
+import enum
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import CreateOptionsC, IterRecordC, LmConfigC, LmReportC, ptr
+
+
+class IndexError(builtins.IndexError):  # noqa: A001 - mirrors traceopt::IndexError
+    def __init__(self, msg, position):
+        super().__init__(msg)
+        self.position = position
+
+
+class CheiralityError(RuntimeError):
+    def __init__(self, msg, observation):
+        super().__init__(msg)
+        self.observation = observation
+
+
+class NotSpdError(RuntimeError):
+    def __init__(self, msg, pivot=-1):
+        super().__init__(msg)
+        self.pivot = pivot
+
+
+class NumericalBreakdownError(RuntimeError):
+    pass
+
+
+class UnsupportedOperationError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure (no reference counterpart)."""
+
+
+def _raise(code: int):
+    lib = _lib.load()
+    msg = (lib.bae_last_error() or b"").decode()
+    idx = int(lib.bae_last_error_index())
+    if code == 1:
+        raise ValueError(msg)
+    if code == 2:
+        raise IndexError(msg, idx)
+    if code == 3:
+        raise CheiralityError(msg, idx)
+    if code == 4:
+        raise NotSpdError(msg, idx)
+    if code == 5:
+        raise NumericalBreakdownError(msg)
+    if code == 6:
+        raise UnsupportedOperationError(msg)
+    raise DeviceError(f"[{code}] {msg}")
+
+
+def _check(code: int):
+    if code != 0:
+        _raise(code)
+
+
+class SolverChoice(enum.IntEnum):
+    cholesky = 0
+    pcg = 1
+
+
+class TerminationReason(enum.IntEnum):
+    plateau = 0
+    max_iters = 1
+    solver_failure = 2
+
+
+@dataclasses.dataclass
+class LmConfig:
+    initial_damping: float = 1e-6
+    damping_min: float = 1e-16
+    damping_max: float = 1e16
+    damping_up: float = 2.0
+    damping_down: float = 0.5
+    clamp_min: float = 1e-6
+    clamp_max: float = 1e32
+    max_iterations: int = 10
+    plateau_patience: int = 3
+    plateau_rel_tol: float = 1e-6
+    solver: SolverChoice = SolverChoice.cholesky
+    pcg_tol: float = 1e-8
+    pcg_max_iters: int = 0
+    use_caches: bool = True
+
+    def to_c(self) -> LmConfigC:
+        c = LmConfigC()
+        for f in ("initial_damping", "damping_min", "damping_max", "damping_up", "damping_down", "clamp_min",
+                  "clamp_max", "plateau_rel_tol", "pcg_tol"):
+            setattr(c, f, float(getattr(self, f)))
+        c.pcg_max_iters = int(self.pcg_max_iters)
+        c.max_iterations = int(self.max_iterations)
+        c.plateau_patience = int(self.plateau_patience)
+        c.solver = int(self.solver)
+        c.use_caches = 1 if self.use_caches else 0
+        return c
+
+
+@dataclasses.dataclass
+class LmIterationRecord:
+    iteration: int
+    cost: float
+    mse: float
+    lmbda: float
+    accepted: bool
+    cum_time_s: float
+    pcg_iters: int = 0
+    grad_norm: float = 0.0
+    trial_cost: float = float("nan")
+
+
+@dataclasses.dataclass
+class LmReport:
+    final_cost: float
+    final_mse: float
+    iterations: int
+    trajectory: List[LmIterationRecord]
+    reason: TerminationReason
+    accepted_steps: int = 0
+    rejected_steps: int = 0
+    final_lambda: float = 0.0
+    solve_seconds: float = 0.0
+    total_pcg_iters: int = 0
+
+
+@dataclasses.dataclass
+class LmState:
+    poses: np.ndarray
+    points: np.ndarray
+    lmbda: float
+    iterations: int
+    accepted_steps: int
+    rejected_steps: int
+
+
+@dataclasses.dataclass
+class BsrMatrix:
+    """One Jacobian half (bsr.hpp:42-93): one br x bc block per residual row."""
+    block_rows: int
+    block_cols: int
+    br: int
+    bc: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray  # (nnz, br, bc)
+
+
+@dataclasses.dataclass
+class JacobianPair:
+    j_pose: BsrMatrix
+    j_point: BsrMatrix
+
+
+@dataclasses.dataclass
+class TransposePlan:
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    src_block: np.ndarray
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+class TracedProblem:
+    """Device-resident BA problem (the TracedProblem of problems.hpp:36-82)."""
+
+    def __init__(self, handle, C, P, N):
+        self._h = handle
+        self._C, self._P, self._N = C, P, N
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().bae_destroy(h)
+            self._h = None
+
+    def num_poses(self) -> int:
+        return self._C
+
+    def num_points(self) -> int:
+        return self._P
+
+    def residual_rows(self) -> int:
+        return self._N
+
+    def residual_width(self) -> int:
+        return 2
+
+    def set_parameters(self, poses, points):
+        p7 = _f64(poses, (self._C, 7))
+        p3 = _f64(points, (self._P, 3))
+        _check(_lib.load().bae_set_parameters(self._h, ptr(p7), ptr(p3)))
+
+    def get_parameters(self):
+        p7 = np.empty((self._C, 7))
+        p3 = np.empty((self._P, 3))
+        _check(_lib.load().bae_get_parameters(self._h, ptr(p7), ptr(p3)))
+        return p7, p3
+
+    def evaluate(self) -> np.ndarray:
+        r = np.empty(2 * self._N)
+        cost = ctypes.c_double()
+        _check(_lib.load().bae_evaluate(self._h, ptr(r), ctypes.byref(cost)))
+        return r
+
+    def cost(self) -> float:
+        cost = ctypes.c_double()
+        _check(_lib.load().bae_evaluate(self._h, None, ctypes.byref(cost)))
+        return cost.value
+
+    def jacobian(self) -> JacobianPair:
+        N = self._N
+        jp = np.empty((N, 2, 6))
+        jl = np.empty((N, 2, 3))
+        prp = np.empty(N + 1, np.int64)
+        lrp = np.empty(N + 1, np.int64)
+        pc = np.empty(N, np.int32)
+        lc = np.empty(N, np.int32)
+        _check(_lib.load().bae_jacobian(self._h, ptr(jp), ptr(jl), ptr(prp, ctypes.c_int64), ptr(pc, ctypes.c_int32),
+                                        ptr(lrp, ctypes.c_int64), ptr(lc, ctypes.c_int32)))
+        return JacobianPair(BsrMatrix(N, self._C, 2, 6, prp, pc, jp), BsrMatrix(N, self._P, 2, 3, lrp, lc, jl))
+
+    def transpose_plan(self, which: int) -> TransposePlan:
+        cols = self._C if which == 0 else self._P
+        rp = np.empty(cols + 1, np.int64)
+        ci = np.empty(self._N, np.int32)
+        sb = np.empty(self._N, np.int64)
+        _check(_lib.load().bae_transpose_plan(self._h, which, ptr(rp, ctypes.c_int64), ptr(ci, ctypes.c_int32),
+                                              ptr(sb, ctypes.c_int64)))
+        return TransposePlan(rp, ci, sb)
+
+    def block_diagonals(self):
+        hcc = np.empty((self._C, 6, 6))
+        gc = np.empty((self._C, 6))
+        hpp = np.empty((self._P, 3, 3))
+        gp = np.empty((self._P, 3))
+        _check(_lib.load().bae_block_diagonals(self._h, ptr(hcc), ptr(gc), ptr(hpp), ptr(gp)))
+        return hcc, gc, hpp, gp
+
+    def solve_step(self, lmbda: float, config: Optional[LmConfig] = None):
+        cfg = (config or LmConfig(solver=SolverChoice.pcg)).to_c()
+        delta = np.empty(6 * self._C + 3 * self._P)
+        iters = ctypes.c_int64()
+        rel = ctypes.c_double()
+        _check(_lib.load().bae_solve_step(self._h, float(lmbda), ctypes.byref(cfg), ptr(delta), ctypes.byref(iters),
+                                          ctypes.byref(rel)))
+        return delta, iters.value, rel.value
+
+    def time_kernel(self, kind: int, reps: int) -> float:
+        ms = ctypes.c_double()
+        _check(_lib.load().bae_time_kernel(self._h, int(kind), int(reps), ctypes.byref(ms)))
+        return ms.value
+
+    def launch_count(self) -> int:
+        return int(_lib.load().bae_launch_count(self._h))
+
+    def stats(self):
+        out = np.empty(6, np.int64)
+        _check(_lib.load().bae_problem_stats(self._h, ptr(out, ctypes.c_int64)))
+        keys = ("observations", "points", "cameras", "tiles", "entries", "max_tile_obs")
+        return dict(zip(keys, (int(v) for v in out)))
+
+
+def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0, tile_obs: int = 0) -> TracedProblem:
+    """make_ba_problem (problems.hpp:87-136) for BAL cameras.
+
+    ``observations`` is ``(cam_idx, pt_idx, pixels)``. Raises ValueError for a
+    wrong intrinsics count or no observations, IndexError(position) for an
+    out-of-range index, CheiralityError(observation) when an initial point
+    lies on a camera plane (the reference's eager forward at construction)."""
+    cam_idx, pt_idx, pixels = observations
+    p7 = _f64(poses).reshape(-1, 7)
+    p3 = _f64(points).reshape(-1, 3)
+    k3 = _f64(intrinsics).reshape(-1, 3)
+    ci, pi = _i32(cam_idx), _i32(pt_idx)
+    px = _f64(pixels).reshape(-1, 2)
+    C, P, N = p7.shape[0], p3.shape[0], ci.shape[0]
+    if k3.shape[0] != C:
+        raise ValueError("make_ba_problem: one intrinsics entry per camera required")
+    if N == 0:
+        raise ValueError("make_ba_problem: no observations")
+    lib = _lib.load()
+    opt = CreateOptionsC()
+    lib.bae_create_options_default(ctypes.byref(opt))
+    opt.device = device
+    opt.tile_obs = tile_obs
+    h = ctypes.c_void_p()
+    _check(lib.bae_create_ba(ptr(p7), C, ptr(p3), P, ptr(k3), ptr(ci, ctypes.c_int32), ptr(pi, ctypes.c_int32),
+                             ptr(px), N, ctypes.byref(opt), ctypes.byref(h)))
+    return TracedProblem(h, C, P, N)
+
+
+def optimize(model: TracedProblem, init_poses, init_points, config: LmConfig,
+             final_state: Optional[dict] = None) -> LmReport:
+    """optimize (lm.hpp:205-255); the model keeps the optimised parameters."""
+    lib = _lib.load()
+    cfg = config.to_c()
+    cap = int(config.max_iterations) + 1
+    recs = (IterRecordC * cap)()
+    rep = LmReportC()
+    p7 = _f64(init_poses, (model.num_poses(), 7))
+    p3 = _f64(init_points, (model.num_points(), 3))
+    out7 = np.empty_like(p7)
+    out3 = np.empty_like(p3)
+    _check(lib.bae_optimize(model._h, ptr(p7), ptr(p3), ctypes.byref(cfg), recs, cap, ctypes.byref(rep), ptr(out7),
+                            ptr(out3)))
+    n = min(cap, rep.iterations + 1)
+    traj = [LmIterationRecord(r.iteration, r.cost, r.mse, r.lmbda, bool(r.accepted), r.cum_time_s, r.pcg_iters,
+                              r.grad_norm, r.trial_cost) for r in recs[:n]]
+    report = LmReport(rep.final_cost, rep.final_mse, rep.iterations, traj, TerminationReason(rep.reason),
+                      rep.accepted_steps, rep.rejected_steps, rep.final_lambda, rep.solve_seconds,
+                      rep.total_pcg_iters)
+    if final_state is not None:
+        final_state.update(dict(poses=out7, points=out3, lmbda=rep.final_lambda, iterations=rep.iterations,
+                                accepted_steps=rep.accepted_steps, rejected_steps=rep.rejected_steps))
+    return report
+
+
+def stop_on_plateau(history, config: LmConfig) -> bool:
+    h = _f64(history)
+    cfg = config.to_c()
+    stop = ctypes.c_int32()
+    _check(_lib.load().bae_stop_on_plateau(ptr(h), h.size, ctypes.byref(cfg), ctypes.byref(stop)))
+    return bool(stop.value)
+
+
+def write_csv(path: str, report: LmReport):
+    """CSV trajectory with the reference CLI's schema (cli.hpp:69-79)."""
+    with open(path, "w") as f:
+        f.write("iter,cost,mse,lambda,accepted,cum_time_s\n")
+        for r in report.trajectory:
+            f.write("%d,%.17g,%.17g,%.17g,%d,%.6f\n" % (r.iteration, r.cost, r.mse, r.lmbda, 1 if r.accepted else 0,
+                                                      r.cum_time_s))

@@ -1,0 +1,255 @@
+// extern "C" boundary (include/bae_b200.h): no exceptions or C++ types cross
+// it. Each entry point maps the reference exception classes (errors.hpp) to
+// return codes and records the message / index for bae_last_error*().
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "bae_b200.h"
+#include "bae_internal.hpp"
+#include "problem.hpp"
+
+struct bae_problem {
+  std::unique_ptr<bae::Problem> impl;
+};
+
+namespace {
+thread_local std::string g_msg;
+thread_local std::int64_t g_index = -1;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    g_msg.clear();
+    g_index = -1;
+    f();
+    return BAE_OK;
+  } catch (const bae::Error& e) {
+    g_msg = e.msg;
+    g_index = e.index;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_msg = "host allocation failed";
+    return BAE_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_msg = e.what();
+    return BAE_ERR_INVALID_ARGUMENT;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* bae_version(void) { return "bae-b200 0.1 (sm_100a, fp64)"; }
+
+void bae_lm_config_default(bae_lm_config* c) {  // LmConfig defaults, lm.hpp:24-37
+  std::memset(c, 0, sizeof(*c));
+  c->initial_damping = 1e-6;
+  c->damping_min = 1e-16;
+  c->damping_max = 1e16;
+  c->damping_up = 2.0;
+  c->damping_down = 0.5;
+  c->clamp_min = 1e-6;
+  c->clamp_max = 1e32;
+  c->plateau_rel_tol = 1e-6;
+  c->pcg_tol = 1e-8;
+  c->pcg_max_iters = 0;
+  c->max_iterations = 10;
+  c->plateau_patience = 3;
+  c->solver = BAE_SOLVER_CHOLESKY;
+  c->use_caches = 1;
+}
+
+void bae_create_options_default(bae_create_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->world = 1;
+}
+
+const char* bae_last_error(void) { return g_msg.c_str(); }
+int64_t bae_last_error_index(void) { return g_index; }
+
+int bae_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    (void)out128;
+    throw bae::Error(BAE_ERR_UNSUPPORTED, "built without NCCL");
+  });
+}
+
+int bae_create_ba(const double* poses7, int32_t C, const double* points3, int32_t P, const double* intr3,
+                  const int32_t* cam_idx, const int32_t* pt_idx, const double* px2, int64_t N,
+                  const bae_create_options* opts, bae_problem** out) {
+  return guarded([&] {
+    if (!out) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null output handle");
+    *out = nullptr;
+    if (N > 0 && (!cam_idx || !pt_idx || !px2)) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null observation arrays");
+    if ((C > 0 && (!poses7 || !intr3)) || (P > 0 && !points3))
+      throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null parameter arrays");
+    if (C < 0 || P < 0) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "negative counts");
+    bae_create_options o;
+    bae_create_options_default(&o);
+    if (opts) o = *opts;
+    if (o.world != 1) throw bae::Error(BAE_ERR_UNSUPPORTED, "multi-rank problems need the NCCL build");
+    auto h = std::make_unique<bae_problem>();
+    h->impl = std::make_unique<bae::Problem>(poses7, C, points3, P, intr3, cam_idx, pt_idx, px2, N, o);
+    *out = h.release();
+  });
+}
+
+void bae_destroy(bae_problem* p) { delete p; }
+
+int32_t bae_num_poses(const bae_problem* p) { return p ? p->impl->num_cameras() : 0; }
+int32_t bae_num_points(const bae_problem* p) { return p ? p->impl->num_points() : 0; }
+int64_t bae_residual_rows(const bae_problem* p) { return p ? p->impl->num_obs() : 0; }
+
+int bae_set_parameters(bae_problem* p, const double* poses7, const double* points3) {
+  return guarded([&] { p->impl->set_parameters(poses7, points3); });
+}
+int bae_get_parameters(bae_problem* p, double* poses7, double* points3) {
+  return guarded([&] { p->impl->get_parameters(poses7, points3); });
+}
+int bae_evaluate(bae_problem* p, double* residuals2, double* cost) {
+  return guarded([&] {
+    const double c = p->impl->evaluate(residuals2);
+    if (cost) *cost = c;
+  });
+}
+int bae_jacobian(bae_problem* p, double* jpose, double* jpoint, int64_t* prp, int32_t* pcol, int64_t* lrp,
+                 int32_t* lcol) {
+  return guarded([&] {
+    if (jpose || jpoint) p->impl->jacobian(jpose, jpoint, nullptr);
+    const bae::Plan& pl = p->impl->plan();
+    const std::int64_t N = pl.N;
+    std::vector<std::int32_t> cam(static_cast<std::size_t>(N)), pt(static_cast<std::size_t>(N));
+    // gather columns from the device-side decomposition (entry camera, tile point)
+    for (int t = 0; t < pl.T; ++t)
+      for (int e = pl.tile_ent_begin[t]; e < pl.tile_ent_begin[t + 1]; ++e)
+        for (int s = pl.ent_obs_begin[e]; s < pl.ent_obs_begin[e + 1]; ++s) {
+          cam[pl.obs_orig[s]] = pl.ent_cam[e];
+          pt[pl.obs_orig[s]] = pl.pt_of_internal[pl.tile_pt_begin[t] + static_cast<int>(pl.obs_lcpt[s] >> 16)];
+        }
+    for (std::int64_t k = 0; k <= N; ++k) {
+      if (prp) prp[k] = k;
+      if (lrp) lrp[k] = k;
+    }
+    if (pcol) std::memcpy(pcol, cam.data(), cam.size() * 4);
+    if (lcol) std::memcpy(lcol, pt.data(), pt.size() * 4);
+  });
+}
+
+int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t* col_idx, int64_t* src_block) {
+  return guarded([&] {
+    const bae::Plan& pl = p->impl->plan();
+    if (which == 0) {
+      // camera segments: entries of each camera, observations re-listed in id order
+      std::vector<std::int64_t> rp(static_cast<std::size_t>(pl.C) + 1, 0);
+      std::vector<std::int32_t> ids;
+      ids.reserve(static_cast<std::size_t>(pl.N));
+      for (int c = 0; c < pl.C; ++c) {
+        const std::size_t start = ids.size();
+        for (int q = pl.cam_ent_ptr[c]; q < pl.cam_ent_ptr[c + 1]; ++q) {
+          const int e = pl.cam_ent[q];
+          for (int s = pl.ent_obs_begin[e]; s < pl.ent_obs_begin[e + 1]; ++s) ids.push_back(pl.obs_orig[s]);
+        }
+        std::sort(ids.begin() + static_cast<std::ptrdiff_t>(start), ids.end());
+        rp[c + 1] = static_cast<std::int64_t>(ids.size());
+      }
+      std::memcpy(row_ptr, rp.data(), rp.size() * 8);
+      std::memcpy(col_idx, ids.data(), ids.size() * 4);
+      for (std::size_t i = 0; i < ids.size(); ++i) src_block[i] = ids[i];
+    } else if (which == 1) {
+      std::vector<std::int64_t> rp(static_cast<std::size_t>(pl.P) + 1, 0);
+      for (int i = 0; i < pl.P; ++i) rp[pl.pt_of_internal[i] + 1] = pl.pt_ptr[i + 1] - pl.pt_ptr[i];
+      for (int p2 = 0; p2 < pl.P; ++p2) rp[p2 + 1] += rp[p2];
+      for (int t = 0; t < pl.T; ++t)
+        for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
+          std::int64_t o = rp[pl.pt_of_internal[i]];
+          for (int q = pl.pt_ptr[i]; q < pl.pt_ptr[i + 1]; ++q, ++o) {
+            const std::int32_t k = pl.obs_orig[pl.tile_obs_begin[t] + pl.ptobs[q]];
+            col_idx[o] = k;
+            src_block[o] = k;
+          }
+        }
+      std::memcpy(row_ptr, rp.data(), rp.size() * 8);
+    } else {
+      throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "which must be 0 (pose) or 1 (point)");
+    }
+  });
+}
+
+int bae_block_diagonals(bae_problem* p, double* hcc36, double* gc6, double* hpp9, double* gp3) {
+  return guarded([&] { p->impl->block_diagonals(hcc36, gc6, hpp9, gp3); });
+}
+
+int bae_optimize(bae_problem* p, const double* init_poses7, const double* init_points3, const bae_lm_config* cfg,
+                 bae_iter_record* traj, int32_t traj_cap, bae_lm_report* report, double* poses_out,
+                 double* points_out) {
+  return guarded([&] {
+    bae_lm_config c;
+    bae_lm_config_default(&c);
+    if (cfg) c = *cfg;
+    std::vector<bae_iter_record> t;
+    bae_lm_report r{};
+    p->impl->optimize(init_poses7, init_points3, c, t, r);
+    if (traj)
+      for (int i = 0; i < std::min<int>(traj_cap, static_cast<int>(t.size())); ++i) traj[i] = t[i];
+    if (report) *report = r;
+    if (poses_out || points_out) p->impl->get_parameters(poses_out, points_out);
+  });
+}
+
+int bae_solve_step(bae_problem* p, double lambda, const bae_lm_config* cfg, double* delta, int64_t* iters,
+                   double* relres) {
+  return guarded([&] {
+    bae_lm_config c;
+    bae_lm_config_default(&c);
+    if (cfg) c = *cfg;
+    p->impl->solve_step(lambda, c, delta, iters, relres);
+  });
+}
+
+int bae_stop_on_plateau(const double* history, int64_t n, const bae_lm_config* cfg, int32_t* stop) {
+  return guarded([&] {  // stop_on_plateau, lm.hpp:104-108
+    if (n <= 0) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "stop_on_plateau: empty history");
+    if (n >= cfg->max_iterations) {
+      *stop = 1;
+      return;
+    }
+    *stop = bae::plateau_stagnation(history, static_cast<std::size_t>(n), cfg->plateau_patience,
+                                    cfg->plateau_rel_tol)
+                ? 1
+                : 0;
+  });
+}
+
+int bae_synth_bal_shaped(int32_t C, int32_t P, int64_t N, uint64_t seed, double pixel_sigma, double pose_sigma,
+                         double point_sigma, double* poses7, double* points3, double* intr3, int32_t* cam_idx,
+                         int32_t* pt_idx, double* px2, double* true_poses7, double* true_points3) {
+  return guarded([&] {
+    bae::synth_bal_shaped(C, P, N, seed, pixel_sigma, pose_sigma, point_sigma, poses7, points3, intr3, cam_idx,
+                          pt_idx, px2, true_poses7, true_points3);
+  });
+}
+
+int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms) {
+  return guarded([&] { *ms = p->impl->time_kernel(kind, reps); });
+}
+
+int64_t bae_launch_count(const bae_problem* p) { return p ? p->impl->launches() : 0; }
+
+int bae_problem_stats(const bae_problem* p, int64_t* out6) {
+  return guarded([&] {
+    const bae::Plan& pl = p->impl->plan();
+    out6[0] = pl.N;
+    out6[1] = pl.P;
+    out6[2] = pl.C;
+    out6[3] = pl.T;
+    out6[4] = pl.E;
+    out6[5] = pl.max_tile_obs;
+  });
+}
+
+}  // extern "C"

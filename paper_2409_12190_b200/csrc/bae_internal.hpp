@@ -1,0 +1,76 @@
+// Internal host-side declarations shared by the planner, the device solver
+// and the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "bae_b200.h"
+
+namespace bae {
+
+// Error carried to the C ABI: code = BAE_ERR_*, index = offending
+// observation / position (IndexError, CheiralityError) or pivot, else -1.
+struct Error {
+  int code;
+  std::string msg;
+  std::int64_t index;
+  Error(int c, std::string m, std::int64_t i = -1) : code(c), msg(std::move(m)), index(i) {}
+};
+
+// Static decomposition of one problem into device work units (setup time,
+// the B200 counterpart of transpose_symbolic / spgemm_symbolic /
+// build_csr_pattern, bsr.hpp:140-160, spgemm.hpp:33-81, assemble.hpp:135-177).
+//
+// Points are renumbered ("internal" order) so that points seen by nearby
+// cameras are adjacent; a tile is a run of consecutive internal points whose
+// observations fit one CTA. Inside a tile, observations are ordered by
+// (local camera, internal point, observation id), so every camera's
+// observations in the tile form one contiguous "entry" segment and every
+// point's observations are listed in `ptobs`.
+struct Plan {
+  int C = 0, P = 0;
+  std::int64_t N = 0;
+  int tile_obs_target = 0, tile_cam_cap = 0;
+
+  std::vector<std::int32_t> pt_of_internal;  // internal -> original point
+  std::vector<std::int32_t> internal_of_pt;  // original -> internal
+
+  int T = 0;
+  std::vector<std::int32_t> tile_obs_begin;  // T+1, global observation slots
+  std::vector<std::int32_t> tile_pt_begin;   // T+1, internal point ids
+  std::vector<std::int32_t> tile_ent_begin;  // T+1, entry ids
+  std::vector<std::int32_t> tile_ws;         // T, big-tile workspace slot or -1
+
+  std::vector<std::uint32_t> obs_lcpt;  // N: local camera | local point << 16
+  std::vector<std::int32_t> obs_orig;   // N: original observation id
+  std::vector<double> obs_px;           // 2N: pixels in slot order
+
+  int E = 0;
+  std::vector<std::int32_t> ent_cam;        // E
+  std::vector<std::int32_t> ent_obs_begin;  // E+1
+  std::vector<std::int32_t> cam_ent_ptr;    // C+1
+  std::vector<std::int32_t> cam_ent;        // E, ascending per camera
+
+  std::vector<std::int32_t> pt_ptr;  // P+1 over internal points, into ptobs
+  std::vector<std::uint16_t> ptobs;  // N: tile-local slots, ascending obs id per point
+
+  int max_tile_obs = 0, max_tile_cams = 0, max_tile_pts = 0;
+  // tiles whose workspace does not fit shared memory run from global scratch
+  int n_big = 0, big_obs = 0, big_cams = 0, big_pts = 0;
+  bool has_empty_camera = false, has_empty_point = false;
+};
+
+// Validation follows make_ba_problem (problems.hpp:90-110): per observation,
+// camera index before point index, IndexError carries the position.
+void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N);
+
+Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2,
+                std::int64_t N, int tile_obs_target, int tile_cam_cap, int smem_tile_obs_cap);
+
+void synth_bal_shaped(int C, int P, std::int64_t N, std::uint64_t seed, double pixel_sigma, double pose_sigma,
+                      double point_sigma, double* poses7, double* points3, double* intr3, std::int32_t* cam_idx,
+                      std::int32_t* pt_idx, double* px2, double* true_poses7, double* true_points3);
+
+}  // namespace bae

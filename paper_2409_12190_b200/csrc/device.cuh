@@ -1,0 +1,298 @@
+// Device-side data layout, tile workspaces and the deterministic reduction
+// primitives shared by all kernels.
+#pragma once
+
+#include <cstdint>
+
+#include "lie.cuh"
+
+namespace bae {
+
+constexpr int kTileThreads = 256;  // CTA size of the tile kernels (8 warps)
+constexpr int kCamRec = 16;        // per camera: R[9] t[3] f k1 k2 pad
+constexpr int kWarpsPerCamBlock = 8;
+
+// PCG state machine (implicit-Schur PCG, restating pcg.hpp:32-129 on the
+// reduced camera system).
+enum PcgState : int { kPcgIter = 0, kPcgVerify = 1, kPcgDone = 2, kPcgBreakdown = 3 };
+enum PcgDir : int { kDirZ = 0, kDirZBetaP = 1, kDirX = 2 };
+
+struct PcgDev {
+  double rz, alpha, beta, bnorm, rnorm, true_norm, tol;
+  long long iters, budget;
+  int state, dir, converged, not_spd;
+};
+
+struct LmDev {
+  double cost;        // cost at the linearisation point
+  double grad_sq;     // ||J^T r||^2 at the linearisation point
+  double new_cost;    // trial cost
+  int trial_bad;      // cheirality / non-finite in the trial step
+  int retract_bad;
+  int err_obs;        // lowest observation on the camera plane (INT_MAX: none)
+  int pad;
+};
+
+// Everything a kernel needs, passed by value.
+struct Dev {
+  int C, P, T, E, N;
+  int nbig;
+  long long big_stride;  // bytes per big-tile workspace
+  const int* tile_obs_begin;
+  const int* tile_pt_begin;
+  const int* tile_ent_begin;
+  const int* tile_ws;
+  const std::uint32_t* obs_lcpt;
+  const int* obs_orig;
+  const double* obs_px;
+  const int* ent_cam;
+  const int* ent_obs_begin;
+  const int* cam_ent_ptr;
+  const int* cam_ent;
+  const int* pt_ptr;
+  const std::uint16_t* ptobs;
+  char* bigws;
+  // parameters
+  double* pose;    // 7C  [t q]
+  double* intr;    // 3C  [f k1 k2]
+  double* camrec;  // 16C
+  double* pts;     // 3P internal order
+  double* pose_t;
+  double* camrec_t;
+  double* pts_t;
+  // linearisation / damping
+  double* hpp;    // 6P
+  double* gp;     // 3P
+  double* hinv;   // 6P
+  double* dp;     // 3P
+  double* hcc;    // 21C
+  double* gc;     // 6C
+  double* hccd;   // 21C damped
+  double* minv;   // 36C
+  double* rhs;    // 6C
+  // PCG vectors (6C each)
+  double* x;
+  double* r;
+  double* z;
+  double* p;
+  double* y;
+  double* partial;    // E * 27
+  double* tile_red;   // T * 2
+  double* block_red;  // grid-reduction scratch
+  unsigned* tickets;  // grid-reduction tickets
+  PcgDev* pcg;
+  LmDev* lm;
+  // stored-Jacobian mode and exports (slot order, component-major [comp][N])
+  double* jstore;  // 18 * N or null
+  double* resid;   // 2 * N or null
+};
+
+// Packed symmetric storage: 6x6 upper triangle row-major (21), 3x3 (6).
+__host__ __device__ constexpr int sym6(int a, int b) {
+  return a <= b ? a * 6 - a * (a - 1) / 2 + (b - a) : b * 6 - b * (b - 1) / 2 + (a - b);
+}
+__host__ __device__ constexpr int sym3(int a, int b) {
+  return a <= b ? a * 3 - a * (a - 1) / 2 + (b - a) : b * 3 - b * (b - 1) / 2 + (a - b);
+}
+
+// clamp-then-scale damping of one diagonal entry (assemble.hpp:94-101).
+__host__ __device__ __forceinline__ double damp_diag(double d, double lambda, double lo, double hi) {
+  const double c = d < lo ? lo : (hi < d ? hi : d);
+  return c * (1.0 + lambda);
+}
+
+// Tile workspace: carved from dynamic shared memory, or from global scratch
+// for the rare tile that does not fit (one very long point track).
+struct Ws {
+  double* cam;
+  double* pt;
+  double* stage;
+  double* piece;
+  int* ent;
+};
+struct WsDims {
+  int camw, ptw, stw, pw;
+};
+__host__ __device__ __forceinline__ long long ws_bytes(WsDims w, int ncam, int npts, int nobs) {
+  const long long nchunk = (nobs + 31) / 32;
+  const long long dbl = (long long)ncam * w.camw + (long long)npts * w.ptw + (long long)nobs * w.stw +
+                        (nchunk + ncam) * w.pw;
+  return dbl * 8 + (long long)(ncam + 1) * 4;
+}
+__device__ __forceinline__ Ws ws_carve(char* base, WsDims w, int ncam, int npts, int nobs) {
+  Ws ws;
+  double* d = reinterpret_cast<double*>(base);
+  const int nchunk = (nobs + 31) / 32;
+  ws.cam = d;
+  d += (long long)ncam * w.camw;
+  ws.pt = d;
+  d += (long long)npts * w.ptw;
+  ws.stage = d;
+  d += (long long)nobs * w.stw;
+  ws.piece = d;
+  d += (long long)(nchunk + ncam) * w.pw;
+  ws.ent = reinterpret_cast<int*>(d);
+  return ws;
+}
+
+struct TileGeom {
+  int ob, nobs, pb, npts, eb, ncam, big;
+};
+__device__ __forceinline__ TileGeom tile_geom(const Dev& d, int t) {
+  TileGeom g;
+  g.ob = d.tile_obs_begin[t];
+  g.nobs = d.tile_obs_begin[t + 1] - g.ob;
+  g.pb = d.tile_pt_begin[t];
+  g.npts = d.tile_pt_begin[t + 1] - g.pb;
+  g.eb = d.tile_ent_begin[t];
+  g.ncam = d.tile_ent_begin[t + 1] - g.eb;
+  g.big = d.tile_ws[t];
+  return g;
+}
+
+// Warp-level segmented reduction over 32 consecutive tile slots. Segments
+// are contiguous runs of equal `seg` (the local camera); the head lane of each
+// run ends up with the run's sum and stores it as a "piece": lane 0 into its
+// chunk slot, any other head into the slot of its camera. The tree shape
+// depends only on the segment boundaries, so the result is deterministic.
+template <int W>
+__device__ __forceinline__ void seg_reduce_pieces(double (&v)[W], int seg, int slot, int nchunk, double* piece) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int os = __shfl_down_sync(0xffffffffu, seg, off);
+    const bool take = (lane + off < 32) && (os == seg);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const double o = __shfl_down_sync(0xffffffffu, v[j], off);
+      if (take) v[j] += o;
+    }
+  }
+  const int ps = __shfl_up_sync(0xffffffffu, seg, 1);
+  if (seg >= 0 && (lane == 0 || ps != seg)) {
+    const int at = (lane == 0) ? (slot >> 5) : (nchunk + seg);
+#pragma unroll
+    for (int j = 0; j < W; ++j) piece[at * W + j] = v[j];
+  }
+}
+
+// Combine the pieces of every tile camera in slot order and write the
+// per-entry partial sums (W doubles per entry).
+template <int W>
+__device__ __forceinline__ void entries_from_pieces(const Ws& ws, int ncam, int nobs, int eb, double* out) {
+  const int nchunk = (nobs + 31) / 32;
+  for (int idx = threadIdx.x; idx < ncam * W; idx += blockDim.x) {
+    const int e = idx / W, j = idx - e * W;
+    const int b = ws.ent[e], en = ws.ent[e + 1];
+    double acc = 0.0;
+    int m = b >> 5;
+    if (b & 31) {
+      acc = ws.piece[(nchunk + e) * W + j];
+      ++m;
+    }
+    for (; (m << 5) < en; ++m) acc += ws.piece[m * W + j];
+    out[(long long)(eb + e) * W + j] = acc;
+  }
+}
+
+// Fixed-order block sum of one double per thread (result valid in thread 0).
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) s += scratch[i];
+  }
+  return s;
+}
+
+// Last-block-done grid reduction of K doubles per block. Every block calls it
+// with its block totals (thread 0's vals); returns true in the last block,
+// whose thread 0 receives the grid totals summed in block order.
+template <int K>
+__device__ __forceinline__ bool grid_reduce(const double (&vals)[K], double* scratch, unsigned* ticket,
+                                            double (&tot)[K]) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) scratch[(long long)blockIdx.x * K + k] = vals[k];
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b)
+#pragma unroll
+      for (int k = 0; k < K; ++k) tot[k] += ((volatile double*)scratch)[(long long)b * K + k];
+    *ticket = 0u;
+  }
+  return true;
+}
+
+// Cholesky-based inverse of a packed symmetric n x n matrix (n = 3 or 6).
+// Returns false unless every pivot is positive and finite (NotSpdError,
+// cholesky.hpp:229).
+template <int n>
+__host__ __device__ __forceinline__ bool spd_inverse(const double* a, double* inv_full) {
+  double l[n][n];
+#pragma unroll
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int j = 0; j < n; ++j) l[i][j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < n; ++j) {
+    double dsum = (n == 6) ? a[sym6(j, j)] : a[sym3(j, j)];
+#pragma unroll
+    for (int k = 0; k < j; ++k) dsum -= l[j][k] * l[j][k];
+    if (!(dsum > 0.0) || !isfinite(dsum)) return false;
+    const double ljj = sqrt(dsum);
+    l[j][j] = ljj;
+    const double il = 1.0 / ljj;
+#pragma unroll
+    for (int i = j + 1; i < n; ++i) {
+      double s = (n == 6) ? a[sym6(i, j)] : a[sym3(i, j)];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s -= l[i][k] * l[j][k];
+      l[i][j] = s * il;
+    }
+  }
+  // M = L^-1 (lower triangular)
+  double m[n][n];
+#pragma unroll
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int j = 0; j < n; ++j) m[i][j] = 0.0;
+    m[i][i] = 1.0 / l[i][i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = j; k < i; ++k) s += l[i][k] * m[k][j];
+      m[i][j] = -s * m[i][i];
+    }
+  }
+  // A^-1 = M^T M
+#pragma unroll
+  for (int i = 0; i < n; ++i)
+#pragma unroll
+    for (int j = i; j < n; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = j; k < n; ++k) s += m[k][i] * m[k][j];
+      inv_full[i * n + j] = s;
+      inv_full[j * n + i] = s;
+    }
+  return true;
+}
+
+}  // namespace bae

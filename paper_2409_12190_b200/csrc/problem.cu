@@ -1,0 +1,534 @@
+// Device-resident BA problem and the Levenberg-Marquardt driver.
+//
+// Host orchestration mirrors lm_step / optimize (lm.hpp:115-255) while every
+// O(N) operation runs on the GPU: linearisation (K1, fused residual +
+// Jacobian + block reductions), damping and Schur preparation, the
+// implicit-Schur PCG (one CUDA graph per chunk of iterations, device-side
+// convergence state), back-substitution, retraction and trial cost. Per LM
+// iteration the host reads back one small status record.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "problem.hpp"
+
+namespace bae {
+
+namespace {
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(BAE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+constexpr int kSmemLimit = 200 * 1024;
+constexpr int kPcgChunk = 8;
+}  // namespace
+
+template <class T>
+T* Problem::dalloc(std::size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+  allocs_.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* Problem::upload(const std::vector<T>& v) {
+  T* p = dalloc<T>(v.size());
+  if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+
+Problem::Problem(const double* poses7, int C, const double* points3, int P, const double* intr3,
+                 const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2, std::int64_t N,
+                 const bae_create_options& opt)
+    : opt_(opt) {
+  validate_inputs(C, P, cam_idx, pt_idx, N);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(BAE_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+  if (opt.device < 0 || opt.device >= ndev) throw Error(BAE_ERR_INVALID_ARGUMENT, "bad device ordinal");
+  ck(cudaSetDevice(opt.device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  const int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : 512;
+  plan_ = build_plan(C, P, cam_idx, pt_idx, px2, N, tile_obs, 128, 1 << 30);
+  intr_host_.assign(intr3, intr3 + 3 * static_cast<std::size_t>(C));
+
+  // Workspace placement: shared memory unless a tile needs more than kSmemLimit.
+  Plan& pl = plan_;
+  long long big_stride = 0;
+  int nbig = 0;
+  for (int t = 0; t < pl.T; ++t) {
+    const int nobs = pl.tile_obs_begin[t + 1] - pl.tile_obs_begin[t];
+    const int npts = pl.tile_pt_begin[t + 1] - pl.tile_pt_begin[t];
+    const int ncam = pl.tile_ent_begin[t + 1] - pl.tile_ent_begin[t];
+    long long need = 0;
+    for (int k = 0; k < kWsKinds; ++k) need = std::max(need, tile_ws_bytes(k, ncam, npts, nobs));
+    if (need > kSmemLimit) {
+      pl.tile_ws[t] = nbig++;
+      big_stride = std::max(big_stride, need);
+    } else {
+      pl.tile_ws[t] = -1;
+      auto upd = [&](int& slot, int kind) {
+        slot = std::max<int>(slot, static_cast<int>(tile_ws_bytes(kind, ncam, npts, nobs)));
+      };
+      upd(sm_.lin, kWsLin);
+      upd(sm_.cost, kWsCost);
+      upd(sm_.prep, kWsPrep);
+      upd(sm_.schur, kWsSchur);
+      upd(sm_.trial, kWsTrial);
+    }
+  }
+  big_stride = (big_stride + 255) / 256 * 256;
+  set_smem_limits(kSmemLimit);
+
+  Dev& d = d_;
+  d.C = C;
+  d.P = P;
+  d.T = pl.T;
+  d.E = pl.E;
+  d.N = static_cast<int>(N);
+  d.nbig = nbig;
+  d.big_stride = big_stride;
+  d.tile_obs_begin = upload(pl.tile_obs_begin);
+  d.tile_pt_begin = upload(pl.tile_pt_begin);
+  d.tile_ent_begin = upload(pl.tile_ent_begin);
+  d.tile_ws = upload(pl.tile_ws);
+  d.obs_lcpt = upload(pl.obs_lcpt);
+  d.obs_orig = upload(pl.obs_orig);
+  d.obs_px = upload(pl.obs_px);
+  d.ent_cam = upload(pl.ent_cam);
+  d.ent_obs_begin = upload(pl.ent_obs_begin);
+  d.cam_ent_ptr = upload(pl.cam_ent_ptr);
+  d.cam_ent = upload(pl.cam_ent);
+  d.pt_ptr = upload(pl.pt_ptr);
+  d.ptobs = upload(pl.ptobs);
+  d.bigws = nbig ? dalloc<char>(static_cast<std::size_t>(nbig) * big_stride) : nullptr;
+  d.pose = dalloc<double>(7 * static_cast<std::size_t>(C));
+  d.intr = upload(intr_host_);
+  d.camrec = dalloc<double>(kCamRec * static_cast<std::size_t>(C));
+  d.pts = dalloc<double>(3 * static_cast<std::size_t>(P));
+  d.pose_t = dalloc<double>(7 * static_cast<std::size_t>(C));
+  d.camrec_t = dalloc<double>(kCamRec * static_cast<std::size_t>(C));
+  d.pts_t = dalloc<double>(3 * static_cast<std::size_t>(P));
+  d.hpp = dalloc<double>(6 * static_cast<std::size_t>(P));
+  d.gp = dalloc<double>(3 * static_cast<std::size_t>(P));
+  d.hinv = dalloc<double>(6 * static_cast<std::size_t>(P));
+  d.dp = dalloc<double>(3 * static_cast<std::size_t>(P));
+  d.hcc = dalloc<double>(21 * static_cast<std::size_t>(C));
+  d.gc = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.hccd = dalloc<double>(21 * static_cast<std::size_t>(C));
+  d.minv = dalloc<double>(36 * static_cast<std::size_t>(C));
+  d.rhs = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.x = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.r = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.z = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.p = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.y = dalloc<double>(6 * static_cast<std::size_t>(C));
+  d.partial = dalloc<double>(27 * static_cast<std::size_t>(std::max(pl.E, 1)));
+  d.tile_red = dalloc<double>(2 * static_cast<std::size_t>(pl.T));
+  const int max_blocks = std::max((C + kWarpsPerCamBlock - 1) / kWarpsPerCamBlock, (C + 127) / 128) + 1;
+  d.block_red = dalloc<double>(4 * static_cast<std::size_t>(max_blocks));
+  d.tickets = dalloc<unsigned>(16);
+  ck(cudaMemset(d.tickets, 0, 16 * sizeof(unsigned)), "memset");
+  d.pcg = dalloc<PcgDev>(1);
+  d.lm = dalloc<LmDev>(1);
+  d.jstore = nullptr;
+  d.resid = nullptr;
+  ck(cudaMallocHost(&pcg_host_, sizeof(PcgDev)), "cudaMallocHost");
+  ck(cudaMallocHost(&lm_host_, sizeof(LmDev)), "cudaMallocHost");
+  ck(cudaMemset(d.pcg, 0, sizeof(PcgDev)), "memset");
+
+  set_parameters(poses7, points3);
+  // Eager forward at construction, as make_ba_problem's graph does
+  // (trace.hpp:152,385): cheirality surfaces here with the observation id.
+  evaluate(nullptr);
+}
+
+Problem::~Problem() {
+  cudaSetDevice(opt_.device);
+  if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
+  for (void* p : allocs_) cudaFree(p);
+  if (pcg_host_) cudaFreeHost(pcg_host_);
+  if (lm_host_) cudaFreeHost(lm_host_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Problem::activate() { ck(cudaSetDevice(opt_.device), "cudaSetDevice"); }
+
+void Problem::sync() { ck(cudaStreamSynchronize(stream_), "kernel execution"); }
+
+void Problem::set_parameters(const double* poses7, const double* points3) {
+  activate();
+  const int C = d_.C, P = d_.P;
+  std::vector<double> pts(3 * static_cast<std::size_t>(P));
+  for (int i = 0; i < P; ++i) {
+    const int p = plan_.pt_of_internal[i];
+    pts[3 * i] = points3[3 * p];
+    pts[3 * i + 1] = points3[3 * p + 1];
+    pts[3 * i + 2] = points3[3 * p + 2];
+  }
+  ck(cudaMemcpyAsync(d_.pose, poses7, 7 * sizeof(double) * C, cudaMemcpyHostToDevice, stream_), "H2D poses");
+  ck(cudaMemcpyAsync(d_.pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D points");
+  launch_camrec(d_, false, stream_);
+  launches_ += kLaunchesCamrec;
+  sync();
+}
+
+void Problem::get_parameters(double* poses7, double* points3) {
+  activate();
+  const int C = d_.C, P = d_.P;
+  if (poses7) ck(cudaMemcpy(poses7, d_.pose, 7 * sizeof(double) * C, cudaMemcpyDeviceToHost), "D2H poses");
+  if (points3) {
+    std::vector<double> pts(3 * static_cast<std::size_t>(P));
+    ck(cudaMemcpy(pts.data(), d_.pts, pts.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H points");
+    for (int i = 0; i < P; ++i) {
+      const int p = plan_.pt_of_internal[i];
+      points3[3 * p] = pts[3 * i];
+      points3[3 * p + 1] = pts[3 * i + 1];
+      points3[3 * p + 2] = pts[3 * i + 2];
+    }
+  }
+}
+
+void Problem::reset_lm_status() {
+  LmDev z{};
+  z.err_obs = INT_MAX;
+  ck(cudaMemcpyAsync(d_.lm, &z, sizeof(LmDev), cudaMemcpyHostToDevice, stream_), "H2D lm");
+}
+
+void Problem::read_lm() {
+  ck(cudaMemcpyAsync(lm_host_, d_.lm, sizeof(LmDev), cudaMemcpyDeviceToHost, stream_), "D2H lm");
+  sync();
+}
+
+void Problem::unpermute_slots(const std::vector<double>& src, int comps, double* dst) const {
+  // src: component-major [comp][N] in slot order -> dst: [N][comps] original order
+  const std::int64_t N = plan_.N;
+  for (std::int64_t s = 0; s < N; ++s) {
+    const std::int64_t k = plan_.obs_orig[s];
+    for (int j = 0; j < comps; ++j) dst[k * comps + j] = src[static_cast<std::size_t>(j) * N + s];
+  }
+}
+
+double Problem::evaluate(double* resid2) {
+  activate();
+  reset_lm_status();
+  double* rbuf = nullptr;
+  if (resid2) {
+    ck(cudaMalloc(&rbuf, 2 * sizeof(double) * plan_.N), "cudaMalloc");
+    d_.resid = rbuf;
+  }
+  launch_cost(d_, sm_, false, stream_);
+  launches_ += kLaunchesCost;
+  d_.resid = nullptr;
+  read_lm();
+  if (lm_host_->err_obs != INT_MAX) {
+    if (rbuf) cudaFree(rbuf);
+    throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
+  }
+  if (rbuf) {
+    std::vector<double> h(2 * static_cast<std::size_t>(plan_.N));
+    ck(cudaMemcpy(h.data(), rbuf, h.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H resid");
+    cudaFree(rbuf);
+    unpermute_slots(h, 2, resid2);
+  }
+  return lm_host_->cost;
+}
+
+void Problem::linearize() {
+  reset_lm_status();
+  launch_linearize(d_, sm_, false, stream_);
+  launches_ += kLaunchesLinearize;
+  read_lm();
+  if (lm_host_->err_obs != INT_MAX)
+    throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
+}
+
+void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
+  activate();
+  const std::int64_t N = plan_.N;
+  double* js = nullptr;
+  double* rs = nullptr;
+  ck(cudaMalloc(&js, 18 * sizeof(double) * N), "cudaMalloc");
+  ck(cudaMalloc(&rs, 2 * sizeof(double) * N), "cudaMalloc");
+  d_.jstore = js;
+  d_.resid = rs;
+  reset_lm_status();
+  launch_linearize(d_, sm_, true, stream_);
+  launches_ += kLaunchesLinearize;
+  d_.jstore = nullptr;
+  d_.resid = nullptr;
+  read_lm();
+  std::vector<double> hj(18 * static_cast<std::size_t>(N)), hr(2 * static_cast<std::size_t>(N));
+  ck(cudaMemcpy(hj.data(), js, hj.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H J");
+  ck(cudaMemcpy(hr.data(), rs, hr.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H r");
+  cudaFree(js);
+  cudaFree(rs);
+  if (lm_host_->err_obs != INT_MAX)
+    throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
+  for (std::int64_t s = 0; s < N; ++s) {
+    const std::int64_t k = plan_.obs_orig[s];
+    if (jpose)
+      for (int j = 0; j < 12; ++j) jpose[k * 12 + j] = hj[static_cast<std::size_t>(j) * N + s];
+    if (jpoint)
+      for (int j = 0; j < 6; ++j) jpoint[k * 6 + j] = hj[static_cast<std::size_t>(12 + j) * N + s];
+    if (resid2) {
+      resid2[2 * k] = hr[s];
+      resid2[2 * k + 1] = hr[N + s];
+    }
+  }
+}
+
+void Problem::block_diagonals(double* hcc36, double* gc6, double* hpp9, double* gp3) {
+  activate();
+  linearize();
+  const int C = d_.C, P = d_.P;
+  std::vector<double> h(21 * static_cast<std::size_t>(C)), g(6 * static_cast<std::size_t>(C));
+  std::vector<double> hp(6 * static_cast<std::size_t>(P)), gpv(3 * static_cast<std::size_t>(P));
+  ck(cudaMemcpy(h.data(), d_.hcc, h.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  ck(cudaMemcpy(g.data(), d_.gc, g.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  ck(cudaMemcpy(hp.data(), d_.hpp, hp.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  ck(cudaMemcpy(gpv.data(), d_.gp, gpv.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+  for (int c = 0; c < C; ++c)
+    for (int a = 0; a < 6; ++a) {
+      if (gc6) gc6[c * 6 + a] = g[c * 6 + a];
+      for (int b = 0; b < 6; ++b)
+        if (hcc36) hcc36[c * 36 + a * 6 + b] = h[c * 21 + sym6(a, b)];
+    }
+  for (int i = 0; i < P; ++i) {
+    const int p = plan_.pt_of_internal[i];
+    for (int a = 0; a < 3; ++a) {
+      if (gp3) gp3[p * 3 + a] = gpv[i * 3 + a];
+      for (int b = 0; b < 3; ++b)
+        if (hpp9) hpp9[p * 9 + a * 3 + b] = hp[i * 6 + sym3(a, b)];
+    }
+  }
+}
+
+void Problem::build_pcg_graph() {
+  if (pcg_graph_) return;
+  cudaGraph_t g;
+  ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
+  for (int i = 0; i < kPcgChunk; ++i) launch_pcg_iteration(d_, sm_, stream_);
+  ck(cudaStreamEndCapture(stream_, &g), "end capture");
+  ck(cudaGraphInstantiate(&pcg_graph_, g, 0), "graph instantiate");
+  cudaGraphDestroy(g);
+}
+
+// Damping + Schur preparation + PCG for one lambda; returns false when the
+// damped system is not SPD or the recurrence broke down (lm.hpp:146-152).
+bool Problem::solve(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
+  const long long budget = cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * d_.C);
+  ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+  launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_);
+  launches_ += kLaunchesPrep;
+  build_pcg_graph();
+  for (;;) {
+    ck(cudaGraphLaunch(pcg_graph_, stream_), "graph launch");
+    launches_ += kLaunchesPcgIter * kPcgChunk;
+    ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+    sync();
+    if (pcg_host_->state >= kPcgDone) break;
+  }
+  info.iters = pcg_host_->iters;
+  info.converged = pcg_host_->converged != 0;
+  info.rel_residual = pcg_host_->bnorm > 0 ? (pcg_host_->converged ? pcg_host_->true_norm : pcg_host_->rnorm) /
+                                                 pcg_host_->bnorm
+                                           : 0.0;
+  return pcg_host_->state == kPcgDone && !pcg_host_->not_spd;
+}
+
+void Problem::solve_step(double lambda, const bae_lm_config& cfg, double* delta, std::int64_t* iters,
+                         double* relres) {
+  activate();
+  linearize();
+  SolveInfo info;
+  if (!solve(lambda, cfg, info)) throw Error(BAE_ERR_NUMERICAL_BREAKDOWN, "damped system not SPD or PCG breakdown");
+  reset_lm_status();
+  launch_trial(d_, sm_, stream_);
+  launches_ += kLaunchesTrial;
+  sync();
+  const int C = d_.C, P = d_.P;
+  ck(cudaMemcpy(delta, d_.x, 6 * sizeof(double) * C, cudaMemcpyDeviceToHost), "D2H dc");
+  std::vector<double> dp(3 * static_cast<std::size_t>(P));
+  ck(cudaMemcpy(dp.data(), d_.dp, dp.size() * 8, cudaMemcpyDeviceToHost), "D2H dp");
+  for (int i = 0; i < P; ++i) {
+    const int p = plan_.pt_of_internal[i];
+    for (int a = 0; a < 3; ++a) delta[6 * static_cast<std::size_t>(C) + 3 * p + a] = dp[3 * i + a];
+  }
+  if (iters) *iters = info.iters;
+  if (relres) *relres = info.rel_residual;
+}
+
+static void validate_config(const bae_lm_config& c) {  // lm.hpp:39-45
+  if (!(c.damping_min <= c.initial_damping && c.initial_damping <= c.damping_max))
+    throw Error(BAE_ERR_INVALID_ARGUMENT, "LmConfig: damping out of bounds");
+  if (!(c.damping_up > 0.0 && c.damping_down > 0.0))
+    throw Error(BAE_ERR_INVALID_ARGUMENT, "LmConfig: damping factors must be positive");
+  if (c.plateau_patience < 1) throw Error(BAE_ERR_INVALID_ARGUMENT, "LmConfig: patience must be >= 1");
+}
+
+bool plateau_stagnation(const double* h, std::size_t n, int patience, double tol) {  // lm.hpp:89-98
+  if (n < static_cast<std::size_t>(patience) + 1) return false;
+  for (std::size_t i = n - static_cast<std::size_t>(patience); i < n; ++i) {
+    const double prev = h[i - 1];
+    const double imp = prev > 0.0 ? (prev - h[i]) / prev : 0.0;
+    if (imp >= tol) return false;
+  }
+  return true;
+}
+
+void Problem::optimize(const double* poses7, const double* points3, const bae_lm_config& cfg,
+                       std::vector<bae_iter_record>& traj, bae_lm_report& rep) {
+  activate();
+  validate_config(cfg);
+  if (cfg.solver != BAE_SOLVER_PCG)
+    throw Error(BAE_ERR_UNSUPPORTED, "solver: only the implicit-Schur PCG path is available on the device");
+  if (plan_.has_empty_camera || plan_.has_empty_point)
+    throw Error(BAE_ERR_INVALID_ARGUMENT, "diagonal op: missing diagonal entry");  // csr.hpp:53
+  if (poses7 || points3) set_parameters(poses7, points3);
+  const double n_obs = static_cast<double>(plan_.N);
+
+  // Initial evaluate (lm.hpp:217-220); the linearisation computes the cost
+  // together with the first step's normal-equation blocks.
+  linearize();
+  double cost = lm_host_->cost;
+  double grad = std::sqrt(lm_host_->grad_sq);
+  std::vector<double> history{cost};
+  double lambda = cfg.initial_damping;
+  traj.clear();
+  traj.push_back({0, 1, cost, cost / n_obs, lambda, 0.0, 0, grad, cost});
+  int iterations = 0, accepted_steps = 0, rejected_steps = 0;
+  long long total_pcg = 0;
+  bool need_lin = false;
+  rep = bae_lm_report{};
+  rep.reason = BAE_TERM_MAX_ITERS;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (iterations < cfg.max_iterations) {
+    const double lambda_used = lambda;
+    const bool saturated = lambda >= cfg.damping_max;
+    if (need_lin) {
+      linearize();
+      grad = std::sqrt(lm_host_->grad_sq);
+      need_lin = false;
+    }
+    SolveInfo info;
+    const bool ok = solve(lambda_used, cfg, info);
+    total_pcg += info.iters;
+    bool accepted = false;
+    double trial_cost = std::numeric_limits<double>::quiet_NaN();
+    if (ok) {
+      reset_lm_status();
+      launch_trial(d_, sm_, stream_);
+      launches_ += kLaunchesTrial;
+      read_lm();
+      trial_cost = (lm_host_->retract_bad || lm_host_->trial_bad) ? std::numeric_limits<double>::infinity()
+                                                                   : lm_host_->new_cost;
+      if (trial_cost < cost) {
+        launch_commit(d_, stream_);
+        launches_ += kLaunchesCommit;
+        cost = trial_cost;
+        history.push_back(cost);
+        ++accepted_steps;
+        accepted = true;
+        need_lin = true;
+      }
+    }
+    if (accepted) {
+      lambda = std::max(lambda * cfg.damping_down, cfg.damping_min);
+    } else {
+      ++rejected_steps;
+      lambda = std::min(lambda * cfg.damping_up, cfg.damping_max);
+    }
+    ++iterations;
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    traj.push_back({iterations, accepted ? 1 : 0, history.back(), history.back() / n_obs, lambda_used, el,
+                    info.iters, grad, trial_cost});
+    if (!accepted && saturated) {
+      rep.reason = BAE_TERM_SOLVER_FAILURE;
+      break;
+    }
+    if (history.back() == 0.0 ||
+        plateau_stagnation(history.data(), history.size(), cfg.plateau_patience, cfg.plateau_rel_tol)) {
+      rep.reason = BAE_TERM_PLATEAU;
+      break;
+    }
+  }
+  sync();
+  rep.iterations = iterations;
+  rep.final_cost = history.back();
+  rep.final_mse = rep.final_cost / n_obs;
+  rep.accepted_steps = accepted_steps;
+  rep.rejected_steps = rejected_steps;
+  rep.final_lambda = lambda;
+  rep.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  rep.total_pcg_iters = total_pcg;
+}
+
+double Problem::time_kernel(int kind, int reps) {
+  activate();
+  if (reps < 1) reps = 1;
+  cudaEvent_t a, b;
+  ck(cudaEventCreate(&a), "event");
+  ck(cudaEventCreate(&b), "event");
+  bae_lm_config cfg;
+  bae_lm_config_default(&cfg);
+  if (kind == 1 || kind == 2) {
+    linearize();
+    SolveInfo info;
+    cfg.pcg_max_iters = 1;
+    solve(1e-4, cfg, info);
+    // force the state machine to keep iterating on the current direction
+    PcgDev s = *pcg_host_;
+    s.state = kPcgIter;
+    s.dir = kDirZBetaP;
+    s.budget = LLONG_MAX;
+    s.tol = 0.0;
+    ck(cudaMemcpy(d_.pcg, &s, sizeof(PcgDev), cudaMemcpyHostToDevice), "H2D pcg");
+  }
+  double* js = nullptr;
+  if (kind == 3) {
+    ck(cudaMalloc(&js, 18 * sizeof(double) * plan_.N), "cudaMalloc");
+    d_.jstore = js;
+  }
+  auto launch = [&]() {
+    switch (kind) {
+      case 0:
+        launch_linearize(d_, sm_, false, stream_);
+        launches_ += kLaunchesLinearize;
+        break;
+      case 1:
+        launch_schur_only(d_, sm_, stream_);
+        launches_ += 1;
+        break;
+      case 2:
+        launch_pcg_iteration(d_, sm_, stream_);
+        launches_ += kLaunchesPcgIter;
+        break;
+      case 3:
+        launch_linearize(d_, sm_, true, stream_);
+        launches_ += kLaunchesLinearize;
+        break;
+      default:
+        throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");
+    }
+  };
+  launch();  // warm-up
+  sync();
+  ck(cudaEventRecord(a, stream_), "record");
+  for (int i = 0; i < reps; ++i) launch();
+  ck(cudaEventRecord(b, stream_), "record");
+  sync();
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+  d_.jstore = nullptr;
+  if (js) cudaFree(js);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms / reps;
+}
+
+}  // namespace bae

@@ -1,0 +1,75 @@
+// Device-resident BA problem (one GPU / one rank).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "bae_internal.hpp"
+#include "kernels.cuh"
+
+namespace bae {
+
+struct SolveInfo {
+  long long iters = 0;
+  bool converged = false;
+  double rel_residual = 0.0;
+};
+
+bool plateau_stagnation(const double* h, std::size_t n, int patience, double tol);
+
+class Problem {
+ public:
+  Problem(const double* poses7, int C, const double* points3, int P, const double* intr3,
+          const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2, std::int64_t N,
+          const bae_create_options& opt);
+  ~Problem();
+  Problem(const Problem&) = delete;
+  Problem& operator=(const Problem&) = delete;
+
+  int num_cameras() const { return d_.C; }
+  int num_points() const { return d_.P; }
+  std::int64_t num_obs() const { return plan_.N; }
+  const Plan& plan() const { return plan_; }
+  long long launches() const { return launches_; }
+  const Dev& dev() const { return d_; }
+
+  void activate();
+  void set_parameters(const double* poses7, const double* points3);
+  void get_parameters(double* poses7, double* points3);
+  double evaluate(double* resid2);
+  void jacobian(double* jpose, double* jpoint, double* resid2);
+  void block_diagonals(double* hcc36, double* gc6, double* hpp9, double* gp3);
+  void solve_step(double lambda, const bae_lm_config& cfg, double* delta, std::int64_t* iters, double* relres);
+  void optimize(const double* poses7, const double* points3, const bae_lm_config& cfg,
+                std::vector<bae_iter_record>& traj, bae_lm_report& rep);
+  double time_kernel(int kind, int reps);
+
+ private:
+  template <class T>
+  T* dalloc(std::size_t n);
+  template <class T>
+  T* upload(const std::vector<T>& v);
+  void sync();
+  void reset_lm_status();
+  void read_lm();
+  void linearize();
+  bool solve(double lambda, const bae_lm_config& cfg, SolveInfo& info);
+  void build_pcg_graph();
+  void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
+
+  bae_create_options opt_;
+  Plan plan_;
+  Dev d_{};
+  SmemSizes sm_;
+  cudaStream_t stream_ = nullptr;
+  cudaGraphExec_t pcg_graph_ = nullptr;
+  std::vector<void*> allocs_;
+  std::vector<double> intr_host_;
+  PcgDev* pcg_host_ = nullptr;
+  LmDev* lm_host_ = nullptr;
+  long long launches_ = 0;
+};
+
+}  // namespace bae

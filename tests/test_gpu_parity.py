@@ -1,0 +1,155 @@
+"""GPU parity: the sm_100a path through the C ABI vs the CPU oracle
+(restatement of the reference hot path). Tolerances are the north star's
+(BASELINE.json): bit-exact index structure, per-iteration cost 1e-6 relative,
+parameters 1e-5 relative; kernel values 1e-12 relative with a unit floor
+(acceptance.cpp:51-62)."""
+import numpy as np
+import pytest
+
+import paper_2409_12190_b200 as bae
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene(C=12, P=300, N=1500, seed=3):
+    return bae.synthetic.bal_shaped(C, P, N, seed=seed)
+
+
+def _pair(s, oracle, **kw):
+    gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations, **kw)
+    ref = oracle.Problem(s.poses, s.points, s.intrinsics, s.cam_idx, s.pt_idx, s.pixels)
+    return gpu, ref
+
+
+def _blocks_match(a, b, tol):
+    # per-block comparison with a unit absolute floor (acceptance.cpp:51-62)
+    scale = np.maximum(1.0, np.abs(b).reshape(b.shape[0], -1).max(axis=1))
+    err = np.abs(a - b).reshape(a.shape[0], -1).max(axis=1)
+    return bool(np.all(err <= tol * scale)), float((err / scale).max())
+
+
+def test_residual_matches_oracle(oracle):
+    s = _scene()
+    gpu, ref = _pair(s, oracle)
+    r_gpu = gpu.evaluate()
+    r_ref, c_ref = ref.evaluate()
+    assert np.allclose(r_gpu, r_ref, rtol=1e-12, atol=1e-10)
+    assert abs(gpu.cost() - c_ref) <= 1e-12 * c_ref
+
+
+def test_jacobian_values_and_pattern(oracle):
+    s = _scene(seed=4)
+    gpu, ref = _pair(s, oracle)
+    jg = gpu.jacobian()
+    jr = ref.jacobian()
+    ok, worst = _blocks_match(jg.j_pose.values, jr["j_pose"], 1e-12)
+    assert ok, worst
+    ok, worst = _blocks_match(jg.j_point.values, jr["j_point"], 1e-12)
+    assert ok, worst
+    # bit-exact index structure (one block per row at the gather column)
+    assert np.array_equal(jg.j_pose.row_ptr, jr["pose_row_ptr"])
+    assert np.array_equal(jg.j_pose.col_idx, jr["pose_col"])
+    assert np.array_equal(jg.j_point.row_ptr, jr["point_row_ptr"])
+    assert np.array_equal(jg.j_point.col_idx, jr["point_col"])
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_transpose_plans_bit_exact(oracle, which):
+    s = _scene(C=20, P=500, N=2600, seed=5)
+    gpu, ref = _pair(s, oracle, tile_obs=64)  # many tiles
+    tg = gpu.transpose_plan(which)
+    rp, ci, sb = ref.transpose_plan(which)
+    assert np.array_equal(tg.row_ptr, rp)
+    assert np.array_equal(tg.col_idx, ci)
+    assert np.array_equal(tg.src_block, sb)
+
+
+def test_block_diagonals_match_normal_matrix(oracle):
+    s = _scene(C=6, P=60, N=240, seed=6)
+    gpu, ref = _pair(s, oracle)
+    hcc, gc, hpp, gp = gpu.block_diagonals()
+    A, b = ref.normal_dense(0.0, cmin=-1e300, cmax=1e300)  # undamped
+    C, P = s.poses.shape[0], s.points.shape[0]
+    for c in range(C):
+        blk = A[6 * c:6 * c + 6, 6 * c:6 * c + 6]
+        assert np.allclose(hcc[c], blk, rtol=1e-11, atol=1e-9 * np.abs(blk).max())
+        assert np.allclose(-gc[c], b[6 * c:6 * c + 6], rtol=1e-11, atol=1e-9 * np.abs(b).max())
+    o = 6 * C
+    for p in range(P):
+        blk = A[o + 3 * p:o + 3 * p + 3, o + 3 * p:o + 3 * p + 3]
+        assert np.allclose(hpp[p], blk, rtol=1e-11, atol=1e-12 * np.abs(blk).max())
+        assert np.allclose(-gp[p], b[o + 3 * p:o + 3 * p + 3], rtol=1e-11, atol=1e-9 * np.abs(b).max())
+
+
+@pytest.mark.parametrize("lmbda", [1e-4, 1e-1, 10.0])
+def test_schur_pcg_step_matches_cholesky(oracle, lmbda):
+    s = _scene(C=10, P=200, N=900, seed=7)
+    gpu, ref = _pair(s, oracle)
+    cfg = bae.LmConfig(solver=bae.SolverChoice.pcg, pcg_tol=1e-13, pcg_max_iters=2000)
+    dg, iters, rel = gpu.solve_step(lmbda, cfg)
+    dr, _ = ref.solve_step(lmbda, bae.LmConfig())
+    assert iters > 0
+    assert np.linalg.norm(dg - dr) <= 1e-8 * np.linalg.norm(dr), (np.linalg.norm(dg - dr) / np.linalg.norm(dr))
+
+
+def test_lm_trajectory_matches_oracle_ladybug(oracle):
+    s = bae.synthetic.config_scene("ladybug-49")
+    gpu, ref = _pair(s, oracle)
+    cfg_g = bae.LmConfig(max_iterations=15, solver=bae.SolverChoice.pcg, pcg_tol=1e-12)
+    rep = bae.optimize(gpu, s.poses, s.points, cfg_g)
+    oracle.set_threads(8)
+    oref = ref.optimize(bae.LmConfig(max_iterations=15))  # reference default: Cholesky (exact)
+    n = min(len(rep.trajectory), len(oref["trajectory"]))
+    assert n >= 4
+    for a, b in zip(rep.trajectory[:n], oref["trajectory"][:n]):
+        assert a.accepted == b["accepted"]
+        assert abs(a.cost - b["cost"]) <= 1e-6 * b["cost"], (a.iteration, a.cost, b["cost"])
+        assert a.lmbda == b["lmbda"]
+    assert abs(rep.final_cost - oref["final_cost"]) <= 1e-6 * oref["final_cost"]
+    p7, p3 = gpu.get_parameters()
+    assert np.abs(p3 - oref["points"]).max() <= 1e-5 * max(1.0, np.abs(oref["points"]).max())
+    assert np.abs(p7 - oref["poses"]).max() <= 1e-5 * max(1.0, np.abs(oref["poses"]).max())
+
+
+def test_cheirality_reports_lowest_observation(oracle):
+    s = _scene(C=4, P=40, N=120, seed=8)
+    pts = s.points.copy()
+    # put point pt_idx[k] on camera cam_idx[k]'s plane for two observations
+    ks = [57, 91]
+    for k in ks:
+        c, p = s.cam_idx[k], s.pt_idx[k]
+        q = s.poses[c, 3:]
+        x, y, z, w = q
+        R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                      [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                      [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+        pts[p] = R.T @ (np.array([0.3, 0.1, 0.0]) - s.poses[c, :3])
+    moved = {int(s.pt_idx[k]) for k in ks}
+    with pytest.raises(bae.CheiralityError) as e:
+        bae.make_ba_problem(s.poses, pts, s.intrinsics, s.observations)
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.Problem(s.poses, pts, s.intrinsics, s.cam_idx, s.pt_idx, s.pixels)
+    assert e.value.observation == eo.value.index
+    assert int(s.pt_idx[e.value.observation]) in moved
+
+
+def test_index_error_position():
+    s = _scene(C=4, P=40, N=120, seed=9)
+    ci = s.cam_idx.copy()
+    pi = s.pt_idx.copy()
+    pi[17] = 40
+    with pytest.raises(bae.IndexError) as e:
+        bae.make_ba_problem(s.poses, s.points, s.intrinsics, (ci, pi, s.pixels))
+    assert e.value.position == 17
+    ci[5] = -1
+    with pytest.raises(bae.IndexError) as e:
+        bae.make_ba_problem(s.poses, s.points, s.intrinsics, (ci, pi, s.pixels))
+    assert e.value.position == 5
+
+
+def test_launch_counter_moves():
+    s = _scene()
+    gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+    n0 = gpu.launch_count()
+    bae.optimize(gpu, s.poses, s.points, bae.LmConfig(max_iterations=2, solver=bae.SolverChoice.pcg))
+    assert gpu.launch_count() > n0 + 10
