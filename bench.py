@@ -1,0 +1,303 @@
+"""Benchmark of the B200 BA hot path (BASELINE.json metric: LM iterations/s and
+time-to-converge on BAL-shaped BA; obs/s of the fused residual+Jacobian).
+
+One "step" = one complete LM solve (optimize, lm.hpp:205-255, LmConfig
+defaults with solver=pcg and max_iterations=50 as in the reference CLI,
+cli.hpp:25) of the synthetic Trafalgar-257-shaped problem (BASELINE.json
+configs[1]) from the same initial parameters. value = LM iterations per
+second over the K timed solves (device time, CUDA events on the solver
+stream), max over ranks; time_to_converge_s = mean device time per solve.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config NAME]
+
+--impl reference times the reference's CPU algorithm (the oracle port of
+traceopt, oracle/; the reference itself needs Eigen and cannot be built here,
+DESIGN.md) on this host's cores, on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE_CFG = "trafalgar-257"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_init(n):
+    rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        return rank, world, dist
+    return 0, 1, None
+
+
+def _max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def _cpu_sample(scene, cfg_name, threads, lm_iters=2):
+    """Reference algorithm (oracle port) on the host: `lm_iters` LM iterations
+    with the reference default (Cholesky) solver; returns LM iters/s."""
+    from oracle import oracle as O
+    from paper_2409_12190_b200.api import LmConfig
+    O.set_threads(threads)
+    prob = O.Problem(scene.poses, scene.points, scene.intrinsics, scene.cam_idx, scene.pt_idx, scene.pixels)
+    t0 = time.perf_counter()
+    rep = prob.optimize(LmConfig(max_iterations=lm_iters))
+    el = time.perf_counter() - t0
+    return rep["iterations"] / el, el, rep
+
+
+def run_reference(args):
+    rank, world, dist = _dist_init(args.gpus)
+    if rank != 0:
+        return
+    import paper_2409_12190_b200 as bae
+    scene = bae.synthetic.config_scene(args.config)
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, el, rep = _cpu_sample(scene, args.config, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    C, P, N = bae.synthetic.CONFIGS[args.config]
+    sample = f"2 LM iterations (Cholesky, the reference default) of {args.config} per step"
+    line = {"impl": "reference", "metric": "lm_iters_per_s", "value": value, "unit": "LM iter/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * 2 / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count)",
+            "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM + Cholesky"},
+            "cpu_baseline": {"value": value, "unit": "LM iter/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "LM iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    rank, world, dist = _dist_init(args.gpus)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    import paper_2409_12190_b200 as bae
+    from paper_2409_12190_b200.api import LmConfig, SolverChoice
+
+    C, P, N = bae.synthetic.CONFIGS[args.config]
+    # N > 1 without the NCCL build: independent replicas (one problem per rank, seed offset by rank)
+    scene = bae.synthetic.bal_shaped(C, P, N, seed=C + rank)
+    cfg = LmConfig(max_iterations=50, solver=SolverChoice.pcg)
+    prob = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local)
+    stats = prob.stats()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def one_solve():
+        prob.set_parameters(scene.poses, scene.points)  # untimed: inputs resident before the timed solve
+        flush.zero_()  # L2 flush between timed steps (L2 = 126 MB; 256 MB written)
+        torch.cuda.synchronize()
+        rep = bae.optimize(prob, None, None, cfg)
+        return rep
+
+    for _ in range(args.warmup):
+        one_solve()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = prob.launch_count()
+    dev_s, iters, pcg = 0.0, 0, 0
+    reports = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            rep = one_solve()
+            reports.append(rep)
+            dev_s += rep.device_seconds
+            iters += rep.iterations
+            pcg += rep.total_pcg_iters
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = prob.launch_count() - launches0
+    dev_max = _max_over_ranks(dist, dev_s)
+    iters_all = _sum_over_ranks(dist, iters)
+    value = iters_all / dev_max  # whole-job LM iterations / s
+
+    # --- kernel-level measurements (device events on the solver stream) ---
+    ms_lin = prob.time_kernel(0, 20)
+    ms_sx = prob.time_kernel(1, 50)
+    ms_pcg = prob.time_kernel(2, 50)
+    peak, peak_kind = _peaks()
+    # SURVEY.md 8(d) algorithmic bytes per unit: K5 (S*p per PCG iteration)
+    alg_sx = 280 * N + 48 * P + 800 * C
+    achieved = alg_sx / (ms_sx * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config, {}).get("k_schur_tiles")
+        except Exception:
+            traffic = None
+
+    # --- end to end through the C ABI with host buffers (create + solve + read back) ---
+    e2e_iters, e2e_s = 0, 0.0
+    for i in range(max(1, min(args.steps, 3)) + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        p2 = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local)
+        st = {}
+        r2 = bae.optimize(p2, scene.poses, scene.points, cfg, final_state=st)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        del p2
+        if i > 0:  # first one warms host allocations
+            e2e_iters += r2.iterations
+            e2e_s += el
+    e2e_max = _max_over_ranks(dist, e2e_s)
+    e2e_value = _sum_over_ranks(dist, e2e_iters) / e2e_max
+    h2d = 56 * C + 24 * P + 24 * C + 24 * N + 56 * C + 24 * P  # create inputs + optimize init params
+    d2h = 56 * C + 24 * P
+
+    clocks = clk.summary()
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            v, el, _ = _cpu_sample(scene, args.config, os.cpu_count() or 1)
+            cpu = {"value": v, "unit": "LM iter/s", "cores": os.cpu_count() or 1, "kind": "port",
+                   "sample": f"2 LM iterations of the reference algorithm (oracle port, Cholesky) on "
+                             f"{args.config}, {el:.1f} s"}
+        last = reports[-1]
+        line = {
+            "metric": "lm_iters_per_s", "value": value, "unit": "LM iter/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * dev_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count + rank)",
+            "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM (LmConfig defaults, solver=pcg, "
+                                   f"max_iterations=50) from the same initial state each step",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (256 MB write) between steps",
+                       "tiles": stats["tiles"], "tile_camera_entries": stats["entries"]},
+            "time_to_converge_s": dev_max / args.steps,
+            "lm_iterations_per_solve": last.iterations, "pcg_iterations_per_solve": last.total_pcg_iters,
+            "final_mse": last.final_mse, "termination": last.reason.name,
+            "obs_per_s_residual_jacobian": N / (ms_lin * 1e-3),
+            "kernel_us": {"linearize": ms_lin * 1e3, "schur_tiles": ms_sx * 1e3, "pcg_iteration": ms_pcg * 1e3},
+            "roofline": {"bound": "hbm", "kernel": "k_schur_tiles (implicit Schur S*p, per PCG iteration)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_kind,
+                         "algorithmic_bytes": "SURVEY 8(d) K5: 280 N + 48 P + 800 C per launch"},
+            "e2e": {"value": e2e_value, "unit": "LM iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=BASE_CFG)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -93,6 +93,7 @@ typedef struct bae_lm_report {
   double final_lambda;
   double solve_seconds;   /* wall time of the LM loop (lm.hpp:222-232) */
   int64_t total_pcg_iters;
+  double device_seconds;  /* CUDA-event time of the LM loop on the solver stream */
 } bae_lm_report;
 
 /* Creation options (no reference counterpart; NULL = defaults). */

@@ -57,6 +57,7 @@ class LmReportC(ctypes.Structure):
         ("final_lambda", ctypes.c_double),
         ("solve_seconds", ctypes.c_double),
         ("total_pcg_iters", ctypes.c_int64),
+        ("device_seconds", ctypes.c_double),
     ]
 
 

@@ -151,6 +151,7 @@ class LmReport:
     final_lambda: float = 0.0
     solve_seconds: float = 0.0
     total_pcg_iters: int = 0
+    device_seconds: float = 0.0
 
 
 @dataclasses.dataclass
@@ -336,10 +337,11 @@ def optimize(model: TracedProblem, init_poses, init_points, config: LmConfig,
     cap = int(config.max_iterations) + 1
     recs = (IterRecordC * cap)()
     rep = LmReportC()
-    p7 = _f64(init_poses, (model.num_poses(), 7))
-    p3 = _f64(init_points, (model.num_points(), 3))
-    out7 = np.empty_like(p7)
-    out3 = np.empty_like(p3)
+    # init_poses / init_points = None: start from the parameters already on the device
+    p7 = None if init_poses is None else _f64(init_poses, (model.num_poses(), 7))
+    p3 = None if init_points is None else _f64(init_points, (model.num_points(), 3))
+    out7 = np.empty((model.num_poses(), 7))
+    out3 = np.empty((model.num_points(), 3))
     _check(lib.bae_optimize(model._h, ptr(p7), ptr(p3), ctypes.byref(cfg), recs, cap, ctypes.byref(rep), ptr(out7),
                             ptr(out3)))
     n = min(cap, rep.iterations + 1)
@@ -347,7 +349,7 @@ def optimize(model: TracedProblem, init_poses, init_points, config: LmConfig,
                               r.grad_norm, r.trial_cost) for r in recs[:n]]
     report = LmReport(rep.final_cost, rep.final_mse, rep.iterations, traj, TerminationReason(rep.reason),
                       rep.accepted_steps, rep.rejected_steps, rep.final_lambda, rep.solve_seconds,
-                      rep.total_pcg_iters)
+                      rep.total_pcg_iters, rep.device_seconds)
     if final_state is not None:
         final_state.update(dict(poses=out7, points=out3, lmbda=rep.final_lambda, iterations=rep.iterations,
                                 accepted_steps=rep.accepted_steps, rejected_steps=rep.rejected_steps))

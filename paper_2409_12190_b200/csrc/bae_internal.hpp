@@ -67,7 +67,7 @@ struct Plan {
 void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N);
 
 Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2,
-                std::int64_t N, int tile_obs_target, int tile_cam_cap, int smem_tile_obs_cap);
+                std::int64_t N, int tile_obs_target, int tile_cam_cap, int tile_pts_cap, int smem_tile_obs_cap);
 
 void synth_bal_shaped(int C, int P, std::int64_t N, std::uint64_t seed, double pixel_sigma, double pose_sigma,
                       double point_sigma, double* poses7, double* points3, double* intr3, std::int32_t* cam_idx,

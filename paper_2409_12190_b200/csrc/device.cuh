@@ -85,7 +85,73 @@ struct Dev {
   // stored-Jacobian mode and exports (slot order, component-major [comp][N])
   double* jstore;  // 18 * N or null
   double* resid;   // 2 * N or null
+  unsigned long long* trace;  // per-tile phase timestamps (BAE_TRACE) or null
+  // pipelined small tiles: per-tile descriptor {blob offset / 16, blob bytes,
+  // first point, point count} and the packed per-tile index blobs
+  const int4* tile_desc;
+  const char* tile_blob;
+  const int* small_tiles;
+  const int* big_tiles;
+  int n_small, n_big_tiles;
 };
+
+// ---- pipelined warp-tiles: fixed caps and the per-warp shared-memory map ----
+// A small tile has at most kPipeObs observations, kPipeCams cameras and
+// kPipePts points; its index blob is
+//   [hdr int x8: ob nobs pb npts eb ncam 0 0 | camid[ncam] | ent[ncam+1] |
+//    pptr[npts+1] | lcpt u32[nobs] | ptl u16[nobs] ] padded to 16 bytes.
+constexpr int kPipeObs = 64, kPipeCams = 16, kPipePts = 32;
+constexpr int kBlobCap = 32 + 4 * kPipeCams + 4 * (kPipeCams + 1) + 4 * (kPipePts + 1) + 6 * kPipeObs + 16;
+constexpr int kBufBlob = 0;
+constexpr int kBufPts = (kBlobCap + 15) / 16 * 16;                  // point window (+8 B alignment slack)
+constexpr int kBufHinv = kBufPts + (kPipePts * 24 + 16 + 15) / 16 * 16;
+constexpr int kBufCam = kBufHinv + kPipePts * 48;                   // camera records, 128 B each
+constexpr int kBufVz = kBufCam + kPipeCams * 128;                   // direction (x or z), 48 B each
+constexpr int kBufVp = kBufVz + kPipeCams * 48;                     // p (for z + beta p)
+constexpr int kBufBytes = kBufVp + kPipeCams * 48;
+constexpr int kScrStage = 2 * kBufBytes;                            // stage [6][kPipeObs] doubles
+constexpr int kScrTp = kScrStage + 6 * kPipeObs * 8;                // t_p [kPipePts][3]
+constexpr int kScrBar = kScrTp + kPipePts * 24;                     // 4 mbarriers
+constexpr int kPipeWarpBytes = (kScrBar + 32 + 127) / 128 * 128;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok = 0;
+  long long spins = 0;
+  do {
+    if (++spins > (1ll << 22)) __trap();  // a lost transaction must fail loudly, never hang
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// TMA bulk copy global -> shared (16 B aligned, size a multiple of 16),
+// completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Packed symmetric storage: 6x6 upper triangle row-major (21), 3x3 (6).
 __host__ __device__ constexpr int sym6(int a, int b) {
@@ -108,7 +174,11 @@ struct Ws {
   double* pt;
   double* stage;
   double* piece;
-  int* ent;
+  int* ent;                 // ncam + 1 entry boundaries (tile-local slots)
+  int* pptr;                // npts + 1 point-list offsets (tile-local)
+  std::uint32_t* lcpt;      // nobs local camera | local point << 16
+  std::uint16_t* ptl;       // nobs slots grouped by point
+  int* camid;               // ncam global camera ids
 };
 struct WsDims {
   int camw, ptw, stw, pw;
@@ -117,7 +187,9 @@ __host__ __device__ __forceinline__ long long ws_bytes(WsDims w, int ncam, int n
   const long long nchunk = (nobs + 31) / 32;
   const long long dbl = (long long)ncam * w.camw + (long long)npts * w.ptw + (long long)nobs * w.stw +
                         (nchunk + ncam) * w.pw;
-  return dbl * 8 + (long long)(ncam + 1) * 4;
+  // ints: ent, pptr, lcpt ; shorts: ptl
+  return dbl * 8 + (long long)(ncam + 1) * 4 + (long long)(npts + 1) * 4 + (long long)nobs * 4 +
+         ((long long)nobs * 2 + 15) / 16 * 16 + (long long)ncam * 4;
 }
 __device__ __forceinline__ Ws ws_carve(char* base, WsDims w, int ncam, int npts, int nobs) {
   Ws ws;
@@ -132,11 +204,15 @@ __device__ __forceinline__ Ws ws_carve(char* base, WsDims w, int ncam, int npts,
   ws.piece = d;
   d += (long long)(nchunk + ncam) * w.pw;
   ws.ent = reinterpret_cast<int*>(d);
+  ws.pptr = ws.ent + (ncam + 1);
+  ws.lcpt = reinterpret_cast<std::uint32_t*>(ws.pptr + (npts + 1));
+  ws.ptl = reinterpret_cast<std::uint16_t*>(ws.lcpt + nobs);
+  ws.camid = reinterpret_cast<int*>(reinterpret_cast<char*>(ws.ptl) + ((long long)nobs * 2 + 15) / 16 * 16);
   return ws;
 }
 
 struct TileGeom {
-  int ob, nobs, pb, npts, eb, ncam, big;
+  int ob, nobs, pb, npts, eb, ncam, big, trace_id;
 };
 __device__ __forceinline__ TileGeom tile_geom(const Dev& d, int t) {
   TileGeom g;
@@ -147,6 +223,7 @@ __device__ __forceinline__ TileGeom tile_geom(const Dev& d, int t) {
   g.eb = d.tile_ent_begin[t];
   g.ncam = d.tile_ent_begin[t + 1] - g.eb;
   g.big = d.tile_ws[t];
+  g.trace_id = t;
   return g;
 }
 

@@ -1,6 +1,13 @@
 // sm_100a kernels of the BA hot path. FP64 throughout (the reference is FP64,
-// SPEC.md:332). All camera-side sums are deterministic segmented reductions
-// (no floating-point atomics); see device.cuh.
+// SPEC.md:332). All sums are deterministic: fixed-order staged reductions and
+// fixed shuffle trees, no floating-point atomics.
+//
+// Work decomposition. A tile (Plan, bae_internal.hpp) is a run of points and
+// their observations, processed by ONE WARP with its own shared-memory
+// workspace slice; a CTA hosts several independent warp-tiles. Phases inside a
+// tile are separated by __syncwarp only, so a tile never waits on another
+// tile, and a tile's global loads are issued in batches (one memory latency
+// per dependent stage).
 //
 // Per-observation algebra (one observation k, camera c, point p, camera-frame
 // point y = R p + t, D = d(pixel)/d(y) from camera.hpp:59-71):
@@ -10,6 +17,9 @@
 //   J_p t   = D (R t)                         J_p^T u = R^T (D^T u)
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -17,16 +27,8 @@
 namespace bae {
 
 // ---------------------------------------------------------------------------
-// shared helpers
+// per-observation math
 // ---------------------------------------------------------------------------
-
-__device__ __forceinline__ char* tile_base(const Dev& d, const TileGeom& g, char* smem) {
-  return g.big >= 0 ? d.bigws + (long long)g.big * d.big_stride : smem;
-}
-
-__device__ __forceinline__ void load_entries(const Dev& d, const TileGeom& g, const Ws& ws) {
-  for (int l = threadIdx.x; l <= g.ncam; l += blockDim.x) ws.ent[l] = d.ent_obs_begin[g.eb + l] - g.ob;
-}
 
 // y = R p + t and D for one observation from a 15-double camera record
 // (R[9] t[3] f k1 k2).
@@ -62,7 +64,6 @@ __device__ __forceinline__ void jac_pt(const double* D, const double* R, double*
 
 // s = J_p^T J_c v  (3-vector) using the factored forms.
 __device__ __forceinline__ void jpt_jc_v(const double* D, const P3& y, const double* R, const double* v, double* s) {
-  // a = v_rho + v_omega x y
   const double ax = v[0] + (v[4] * y.z - v[5] * y.y);
   const double ay = v[1] + (v[5] * y.x - v[3] * y.z);
   const double az = v[2] + (v[3] * y.y - v[4] * y.x);
@@ -94,19 +95,127 @@ __device__ __forceinline__ void jct_jp_t(const double* D, const P3& y, const dou
   z[5] = y.x * g1 - y.y * g0;
 }
 
-__device__ __forceinline__ void load_camrec(const Dev& d, const TileGeom& g, const Ws& ws, int camw, const double* rec) {
-  for (int idx = threadIdx.x; idx < g.ncam * 15; idx += blockDim.x) {
-    const int l = idx / 15, j = idx - l * 15;
-    ws.cam[l * camw + j] = rec[(long long)d.ent_cam[g.eb + l] * kCamRec + j];
+// Forward residual exactly as the reference evaluates it: quaternion rotate
+// (trace.hpp:439-452, lie.hpp:88-93), bal_project_cam (camera.hpp:50-57),
+// sub as p0 + (-1) p1 (trace.hpp:488-497). cam: [t3 q4 f k1 k2].
+__device__ __forceinline__ bool residual(const double* cam, const double* pt, double2 px, double& r0, double& r1,
+                                         P3& y) {
+  const P3 yr = quat_rotate({cam[3], cam[4], cam[5], cam[6]}, {pt[0], pt[1], pt[2]});
+  y = {yr.x + cam[0], yr.y + cam[1], yr.z + cam[2]};
+  double u, w;
+  if (!bal_project(y, cam[7], cam[8], cam[9], u, w)) return false;
+  r0 = u + -1.0 * px.x;
+  r1 = w + -1.0 * px.y;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// warp-tile infrastructure
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Batched warp copy global -> workspace: each lane issues kBatch independent,
+// unconditional loads (indices clamped into range) before its first store.
+// `addr(i)` returns the source address of element i.
+constexpr int kBatch = 8;
+template <class T, class Addr, class Store>
+__device__ __forceinline__ void warp_copy(int n, Addr addr, Store store) {
+  for (int base = lane_id(); base < n; base += kBatch * 32) {
+    T v[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) v[b] = *addr(min(base + b * 32, n - 1));
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b)
+      if (base + b * 32 < n) store(base + b * 32, v[b]);
   }
 }
 
-__device__ __forceinline__ void load_points(const Ws& ws, int ptw, const double* src, int pb, int npts) {
-  for (int idx = threadIdx.x; idx < npts * 3; idx += blockDim.x) {
-    const int lp = idx / 3, j = idx - lp * 3;
-    ws.pt[lp * ptw + j] = src[(long long)pb * 3 + idx];
+// Tile index data: entry boundaries, camera ids, point-list offsets, slot
+// camera/point codes and the point lists (all independent loads).
+__device__ __forceinline__ void load_tile_index(const Dev& d, const TileGeom& g, const Ws& ws) {
+  const int* eo = d.ent_obs_begin + g.eb;
+  const int* ec = d.ent_cam + g.eb;
+  const int* pp = d.pt_ptr + g.pb;
+  const std::uint32_t* lc = d.obs_lcpt + g.ob;
+  const std::uint16_t* pl = d.ptobs + g.ob;
+  warp_copy<int>(g.ncam + 1, [&](int i) { return eo + i; }, [&](int i, int v) { ws.ent[i] = v - g.ob; });
+  warp_copy<int>(g.ncam, [&](int i) { return ec + i; }, [&](int i, int v) { ws.camid[i] = v; });
+  warp_copy<int>(g.npts + 1, [&](int i) { return pp + i; }, [&](int i, int v) { ws.pptr[i] = v - g.ob; });
+  warp_copy<std::uint32_t>(g.nobs, [&](int i) { return lc + i; }, [&](int i, std::uint32_t v) { ws.lcpt[i] = v; });
+  warp_copy<std::uint16_t>(g.nobs, [&](int i) { return pl + i; }, [&](int i, std::uint16_t v) { ws.ptl[i] = v; });
+}
+
+// W consecutive doubles per point from src[(pb + lp) * W] into ws.pt[lp * ptw + off].
+template <int W>
+__device__ __forceinline__ void load_point_fields(const Ws& ws, int ptw, int off, const double* src, int pb,
+                                                  int npts) {
+  const double* base = src + (long long)pb * W;
+  warp_copy<double>(
+      npts * W, [&](int i) { return base + i; },
+      [&](int i, double v) {
+        const int lp = i / W;
+        ws.pt[lp * ptw + off + (i - lp * W)] = v;
+      });
+}
+
+// W consecutive doubles per camera from src[camid * stride] into
+// ws.cam[l * camw + off]. Needs ws.camid (load_tile_index + __syncwarp).
+template <int W>
+__device__ __forceinline__ void load_cam_fields(const Ws& ws, int ncam, int camw, int off, const double* src,
+                                                int stride) {
+  warp_copy<double>(
+      ncam * W,
+      [&](int i) {
+        const int l = i / W;
+        return src + (long long)ws.camid[l] * stride + (i - l * W);
+      },
+      [&](int i, double v) {
+        const int l = i / W;
+        ws.cam[l * camw + off + (i - l * W)] = v;
+      });
+}
+
+// Per (tile camera, component): sum of the staged W-vectors over the
+// camera's slot range, in slot order (two interleaved partial sums).
+template <int W, int SW>
+__device__ __forceinline__ void entries_from_stage(const Ws& ws, int ncam, int eb, double* out) {
+  for (int idx = lane_id(); idx < ncam * W; idx += 32) {
+    const int e = idx / W, j = idx - e * W;
+    const int b = ws.ent[e], en = ws.ent[e + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int q = b;
+    for (; q + 1 < en; q += 2) {
+      a0 += ws.stage[q * SW + j];
+      a1 += ws.stage[(q + 1) * SW + j];
+    }
+    if (q < en) a0 += ws.stage[q * SW + j];
+    out[(long long)(eb + e) * W + j] = a0 + a1;
   }
 }
+
+// Workspace base of a tile: this warp's slice of dynamic shared memory, or a
+// global slot for the rare tile that does not fit (one very long track).
+// kShared is a compile-time constant so the compiler emits LDS/STS.
+template <bool kShared>
+__device__ __forceinline__ char* ws_base(const Dev& d, const TileGeom& g, char* smem, int slice) {
+  return kShared ? smem + (threadIdx.x >> 5) * slice : d.bigws + (long long)g.big * d.big_stride;
+}
+
+// Dispatch one warp-tile body on shared or global workspace.
+#define BAE_TILE_DISPATCH(body, ...) \
+  do {                               \
+    if (g.big >= 0)                  \
+      body<false>(__VA_ARGS__);      \
+    else                             \
+      body<true>(__VA_ARGS__);       \
+  } while (0)
 
 // ---------------------------------------------------------------------------
 // K-rec: camera records (R from the quaternion, lie.hpp:68-70) after any
@@ -135,155 +244,146 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
 //   per point : H_pp (6), g_p (3)          -> hpp, gp
 //   per entry : H_cc (21), g_c (6) partial -> partial[e][27]
 //   per tile  : sum r^2, sum |g_p|^2       -> tile_red
-// The forward residual follows the reference (quaternion rotate, trace.hpp:
-// 439-452; bal_cam, :464-474); its Jacobian uses that forward value y.
+// The forward residual follows the reference (quaternion rotate); its
+// Jacobian uses that forward value y (trace.hpp:612-629).
+// cam: [t3 q4 f k1 k2 R9] (19) ; pt: p3 ; stage: Jc12 Jp6 r2 (20)
 // ---------------------------------------------------------------------------
-constexpr WsDims kLinWs{19, 3, 9, 27};
+constexpr WsDims kLinWs{19, 3, 20, 0};
 
-__global__ void __launch_bounds__(kTileThreads) k_linearize(Dev d, int write_jac) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ double red[32];
-  const int t = blockIdx.x;
-  const TileGeom g = tile_geom(d, t);
-  const Ws ws = ws_carve(tile_base(d, g, smem), kLinWs, g.ncam, g.npts, g.nobs);
-  // cameras: [t3 q4 f k1 k2 R9]
-  for (int idx = threadIdx.x; idx < g.ncam * 19; idx += blockDim.x) {
-    const int l = idx / 19, j = idx - l * 19;
-    const long long c = d.ent_cam[g.eb + l];
-    double v;
-    if (j < 7)
-      v = d.pose[c * 7 + j];
-    else if (j < 10)
-      v = d.intr[c * 3 + (j - 7)];
-    else
-      v = d.camrec[c * kCamRec + (j - 10)];
-    ws.cam[idx] = v;
-  }
-  load_points(ws, 3, d.pts, g.pb, g.npts);
-  load_entries(d, g, ws);
-  __syncthreads();
-
-  const int nchunk = (g.nobs + 31) / 32;
+template <bool kShared>
+__device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t,
+                                         int write_jac) {
+  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kLinWs, g.ncam, g.npts, g.nobs);
+  const int lane = lane_id();
+  load_point_fields<3>(ws, 3, 0, d.pts, g.pb, g.npts);
+  load_tile_index(d, g, ws);
+  __syncwarp();
+  load_cam_fields<7>(ws, g.ncam, 19, 0, d.pose, 7);
+  load_cam_fields<3>(ws, g.ncam, 19, 7, d.intr, 3);
+  load_cam_fields<9>(ws, g.ncam, 19, 10, d.camrec, kCamRec);
+  __syncwarp();
   double cost = 0.0;
   int bad = INT_MAX;
-  for (int base = 0; base < g.nobs; base += blockDim.x) {
-    const int s = base + threadIdx.x;
-    double v27[27];
+  for (int s = lane; s < g.nobs; s += 32) {
+    const std::uint32_t lcpt = ws.lcpt[s];
+    const double* cam = ws.cam + (lcpt & 0xffff) * 19;
+    const double* pt = ws.pt + (lcpt >> 16) * 3;
+    const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
+    double* st = ws.stage + s * 20;
+    double r0 = 0.0, r1 = 0.0;
+    P3 y;
+    if (residual(cam, pt, px, r0, r1, y)) {
+      double D[6];
+      bal_dproj(y, cam[7], cam[8], cam[9], D);
+      jac_cam(D, y, st);
+      jac_pt(D, cam + 10, st + 12);
+      st[18] = r0;
+      st[19] = r1;
+      cost += r0 * r0 + r1 * r1;
+      if (write_jac && d.jstore) {
+        const long long gs = g.ob + s;
 #pragma unroll
-    for (int j = 0; j < 27; ++j) v27[j] = 0.0;
-    int seg = -1;
-    if (s < g.nobs) {
-      const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
-      const int lc = lcpt & 0xffff, lp = lcpt >> 16;
-      seg = lc;
-      const double* cam = ws.cam + lc * 19;
-      const double* pt = ws.pt + lp * 3;
-      const P3 yr = quat_rotate({cam[3], cam[4], cam[5], cam[6]}, {pt[0], pt[1], pt[2]});
-      const P3 y{yr.x + cam[0], yr.y + cam[1], yr.z + cam[2]};
-      double u = 0.0, w = 0.0;
-      double r0 = 0.0, r1 = 0.0;
-      double stg[9];
-#pragma unroll
-      for (int j = 0; j < 9; ++j) stg[j] = 0.0;
-      if (bal_project(y, cam[7], cam[8], cam[9], u, w)) {
-        const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
-        r0 = u + -1.0 * px.x;
-        r1 = w + -1.0 * px.y;
-        double D[6], Jc[12], Jp[6];
-        bal_dproj(y, cam[7], cam[8], cam[9], D);
-        jac_cam(D, y, Jc);
-        jac_pt(D, cam + 10, Jp);
-        int q = 0;
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int b = a; b < 6; ++b) v27[q++] = Jc[a] * Jc[b] + Jc[6 + a] * Jc[6 + b];
-#pragma unroll
-        for (int a = 0; a < 6; ++a) v27[21 + a] = Jc[a] * r0 + Jc[6 + a] * r1;
-        q = 0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = a; b < 3; ++b) stg[q++] = Jp[a] * Jp[b] + Jp[3 + a] * Jp[3 + b];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) stg[6 + a] = Jp[a] * r0 + Jp[3 + a] * r1;
-        if (write_jac && d.jstore) {
-          const long long gs = g.ob + s;
-#pragma unroll
-          for (int j = 0; j < 12; ++j) d.jstore[(long long)j * d.N + gs] = Jc[j];
-#pragma unroll
-          for (int j = 0; j < 6; ++j) d.jstore[(long long)(12 + j) * d.N + gs] = Jp[j];
-        }
-        if (d.resid) {
-          d.resid[g.ob + s] = r0;
-          d.resid[(long long)d.N + g.ob + s] = r1;
-        }
-        cost += r0 * r0 + r1 * r1;
-      } else {
-        bad = min(bad, d.obs_orig[g.ob + s]);
+        for (int j = 0; j < 18; ++j) d.jstore[(long long)j * d.N + gs] = st[j];
       }
+      if (d.resid) {
+        d.resid[g.ob + s] = r0;
+        d.resid[(long long)d.N + g.ob + s] = r1;
+      }
+    } else {
+      bad = min(bad, d.obs_orig[g.ob + s]);
 #pragma unroll
-      for (int j = 0; j < 9; ++j) ws.stage[s * 9 + j] = stg[j];
+      for (int j = 0; j < 20; ++j) st[j] = 0.0;
     }
-    seg_reduce_pieces<27>(v27, seg, s, nchunk, ws.piece);
   }
   if (bad != INT_MAX) atomicMin(&d.lm->err_obs, bad);
-  __syncthreads();
-  entries_from_pieces<27>(ws, g.ncam, g.nobs, g.eb, d.partial);
+  __syncwarp();
+  // camera side: (entry, component) tasks over the H_cc upper triangle + g_c
+  for (int idx = lane; idx < g.ncam * 27; idx += 32) {
+    const int e = idx / 27, j = idx - e * 27;
+    int a, b;
+    if (j < 21) {  // row-major upper-triangle index -> (a, b)
+      a = 0;
+      int rem = j;
+      while (rem >= 6 - a) {
+        rem -= 6 - a;
+        ++a;
+      }
+      b = a + rem;
+    } else {
+      a = j - 21;
+      b = -1;
+    }
+    double acc = 0.0;
+    for (int q = ws.ent[e]; q < ws.ent[e + 1]; ++q) {
+      const double* st = ws.stage + q * 20;
+      acc += b >= 0 ? st[a] * st[b] + st[6 + a] * st[6 + b] : st[a] * st[18] + st[6 + a] * st[19];
+    }
+    d.partial[(long long)(g.eb + e) * 27 + j] = acc;
+  }
+  // point side: H_pp (6) and g_p (3) per point, observations in id order
   double gsq = 0.0;
-  for (int lp = threadIdx.x; lp < g.npts; lp += blockDim.x) {
-    const int ip = g.pb + lp;
+  for (int lp = lane; lp < g.npts; lp += 32) {
     double h[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) h[j] = 0.0;
-    for (int q = d.pt_ptr[ip]; q < d.pt_ptr[ip + 1]; ++q) {
-      const double* st = ws.stage + d.ptobs[q] * 9;
+    for (int q = ws.pptr[lp]; q < ws.pptr[lp + 1]; ++q) {
+      const double* st = ws.stage + ws.ptl[q] * 20;
+      const double* jp = st + 12;
+      int k = 0;
 #pragma unroll
-      for (int j = 0; j < 9; ++j) h[j] += st[j];
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b) h[k++] += jp[a] * jp[b] + jp[3 + a] * jp[3 + b];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) h[6 + a] += jp[a] * st[18] + jp[3 + a] * st[19];
     }
+    const long long ip = g.pb + lp;
 #pragma unroll
-    for (int j = 0; j < 6; ++j) d.hpp[(long long)ip * 6 + j] = h[j];
+    for (int j = 0; j < 6; ++j) d.hpp[ip * 6 + j] = h[j];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) d.gp[(long long)ip * 3 + j] = h[6 + j];
+    for (int j = 0; j < 3; ++j) d.gp[ip * 3 + j] = h[6 + j];
     gsq += h[6] * h[6] + h[7] * h[7] + h[8] * h[8];
   }
-  const double cs = block_sum(cost, red);
-  const double gs = block_sum(gsq, red);
-  if (threadIdx.x == 0) {
-    d.tile_red[t * 2] = cs;
-    d.tile_red[t * 2 + 1] = gs;
+  cost = warp_sum(cost);
+  gsq = warp_sum(gsq);
+  if (lane == 0) {
+    d.tile_red[t * 2] = cost;
+    d.tile_red[t * 2 + 1] = gsq;
   }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_jac) {
+  extern __shared__ __align__(16) char smem[];
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= d.T) return;
+  const TileGeom g = tile_geom(d, t);
+  BAE_TILE_DISPATCH(lin_tile, d, g, smem, slice, t, write_jac);
 }
 
 // Residual only (evaluate + squared_norm, problems.hpp:66, lm.hpp:81-85) at
-// the current (trial = 0) or trial (trial = 1) parameters.
-__global__ void __launch_bounds__(kTileThreads) k_cost(Dev d, int trial) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ double red[32];
-  const int t = blockIdx.x;
-  const TileGeom g = tile_geom(d, t);
-  const WsDims wd{10, 3, 0, 0};
-  const Ws ws = ws_carve(tile_base(d, g, smem), wd, g.ncam, g.npts, g.nobs);
-  const double* pose = trial ? d.pose_t : d.pose;
-  for (int idx = threadIdx.x; idx < g.ncam * 10; idx += blockDim.x) {
-    const int l = idx / 10, j = idx - l * 10;
-    const long long c = d.ent_cam[g.eb + l];
-    ws.cam[idx] = j < 7 ? pose[c * 7 + j] : d.intr[c * 3 + (j - 7)];
-  }
-  load_points(ws, 3, trial ? d.pts_t : d.pts, g.pb, g.npts);
-  __syncthreads();
+// the current parameters; writes resid when requested.
+constexpr WsDims kCostWs{10, 3, 0, 0};
+
+template <bool kShared>
+__device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t) {
+  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kCostWs, g.ncam, g.npts, g.nobs);
+  const int lane = lane_id();
+  load_point_fields<3>(ws, 3, 0, d.pts, g.pb, g.npts);
+  load_tile_index(d, g, ws);
+  __syncwarp();
+  load_cam_fields<7>(ws, g.ncam, 10, 0, d.pose, 7);
+  load_cam_fields<3>(ws, g.ncam, 10, 7, d.intr, 3);
+  __syncwarp();
   double cost = 0.0;
   int bad = INT_MAX;
-  for (int s = threadIdx.x; s < g.nobs; s += blockDim.x) {
-    const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
-    const double* cam = ws.cam + (lcpt & 0xffff) * 10;
-    const double* pt = ws.pt + (lcpt >> 16) * 3;
-    const P3 yr = quat_rotate({cam[3], cam[4], cam[5], cam[6]}, {pt[0], pt[1], pt[2]});
-    double u, w;
-    if (bal_project({yr.x + cam[0], yr.y + cam[1], yr.z + cam[2]}, cam[7], cam[8], cam[9], u, w)) {
-      const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
-      const double r0 = u + -1.0 * px.x, r1 = w + -1.0 * px.y;
-      if (d.resid && !trial) {
+  for (int s = lane; s < g.nobs; s += 32) {
+    const std::uint32_t lcpt = ws.lcpt[s];
+    const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
+    double r0, r1;
+    P3 y;
+    if (residual(ws.cam + (lcpt & 0xffff) * 10, ws.pt + (lcpt >> 16) * 3, px, r0, r1, y)) {
+      if (d.resid) {
         d.resid[g.ob + s] = r0;
         d.resid[(long long)d.N + g.ob + s] = r1;
       }
@@ -292,24 +392,27 @@ __global__ void __launch_bounds__(kTileThreads) k_cost(Dev d, int trial) {
       bad = min(bad, d.obs_orig[g.ob + s]);
     }
   }
-  if (bad != INT_MAX) {
-    if (trial)
-      atomicExch(&d.lm->trial_bad, 1);
-    else
-      atomicMin(&d.lm->err_obs, bad);
-  }
-  const double cs = block_sum(cost, red);
-  if (threadIdx.x == 0) d.tile_red[t * 2] = cs;
+  if (bad != INT_MAX) atomicMin(&d.lm->err_obs, bad);
+  cost = warp_sum(cost);
+  if (lane == 0) d.tile_red[t * 2] = cost;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_cost(Dev d, int slice) {
+  extern __shared__ __align__(16) char smem[];
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= d.T) return;
+  const TileGeom g = tile_geom(d, t);
+  BAE_TILE_DISPATCH(cost_tile, d, g, smem, slice, t);
 }
 
 // ---------------------------------------------------------------------------
-// Camera-side reduction after K1: H_cc, g_c per camera (warp per camera,
-// lane-strided over the camera's entries, fixed xor tree), then the grid
-// totals cost / ||J^T r||^2 (last block).
+// Camera-side reductions: warp per camera, lane-strided over the camera's
+// entries in entry order, fixed xor tree.
 // ---------------------------------------------------------------------------
 template <int W>
 __device__ __forceinline__ void warp_entry_sum(const Dev& d, int c, double (&acc)[W]) {
-  const int lane = threadIdx.x & 31;
+  const int lane = lane_id();
 #pragma unroll
   for (int j = 0; j < W; ++j) acc[j] = 0.0;
   for (int q = d.cam_ent_ptr[c] + lane; q < d.cam_ent_ptr[c + 1]; q += 32) {
@@ -318,15 +421,13 @@ __device__ __forceinline__ void warp_entry_sum(const Dev& d, int c, double (&acc
     for (int j = 0; j < W; ++j) acc[j] += src[j];
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-    for (int j = 0; j < W; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+  for (int j = 0; j < W; ++j) acc[j] = warp_sum(acc[j]);
 }
 
 __global__ void k_cam_linearize(Dev d) {
   __shared__ double red[32];
   const int c = blockIdx.x * kWarpsPerCamBlock + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int lane = lane_id();
   double gsq = 0.0;
   if (c < d.C) {
     double acc[27];
@@ -346,7 +447,6 @@ __global__ void k_cam_linearize(Dev d) {
   double tot[1];
   if (grid_reduce<1>(vals, d.block_red, d.tickets + 0, tot)) {
     // tile totals in tile order
-    __shared__ double tcost, tg;
     double a = 0.0, b = 0.0;
     for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) {
       a += d.tile_red[tt * 2];
@@ -356,15 +456,13 @@ __global__ void k_cam_linearize(Dev d) {
     __syncthreads();
     b = block_sum(b, red);
     if (threadIdx.x == 0) {
-      tcost = a;
-      tg = b;
-      d.lm->cost = tcost;
-      d.lm->grad_sq = tg + tot[0];
+      d.lm->cost = a;
+      d.lm->grad_sq = b + tot[0];
     }
   }
 }
 
-// Total of the per-tile costs (after k_cost), fixed order, one block.
+// Total of the per-tile costs, fixed order, one block.
 __global__ void k_sum_tiles(Dev d, int trial) {
   __shared__ double red[32];
   double a = 0.0;
@@ -372,7 +470,7 @@ __global__ void k_sum_tiles(Dev d, int trial) {
   a = block_sum(a, red);
   if (threadIdx.x == 0) {
     if (trial)
-      d.lm->new_cost = (d.lm->trial_bad || !isfinite(a)) ? INFINITY : a;
+      d.lm->new_cost = (d.lm->trial_bad || d.lm->retract_bad || !isfinite(a)) ? INFINITY : a;
     else
       d.lm->cost = a;
   }
@@ -382,19 +480,21 @@ __global__ void k_sum_tiles(Dev d, int trial) {
 // K3/K4 prep for one damping value: per point H~_pp^-1 and v = H~_pp^-1 g_p;
 // per entry the Schur right-hand side (J_c^T J_p v) and the block-Jacobi
 // blocks (W H~_pp^-1 W^T, W = J_c^T J_p) of S's diagonal.
+// cam: R9 t3 f k1 k2 (15) ; pt: p3 hinv6 v3 (12) ; stage 27
 // ---------------------------------------------------------------------------
-constexpr WsDims kPrepWs{15, 12, 0, 27};  // pt: p3 hinv6 v3
+constexpr WsDims kPrepWs{15, 12, 27, 0};
 
-__global__ void __launch_bounds__(kTileThreads) k_prep(Dev d, double lambda, double clo, double chi) {
-  extern __shared__ __align__(16) char smem[];
-  const int t = blockIdx.x;
-  const TileGeom g = tile_geom(d, t);
-  const Ws ws = ws_carve(tile_base(d, g, smem), kPrepWs, g.ncam, g.npts, g.nobs);
-  load_camrec(d, g, ws, 15, d.camrec);
-  load_points(ws, 12, d.pts, g.pb, g.npts);
-  load_entries(d, g, ws);
+template <bool kShared>
+__device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char* smem, int slice, double lambda,
+                                          double clo, double chi) {
+  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kPrepWs, g.ncam, g.npts, g.nobs);
+  const int lane = lane_id();
+  load_point_fields<3>(ws, 12, 0, d.pts, g.pb, g.npts);
+  load_tile_index(d, g, ws);
+  __syncwarp();
+  load_cam_fields<15>(ws, g.ncam, 15, 0, d.camrec, kCamRec);
   int fail = 0;
-  for (int lp = threadIdx.x; lp < g.npts; lp += blockDim.x) {
+  for (int lp = lane; lp < g.npts; lp += 32) {
     const long long ip = g.pb + lp;
     double h[6], inv[9];
 #pragma unroll
@@ -420,61 +520,60 @@ __global__ void __launch_bounds__(kTileThreads) k_prep(Dev d, double lambda, dou
     sp[11] = inv[6] * g0 + inv[7] * g1 + inv[8] * g2;
   }
   if (fail) atomicExch(&d.pcg->not_spd, 1);
-  __syncthreads();
-  const int nchunk = (g.nobs + 31) / 32;
-  for (int base = 0; base < g.nobs; base += blockDim.x) {
-    const int s = base + threadIdx.x;
-    double v27[27];
+  __syncwarp();
+  for (int s = lane; s < g.nobs; s += 32) {
+    const std::uint32_t lcpt = ws.lcpt[s];
+    const double* cam = ws.cam + (lcpt & 0xffff) * 15;
+    const double* sp = ws.pt + (lcpt >> 16) * 12;
+    P3 y;
+    double D[6], Jc[12], Jp[6];
+    obs_geometry(cam, sp, y, D);
+    jac_cam(D, y, Jc);
+    jac_pt(D, cam, Jp);
+    double W[18];  // 6x3
 #pragma unroll
-    for (int j = 0; j < 27; ++j) v27[j] = 0.0;
-    int seg = -1;
-    if (s < g.nobs) {
-      const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
-      const int lc = lcpt & 0xffff, lp = lcpt >> 16;
-      seg = lc;
-      const double* cam = ws.cam + lc * 15;
-      const double* sp = ws.pt + lp * 12;
-      P3 y;
-      double D[6], Jc[12], Jp[6];
-      obs_geometry(cam, sp, y, D);
-      jac_cam(D, y, Jc);
-      jac_pt(D, cam, Jp);
-      double W[18];  // 6x3
+    for (int a = 0; a < 6; ++a)
 #pragma unroll
-      for (int a = 0; a < 6; ++a)
+      for (int j = 0; j < 3; ++j) W[a * 3 + j] = Jc[a] * Jp[j] + Jc[6 + a] * Jp[3 + j];
+    const double* hi = sp + 3;  // packed xx xy xz yy yz zz
+    const double H[9] = {hi[0], hi[1], hi[2], hi[1], hi[3], hi[4], hi[2], hi[4], hi[5]};
+    double WH[18];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) W[a * 3 + j] = Jc[a] * Jp[j] + Jc[6 + a] * Jp[3 + j];
-      const double* hi = sp + 3;  // packed xx xy xz yy yz zz
-      const double H[9] = {hi[0], hi[1], hi[2], hi[1], hi[3], hi[4], hi[2], hi[4], hi[5]};
-      double WH[18];
+    for (int a = 0; a < 6; ++a)
 #pragma unroll
-      for (int a = 0; a < 6; ++a)
+      for (int j = 0; j < 3; ++j)
+        WH[a * 3 + j] = W[a * 3] * H[j] + W[a * 3 + 1] * H[3 + j] + W[a * 3 + 2] * H[6 + j];
+    double* st = ws.stage + s * 27;
+    int q = 0;
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
-          WH[a * 3 + j] = W[a * 3] * H[j] + W[a * 3 + 1] * H[3 + j] + W[a * 3 + 2] * H[6 + j];
-      int q = 0;
+    for (int a = 0; a < 6; ++a)
 #pragma unroll
-      for (int a = 0; a < 6; ++a)
+      for (int b = a; b < 6; ++b)
+        st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
+    const double* vp = sp + 9;
 #pragma unroll
-        for (int b = a; b < 6; ++b)
-          v27[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
-      const double* vp = sp + 9;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) v27[21 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
-    }
-    seg_reduce_pieces<27>(v27, seg, s, nchunk, ws.piece);
+    for (int a = 0; a < 6; ++a) st[21 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
   }
-  __syncthreads();
-  entries_from_pieces<27>(ws, g.ncam, g.nobs, g.eb, d.partial);
+  __syncwarp();
+  entries_from_stage<27, 27>(ws, g.ncam, g.eb, d.partial);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, double clo, double chi) {
+  extern __shared__ __align__(16) char smem[];
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= d.T) return;
+  const TileGeom g = tile_geom(d, t);
+  BAE_TILE_DISPATCH(prep_tile, d, g, smem, slice, lambda, clo, chi);
 }
 
 // Camera side of the prep: damped H~_cc, block-Jacobi inverse of S_cc
 // (falls back to H~_cc^-1 when the 6x6 Schur block is not numerically SPD),
-// Schur RHS, and PCG initialisation x = 0, r = b, z = M^-1 r, p = z.
+// Schur RHS, and PCG initialisation x = 0, r = b, z = M^-1 r.
 __global__ void k_cam_prep(Dev d, double lambda, double clo, double chi, double tol, long long budget) {
   __shared__ double red[32];
   const int c = blockIdx.x * kWarpsPerCamBlock + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int lane = lane_id();
   double rr = 0.0, rz = 0.0;
   int fail = 0;
   if (c < d.C) {
@@ -551,15 +650,19 @@ __global__ void k_cam_prep(Dev d, double lambda, double clo, double chi, double 
 // (z, z + beta p, or x when verifying the true residual):
 //   s_k = J_p^T J_c v_c(k);  w_p = sum_k s_k;  t_p = H~_pp^-1 w_p;
 //   partial[e] = sum_{k in e} J_c^T J_p t_p(k)
-// The camera kernel then forms y = H~_cc v - sum partial.
-// D and y of the first kCacheRounds rounds stay in registers between the two
-// observation phases; longer tiles recompute them.
+// The camera part then forms y = H~_cc v - sum partial.
+// Only data shared across lanes goes through shared memory: the tile's
+// camera records + direction (cam, 24 per camera), the per-observation
+// exchange vectors (stage, SoA [6][nobs]) and t_p (pt, 3 per point).
+// Observation and point data are read straight from global memory by the
+// lane that owns them. D and y of a lane's first kCacheRounds observations
+// stay in registers between the two observation phases.
 // ---------------------------------------------------------------------------
-constexpr WsDims kSxWs{21, 6, 3, 6};  // cam: R9 t3 f k1 k2 v6 ; pt: p3 t3
+constexpr WsDims kSxWs{24, 3, 6, 0};
 constexpr int kCacheRounds = 2;
 
 // The PCG direction is formed lazily (p = z + beta p) by both the tile and
-// the camera kernel with the same fused expression, so both see identical bits.
+// the camera part with the same fused expression, so both see identical bits.
 __device__ __forceinline__ double dir_component(const PcgDev& s, const Dev& d, long long o) {
   return s.dir == kDirX ? d.x[o] : (s.dir == kDirZ ? d.z[o] : fma(s.beta, d.p[o], d.z[o]));
 }
@@ -568,224 +671,611 @@ __device__ __forceinline__ void dir_vector(const PcgDev& s, const Dev& d, long l
   for (int j = 0; j < 6; ++j) v[j] = dir_component(s, d, c * 6 + j);
 }
 
-template <bool kVecIsDelta>
-__device__ __forceinline__ void sx_tile_body(const Dev& d, const TileGeom& g, const Ws& ws) {
-  const int nchunk = (g.nobs + 31) / 32;
-  const int nrounds = (g.nobs + blockDim.x - 1) / blockDim.x;
-  double cD[kCacheRounds][6];
-  P3 cy[kCacheRounds];
-  // phase 1
+// Copy the 16-double records (and optionally a 6-vector per camera from
+// `vec6`) of the tile's cameras into ws.cam[l * ld + ...]; two cameras per
+// pass (lane -> camera l0 + lane/16, field lane%16). Small tiles resolve the
+// camera id by shuffling it from the lane that loaded it.
+template <bool kSmall, class Vec6>
+__device__ __forceinline__ void copy_tile_cams(const Dev& d, const TileGeom& g, const Ws& ws, int ld,
+                                               const double* rec, int mycam, Vec6 vec6) {
+  const int lane = lane_id(), sub = lane >> 4, j = lane & 15;
+#pragma unroll 4
+  for (int l0 = 0; l0 < g.ncam; l0 += 2) {
+    const int l = min(l0 + sub, g.ncam - 1);
+    const int c = kSmall ? __shfl_sync(0xffffffffu, mycam, l & 31) : d.ent_cam[g.eb + l];
+    const double r = rec[(long long)c * kCamRec + j];
+    const double v = j < 6 ? vec6(c, j) : 0.0;
+    if (l0 + sub < g.ncam) {
+      ws.cam[l * ld + j] = r;
+      if (j < 6) ws.cam[l * ld + 16 + j] = v;
+    }
+  }
+}
+
+// Camera records (16 doubles) + the PCG direction (6) of the tile's cameras
+// into ws.cam[l * 24]; 16 lanes per camera, two cameras per pass. The
+// direction kind is warp-uniform and hoisted out of the loop.
+template <bool kSmall>
+__device__ __forceinline__ void sx_copy_cams(const Dev& d, const PcgDev& st, const TileGeom& g, const Ws& ws,
+                                             int mycam) {
+  const int lane = lane_id(), sub = lane >> 4, j = lane & 15;
+  const int dir = st.dir;
+  const double beta = st.beta;
+  const double* va = dir == kDirX ? d.x : d.z;  // first term
+#pragma unroll 4
+  for (int l0 = 0; l0 < g.ncam; l0 += 2) {
+    const int l = min(l0 + sub, g.ncam - 1);
+    const int c = kSmall ? __shfl_sync(0xffffffffu, mycam, l & 31) : d.ent_cam[g.eb + l];
+    const long long o = (long long)c * 6 + min(j, 5);
+    const double r = d.camrec[(long long)c * kCamRec + j];
+    double v = va[o];
+    if (dir == kDirZBetaP) v = fma(beta, d.p[o], v);  // same fused expression as dir_component
+    if (l0 + sub < g.ncam) {
+      ws.cam[l * 24 + j] = r;
+      if (j < 6) ws.cam[l * 24 + 16 + j] = v;
+    }
+  }
+}
+
+template <bool kSmall>
+__device__ __forceinline__ void sx_tile_impl(const Dev& d, const PcgDev& st, const TileGeom& g, char* smem,
+                                             int slice) {
+  const Ws ws = ws_carve(ws_base<kSmall>(d, g, smem, slice), kSxWs, g.ncam, g.npts, g.nobs);
+  const int lane = lane_id();
+  const int nobs = g.nobs;
+  if (d.trace && lane == 0) d.trace[(long long)g.trace_id * 8 + 0] = global_ns();
+  // ---- level-2 loads (depend only on the tile geometry), all in flight together
+  std::uint32_t lc[kCacheRounds];
+  std::uint16_t pl[kCacheRounds];
 #pragma unroll
   for (int r = 0; r < kCacheRounds; ++r) {
-    const int s = r * blockDim.x + threadIdx.x;
-    if (r < nrounds && s < g.nobs) {
-      const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
-      const double* cam = ws.cam + (lcpt & 0xffff) * 21;
-      obs_geometry(cam, ws.pt + (lcpt >> 16) * 6, cy[r], cD[r]);
-      jpt_jc_v(cD[r], cy[r], cam, cam + 15, ws.stage + s * 3);
+    const int s = min(r * 32 + lane, nobs - 1);
+    lc[r] = d.obs_lcpt[g.ob + s];
+    pl[r] = d.ptobs[g.ob + s];
+  }
+  const int pp0 = d.pt_ptr[g.pb + min(lane, g.npts)];
+  const int pp1 = d.pt_ptr[g.pb + min(lane + 32, g.npts)];
+  const int eo0 = d.ent_obs_begin[g.eb + min(lane, g.ncam)];
+  const int eo1 = d.ent_obs_begin[g.eb + min(lane + 32, g.ncam)];
+  const int mycam = kSmall ? d.ent_cam[g.eb + min(lane, g.ncam - 1)] : 0;
+  // ---- level-3 loads: point coordinates of the lane's observations
+  double px[kCacheRounds][3];
+#pragma unroll
+  for (int r = 0; r < kCacheRounds; ++r) {
+    const double* p = d.pts + (long long)(g.pb + (lc[r] >> 16)) * 3;
+    px[r][0] = p[0];
+    px[r][1] = p[1];
+    px[r][2] = p[2];
+  }
+  // index data into the workspace
+#pragma unroll
+  for (int r = 0; r < kCacheRounds; ++r)
+    if (r * 32 + lane < nobs) ws.ptl[r * 32 + lane] = pl[r];
+  for (int s = kCacheRounds * 32 + lane; s < nobs; s += 32) ws.ptl[s] = d.ptobs[g.ob + s];
+  if (lane <= g.npts) ws.pptr[lane] = pp0 - g.ob;
+  if (lane + 32 <= g.npts) ws.pptr[lane + 32] = pp1 - g.ob;
+  for (int i = lane + 64; i <= g.npts; i += 32) ws.pptr[i] = d.pt_ptr[g.pb + i] - g.ob;
+  if (lane <= g.ncam) ws.ent[lane] = eo0 - g.ob;
+  if (lane + 32 <= g.ncam) ws.ent[lane + 32] = eo1 - g.ob;
+  for (int i = lane + 64; i <= g.ncam; i += 32) ws.ent[i] = d.ent_obs_begin[g.eb + i] - g.ob;
+  sx_copy_cams<kSmall>(d, st, g, ws, mycam);
+  __syncwarp();
+  if (d.trace && lane == 0) d.trace[(long long)g.trace_id * 8 + 1] = global_ns();
+  // phase 1: s_k = J_p^T J_c v
+  double cD[kCacheRounds][6];
+  P3 cy[kCacheRounds];
+#pragma unroll
+  for (int r = 0; r < kCacheRounds; ++r) {
+    const int s = r * 32 + lane;
+    if (s < nobs) {
+      const double* cam = ws.cam + (lc[r] & 0xffff) * 24;
+      obs_geometry(cam, px[r], cy[r], cD[r]);
+      double sv[3];
+      jpt_jc_v(cD[r], cy[r], cam, cam + 16, sv);
+      ws.stage[s] = sv[0];
+      ws.stage[nobs + s] = sv[1];
+      ws.stage[2 * nobs + s] = sv[2];
     }
   }
-  for (int r = kCacheRounds; r < nrounds; ++r) {
-    const int s = r * blockDim.x + threadIdx.x;
-    if (s < g.nobs) {
-      const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
-      const double* cam = ws.cam + (lcpt & 0xffff) * 21;
-      P3 y;
-      double D[6];
-      obs_geometry(cam, ws.pt + (lcpt >> 16) * 6, y, D);
-      jpt_jc_v(D, y, cam, cam + 15, ws.stage + s * 3);
-    }
+  for (int s = kCacheRounds * 32 + lane; s < nobs; s += 32) {  // long tiles
+    const std::uint32_t l = d.obs_lcpt[g.ob + s];
+    const double* cam = ws.cam + (l & 0xffff) * 24;
+    const double* p = d.pts + (long long)(g.pb + (l >> 16)) * 3;
+    const double pp[3] = {p[0], p[1], p[2]};
+    P3 y;
+    double D[6], sv[3];
+    obs_geometry(cam, pp, y, D);
+    jpt_jc_v(D, y, cam, cam + 16, sv);
+    ws.stage[s] = sv[0];
+    ws.stage[nobs + s] = sv[1];
+    ws.stage[2 * nobs + s] = sv[2];
   }
-  __syncthreads();
-  // point phase
-  for (int lp = threadIdx.x; lp < g.npts; lp += blockDim.x) {
-    const int ip = g.pb + lp;
+  __syncwarp();
+  if (d.trace && lane == 0) d.trace[(long long)g.trace_id * 8 + 2] = global_ns();
+  // point phase: t_p = H~_pp^-1 sum_k s_k (observations in id order)
+  for (int lp = lane; lp < g.npts; lp += 32) {
+    const long long ip = g.pb + lp;
+    const double* hi = d.hinv + ip * 6;
+    const double h0 = hi[0], h1 = hi[1], h2 = hi[2], h3 = hi[3], h4 = hi[4], h5 = hi[5];
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-    for (int q = d.pt_ptr[ip]; q < d.pt_ptr[ip + 1]; ++q) {
-      const double* st = ws.stage + d.ptobs[q] * 3;
-      w0 += st[0];
-      w1 += st[1];
-      w2 += st[2];
+    const int q1 = ws.pptr[lp + 1];
+    for (int q = ws.pptr[lp]; q < q1; ++q) {
+      const int s = ws.ptl[q];
+      w0 += ws.stage[s];
+      w1 += ws.stage[nobs + s];
+      w2 += ws.stage[2 * nobs + s];
     }
-    const double* hi = d.hinv + (long long)ip * 6;
-    double* tp = ws.pt + lp * 6 + 3;
-    tp[0] = hi[0] * w0 + hi[1] * w1 + hi[2] * w2;
-    tp[1] = hi[1] * w0 + hi[3] * w1 + hi[4] * w2;
-    tp[2] = hi[2] * w0 + hi[4] * w1 + hi[5] * w2;
+    ws.pt[lp * 3] = h0 * w0 + h1 * w1 + h2 * w2;
+    ws.pt[lp * 3 + 1] = h1 * w0 + h3 * w1 + h4 * w2;
+    ws.pt[lp * 3 + 2] = h2 * w0 + h4 * w1 + h5 * w2;
   }
-  __syncthreads();
-  // phase 3
-  for (int r = 0; r < nrounds; ++r) {
-    const int s = r * blockDim.x + threadIdx.x;
-    double z6[6] = {0, 0, 0, 0, 0, 0};
-    int seg = -1;
-    if (s < g.nobs) {
-      const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
-      const int lc = lcpt & 0xffff, lp = lcpt >> 16;
-      seg = lc;
-      const double* cam = ws.cam + lc * 21;
-      const double* tp = ws.pt + lp * 6 + 3;
-      if (r < kCacheRounds) {
-        // select the cached round without dynamic register indexing
-        double D[6];
-        P3 y;
+  __syncwarp();
+  if (d.trace && lane == 0) d.trace[(long long)g.trace_id * 8 + 3] = global_ns();
+  // phase 3: z_k = J_c^T J_p t_p -> stage rows 0..5 (overwrites s_k)
 #pragma unroll
-        for (int rr = 0; rr < kCacheRounds; ++rr)
-          if (rr == r) {
+  for (int r = 0; r < kCacheRounds; ++r) {
+    const int s = r * 32 + lane;
+    if (s < nobs) {
+      const double* cam = ws.cam + (lc[r] & 0xffff) * 24;
+      double z[6];
+      jct_jp_t(cD[r], cy[r], cam, ws.pt + (lc[r] >> 16) * 3, z);
 #pragma unroll
-            for (int j = 0; j < 6; ++j) D[j] = cD[rr][j];
-            y = cy[rr];
-          }
-        jct_jp_t(D, y, cam, tp, z6);
+      for (int j = 0; j < 6; ++j) ws.stage[j * nobs + s] = z[j];
+    }
+  }
+  for (int s = kCacheRounds * 32 + lane; s < nobs; s += 32) {
+    const std::uint32_t l = d.obs_lcpt[g.ob + s];
+    const double* cam = ws.cam + (l & 0xffff) * 24;
+    const double* p = d.pts + (long long)(g.pb + (l >> 16)) * 3;
+    const double pp[3] = {p[0], p[1], p[2]};
+    P3 y;
+    double D[6], z[6];
+    obs_geometry(cam, pp, y, D);
+    jct_jp_t(D, y, cam, ws.pt + (l >> 16) * 3, z);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) ws.stage[j * nobs + s] = z[j];
+  }
+  __syncwarp();
+  if (d.trace && lane == 0) d.trace[(long long)g.trace_id * 8 + 4] = global_ns();
+  // one lane per tile camera: its 6-vector summed over its slot range, slot order
+  for (int e = lane; e < g.ncam; e += 32) {
+    const int b = ws.ent[e], en = ws.ent[e + 1];
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    for (int q = b; q < en; ++q)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) a[j] += ws.stage[j * nobs + q];
+    double* out = d.partial + (long long)(g.eb + e) * 6;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) out[j] = a[j];
+  }
+  __syncwarp();  // the slice is reused by this warp's next tile
+}
+
+__device__ __forceinline__ void sx_tile(const Dev& d, const PcgDev& st, int t, char* smem, int slice) {
+  const TileGeom g = tile_geom(d, t);
+  if (g.nobs == 0) return;
+  if (g.big >= 0)
+    sx_tile_impl<false>(d, st, g, smem, slice);
+  else
+    sx_tile_impl<true>(d, st, g, smem, slice);
+}
+
+// ---------------------------------------------------------------------------
+// K5 pipelined: the same implicit Schur product for small tiles, with every
+// tile input brought in by TMA bulk copies (cp.async.bulk + mbarrier) into a
+// per-warp double buffer. While a warp computes tile i, the index blob, point
+// window and H~_pp^-1 of its next tile are in flight (level A); the next
+// tile's camera records and direction vectors (level C, addressed by the
+// blob's camera ids) are issued right after phase 1. A tile's memory latency
+// is thus overlapped with the previous tile's arithmetic.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pipe_issue_a(const Dev& d, int t, char* buf, unsigned long long* bar) {
+  fence_proxy_async();
+  __syncwarp();
+  if (lane_id() == 0) {
+    const int4 ds = d.tile_desc[t];  // blob/16, blob bytes, first point, points
+    const long long pb = ds.z;
+    const int npts = ds.w;
+    const char* ps = reinterpret_cast<const char*>(d.pts + pb * 3);
+    const unsigned long long a0 = reinterpret_cast<unsigned long long>(ps) & ~15ull;
+    const unsigned long long a1 = (reinterpret_cast<unsigned long long>(ps + npts * 24) + 15) & ~15ull;
+    const unsigned pbytes = static_cast<unsigned>(a1 - a0);
+    const unsigned hbytes = static_cast<unsigned>(npts) * 48u;
+    mbar_expect_tx(bar, static_cast<unsigned>(ds.y) + pbytes + hbytes);
+    bulk_g2s(buf + kBufBlob, d.tile_blob + static_cast<long long>(ds.x) * 16, static_cast<unsigned>(ds.y), bar);
+    bulk_g2s(buf + kBufPts, reinterpret_cast<const void*>(a0), pbytes, bar);
+    bulk_g2s(buf + kBufHinv, d.hinv + pb * 6, hbytes, bar);
+  }
+}
+
+__device__ __forceinline__ void pipe_issue_c(const Dev& d, const PcgDev& st, char* buf, unsigned long long* bar) {
+  const int* hdr = reinterpret_cast<const int*>(buf + kBufBlob);
+  const int ncam = hdr[5];
+  const bool two = st.dir == kDirZBetaP;
+  const double* va = st.dir == kDirX ? d.x : d.z;
+  fence_proxy_async();
+  __syncwarp();
+  const int lane = lane_id();
+  if (lane == 0) mbar_expect_tx(bar, static_cast<unsigned>(ncam) * (two ? 224u : 176u));
+  __syncwarp();
+  if (lane < ncam) {
+    const long long c = hdr[8 + lane];
+    bulk_g2s(buf + kBufCam + lane * 128, d.camrec + c * kCamRec, 128u, bar);
+    bulk_g2s(buf + kBufVz + lane * 48, va + c * 6, 48u, bar);
+    if (two) bulk_g2s(buf + kBufVp + lane * 48, d.p + c * 6, 48u, bar);
+  }
+}
+
+// Computes one small tile whose level-A and level-C data have landed in
+// `buf`; `next` (optional) issues the next tile's level C after phase 1.
+template <class Next>
+__device__ __forceinline__ void sx_pipe_tile(const Dev& d, const PcgDev& st, char* buf, char* wsm, Next next) {
+  const int lane = lane_id();
+  const int* hdr = reinterpret_cast<const int*>(buf + kBufBlob);
+  const int nobs = hdr[1], pb = hdr[2], npts = hdr[3], eb = hdr[4], ncam = hdr[5];
+  const int* ent = hdr + 8 + ncam;
+  const int* pptr = ent + ncam + 1;
+  const std::uint32_t* lcpt = reinterpret_cast<const std::uint32_t*>(pptr + npts + 1);
+  const std::uint16_t* ptl = reinterpret_cast<const std::uint16_t*>(lcpt + nobs);
+  const double* pts = reinterpret_cast<const double*>(buf + kBufPts + ((pb * 24) & 15));
+  const double* hinv = reinterpret_cast<const double*>(buf + kBufHinv);
+  const double* cams = reinterpret_cast<const double*>(buf + kBufCam);
+  double* vz = reinterpret_cast<double*>(buf + kBufVz);
+  double* stage = reinterpret_cast<double*>(wsm + kScrStage);
+  double* tp = reinterpret_cast<double*>(wsm + kScrTp);
+  if (st.dir == kDirZBetaP) {  // v = z + beta p, the same fused expression as the camera part
+    const double* vp = reinterpret_cast<const double*>(buf + kBufVp);
+    for (int i = lane; i < ncam * 6; i += 32) vz[i] = fma(st.beta, vp[i], vz[i]);
+    __syncwarp();
+  }
+  // phase 1: s_k = J_p^T J_c v
+  double cD[2][6];
+  P3 cy[2];
+  std::uint32_t lc[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int s = r * 32 + lane;
+    lc[r] = lcpt[min(s, nobs - 1)];
+    if (s < nobs) {
+      const int l = lc[r] & 0xffff;
+      const double* cam = cams + l * 16;
+      obs_geometry(cam, pts + (lc[r] >> 16) * 3, cy[r], cD[r]);
+      double sv[3];
+      jpt_jc_v(cD[r], cy[r], cam, vz + l * 6, sv);
+      stage[s] = sv[0];
+      stage[kPipeObs + s] = sv[1];
+      stage[2 * kPipeObs + s] = sv[2];
+    }
+  }
+  __syncwarp();
+  next();  // the next tile's camera gathers fly during the rest of this tile
+  // point phase: t_p = H~_pp^-1 sum_k s_k (observations in id order)
+  if (lane < npts) {
+    const double* hi = hinv + lane * 6;
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    for (int q = pptr[lane]; q < pptr[lane + 1]; ++q) {
+      const int s = ptl[q];
+      w0 += stage[s];
+      w1 += stage[kPipeObs + s];
+      w2 += stage[2 * kPipeObs + s];
+    }
+    tp[lane * 3] = hi[0] * w0 + hi[1] * w1 + hi[2] * w2;
+    tp[lane * 3 + 1] = hi[1] * w0 + hi[3] * w1 + hi[4] * w2;
+    tp[lane * 3 + 2] = hi[2] * w0 + hi[4] * w1 + hi[5] * w2;
+  }
+  __syncwarp();
+  // phase 3: z_k = J_c^T J_p t_p -> stage rows 0..5
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int s = r * 32 + lane;
+    if (s < nobs) {
+      double z[6];
+      jct_jp_t(cD[r], cy[r], cams + (lc[r] & 0xffff) * 16, tp + (lc[r] >> 16) * 3, z);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) stage[j * kPipeObs + s] = z[j];
+    }
+  }
+  __syncwarp();
+  // one lane per tile camera: its 6-vector over its slot range, slot order
+  if (lane < ncam) {
+    double a[6] = {0, 0, 0, 0, 0, 0};
+    for (int q = ent[lane]; q < ent[lane + 1]; ++q)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) a[j] += stage[j * kPipeObs + q];
+    double* out = d.partial + static_cast<long long>(eb + lane) * 6;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) out[j] = a[j];
+  }
+  __syncwarp();
+}
+
+// Per-warp pipeline state: mbarriers A0 A1 C0 C1 live at wsm + kScrBar and
+// are initialised once per kernel; their phase parities persist across calls.
+struct PipeState {
+  unsigned pa0 = 0, pa1 = 0, pc0 = 0, pc1 = 0;
+};
+__device__ __forceinline__ void pipe_init(char* wsm) {
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + kScrBar);
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mbar_init(bar + k, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+}
+
+// All small tiles of this warp (gwarp, gwarp + nwarps, ...), software
+// pipelined through the two buffers of the warp's shared-memory slice.
+__device__ __forceinline__ void sx_pipelined(const Dev& d, const PcgDev& st, char* wsm, int gwarp, int nwarps,
+                                             PipeState& ps) {
+  char* buf[2] = {wsm, wsm + kBufBytes};
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + kScrBar);  // A0 A1 C0 C1
+  unsigned& pa0 = ps.pa0;
+  unsigned& pa1 = ps.pa1;
+  unsigned& pc0 = ps.pc0;
+  unsigned& pc1 = ps.pc1;
+  int i = gwarp;
+  if (i >= d.n_small) return;
+  pipe_issue_a(d, d.small_tiles[i], buf[0], bar + 0);
+  mbar_wait(bar + 0, pa0);
+  pa0 ^= 1;
+  pipe_issue_c(d, st, buf[0], bar + 2);
+  int b = 0;
+  for (; i < d.n_small; i += nwarps) {
+    const int in = i + nwarps;
+    const bool more = in < d.n_small;
+    if (more) pipe_issue_a(d, d.small_tiles[in], buf[b ^ 1], bar + (b ^ 1));
+    if (b == 0) {
+      mbar_wait(bar + 2, pc0);
+      pc0 ^= 1;
+    } else {
+      mbar_wait(bar + 3, pc1);
+      pc1 ^= 1;
+    }
+    sx_pipe_tile(d, st, buf[b], wsm, [&] {
+      if (!more) return;
+      if (b == 0) {
+        mbar_wait(bar + 1, pa1);
+        pa1 ^= 1;
       } else {
-        P3 y;
-        double D[6];
-        obs_geometry(cam, ws.pt + lp * 6, y, D);
-        jct_jp_t(D, y, cam, tp, z6);
+        mbar_wait(bar + 0, pa0);
+        pa0 ^= 1;
+      }
+      pipe_issue_c(d, st, buf[b ^ 1], bar + 2 + (b ^ 1));
+    });
+    b ^= 1;
+  }
+}
+
+// K5 camera part for one camera (warp): y_c = H~_cc v_c - sum partial,
+// p <- v. Returns v.y (lane 0).
+__device__ __forceinline__ double sx_camera(const Dev& d, const PcgDev& st, int c) {
+  double acc[6];
+  warp_entry_sum<6>(d, c, acc);
+  double pap = 0.0;
+  if (lane_id() == 0) {
+    double v[6];
+    dir_vector(st, d, c, v);
+    const double* h = d.hccd + (long long)c * 21;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      double hv = 0.0;
+#pragma unroll
+      for (int b = 0; b < 6; ++b) hv += h[sym6(a, b)] * v[b];
+      const double yy = hv - acc[a];
+      d.y[(long long)c * 6 + a] = yy;
+      if (st.dir != kDirX) d.p[(long long)c * 6 + a] = v[a];
+      pap += v[a] * yy;
+    }
+  }
+  return pap;
+}
+
+// PCG vector update for one camera (pcg.hpp:78-117): accumulates r.r, r.z.
+__device__ __forceinline__ void pcg_camera_update(const Dev& d, const PcgDev& st, double alpha, int c, double& rr,
+                                                  double& rz) {
+  double rv[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    const long long o = (long long)c * 6 + a;
+    if (st.state == kPcgIter) {
+      d.x[o] += alpha * d.p[o];
+      rv[a] = d.r[o] - alpha * d.y[o];
+    } else {  // verify: true residual b - S x
+      rv[a] = d.rhs[o] - d.y[o];
+    }
+    d.r[o] = rv[a];
+    rr += rv[a] * rv[a];
+  }
+  const double* m = d.minv + (long long)c * 36;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    double zz = 0.0;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) zz += m[a * 6 + b] * rv[b];
+    d.z[(long long)c * 6 + a] = zz;
+    rz += rv[a] * zz;
+  }
+}
+
+// Recurrence / true-residual state machine (pcg.hpp:68-129) on the grid
+// totals r.r and r.z; identical in every block that evaluates it.
+__host__ __device__ __forceinline__ void pcg_decide(PcgDev& o, double rr, double rz_new) {
+  const double rnorm = sqrt(rr);
+  o.rnorm = rnorm;
+  if (o.state == kPcgIter) {
+    o.iters += 1;
+    if (!isfinite(rnorm)) {
+      o.state = kPcgBreakdown;
+    } else if (rnorm <= o.tol * o.bnorm) {
+      o.state = kPcgVerify;  // confirm with the true residual (pcg.hpp:86-109)
+      o.dir = kDirX;
+    } else {
+      const double beta = rz_new / o.rz;
+      if (!isfinite(beta)) {
+        o.state = kPcgBreakdown;
+      } else {
+        o.beta = beta;
+        o.rz = rz_new;
+        o.dir = kDirZBetaP;
+        if (o.iters >= o.budget) o.state = kPcgDone;
       }
     }
-    seg_reduce_pieces<6>(z6, seg, s, nchunk, ws.piece);
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kTileThreads) k_schur_tiles(Dev d) {
-  extern __shared__ __align__(16) char smem[];
-  const PcgDev s = *d.pcg;
-  if (s.state >= kPcgDone) return;
-  const TileGeom g = tile_geom(d, blockIdx.x);
-  const Ws ws = ws_carve(tile_base(d, g, smem), kSxWs, g.ncam, g.npts, g.nobs);
-  for (int idx = threadIdx.x; idx < g.ncam * 21; idx += blockDim.x) {
-    const int l = idx / 21, j = idx - l * 21;
-    const long long c = d.ent_cam[g.eb + l];
-    double v;
-    if (j < 15) {
-      v = d.camrec[c * kCamRec + j];
-    } else {
-      const long long o = c * 6 + (j - 15);
-      v = dir_component(s, d, o);
+  } else {
+    o.true_norm = rnorm;
+    if (rnorm <= o.tol * o.bnorm) {
+      o.state = kPcgDone;
+      o.converged = 1;
+    } else {  // restart from the true residual
+      o.rz = rz_new;
+      o.beta = 0.0;
+      o.dir = kDirZ;
+      o.state = (o.iters >= o.budget) ? kPcgDone : kPcgIter;
     }
-    ws.cam[idx] = v;
   }
-  load_points(ws, 6, d.pts, g.pb, g.npts);
-  load_entries(d, g, ws);
-  __syncthreads();
-  sx_tile_body<false>(d, g, ws);
-  entries_from_pieces<6>(ws, g.ncam, g.nobs, g.eb, d.partial);
 }
 
-// K5 camera part: y_c = H~_cc v_c - sum partial; p <- v (direction update);
-// dot(v, y) -> alpha = rz / pAp in the last block.
+// Standalone S*v tile pass (graph-mode PCG and kernel timing): persistent
+// grid, pipelined small tiles, then the rare big tiles from global scratch.
+__device__ __forceinline__ void sx_all_tiles(const Dev& d, const PcgDev& st, char* smem, int gwarp, int nwarps,
+                                             PipeState& ps) {
+  sx_pipelined(d, st, smem + (threadIdx.x >> 5) * kPipeWarpBytes, gwarp, nwarps, ps);
+  for (int i = gwarp; i < d.n_big_tiles; i += nwarps) sx_tile(d, st, d.big_tiles[i], smem, 0);
+}
+
+__global__ void __launch_bounds__(256, 2) k_schur_tiles(Dev d, int slice) {
+  extern __shared__ __align__(128) char smem[];
+  const PcgDev st = *d.pcg;
+  if (st.state >= kPcgDone) return;
+  const int wpb = blockDim.x >> 5;
+  pipe_init(smem + (threadIdx.x >> 5) * kPipeWarpBytes);
+  PipeState ps;
+  sx_all_tiles(d, st, smem, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, ps);
+}
+
 __global__ void k_schur_cams(Dev d) {
   __shared__ double red[32];
-  const PcgDev s = *d.pcg;
-  if (s.state >= kPcgDone) return;
+  const PcgDev st = *d.pcg;
+  if (st.state >= kPcgDone) return;
   const int c = blockIdx.x * kWarpsPerCamBlock + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  double pap = 0.0;
-  if (c < d.C) {
-    double acc[6];
-    warp_entry_sum<6>(d, c, acc);
-    if (lane == 0) {
-      double v[6];
-      dir_vector(s, d, c, v);
-      const double* h = d.hccd + (long long)c * 21;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        double hv = 0.0;
-#pragma unroll
-        for (int b = 0; b < 6; ++b) hv += h[sym6(a, b)] * v[b];
-        const double yy = hv - acc[a];
-        d.y[(long long)c * 6 + a] = yy;
-        if (s.dir != kDirX) d.p[(long long)c * 6 + a] = v[a];
-        pap += v[a] * yy;
-      }
-    }
-  }
+  const double pap = c < d.C ? sx_camera(d, st, c) : 0.0;
   const double bs = block_sum(pap, red);
   const double vals[1] = {bs};
   double tot[1];
   if (grid_reduce<1>(vals, d.block_red, d.tickets + 2, tot) && threadIdx.x == 0) {
-    if (s.dir != kDirX) {
-      const double alpha = s.rz / tot[0];
+    if (st.dir != kDirX) {
+      const double alpha = st.rz / tot[0];
       d.pcg->alpha = alpha;
       if (!isfinite(alpha)) d.pcg->state = kPcgBreakdown;  // pcg.hpp:77
     }
   }
 }
 
-// PCG vector update (pcg.hpp:78-117) on the camera vectors, with the
-// recurrence / true-residual state machine in the last block.
 __global__ void k_pcg_update(Dev d) {
   __shared__ double red[32];
-  const PcgDev s = *d.pcg;
-  if (s.state >= kPcgDone) return;
+  const PcgDev st = *d.pcg;
+  if (st.state >= kPcgDone) return;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double rr = 0.0, rz = 0.0;
-  if (c < d.C) {
-    double rv[6];
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      const long long o = (long long)c * 6 + a;
-      if (s.state == kPcgIter) {
-        d.x[o] += s.alpha * d.p[o];
-        rv[a] = d.r[o] - s.alpha * d.y[o];
-      } else {  // verify: true residual b - S x
-        rv[a] = d.rhs[o] - d.y[o];
-      }
-      d.r[o] = rv[a];
-      rr += rv[a] * rv[a];
-    }
-    const double* m = d.minv + (long long)c * 36;
-#pragma unroll
-    for (int a = 0; a < 6; ++a) {
-      double zz = 0.0;
-#pragma unroll
-      for (int b = 0; b < 6; ++b) zz += m[a * 6 + b] * rv[b];
-      d.z[(long long)c * 6 + a] = zz;
-      rz += rv[a] * zz;
-    }
-  }
+  if (c < d.C) pcg_camera_update(d, st, st.alpha, c, rr, rz);
   const double v0 = block_sum(rr, red);
   __syncthreads();
   const double v1 = block_sum(rz, red);
   const double vals[2] = {v0, v1};
   double tot[2];
   if (grid_reduce<2>(vals, d.block_red, d.tickets + 3, tot) && threadIdx.x == 0) {
-    PcgDev& o = *d.pcg;
-    const double rnorm = sqrt(tot[0]);
-    o.rnorm = rnorm;
-    if (s.state == kPcgIter) {
-      o.iters = s.iters + 1;
-      if (!isfinite(rnorm)) {
-        o.state = kPcgBreakdown;
-      } else if (rnorm <= s.tol * s.bnorm) {
-        o.state = kPcgVerify;  // confirm with the true residual (pcg.hpp:86-109)
-        o.dir = kDirX;
-      } else {
-        const double beta = tot[1] / s.rz;
-        if (!isfinite(beta)) {
-          o.state = kPcgBreakdown;
-        } else {
-          o.beta = beta;
-          o.rz = tot[1];
-          o.dir = kDirZBetaP;
-          if (o.iters >= s.budget) o.state = kPcgDone;
-        }
-      }
-    } else {
-      o.true_norm = rnorm;
-      if (rnorm <= s.tol * s.bnorm) {
-        o.state = kPcgDone;
-        o.converged = 1;
-      } else {  // restart from the true residual
-        o.rz = tot[1];
-        o.beta = 0.0;
-        o.dir = kDirZ;
-        o.state = (s.iters >= s.budget) ? kPcgDone : kPcgIter;
+    PcgDev o = st;
+    pcg_decide(o, tot[0], tot[1]);
+    *d.pcg = o;
+  }
+}
+
+// Sum of per-block partials in block order, identical in every block (one
+// warp: lane-strided sums, fixed xor tree). Valid in all lanes.
+template <int K>
+__device__ __forceinline__ void sum_block_partials(const double* part, int nblocks, double (&tot)[K]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int k = 0; k < K; ++k) tot[k] = 0.0;
+  for (int b = lane; b < nblocks; b += 32)
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] += __ldcg(part + (long long)b * K + k);
+#pragma unroll
+  for (int k = 0; k < K; ++k) tot[k] = warp_sum(tot[k]);
+}
+
+// Whole PCG solve in one cooperative launch: warp-tiles, camera reduction and
+// vector update separated by grid barriers; the scalar recurrence is
+// evaluated redundantly (bit-identically) by every block, so no block waits
+// on another for alpha / beta. Runs up to max_iters iterations per launch.
+__global__ void __launch_bounds__(256, 2) k_pcg_persistent(Dev d, int slice, long long max_iters) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) char smem[];
+  __shared__ double red[32];
+  __shared__ PcgDev st;
+  __shared__ double s_tot[2];
+  if (threadIdx.x == 0) st = *d.pcg;
+  __syncthreads();
+  double* partB = d.block_red;              // gridDim doubles
+  double* partC = d.block_red + gridDim.x;  // 2 * gridDim doubles
+  const int wpb = blockDim.x >> 5;
+  const int gwarp = blockIdx.x * wpb + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * wpb;
+  const long long stop_at = st.iters + max_iters;
+  pipe_init(smem + (threadIdx.x >> 5) * kPipeWarpBytes);
+  PipeState ps;
+  while (st.state < kPcgDone && st.iters < stop_at) {
+    const PcgDev cur = st;
+    // A: warp-tiles (pipelined small tiles, then big tiles)
+    sx_all_tiles(d, cur, smem, gwarp, nwarps, ps);
+    grid.sync();
+    // B: cameras (warp per camera)
+    double pap = 0.0;
+    for (int c = gwarp; c < d.C; c += nwarps) pap += sx_camera(d, cur, c);
+    pap = block_sum(pap, red);
+    if (threadIdx.x == 0) partB[blockIdx.x] = pap;
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double tot[1];
+      sum_block_partials<1>(partB, gridDim.x, tot);
+      if (threadIdx.x == 0) s_tot[0] = tot[0];
+    }
+    __syncthreads();
+    double alpha = 0.0;
+    if (cur.state == kPcgIter) {
+      alpha = cur.rz / s_tot[0];
+      if (!isfinite(alpha)) {  // pcg.hpp:77: identical decision in every block
+        if (threadIdx.x == 0) st.state = kPcgBreakdown;
+        __syncthreads();
+        break;
       }
     }
+    // C: vector update (thread per camera)
+    double rr = 0.0, rz = 0.0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C; c += gridDim.x * blockDim.x)
+      pcg_camera_update(d, cur, alpha, c, rr, rz);
+    rr = block_sum(rr, red);
+    __syncthreads();
+    rz = block_sum(rz, red);
+    if (threadIdx.x == 0) {
+      partC[2 * blockIdx.x] = rr;
+      partC[2 * blockIdx.x + 1] = rz;
+    }
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double tot[2];
+      sum_block_partials<2>(partC, gridDim.x, tot);
+      if (threadIdx.x == 0) {
+        PcgDev o = cur;
+        o.alpha = alpha;
+        pcg_decide(o, tot[0], tot[1]);
+        st = o;
+      }
+    }
+    __syncthreads();
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d.pcg = st;
 }
 
 // ---------------------------------------------------------------------------
@@ -825,47 +1315,38 @@ __global__ void k_cam_retract(Dev d) {
   rec[15] = 0.0;
 }
 
-// cam: R9 t3 f k1 k2 dc6 | trial t3 q4  (28) ; pt: p3 ptrial3
+// cam: R9 t3 f k1 k2 dc6 | trial t3 q4 (28), intr at 12..14 ; pt: p3 ptrial3 ; stage 3
 constexpr WsDims kTrialWs{28, 6, 3, 0};
 
-__global__ void __launch_bounds__(kTileThreads) k_backsub_trial(Dev d) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ double red[32];
-  const int t = blockIdx.x;
-  const TileGeom g = tile_geom(d, t);
-  const Ws ws = ws_carve(tile_base(d, g, smem), kTrialWs, g.ncam, g.npts, g.nobs);
-  for (int idx = threadIdx.x; idx < g.ncam * 28; idx += blockDim.x) {
-    const int l = idx / 28, j = idx - l * 28;
-    const long long c = d.ent_cam[g.eb + l];
-    double v;
-    if (j < 15)
-      v = d.camrec[c * kCamRec + j];
-    else if (j < 21)
-      v = d.x[c * 6 + (j - 15)];
-    else
-      v = d.pose_t[c * 7 + (j - 21)];
-    ws.cam[idx] = v;
-  }
-  load_points(ws, 6, d.pts, g.pb, g.npts);
-  __syncthreads();
-  for (int s = threadIdx.x; s < g.nobs; s += blockDim.x) {
-    const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
+template <bool kShared>
+__device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t) {
+  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kTrialWs, g.ncam, g.npts, g.nobs);
+  const int lane = lane_id();
+  load_point_fields<3>(ws, 6, 0, d.pts, g.pb, g.npts);
+  load_tile_index(d, g, ws);
+  __syncwarp();
+  load_cam_fields<15>(ws, g.ncam, 28, 0, d.camrec, kCamRec);
+  load_cam_fields<6>(ws, g.ncam, 28, 15, d.x, 6);
+  load_cam_fields<7>(ws, g.ncam, 28, 21, d.pose_t, 7);
+  __syncwarp();
+  for (int s = lane; s < g.nobs; s += 32) {
+    const std::uint32_t lcpt = ws.lcpt[s];
     const double* cam = ws.cam + (lcpt & 0xffff) * 28;
     P3 y;
     double D[6];
     obs_geometry(cam, ws.pt + (lcpt >> 16) * 6, y, D);
     jpt_jc_v(D, y, cam, cam + 15, ws.stage + s * 3);
   }
-  __syncthreads();
+  __syncwarp();
   // Delta p = H~_pp^-1 (-g_p - sum_k J_p^T J_c dc), p_trial = p + Delta p
-  for (int lp = threadIdx.x; lp < g.npts; lp += blockDim.x) {
+  for (int lp = lane; lp < g.npts; lp += 32) {
     const long long ip = g.pb + lp;
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-    for (int q = d.pt_ptr[ip]; q < d.pt_ptr[ip + 1]; ++q) {
-      const double* st = ws.stage + d.ptobs[q] * 3;
-      w0 += st[0];
-      w1 += st[1];
-      w2 += st[2];
+    for (int q = ws.pptr[lp]; q < ws.pptr[lp + 1]; ++q) {
+      const double* sv = ws.stage + ws.ptl[q] * 3;
+      w0 += sv[0];
+      w1 += sv[1];
+      w2 += sv[2];
     }
     const double b0 = -d.gp[ip * 3] - w0, b1 = -d.gp[ip * 3 + 1] - w1, b2 = -d.gp[ip * 3 + 2] - w2;
     const double* hi = d.hinv + ip * 6;
@@ -884,26 +1365,35 @@ __global__ void __launch_bounds__(kTileThreads) k_backsub_trial(Dev d) {
     d.pts_t[ip * 3 + 1] = n1;
     d.pts_t[ip * 3 + 2] = n2;
   }
-  __syncthreads();
+  __syncwarp();
   double cost = 0.0;
   int bad = 0;
-  for (int s = threadIdx.x; s < g.nobs; s += blockDim.x) {
-    const std::uint32_t lcpt = d.obs_lcpt[g.ob + s];
+  for (int s = lane; s < g.nobs; s += 32) {
+    const std::uint32_t lcpt = ws.lcpt[s];
     const double* cam = ws.cam + (lcpt & 0xffff) * 28;
     const double* pt = ws.pt + (lcpt >> 16) * 6 + 3;
-    const P3 yr = quat_rotate({cam[24], cam[25], cam[26], cam[27]}, {pt[0], pt[1], pt[2]});
-    double u, w;
-    if (bal_project({yr.x + cam[21], yr.y + cam[22], yr.z + cam[23]}, cam[12], cam[13], cam[14], u, w)) {
-      const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
-      const double r0 = u + -1.0 * px.x, r1 = w + -1.0 * px.y;
+    // trial camera in the [t3 q4 f k1 k2] layout of residual()
+    const double tc[10] = {cam[21], cam[22], cam[23], cam[24], cam[25], cam[26], cam[27], cam[12], cam[13], cam[14]};
+    const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
+    double r0, r1;
+    P3 y;
+    if (residual(tc, pt, px, r0, r1, y))
       cost += r0 * r0 + r1 * r1;
-    } else {
+    else
       bad = 1;  // CheiralityError in the trial evaluate -> cost = inf (lm.hpp:176-181)
-    }
   }
   if (bad) atomicExch(&d.lm->trial_bad, 1);
-  const double cs = block_sum(cost, red);
-  if (threadIdx.x == 0) d.tile_red[t * 2] = cs;
+  cost = warp_sum(cost);
+  if (lane == 0) d.tile_red[t * 2] = cost;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_backsub_trial(Dev d, int slice) {
+  extern __shared__ __align__(16) char smem[];
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= d.T) return;
+  const TileGeom g = tile_geom(d, t);
+  BAE_TILE_DISPATCH(trial_tile, d, g, smem, slice, t);
 }
 
 // Accept: trial parameters become current (lm.hpp:183-189).
@@ -917,14 +1407,12 @@ __global__ void k_commit(Dev d) {
 // ---------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------
-static inline long long lin_bytes(int ncam, int npts, int nobs) { return ws_bytes(kLinWs, ncam, npts, nobs); }
-
 long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) {
   switch (kind) {
     case kWsLin:
-      return lin_bytes(ncam, npts, nobs);
+      return ws_bytes(kLinWs, ncam, npts, nobs);
     case kWsCost:
-      return ws_bytes(WsDims{10, 3, 0, 0}, ncam, npts, nobs);
+      return ws_bytes(kCostWs, ncam, npts, nobs);
     case kWsPrep:
       return ws_bytes(kPrepWs, ncam, npts, nobs);
     case kWsSchur:
@@ -941,38 +1429,68 @@ void set_smem_limits(int max_bytes) {
   cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_schur_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_backsub_trial, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+  cudaFuncSetAttribute(k_pcg_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
 }
 
 static inline int cam_blocks(int C) { return (C + kWarpsPerCamBlock - 1) / kWarpsPerCamBlock; }
 static inline int elt_blocks(long long n, int bs) { return (int)((n + bs - 1) / bs); }
+static inline int tile_blocks(int T, const TileLaunch& tl) { return (T + tl.wpb - 1) / tl.wpb; }
+static int schur_grid(const Dev& d, const SmemSizes& sm);
 
 void launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
   k_camrec<<<elt_blocks(d.C, 128), 128, 0, s>>>(trial ? d.pose_t : d.pose, d.intr, trial ? d.camrec_t : d.camrec, d.C);
 }
 void launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s) {
-  k_linearize<<<d.T, kTileThreads, sm.lin, s>>>(d, write_jac ? 1 : 0);
+  k_linearize<<<tile_blocks(d.T, sm.lin), 32 * sm.lin.wpb, sm.lin.wpb * sm.lin.slice, s>>>(d, sm.lin.slice,
+                                                                                         write_jac ? 1 : 0);
   k_cam_linearize<<<cam_blocks(d.C), 32 * kWarpsPerCamBlock, 0, s>>>(d);
 }
-void launch_cost(const Dev& d, const SmemSizes& sm, bool trial, cudaStream_t s) {
-  k_cost<<<d.T, kTileThreads, sm.cost, s>>>(d, trial ? 1 : 0);
-  k_sum_tiles<<<1, 1024, 0, s>>>(d, trial ? 1 : 0);
+void launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
+  k_cost<<<tile_blocks(d.T, sm.cost), 32 * sm.cost.wpb, sm.cost.wpb * sm.cost.slice, s>>>(d, sm.cost.slice);
+  k_sum_tiles<<<1, 1024, 0, s>>>(d, 0);
 }
 void launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
                  long long budget, cudaStream_t s) {
-  k_prep<<<d.T, kTileThreads, sm.prep, s>>>(d, lambda, clo, chi);
+  k_prep<<<tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s>>>(d, sm.prep.slice, lambda,
+                                                                                         clo, chi);
   k_cam_prep<<<cam_blocks(d.C), 32 * kWarpsPerCamBlock, 0, s>>>(d, lambda, clo, chi, tol, budget);
 }
 void launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
-  k_schur_tiles<<<d.T, kTileThreads, sm.schur, s>>>(d);
+  k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
   k_schur_cams<<<cam_blocks(d.C), 32 * kWarpsPerCamBlock, 0, s>>>(d);
   k_pcg_update<<<elt_blocks(d.C, 128), 128, 0, s>>>(d);
 }
+static int resident_grid(const void* fn, int threads, int smem) {
+  int per_sm = 0, dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  return std::max(1, per_sm * nsm);
+}
+int pcg_persistent_grid(const Dev& d, const SmemSizes& sm) {
+  const int cap = resident_grid((const void*)k_pcg_persistent, 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice);
+  const int want = std::max(std::max(tile_blocks(d.T, sm.schur), (d.C + sm.schur.wpb - 1) / sm.schur.wpb), 1);
+  return std::max(1, std::min(cap, want));
+}
+static int schur_grid(const Dev& d, const SmemSizes& sm) {
+  static int cap = 0;
+  if (!cap) cap = resident_grid((const void*)k_schur_tiles, 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice);
+  return std::max(1, std::min(cap, tile_blocks(d.T, sm.schur)));
+}
+cudaError_t launch_pcg_persistent(const Dev& d, const SmemSizes& sm, int grid, long long max_iters, cudaStream_t s) {
+  Dev dd = d;
+  int slice = sm.schur.slice;
+  void* args[] = {&dd, &slice, &max_iters};
+  return cudaLaunchCooperativeKernel((void*)k_pcg_persistent, dim3(grid), dim3(32 * sm.schur.wpb), args,
+                                     sm.schur.wpb * sm.schur.slice, s);
+}
 void launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
-  k_schur_tiles<<<d.T, kTileThreads, sm.schur, s>>>(d);
+  k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
 }
 void launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
   k_cam_retract<<<elt_blocks(d.C, 128), 128, 0, s>>>(d);
-  k_backsub_trial<<<d.T, kTileThreads, sm.trial, s>>>(d);
+  k_backsub_trial<<<tile_blocks(d.T, sm.trial), 32 * sm.trial.wpb, sm.trial.wpb * sm.trial.slice, s>>>(
+      d, sm.trial.slice);
   k_sum_tiles<<<1, 1024, 0, s>>>(d, 1);
 }
 void launch_commit(const Dev& d, cudaStream_t s) {

@@ -29,7 +29,7 @@ void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32
 }
 
 Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2,
-                std::int64_t N, int tile_obs_target, int tile_cam_cap, int smem_tile_obs_cap) {
+                std::int64_t N, int tile_obs_target, int tile_cam_cap, int tile_pts_cap, int smem_tile_obs_cap) {
   Plan pl;
   pl.C = C;
   pl.P = P;
@@ -95,7 +95,8 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
     const int p = pl.pt_of_internal[i];
     const int m = pcnt[p + 1] - pcnt[p];
     int newc = distinct_new(p, t);
-    if (t_pts > 0 && (t_obs + m > tile_obs_target || static_cast<int>(cur_cams.size()) + newc > tile_cam_cap)) {
+    if (t_pts > 0 && (t_obs + m > tile_obs_target || static_cast<int>(cur_cams.size()) + newc > tile_cam_cap ||
+                      t_pts + 1 > tile_pts_cap)) {
       tile_cams.push_back(cur_cams);
       cur_cams.clear();
       pl.tile_pt_begin.push_back(i);

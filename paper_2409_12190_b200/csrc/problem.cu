@@ -10,7 +10,10 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <limits>
 
 #include "problem.hpp"
@@ -22,6 +25,8 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(BAE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 constexpr int kSmemLimit = 200 * 1024;
+constexpr int kSliceLimit = 48 * 1024;    // per-warp tile workspace
+constexpr int kCtaSmemBudget = 100 * 1024; // two CTAs per SM
 constexpr int kPcgChunk = 8;
 }  // namespace
 
@@ -52,35 +57,73 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (opt.device < 0 || opt.device >= ndev) throw Error(BAE_ERR_INVALID_ARGUMENT, "bad device ordinal");
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
-  const int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : 512;
-  plan_ = build_plan(C, P, cam_idx, pt_idx, px2, N, tile_obs, 128, 1 << 30);
+  int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : 64;
+  if (const char* t = std::getenv("BAE_TILE_OBS")) tile_obs = std::max(8, std::atoi(t));
+  int tile_cams = 32;
+  if (const char* t = std::getenv("BAE_TILE_CAMS")) tile_cams = std::max(1, std::atoi(t));
+  if (const char* m = std::getenv("BAE_PCG_MODE")) use_graph_pcg_ = std::string(m) == "graph";
+  plan_ = build_plan(C, P, cam_idx, pt_idx, px2, N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
+                     kPipePts, 1 << 30);
   intr_host_.assign(intr3, intr3 + 3 * static_cast<std::size_t>(C));
 
-  // Workspace placement: shared memory unless a tile needs more than kSmemLimit.
+  // Tile classes. "Small" tiles (within the kPipe* caps) take the pipelined
+  // TMA path of the Schur product and a per-warp shared-memory slice in the
+  // other tile kernels; any other tile (one very long track) runs every kind
+  // from a global workspace slot.
   Plan& pl = plan_;
   long long big_stride = 0;
   int nbig = 0;
+  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial};
+  std::vector<int4> desc(static_cast<std::size_t>(pl.T), int4{0, 0, 0, 0});
+  std::vector<char> blob;
+  std::vector<int> small_tiles, big_tiles;
   for (int t = 0; t < pl.T; ++t) {
-    const int nobs = pl.tile_obs_begin[t + 1] - pl.tile_obs_begin[t];
-    const int npts = pl.tile_pt_begin[t + 1] - pl.tile_pt_begin[t];
-    const int ncam = pl.tile_ent_begin[t + 1] - pl.tile_ent_begin[t];
+    const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
+    const int nobs = pl.tile_obs_begin[t + 1] - ob;
+    const int npts = pl.tile_pt_begin[t + 1] - pb;
+    const int ncam = pl.tile_ent_begin[t + 1] - eb;
     long long need = 0;
     for (int k = 0; k < kWsKinds; ++k) need = std::max(need, tile_ws_bytes(k, ncam, npts, nobs));
-    if (need > kSmemLimit) {
+    const bool small = nobs > 0 && nobs <= kPipeObs && ncam <= kPipeCams && npts <= kPipePts && need <= kSliceLimit;
+    if (!small) {
       pl.tile_ws[t] = nbig++;
       big_stride = std::max(big_stride, need);
-    } else {
-      pl.tile_ws[t] = -1;
-      auto upd = [&](int& slot, int kind) {
-        slot = std::max<int>(slot, static_cast<int>(tile_ws_bytes(kind, ncam, npts, nobs)));
-      };
-      upd(sm_.lin, kWsLin);
-      upd(sm_.cost, kWsCost);
-      upd(sm_.prep, kWsPrep);
-      upd(sm_.schur, kWsSchur);
-      upd(sm_.trial, kWsTrial);
+      big_tiles.push_back(t);
+      continue;
     }
+    pl.tile_ws[t] = -1;
+    for (int k = 0; k < kWsKinds; ++k)
+      kinds[k]->slice = std::max<int>(kinds[k]->slice, static_cast<int>(tile_ws_bytes(k, ncam, npts, nobs)));
+    // index blob: hdr | camid | ent | pptr | lcpt | ptl, padded to 16 bytes
+    const std::size_t off = blob.size();
+    const int bytes = (32 + 4 * ncam + 4 * (ncam + 1) + 4 * (npts + 1) + 6 * nobs + 15) / 16 * 16;
+    blob.resize(off + static_cast<std::size_t>(bytes), 0);
+    int* w = reinterpret_cast<int*>(blob.data() + off);
+    w[0] = ob;
+    w[1] = nobs;
+    w[2] = pb;
+    w[3] = npts;
+    w[4] = eb;
+    w[5] = ncam;
+    int* q = w + 8;
+    for (int l = 0; l < ncam; ++l) *q++ = pl.ent_cam[eb + l];
+    for (int l = 0; l <= ncam; ++l) *q++ = pl.ent_obs_begin[eb + l] - ob;
+    for (int i = 0; i <= npts; ++i) *q++ = pl.pt_ptr[pb + i] - ob;
+    std::uint32_t* lc = reinterpret_cast<std::uint32_t*>(q);
+    for (int i = 0; i < nobs; ++i) lc[i] = pl.obs_lcpt[ob + i];
+    std::uint16_t* ptl = reinterpret_cast<std::uint16_t*>(lc + nobs);
+    for (int i = 0; i < nobs; ++i) ptl[i] = pl.ptobs[ob + i];
+    desc[t] = int4{static_cast<int>(off / 16), bytes, pb, npts};
+    small_tiles.push_back(t);
   }
+  for (int k = 0; k < kWsKinds; ++k) {
+    TileLaunch& tl = *kinds[k];
+    tl.slice = std::max(16, (tl.slice + 15) / 16 * 16);
+    // up to 8 warp-tiles per CTA, two CTAs per SM within the shared-memory budget
+    tl.wpb = std::max(1, std::min(8, kCtaSmemBudget / tl.slice));
+  }
+  sm_.schur.slice = kPipeWarpBytes;  // pipelined double buffer per warp
+  sm_.schur.wpb = 4;
   big_stride = (big_stride + 255) / 256 * 256;
   set_smem_limits(kSmemLimit);
 
@@ -105,11 +148,18 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.cam_ent = upload(pl.cam_ent);
   d.pt_ptr = upload(pl.pt_ptr);
   d.ptobs = upload(pl.ptobs);
+  if (blob.empty()) blob.resize(16);
+  d.tile_desc = upload(desc);
+  d.tile_blob = upload(blob);
+  d.small_tiles = upload(small_tiles);
+  d.big_tiles = upload(big_tiles);
+  d.n_small = static_cast<int>(small_tiles.size());
+  d.n_big_tiles = static_cast<int>(big_tiles.size());
   d.bigws = nbig ? dalloc<char>(static_cast<std::size_t>(nbig) * big_stride) : nullptr;
   d.pose = dalloc<double>(7 * static_cast<std::size_t>(C));
   d.intr = upload(intr_host_);
   d.camrec = dalloc<double>(kCamRec * static_cast<std::size_t>(C));
-  d.pts = dalloc<double>(3 * static_cast<std::size_t>(P));
+  d.pts = dalloc<double>(3 * static_cast<std::size_t>(P) + 2);  // +16 B: TMA point windows
   d.pose_t = dalloc<double>(7 * static_cast<std::size_t>(C));
   d.camrec_t = dalloc<double>(kCamRec * static_cast<std::size_t>(C));
   d.pts_t = dalloc<double>(3 * static_cast<std::size_t>(P));
@@ -130,13 +180,14 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.partial = dalloc<double>(27 * static_cast<std::size_t>(std::max(pl.E, 1)));
   d.tile_red = dalloc<double>(2 * static_cast<std::size_t>(pl.T));
   const int max_blocks = std::max((C + kWarpsPerCamBlock - 1) / kWarpsPerCamBlock, (C + 127) / 128) + 1;
-  d.block_red = dalloc<double>(4 * static_cast<std::size_t>(max_blocks));
+  d.block_red = dalloc<double>(4 * static_cast<std::size_t>(std::max(max_blocks, 4096)));
   d.tickets = dalloc<unsigned>(16);
   ck(cudaMemset(d.tickets, 0, 16 * sizeof(unsigned)), "memset");
   d.pcg = dalloc<PcgDev>(1);
   d.lm = dalloc<LmDev>(1);
   d.jstore = nullptr;
   d.resid = nullptr;
+  d.trace = nullptr;
   ck(cudaMallocHost(&pcg_host_, sizeof(PcgDev)), "cudaMallocHost");
   ck(cudaMallocHost(&lm_host_, sizeof(LmDev)), "cudaMallocHost");
   ck(cudaMemset(d.pcg, 0, sizeof(PcgDev)), "memset");
@@ -163,15 +214,18 @@ void Problem::sync() { ck(cudaStreamSynchronize(stream_), "kernel execution"); }
 void Problem::set_parameters(const double* poses7, const double* points3) {
   activate();
   const int C = d_.C, P = d_.P;
-  std::vector<double> pts(3 * static_cast<std::size_t>(P));
-  for (int i = 0; i < P; ++i) {
+  std::vector<double> pts(points3 ? 3 * static_cast<std::size_t>(P) : 0);
+  for (int i = 0; points3 && i < P; ++i) {
     const int p = plan_.pt_of_internal[i];
     pts[3 * i] = points3[3 * p];
     pts[3 * i + 1] = points3[3 * p + 1];
     pts[3 * i + 2] = points3[3 * p + 2];
   }
-  ck(cudaMemcpyAsync(d_.pose, poses7, 7 * sizeof(double) * C, cudaMemcpyHostToDevice, stream_), "H2D poses");
-  ck(cudaMemcpyAsync(d_.pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, stream_), "H2D points");
+  if (poses7)
+    ck(cudaMemcpyAsync(d_.pose, poses7, 7 * sizeof(double) * C, cudaMemcpyHostToDevice, stream_), "H2D poses");
+  if (points3)
+    ck(cudaMemcpyAsync(d_.pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, stream_),
+       "H2D points");
   launch_camrec(d_, false, stream_);
   launches_ += kLaunchesCamrec;
   sync();
@@ -221,7 +275,7 @@ double Problem::evaluate(double* resid2) {
     ck(cudaMalloc(&rbuf, 2 * sizeof(double) * plan_.N), "cudaMalloc");
     d_.resid = rbuf;
   }
-  launch_cost(d_, sm_, false, stream_);
+  launch_cost(d_, sm_, stream_);
   launches_ += kLaunchesCost;
   d_.resid = nullptr;
   read_lm();
@@ -325,13 +379,24 @@ bool Problem::solve(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_);
   launches_ += kLaunchesPrep;
-  build_pcg_graph();
-  for (;;) {
-    ck(cudaGraphLaunch(pcg_graph_, stream_), "graph launch");
-    launches_ += kLaunchesPcgIter * kPcgChunk;
-    ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
-    sync();
-    if (pcg_host_->state >= kPcgDone) break;
+  if (use_graph_pcg_) {
+    build_pcg_graph();
+    for (;;) {
+      ck(cudaGraphLaunch(pcg_graph_, stream_), "graph launch");
+      launches_ += kLaunchesPcgIter * kPcgChunk;
+      ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+      sync();
+      if (pcg_host_->state >= kPcgDone) break;
+    }
+  } else {
+    if (pcg_grid_ == 0) pcg_grid_ = pcg_persistent_grid(d_, sm_);
+    for (;;) {
+      ck(launch_pcg_persistent(d_, sm_, pcg_grid_, 4096, stream_), "cooperative launch");
+      launches_ += 1;
+      ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+      sync();
+      if (pcg_host_->state >= kPcgDone) break;
+    }
   }
   info.iters = pcg_host_->iters;
   info.converged = pcg_host_->converged != 0;
@@ -392,6 +457,10 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   if (poses7 || points3) set_parameters(poses7, points3);
   const double n_obs = static_cast<double>(plan_.N);
 
+  cudaEvent_t ev0, ev1;
+  ck(cudaEventCreate(&ev0), "event");
+  ck(cudaEventCreate(&ev1), "event");
+  ck(cudaEventRecord(ev0, stream_), "event record");
   // Initial evaluate (lm.hpp:217-220); the linearisation computes the cost
   // together with the first step's normal-equation blocks.
   linearize();
@@ -457,7 +526,13 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
       break;
     }
   }
+  ck(cudaEventRecord(ev1, stream_), "event record");
   sync();
+  float dev_ms = 0.f;
+  ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event elapsed");
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  rep.device_seconds = dev_ms * 1e-3;
   rep.iterations = iterations;
   rep.final_cost = history.back();
   rep.final_mse = rep.final_cost / n_obs;
@@ -518,6 +593,29 @@ double Problem::time_kernel(int kind, int reps) {
   };
   launch();  // warm-up
   sync();
+  if (kind == 1 && std::getenv("BAE_TRACE")) {
+    unsigned long long* tr = nullptr;
+    ck(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * d_.T), "cudaMalloc");
+    ck(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * d_.T), "memset");
+    d_.trace = tr;
+    launch();
+    sync();
+    d_.trace = nullptr;
+    std::vector<unsigned long long> h(8 * static_cast<std::size_t>(d_.T));
+    ck(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost), "D2H trace");
+    cudaFree(tr);
+    unsigned long long t0 = ~0ULL, t1 = 0;
+    double ph[5] = {0, 0, 0, 0, 0};
+    for (int t = 0; t < d_.T; ++t) {
+      const unsigned long long* r = &h[8 * static_cast<std::size_t>(t)];
+      t0 = std::min(t0, r[0]);
+      t1 = std::max(t1, r[5]);
+      for (int k = 0; k < 5; ++k) ph[k] += double(r[k + 1] - r[k]);
+    }
+    std::fprintf(stderr, "trace: span %.1f us, mean per tile: load %.2f ph1 %.2f pt %.2f ph3 %.2f ent %.2f us\n",
+                 (t1 - t0) * 1e-3, ph[0] / d_.T * 1e-3, ph[1] / d_.T * 1e-3, ph[2] / d_.T * 1e-3,
+                 ph[3] / d_.T * 1e-3, ph[4] / d_.T * 1e-3);
+  }
   ck(cudaEventRecord(a, stream_), "record");
   for (int i = 0; i < reps; ++i) launch();
   ck(cudaEventRecord(b, stream_), "record");

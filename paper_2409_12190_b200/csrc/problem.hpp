@@ -70,6 +70,8 @@ class Problem {
   PcgDev* pcg_host_ = nullptr;
   LmDev* lm_host_ = nullptr;
   long long launches_ = 0;
+  bool use_graph_pcg_ = false;  // BAE_PCG_MODE=graph: per-iteration kernels in CUDA graphs
+  int pcg_grid_ = 0;
 };
 
 }  // namespace bae

@@ -17,6 +17,8 @@ print(f"create {time.time() - t:.2f}s stats {g.stats()}")
 for kind, label in [(0, "linearize"), (1, "schur_tiles"), (2, "pcg_iter"), (3, "jac_store")]:
     ms = g.time_kernel(kind, 20)
     print(f"{label}: {ms * 1e3:.1f} us")
+if iters == 0:
+    sys.exit(0)
 t = time.time()
 rep = bae.optimize(g, s.poses, s.points, bae.LmConfig(max_iterations=iters, solver=bae.SolverChoice.pcg))
 el = time.time() - t
