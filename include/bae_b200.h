@@ -61,8 +61,8 @@ typedef struct bae_lm_config {
   double clamp_min;       /* 1e-6  */
   double clamp_max;       /* 1e32  */
   double plateau_rel_tol; /* 1e-6  */
-  double pcg_tol;         /* 1e-8  (relative, on the reduced camera system) */
-  int64_t pcg_max_iters;  /* 0: max(250, 2 * num_cameras)                     */
+  double pcg_tol;         /* 1e-8  relative to the full rhs -J^T r (pcg.hpp:85) */
+  int64_t pcg_max_iters;  /* 0: max(250, 2 * (cameras + points)), lm.hpp:139-142 */
   int32_t max_iterations; /* 10    */
   int32_t plateau_patience; /* 3   */
   int32_t solver;         /* BAE_SOLVER_*; the reference default is cholesky  */

@@ -85,6 +85,14 @@ struct Dev {
   // stored-Jacobian mode and exports (slot order, component-major [comp][N])
   double* jstore;  // 18 * N or null
   double* resid;   // 2 * N or null
+  // direct solver (dense reduced camera system): per-slot W = J_c^T J_p and
+  // W H~_pp^-1 (36 doubles, slot order), pair list grouped by camera block
+  double* wstore;
+  const int2* pairs;       // (slot k, slot l), c(k) >= c(l), grouped by block
+  const int* blk_ptr;      // nblk + 1
+  const int2* blk_cam;     // (c1, c2), c1 >= c2
+  int nblk;
+  double* schur;           // 6C x 6C, column-major (lower triangle used)
   unsigned long long* trace;  // per-tile phase timestamps (BAE_TRACE) or null
   // pipelined small tiles: per-tile descriptor {blob offset / 16, blob bytes,
   // first point, point count} and the packed per-tile index blobs

@@ -553,6 +553,14 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     const double* vp = sp + 9;
 #pragma unroll
     for (int a = 0; a < 6; ++a) st[21 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
+    if (d.wstore) {  // direct solver: keep W and W H~^-1 of this slot
+      double* w = d.wstore + (long long)(g.ob + s) * 36;
+#pragma unroll
+      for (int j = 0; j < 18; ++j) {
+        w[j] = W[j];
+        w[18 + j] = WH[j];
+      }
+    }
   }
   __syncwarp();
   entries_from_stage<27, 27>(ws, g.ncam, g.eb, d.partial);
@@ -625,7 +633,11 @@ __global__ void k_cam_prep(Dev d, double lambda, double clo, double chi, double 
   double tot[2];
   if (grid_reduce<2>(vals, d.block_red, d.tickets + 1, tot) && threadIdx.x == 0) {
     PcgDev& s = *d.pcg;
-    s.bnorm = sqrt(tot[0]);
+    // Tolerance semantics of the reference (pcg.hpp:85): ||r|| <= tol ||b|| with
+    // b the FULL right-hand side -J^T r. Back-substitution satisfies the point
+    // rows exactly, so the full residual equals the reduced one and the
+    // reference's test is applied unchanged to the reduced recurrence.
+    s.bnorm = sqrt(d.lm->grad_sq);
     s.rz = tot[1];
     s.tol = tol;
     s.iters = 0;
@@ -633,15 +645,61 @@ __global__ void k_cam_prep(Dev d, double lambda, double clo, double chi, double 
     s.dir = kDirZ;
     s.beta = 0.0;
     s.converged = 0;
-    s.true_norm = 0.0;
+    s.true_norm = sqrt(tot[0]);
     if (s.not_spd) {
       s.state = kPcgBreakdown;
-    } else if (s.bnorm == 0.0) {
+    } else if (s.bnorm == 0.0 || tot[0] == 0.0) {  // x = 0 solves the system exactly
       s.state = kPcgDone;
       s.converged = 1;
     } else {
       s.state = kPcgIter;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// F2: dense reduced camera system for the direct solver (the reference's
+// default SolverChoice::cholesky, lm.hpp:132-136). One warp per camera block
+// (c1 >= c2):  S[c1,c2] = delta(c1,c2) H~_cc - sum_{points} sum_{k in c1, l in c2}
+// (W_k H~_pp^-1) W_l^T, pairs in (point, k, l) order, lanes strided over the
+// block's pairs, fixed xor tree; column-major lower triangle for potrf.
+// ---------------------------------------------------------------------------
+__global__ void k_schur_dense(Dev d) {
+  const int blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (blk >= d.nblk) return;
+  const int lane = lane_id();
+  double acc[36];
+#pragma unroll
+  for (int j = 0; j < 36; ++j) acc[j] = 0.0;
+  for (int q = d.blk_ptr[blk] + lane; q < d.blk_ptr[blk + 1]; q += 32) {
+    const int2 pr = d.pairs[q];
+    const double* wh = d.wstore + (long long)pr.x * 36 + 18;  // W_k H~^-1 (6x3)
+    const double* w = d.wstore + (long long)pr.y * 36;        // W_l (6x3)
+    double a[18], b[18];
+#pragma unroll
+    for (int j = 0; j < 18; ++j) {
+      a[j] = wh[j];
+      b[j] = w[j];
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) acc[r * 6 + c] += a[r * 3] * b[c * 3] + a[r * 3 + 1] * b[c * 3 + 1] + a[r * 3 + 2] * b[c * 3 + 2];
+  }
+#pragma unroll
+  for (int j = 0; j < 36; ++j) acc[j] = warp_sum(acc[j]);
+  const int2 cc = d.blk_cam[blk];
+  const long long n = 6LL * d.C;
+  if (lane == 0) {
+    const double* h = d.hccd + (long long)cc.x * 21;
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) {
+        double v = -acc[r * 6 + c];
+        if (cc.x == cc.y) v += h[sym6(r, c)];
+        d.schur[(6LL * cc.y + c) * n + 6LL * cc.x + r] = v;
+      }
   }
 }
 
@@ -1492,6 +1550,9 @@ void launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
   k_backsub_trial<<<tile_blocks(d.T, sm.trial), 32 * sm.trial.wpb, sm.trial.wpb * sm.trial.slice, s>>>(
       d, sm.trial.slice);
   k_sum_tiles<<<1, 1024, 0, s>>>(d, 1);
+}
+void launch_schur_dense(const Dev& d, cudaStream_t s) {
+  if (d.nblk > 0) k_schur_dense<<<(d.nblk + 7) / 8, 256, 0, s>>>(d);
 }
 void launch_commit(const Dev& d, cudaStream_t s) {
   const long long n = std::max<long long>((long long)d.P * 3, (long long)d.C * kCamRec);

@@ -33,6 +33,7 @@ cudaError_t launch_pcg_persistent(const Dev& d, const SmemSizes& sm, int grid, l
 void launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s);
 void launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s);
 void launch_commit(const Dev& d, cudaStream_t s);
+void launch_schur_dense(const Dev& d, cudaStream_t s);
 
 // kernel launches issued per wrapper (for the bench's gpu_launches count)
 constexpr int kLaunchesLinearize = 2, kLaunchesCost = 2, kLaunchesPrep = 2, kLaunchesPcgIter = 3,

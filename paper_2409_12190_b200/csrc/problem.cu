@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -61,7 +62,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (const char* t = std::getenv("BAE_TILE_OBS")) tile_obs = std::max(8, std::atoi(t));
   int tile_cams = 32;
   if (const char* t = std::getenv("BAE_TILE_CAMS")) tile_cams = std::max(1, std::atoi(t));
-  if (const char* m = std::getenv("BAE_PCG_MODE")) use_graph_pcg_ = std::string(m) == "graph";
+  if (const char* m = std::getenv("BAE_PCG_MODE")) use_graph_pcg_ = std::string(m) != "persistent";
   plan_ = build_plan(C, P, cam_idx, pt_idx, px2, N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
                      kPipePts, 1 << 30);
   intr_host_.assign(intr3, intr3 + 3 * static_cast<std::size_t>(C));
@@ -188,6 +189,12 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.jstore = nullptr;
   d.resid = nullptr;
   d.trace = nullptr;
+  d.wstore = nullptr;
+  d.pairs = nullptr;
+  d.blk_ptr = nullptr;
+  d.blk_cam = nullptr;
+  d.nblk = 0;
+  d.schur = nullptr;
   ck(cudaMallocHost(&pcg_host_, sizeof(PcgDev)), "cudaMallocHost");
   ck(cudaMallocHost(&lm_host_, sizeof(LmDev)), "cudaMallocHost");
   ck(cudaMemset(d.pcg, 0, sizeof(PcgDev)), "memset");
@@ -200,6 +207,8 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
 
 Problem::~Problem() {
   cudaSetDevice(opt_.device);
+  if (solver_) cusolverDnDestroy(solver_);
+  if (host_info_) cudaFreeHost(host_info_);
   if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
   for (void* p : allocs_) cudaFree(p);
   if (pcg_host_) cudaFreeHost(pcg_host_);
@@ -247,10 +256,15 @@ void Problem::get_parameters(double* poses7, double* points3) {
   }
 }
 
+// Clears the per-evaluation flags and the trial cost; keeps the cost and
+// ||J^T r||^2 of the current linearisation (needed by the next solve).
 void Problem::reset_lm_status() {
   LmDev z{};
   z.err_obs = INT_MAX;
-  ck(cudaMemcpyAsync(d_.lm, &z, sizeof(LmDev), cudaMemcpyHostToDevice, stream_), "H2D lm");
+  constexpr std::size_t off = offsetof(LmDev, new_cost);
+  ck(cudaMemcpyAsync(reinterpret_cast<char*>(d_.lm) + off, reinterpret_cast<const char*>(&z) + off,
+                     sizeof(LmDev) - off, cudaMemcpyHostToDevice, stream_),
+     "H2D lm");
 }
 
 void Problem::read_lm() {
@@ -372,10 +386,115 @@ void Problem::build_pcg_graph() {
   cudaGraphDestroy(g);
 }
 
-// Damping + Schur preparation + PCG for one lambda; returns false when the
-// damped system is not SPD or the recurrence broke down (lm.hpp:146-152).
+// Damped solve for one lambda with the configured solver; returns false when
+// the damped system is not SPD or the recurrence broke down, which the LM
+// loop turns into a rejected step (lm.hpp:146-152).
 bool Problem::solve(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
-  const long long budget = cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * d_.C);
+  return cfg.solver == BAE_SOLVER_CHOLESKY ? solve_direct(lambda, cfg, info) : solve_pcg(lambda, cfg, info);
+}
+
+// Maximum reduced-system order for the dense direct solve (8.6 GB of FP64).
+constexpr long long kDirectMaxOrder = 32768;
+
+// Pair list of the reduced camera system: for every point, every ordered pair
+// of its observations (k, l) with camera(k) >= camera(l), grouped by camera
+// block (two-pass stable counting sort), point-major inside a block.
+void Problem::build_direct() {
+  if (direct_ready_) return;
+  const long long n = 6LL * d_.C;
+  if (n > kDirectMaxOrder)
+    throw Error(BAE_ERR_UNSUPPORTED, "solver=cholesky: reduced camera system too large for the dense direct solve; "
+                                     "use solver=pcg");
+  const Plan& pl = plan_;
+  std::vector<int> cam_of_slot(static_cast<std::size_t>(pl.N));
+  for (int t = 0; t < pl.T; ++t)
+    for (int e = pl.tile_ent_begin[t]; e < pl.tile_ent_begin[t + 1]; ++e)
+      for (int sl = pl.ent_obs_begin[e]; sl < pl.ent_obs_begin[e + 1]; ++sl) cam_of_slot[sl] = pl.ent_cam[e];
+  std::vector<int2> raw;
+  std::vector<int> slots;
+  for (int t = 0; t < pl.T; ++t) {
+    const int ob = pl.tile_obs_begin[t];
+    for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
+      slots.clear();
+      for (int q = pl.pt_ptr[i]; q < pl.pt_ptr[i + 1]; ++q) slots.push_back(ob + pl.ptobs[q]);
+      for (int k : slots)
+        for (int l : slots)
+          if (cam_of_slot[k] >= cam_of_slot[l]) raw.push_back(int2{k, l});
+    }
+  }
+  const std::size_t np = raw.size();
+  std::vector<int2> tmp(np), sorted(np);
+  std::vector<long long> cnt(static_cast<std::size_t>(d_.C) + 1);
+  auto pass = [&](const std::vector<int2>& in, std::vector<int2>& out, bool by_first) {
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (const int2& p : in) ++cnt[cam_of_slot[by_first ? p.x : p.y] + 1];
+    for (int c = 0; c < d_.C; ++c) cnt[c + 1] += cnt[c];
+    for (const int2& p : in) out[cnt[cam_of_slot[by_first ? p.x : p.y]]++] = p;
+  };
+  pass(raw, tmp, false);
+  pass(tmp, sorted, true);
+  std::vector<int> bptr{0};
+  std::vector<int2> bcam;
+  for (std::size_t q = 0; q < np; ++q) {
+    const int c1 = cam_of_slot[sorted[q].x], c2 = cam_of_slot[sorted[q].y];
+    if (q == 0 || c1 != cam_of_slot[sorted[q - 1].x] || c2 != cam_of_slot[sorted[q - 1].y]) {
+      if (q) bptr.push_back(static_cast<int>(q));
+      bcam.push_back(int2{c1, c2});
+    }
+  }
+  bptr.push_back(static_cast<int>(np));
+  d_.pairs = upload(sorted);
+  d_.blk_ptr = upload(bptr);
+  d_.blk_cam = upload(bcam);
+  d_.nblk = static_cast<int>(bcam.size());
+  d_.schur = dalloc<double>(static_cast<std::size_t>(n) * static_cast<std::size_t>(n));
+  if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw Error(BAE_ERR_CUDA, "cusolverDnCreate failed");
+  cusolverDnSetStream(solver_, stream_);
+  if (cusolverDnDpotrf_bufferSize(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), d_.schur,
+                                  static_cast<int>(n), &potrf_lwork_) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(BAE_ERR_CUDA, "potrf workspace query failed");
+  potrf_work_ = dalloc<double>(static_cast<std::size_t>(std::max(potrf_lwork_, 1)));
+  dev_info_ = dalloc<int>(1);
+  ck(cudaMallocHost(&host_info_, sizeof(int)), "cudaMallocHost");
+  direct_ready_ = true;
+}
+
+// Direct solve of the damped reduced camera system (the reference's default
+// Cholesky solver on the Schur complement instead of the full system):
+// dense S from per-observation W, W H~^-1 (my kernels), LL^T factor and
+// triangular solves (cuSOLVER potrf/potrs, FP64). NotSpd -> rejected step.
+bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
+  build_direct();
+  const long long n = 6LL * d_.C;
+  if (!d_.wstore) d_.wstore = dalloc<double>(36 * static_cast<std::size_t>(plan_.N));
+  ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+  launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_);
+  launches_ += kLaunchesPrep;
+  ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
+  launch_schur_dense(d_, stream_);
+  launches_ += 1;
+  ck(cudaMemcpyAsync(d_.x, d_.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_), "rhs copy");
+  info.iters = 0;
+  if (cusolverDnDpotrf(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), d_.schur, static_cast<int>(n),
+                       potrf_work_, potrf_lwork_, dev_info_) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(BAE_ERR_CUDA, "potrf launch failed");
+  ck(cudaMemcpyAsync(host_info_, dev_info_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H info");
+  ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+  sync();
+  if (*host_info_ != 0 || pcg_host_->not_spd) return false;  // NotSpdError (cholesky.hpp:229)
+  if (cusolverDnDpotrs(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), 1, d_.schur, static_cast<int>(n), d_.x,
+                       static_cast<int>(n), dev_info_) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(BAE_ERR_CUDA, "potrs launch failed");
+  info.converged = true;
+  info.rel_residual = 0.0;
+  return true;
+}
+
+// Damping + Schur preparation + PCG for one lambda.
+bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
+  // budget as the reference computes it from the full system's block columns (lm.hpp:139-142)
+  const long long budget =
+      cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * (d_.C + d_.P));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_);
   launches_ += kLaunchesPrep;
@@ -450,8 +569,9 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
                        std::vector<bae_iter_record>& traj, bae_lm_report& rep) {
   activate();
   validate_config(cfg);
-  if (cfg.solver != BAE_SOLVER_PCG)
-    throw Error(BAE_ERR_UNSUPPORTED, "solver: only the implicit-Schur PCG path is available on the device");
+  if (cfg.solver != BAE_SOLVER_PCG && cfg.solver != BAE_SOLVER_CHOLESKY)
+    throw Error(BAE_ERR_INVALID_ARGUMENT, "LmConfig: unknown solver");
+  if (cfg.solver == BAE_SOLVER_CHOLESKY) build_direct();
   if (plan_.has_empty_camera || plan_.has_empty_point)
     throw Error(BAE_ERR_INVALID_ARGUMENT, "diagonal op: missing diagonal entry");  // csr.hpp:53
   if (poses7 || points3) set_parameters(poses7, points3);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <cstdint>
 #include <vector>
@@ -56,6 +57,9 @@ class Problem {
   void read_lm();
   void linearize();
   bool solve(double lambda, const bae_lm_config& cfg, SolveInfo& info);
+  bool solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info);
+  bool solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info);
+  void build_direct();
   void build_pcg_graph();
   void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
 
@@ -70,7 +74,14 @@ class Problem {
   PcgDev* pcg_host_ = nullptr;
   LmDev* lm_host_ = nullptr;
   long long launches_ = 0;
-  bool use_graph_pcg_ = false;  // BAE_PCG_MODE=graph: per-iteration kernels in CUDA graphs
+  bool use_graph_pcg_ = true;  // BAE_PCG_MODE=persistent: one cooperative launch per solve
+  // direct solver state (built on first use of solver = cholesky)
+  bool direct_ready_ = false;
+  cusolverDnHandle_t solver_ = nullptr;
+  double* potrf_work_ = nullptr;
+  int potrf_lwork_ = 0;
+  int* dev_info_ = nullptr;
+  int* host_info_ = nullptr;
   int pcg_grid_ = 0;
 };
 

@@ -153,3 +153,38 @@ def test_launch_counter_moves():
     n0 = gpu.launch_count()
     bae.optimize(gpu, s.poses, s.points, bae.LmConfig(max_iterations=2, solver=bae.SolverChoice.pcg))
     assert gpu.launch_count() > n0 + 10
+
+
+@pytest.mark.parametrize("lmbda", [1e-6, 1e-2, 3.0])
+def test_direct_step_matches_cholesky(oracle, lmbda):
+    s = _scene(C=8, P=120, N=500, seed=11)
+    gpu, ref = _pair(s, oracle)
+    dg, iters, _ = gpu.solve_step(lmbda, bae.LmConfig())  # reference default: cholesky
+    dr, _ = ref.solve_step(lmbda, bae.LmConfig())
+    assert iters == 0
+    # both are exact solves: the GPU step satisfies the oracle's damped full
+    # system to rounding, and the two steps agree up to the conditioning
+    A, b = ref.normal_dense(lmbda)
+    assert np.linalg.norm(A @ dg - b) <= 1e-9 * np.linalg.norm(b)
+    cond = np.linalg.cond(A)
+    assert np.linalg.norm(dg - dr) <= max(1e-10, 1e-15 * cond) * np.linalg.norm(dr), (
+        np.linalg.norm(dg - dr) / np.linalg.norm(dr), cond)
+
+
+def test_default_config_trajectory_matches_oracle(oracle):
+    """LmConfig defaults (solver = cholesky) end to end: every iteration's
+    cost, decision and damping against the oracle's exact solve."""
+    s = bae.synthetic.config_scene("ladybug-49")
+    gpu, ref = _pair(s, oracle)
+    cfg = bae.LmConfig(max_iterations=20)
+    rep = bae.optimize(gpu, s.poses, s.points, cfg)
+    oracle.set_threads(8)
+    oref = ref.optimize(cfg)
+    assert len(rep.trajectory) == len(oref["trajectory"])
+    assert rep.reason == bae.TerminationReason(oref["reason"])
+    for a, b in zip(rep.trajectory, oref["trajectory"]):
+        assert a.accepted == b["accepted"] and a.lmbda == b["lmbda"]
+        assert abs(a.cost - b["cost"]) <= 1e-9 * b["cost"], (a.iteration, a.cost, b["cost"])
+    p7, p3 = gpu.get_parameters()
+    assert np.abs(p3 - oref["points"]).max() <= 1e-7
+    assert np.abs(p7 - oref["poses"]).max() <= 1e-7
