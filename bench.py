@@ -1,12 +1,16 @@
 """Benchmark of the B200 BA hot path (BASELINE.json metric: LM iterations/s and
 time-to-converge on BAL-shaped BA; obs/s of the fused residual+Jacobian).
 
-One "step" = one complete LM solve (optimize, lm.hpp:205-255, LmConfig
-defaults with solver=pcg and max_iterations=50 as in the reference CLI,
-cli.hpp:25) of the synthetic Trafalgar-257-shaped problem (BASELINE.json
-configs[1]) from the same initial parameters. value = LM iterations per
-second over the K timed solves (device time, CUDA events on the solver
-stream), max over ranks; time_to_converge_s = mean device time per solve.
+One "step" = one complete LM solve (optimize, lm.hpp:205-255) of the
+synthetic Trafalgar-257-shaped problem (BASELINE.json configs[1]) from the
+same initial parameters, with the reference CLI's settings (LmConfig
+defaults, max_iterations = 50, cli.hpp:25) and the reference's default
+solver (SolverChoice::cholesky, lm.hpp:34): on the GPU that is the dense
+reduced-camera-system direct solve. value = LM iterations per second over
+the K timed solves (device time, CUDA events on the solver stream), max over
+ranks; time_to_converge_s = mean device time per solve. The north-star
+implicit-Schur PCG path (solver = pcg) is measured the same way and
+reported under "pcg", with the roofline of its dominant kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config NAME]
 
@@ -178,16 +182,17 @@ def run_b200(args):
     C, P, N = bae.synthetic.CONFIGS[args.config]
     # N > 1 without the NCCL build: independent replicas (one problem per rank, seed offset by rank)
     scene = bae.synthetic.bal_shaped(C, P, N, seed=C + rank)
-    cfg = LmConfig(max_iterations=50, solver=SolverChoice.pcg)
+    cfg = LmConfig(max_iterations=50)  # reference defaults: solver = cholesky
+    cfg_pcg = LmConfig(max_iterations=50, solver=SolverChoice.pcg)
     prob = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local)
     stats = prob.stats()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
-    def one_solve():
+    def one_solve(c=None):
         prob.set_parameters(scene.poses, scene.points)  # untimed: inputs resident before the timed solve
         flush.zero_()  # L2 flush between timed steps (L2 = 126 MB; 256 MB written)
         torch.cuda.synchronize()
-        rep = bae.optimize(prob, None, None, cfg)
+        rep = bae.optimize(prob, None, None, c or cfg)
         return rep
 
     for _ in range(args.warmup):
@@ -212,6 +217,19 @@ def run_b200(args):
     dev_max = _max_over_ranks(dist, dev_s)
     iters_all = _sum_over_ranks(dist, iters)
     value = iters_all / dev_max  # whole-job LM iterations / s
+
+    # --- north-star PCG path, same protocol ---
+    for _ in range(max(1, args.warmup // 2)):
+        one_solve(cfg_pcg)
+    pcg_dev, pcg_it, pcg_inner = 0.0, 0, 0
+    pcg_steps = max(1, min(args.steps, 3))
+    for _ in range(pcg_steps):
+        r = one_solve(cfg_pcg)
+        pcg_dev += r.device_seconds
+        pcg_it += r.iterations
+        pcg_inner += r.total_pcg_iters
+    pcg_dev = _max_over_ranks(dist, pcg_dev)
+    pcg_value = _sum_over_ranks(dist, pcg_it) / pcg_dev
 
     # --- kernel-level measurements (device events on the solver stream) ---
     ms_lin = prob.time_kernel(0, 20)
@@ -262,8 +280,8 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": 1000.0 * dev_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count + rank)",
-            "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM (LmConfig defaults, solver=pcg, "
-                                   f"max_iterations=50) from the same initial state each step",
+            "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM with LmConfig defaults "
+                                   f"(solver=cholesky, max_iterations=50) from the same initial state each step",
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "flushed (256 MB write) between steps",
                        "tiles": stats["tiles"], "tile_camera_entries": stats["entries"]},
@@ -272,6 +290,9 @@ def run_b200(args):
             "final_mse": last.final_mse, "termination": last.reason.name,
             "obs_per_s_residual_jacobian": N / (ms_lin * 1e-3),
             "kernel_us": {"linearize": ms_lin * 1e3, "schur_tiles": ms_sx * 1e3, "pcg_iteration": ms_pcg * 1e3},
+            "pcg": {"lm_iters_per_s": pcg_value, "time_to_converge_s": pcg_dev / pcg_steps,
+                    "pcg_iterations_per_solve": pcg_inner / pcg_steps,
+                    "config": "same workload, solver=pcg (implicit-Schur PCG, block-Jacobi), pcg_tol=1e-8"},
             "roofline": {"bound": "hbm", "kernel": "k_schur_tiles (implicit Schur S*p, per PCG iteration)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "peak_source": peak_kind,

@@ -188,6 +188,12 @@ int bae_synth_bal_shaped(int32_t num_cameras, int32_t num_points, int64_t num_ob
                          double* intrinsics3, int32_t* cam_idx, int32_t* pt_idx,
                          double* pixels2, double* true_poses7, double* true_points3);
 
+/* ---- multi-GPU landmark partition, host only ----------------- */
+/* Contiguous ranges of the internal point order balanced by observation
+ * count: rank_of_point[p] in [0, world). Cameras are replicated. */
+int bae_partition_points(int32_t num_cameras, int32_t num_points, const int32_t* cam_idx, const int32_t* pt_idx,
+                         int64_t num_observations, int32_t world, int32_t* rank_of_point);
+
 /* ---- measurement hooks (bench.py) ------------------------------------------ */
 /* Device-timed (CUDA events on the solver stream) averages over `reps`
  * launches: kind 0 = linearisation (fused residual + Jacobian + block

@@ -364,6 +364,16 @@ def stop_on_plateau(history, config: LmConfig) -> bool:
     return bool(stop.value)
 
 
+def partition_points(num_cameras: int, num_points: int, observations, world: int) -> np.ndarray:
+    """Landmark partition used by the multi-GPU path (host only)."""
+    cam_idx, pt_idx, _ = observations
+    ci, pi = _i32(cam_idx), _i32(pt_idx)
+    out = np.empty(num_points, np.int32)
+    _check(_lib.load().bae_partition_points(num_cameras, num_points, ptr(ci, ctypes.c_int32), ptr(pi, ctypes.c_int32),
+                                            ci.size, world, ptr(out, ctypes.c_int32)))
+    return out
+
+
 def write_csv(path: str, report: LmReport):
     """CSV trajectory with the reference CLI's schema (cli.hpp:69-79)."""
     with open(path, "w") as f:

@@ -234,6 +234,11 @@ int bae_synth_bal_shaped(int32_t C, int32_t P, int64_t N, uint64_t seed, double 
   });
 }
 
+int bae_partition_points(int32_t C, int32_t P, const int32_t* cam_idx, const int32_t* pt_idx, int64_t N,
+                         int32_t world, int32_t* rank_of_point) {
+  return guarded([&] { bae::partition_points(C, P, cam_idx, pt_idx, N, world, rank_of_point); });
+}
+
 int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms) {
   return guarded([&] { *ms = p->impl->time_kernel(kind, reps); });
 }

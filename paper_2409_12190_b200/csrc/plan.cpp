@@ -194,4 +194,29 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
   return pl;
 }
 
+// Landmark partition for multi-GPU runs: contiguous ranges of
+// the internal point order (the order tiles are cut from), balanced by
+// observation count; cameras are replicated on every rank.
+void partition_points(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N,
+                      int world, std::int32_t* rank_of_point) {
+  if (world < 1) throw Error(BAE_ERR_INVALID_ARGUMENT, "partition: world must be >= 1");
+  validate_inputs(C, P, cam_idx, pt_idx, N);
+  std::vector<std::int32_t> cnt(static_cast<std::size_t>(P), 0), mincam(static_cast<std::size_t>(P), C);
+  for (std::int64_t k = 0; k < N; ++k) {
+    ++cnt[pt_idx[k]];
+    mincam[pt_idx[k]] = std::min(mincam[pt_idx[k]], cam_idx[k]);
+  }
+  std::vector<std::int32_t> bucket(static_cast<std::size_t>(C) + 2, 0), order(static_cast<std::size_t>(P));
+  for (int p = 0; p < P; ++p) ++bucket[mincam[p] + 1];
+  std::partial_sum(bucket.begin(), bucket.end(), bucket.begin());
+  for (int p = 0; p < P; ++p) order[bucket[mincam[p]]++] = p;
+  std::int64_t acc = 0;
+  for (int i = 0; i < P; ++i) {
+    const int p = order[i];
+    // rank r owns observations [r N / world, (r+1) N / world) of the prefix
+    rank_of_point[p] = static_cast<std::int32_t>(std::min<std::int64_t>(world - 1, (acc * world) / N));
+    acc += cnt[p];
+  }
+}
+
 }  // namespace bae
