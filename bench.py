@@ -201,6 +201,7 @@ def run_b200(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = prob.launch_count()
+    prob.phase_times(reset=True)
     dev_s, iters, pcg = 0.0, 0, 0
     reports = []
     with ClockSampler(local) as clk:
@@ -214,6 +215,7 @@ def run_b200(args):
     if dist:
         dist.barrier()
     launches = prob.launch_count() - launches0
+    phases = prob.phase_times(reset=True)
     dev_max = _max_over_ranks(dist, dev_s)
     iters_all = _sum_over_ranks(dist, iters)
     value = iters_all / dev_max  # whole-job LM iterations / s
@@ -221,6 +223,7 @@ def run_b200(args):
     # --- north-star PCG path, same protocol ---
     for _ in range(max(1, args.warmup // 2)):
         one_solve(cfg_pcg)
+    prob.phase_times(reset=True)
     pcg_dev, pcg_it, pcg_inner = 0.0, 0, 0
     pcg_steps = max(1, min(args.steps, 3))
     for _ in range(pcg_steps):
@@ -228,6 +231,7 @@ def run_b200(args):
         pcg_dev += r.device_seconds
         pcg_it += r.iterations
         pcg_inner += r.total_pcg_iters
+    pcg_phases = prob.phase_times(reset=True)
     pcg_dev = _max_over_ranks(dist, pcg_dev)
     pcg_value = _sum_over_ranks(dist, pcg_it) / pcg_dev
 
@@ -290,7 +294,8 @@ def run_b200(args):
             "final_mse": last.final_mse, "termination": last.reason.name,
             "obs_per_s_residual_jacobian": N / (ms_lin * 1e-3),
             "kernel_us": {"linearize": ms_lin * 1e3, "schur_tiles": ms_sx * 1e3, "pcg_iteration": ms_pcg * 1e3},
-            "pcg": {"lm_iters_per_s": pcg_value, "time_to_converge_s": pcg_dev / pcg_steps,
+            "phase_ms_per_solve": {k: v / args.steps for k, v in phases.items()},
+            "pcg": {"lm_iters_per_s": pcg_value, "phase_ms_per_solve": {k: v / pcg_steps for k, v in pcg_phases.items()}, "time_to_converge_s": pcg_dev / pcg_steps,
                     "pcg_iterations_per_solve": pcg_inner / pcg_steps,
                     "config": "same workload, solver=pcg (implicit-Schur PCG, block-Jacobi), pcg_tol=1e-8"},
             "roofline": {"bound": "hbm", "kernel": "k_schur_tiles (implicit Schur S*p, per PCG iteration)",

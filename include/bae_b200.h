@@ -203,6 +203,10 @@ int bae_partition_points(int32_t num_cameras, int32_t num_points, const int32_t*
 int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms);
 /* Number of kernel launches issued by this handle since creation. */
 int64_t bae_launch_count(const bae_problem* p);
+/* Device milliseconds accumulated per LM phase since the last reset:
+ * [linearize, prep, assemble (direct), factor+solve (direct), pcg, trial,
+ * commit]; reset != 0 clears after reading. */
+int bae_phase_times(bae_problem* p, double* ms7, int32_t reset);
 /* Static sizes the roofline arithmetic needs: [N, P, C, tiles, tile-camera
  * entries, max obs per tile]. */
 int bae_problem_stats(const bae_problem* p, int64_t* out6);

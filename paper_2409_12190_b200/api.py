@@ -290,6 +290,14 @@ class TracedProblem:
         _check(_lib.load().bae_time_kernel(self._h, int(kind), int(reps), ctypes.byref(ms)))
         return ms.value
 
+    PHASES = ("linearize", "prep", "assemble", "factor", "pcg", "trial", "commit")
+
+    def phase_times(self, reset: bool = False) -> dict:
+        """Device ms per LM phase accumulated since the last reset."""
+        out = np.zeros(7)
+        _check(_lib.load().bae_phase_times(self._h, ptr(out), 1 if reset else 0))
+        return dict(zip(self.PHASES, (float(v) for v in out)))
+
     def launch_count(self) -> int:
         return int(_lib.load().bae_launch_count(self._h))
 

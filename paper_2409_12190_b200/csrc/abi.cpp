@@ -245,6 +245,13 @@ int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms) {
 
 int64_t bae_launch_count(const bae_problem* p) { return p ? p->impl->launches() : 0; }
 
+int bae_phase_times(bae_problem* p, double* ms7, int32_t reset) {
+  return guarded([&] {
+    if (ms7) p->impl->phase_times(ms7);
+    if (reset) p->impl->phase_reset();
+  });
+}
+
 int bae_problem_stats(const bae_problem* p, int64_t* out6) {
   return guarded([&] {
     const bae::Plan& pl = p->impl->plan();

@@ -207,6 +207,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
 
 Problem::~Problem() {
   cudaSetDevice(opt_.device);
+  for (auto& e : ev_pool_) cudaEventDestroy(e);
   if (solver_) cusolverDnDestroy(solver_);
   if (host_info_) cudaFreeHost(host_info_);
   if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
@@ -217,6 +218,36 @@ Problem::~Problem() {
 }
 
 void Problem::activate() { ck(cudaSetDevice(opt_.device), "cudaSetDevice"); }
+
+void Problem::phase_begin(int ph) {
+  if (ev_pool_.empty()) {
+    ev_pool_.resize(512);
+    for (auto& e : ev_pool_) ck(cudaEventCreate(&e), "event");
+  }
+  if (ev_next_ + 2 > static_cast<int>(ev_pool_.size())) phase_collect();
+  ph_cur_ = ph;
+  ck(cudaEventRecord(ev_pool_[ev_next_], stream_), "event record");
+  ev_open_.push_back({ph, ev_next_});
+  ev_next_ += 2;
+}
+
+void Problem::phase_end() {
+  ck(cudaEventRecord(ev_pool_[ev_open_.back().second + 1], stream_), "event record");
+  ph_cur_ = -1;
+}
+
+// Called after a stream synchronisation: accumulates and recycles events.
+void Problem::phase_collect() {
+  if (ev_open_.empty()) return;
+  ck(cudaEventSynchronize(ev_pool_[ev_open_.back().second + 1]), "event sync");
+  for (const auto& o : ev_open_) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, ev_pool_[o.second], ev_pool_[o.second + 1]), "event elapsed");
+    phase_ms_[o.first] += ms;
+  }
+  ev_open_.clear();
+  ev_next_ = 0;
+}
 
 void Problem::sync() { ck(cudaStreamSynchronize(stream_), "kernel execution"); }
 
@@ -308,9 +339,12 @@ double Problem::evaluate(double* resid2) {
 
 void Problem::linearize() {
   reset_lm_status();
+  phase_begin(kPhLinearize);
   launch_linearize(d_, sm_, false, stream_);
+  phase_end();
   launches_ += kLaunchesLinearize;
   read_lm();
+  phase_collect();
   if (lm_host_->err_obs != INT_MAX)
     throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
 }
@@ -468,23 +502,33 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
   const long long n = 6LL * d_.C;
   if (!d_.wstore) d_.wstore = dalloc<double>(36 * static_cast<std::size_t>(plan_.N));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+  phase_begin(kPhPrep);
   launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_);
+  phase_end();
   launches_ += kLaunchesPrep;
+  phase_begin(kPhAssemble);
   ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
   launch_schur_dense(d_, stream_);
+  phase_end();
   launches_ += 1;
   ck(cudaMemcpyAsync(d_.x, d_.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_), "rhs copy");
   info.iters = 0;
+  phase_begin(kPhFactor);
   if (cusolverDnDpotrf(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), d_.schur, static_cast<int>(n),
                        potrf_work_, potrf_lwork_, dev_info_) != CUSOLVER_STATUS_SUCCESS)
     throw Error(BAE_ERR_CUDA, "potrf launch failed");
   ck(cudaMemcpyAsync(host_info_, dev_info_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H info");
   ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
   sync();
-  if (*host_info_ != 0 || pcg_host_->not_spd) return false;  // NotSpdError (cholesky.hpp:229)
+  if (*host_info_ != 0 || pcg_host_->not_spd) {  // NotSpdError (cholesky.hpp:229)
+    phase_end();
+    phase_collect();
+    return false;
+  }
   if (cusolverDnDpotrs(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), 1, d_.schur, static_cast<int>(n), d_.x,
                        static_cast<int>(n), dev_info_) != CUSOLVER_STATUS_SUCCESS)
     throw Error(BAE_ERR_CUDA, "potrs launch failed");
+  phase_end();
   info.converged = true;
   info.rel_residual = 0.0;
   return true;
@@ -496,8 +540,11 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
   const long long budget =
       cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * (d_.C + d_.P));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+  phase_begin(kPhPrep);
   launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_);
+  phase_end();
   launches_ += kLaunchesPrep;
+  phase_begin(kPhPcg);
   if (use_graph_pcg_) {
     build_pcg_graph();
     for (;;) {
@@ -517,6 +564,8 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
       if (pcg_host_->state >= kPcgDone) break;
     }
   }
+  phase_end();
+  phase_collect();
   info.iters = pcg_host_->iters;
   info.converged = pcg_host_->converged != 0;
   info.rel_residual = pcg_host_->bnorm > 0 ? (pcg_host_->converged ? pcg_host_->true_norm : pcg_host_->rnorm) /
@@ -611,13 +660,18 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
     double trial_cost = std::numeric_limits<double>::quiet_NaN();
     if (ok) {
       reset_lm_status();
+      phase_begin(kPhTrial);
       launch_trial(d_, sm_, stream_);
+      phase_end();
       launches_ += kLaunchesTrial;
       read_lm();
+      phase_collect();
       trial_cost = (lm_host_->retract_bad || lm_host_->trial_bad) ? std::numeric_limits<double>::infinity()
                                                                    : lm_host_->new_cost;
       if (trial_cost < cost) {
+        phase_begin(kPhCommit);
         launch_commit(d_, stream_);
+        phase_end();
         launches_ += kLaunchesCommit;
         cost = trial_cost;
         history.push_back(cost);
@@ -648,6 +702,7 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   }
   ck(cudaEventRecord(ev1, stream_), "event record");
   sync();
+  phase_collect();
   float dev_ms = 0.f;
   ck(cudaEventElapsedTime(&dev_ms, ev0, ev1), "event elapsed");
   cudaEventDestroy(ev0);

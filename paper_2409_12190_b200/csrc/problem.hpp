@@ -20,6 +20,19 @@ struct SolveInfo {
 
 bool plateau_stagnation(const double* h, std::size_t n, int patience, double tol);
 
+// Device-time breakdown of the LM loop by phase (CUDA events on the solver
+// stream, accumulated after each synchronising read-back).
+enum Phase : int {
+  kPhLinearize = 0,  // K1 + camera reduction
+  kPhPrep = 1,       // damping, H~pp^-1, Schur RHS / block-Jacobi
+  kPhAssemble = 2,   // dense reduced matrix (direct solver)
+  kPhFactor = 3,     // potrf + potrs (direct solver)
+  kPhPcg = 4,        // PCG iterations
+  kPhTrial = 5,      // retraction, back-substitution, trial cost
+  kPhCommit = 6,     // accept
+  kPhases = 7
+};
+
 class Problem {
  public:
   Problem(const double* poses7, int C, const double* points3, int P, const double* intr3,
@@ -62,6 +75,23 @@ class Problem {
   void build_direct();
   void build_pcg_graph();
   void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
+  void phase_begin(int ph);
+  void phase_end();
+  void phase_collect();
+
+ public:
+  void phase_times(double* out) const {
+    for (int i = 0; i < kPhases; ++i) out[i] = phase_ms_[i];
+  }
+  void phase_reset() {
+    for (double& v : phase_ms_) v = 0.0;
+  }
+
+ private:
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::pair<int, int>> ev_open_;  // (phase, index of start event) pending collection
+  int ev_next_ = 0, ph_cur_ = -1;
+  double phase_ms_[kPhases] = {0, 0, 0, 0, 0, 0, 0};
 
   bae_create_options opt_;
   Plan plan_;
