@@ -8,7 +8,11 @@ defaults, max_iterations = 50, cli.hpp:25) and the reference's default
 solver (SolverChoice::cholesky, lm.hpp:34): on the GPU that is the dense
 reduced-camera-system direct solve. value = LM iterations per second over
 the K timed solves (device time, CUDA events on the solver stream), max over
-ranks; time_to_converge_s = mean device time per solve. The north-star
+ranks; time_to_converge_s = mean device time per solve. With --gpus N > 1
+(torchrun, one process per GPU) the same problem is sharded by landmark over
+the N GPUs (NCCL allreduce of the camera-sized sums), so the
+scaling is strong: value = LM iterations of the one joint solve / the max over
+ranks of the device time. The north-star
 implicit-Schur PCG path (solver = pcg) is measured the same way and
 reported under "pcg", with the roofline of its dominant kernel.
 
@@ -161,7 +165,7 @@ def run_reference(args):
     sample = f"2 LM iterations (Cholesky, the reference default) of {args.config} per step"
     line = {"impl": "reference", "metric": "lm_iters_per_s", "value": value, "unit": "LM iter/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * 2 / value,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count)",
             "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM + Cholesky"},
             "cpu_baseline": {"value": value, "unit": "LM iter/s", "cores": threads, "kind": "port",
@@ -180,12 +184,25 @@ def run_b200(args):
     from paper_2409_12190_b200.api import LmConfig, SolverChoice
 
     C, P, N = bae.synthetic.CONFIGS[args.config]
-    # N > 1 without the NCCL build: independent replicas (one problem per rank, seed offset by rank)
-    scene = bae.synthetic.bal_shaped(C, P, N, seed=C + rank)
+    # One problem for the whole job. N > 1: landmark-sharded over the ranks
+    # -- each rank owns a point partition and its observations,
+    # cameras are replicated, camera-sized partial sums are allreduced with
+    # NCCL (per LM phase, and once per PCG iteration).
+    scene = bae.synthetic.bal_shaped(C, P, N, seed=C)
     cfg = LmConfig(max_iterations=50)  # reference defaults: solver = cholesky
     cfg_pcg = LmConfig(max_iterations=50, solver=SolverChoice.pcg)
-    prob = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local)
+
+    def fresh_id():
+        if world == 1:
+            return {}
+        obj = [bae.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return dict(rank=rank, world=world, nccl_id=obj[0])
+
+    prob = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local,
+                               **fresh_id())
     stats = prob.stats()
+    shard_max_pts = int(_max_over_ranks(dist, prob.shard()[2]))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
     def one_solve(c=None):
@@ -217,8 +234,7 @@ def run_b200(args):
     launches = prob.launch_count() - launches0
     phases = prob.phase_times(reset=True)
     dev_max = _max_over_ranks(dist, dev_s)
-    iters_all = _sum_over_ranks(dist, iters)
-    value = iters_all / dev_max  # whole-job LM iterations / s
+    value = iters / dev_max  # whole-job LM iterations / s (one jointly solved problem)
 
     # --- north-star PCG path, same protocol ---
     for _ in range(max(1, args.warmup // 2)):
@@ -233,7 +249,7 @@ def run_b200(args):
         pcg_inner += r.total_pcg_iters
     pcg_phases = prob.phase_times(reset=True)
     pcg_dev = _max_over_ranks(dist, pcg_dev)
-    pcg_value = _sum_over_ranks(dist, pcg_it) / pcg_dev
+    pcg_value = pcg_it / pcg_dev
 
     # --- kernel-level measurements (device events on the solver stream) ---
     ms_lin = prob.time_kernel(0, 20)
@@ -254,9 +270,13 @@ def run_b200(args):
     # --- end to end through the C ABI with host buffers (create + solve + read back) ---
     e2e_iters, e2e_s = 0, 0.0
     for i in range(max(1, min(args.steps, 3)) + 1):
+        ids = fresh_id()  # a new communicator per problem (outside the timed region)
+        if dist:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        p2 = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local)
+        p2 = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local,
+                                 **ids)
         st = {}
         r2 = bae.optimize(p2, scene.poses, scene.points, cfg, final_state=st)
         torch.cuda.synchronize()
@@ -266,7 +286,7 @@ def run_b200(args):
             e2e_iters += r2.iterations
             e2e_s += el
     e2e_max = _max_over_ranks(dist, e2e_s)
-    e2e_value = _sum_over_ranks(dist, e2e_iters) / e2e_max
+    e2e_value = e2e_iters / e2e_max
     h2d = 56 * C + 24 * P + 24 * C + 24 * N + 56 * C + 24 * P  # create inputs + optimize init params
     d2h = 56 * C + 24 * P
 
@@ -282,11 +302,13 @@ def run_b200(args):
         line = {
             "metric": "lm_iters_per_s", "value": value, "unit": "LM iter/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * dev_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count + rank)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count)",
             "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM with LmConfig defaults "
                                    f"(solver=cholesky, max_iterations=50) from the same initial state each step",
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"landmark-sharded over {world} GPUs (NCCL allreduce of camera vectors)"
+                                       if world > 1 else "single GPU"),
+                       "points_per_rank_max": shard_max_pts,
                        "l2": "flushed (256 MB write) between steps",
                        "tiles": stats["tiles"], "tile_camera_entries": stats["entries"]},
             "time_to_converge_s": dev_max / args.steps,

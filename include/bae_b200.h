@@ -104,10 +104,12 @@ typedef struct bae_create_options {
   int32_t rank;        /* distributed: this rank (default 0)                      */
   int32_t world;       /* distributed: number of ranks (default 1)                */
   int32_t reserved;
-  const void* nccl_id; /* distributed: 128-byte ncclUniqueId from rank 0           */
+  const void* nccl_id; /* distributed: 128-byte ncclUniqueId from rank 0 (one process per GPU) */
+  struct bae_group* group; /* distributed: in-process rank group (one host thread per rank) */
 } bae_create_options;
 
 typedef struct bae_problem bae_problem;
+typedef struct bae_group bae_group;
 
 /* ---- library -------------------------------------------------------------- */
 const char* bae_version(void);
@@ -116,8 +118,27 @@ void bae_create_options_default(bae_create_options* opt);
 /* Message / index of the last failure on this host thread (any entry point). */
 const char* bae_last_error(void);
 int64_t bae_last_error_index(void);
-/* 128-byte NCCL unique id for bae_create_options.nccl_id (rank 0 creates it). */
+/* ---- landmark-sharded problems ------------------------------
+ * A problem created with world > 1 (or with an NCCL id / rank group) is
+ * sharded by landmark: every rank passes the WHOLE problem to bae_create_ba
+ * and keeps the points bae_partition_points assigns to it, with all their
+ * observations; cameras are replicated. Per LM iteration the ranks sum the
+ * camera blocks (27 C + 2 doubles) and, per PCG iteration, the reduced-system
+ * product (6 C doubles); every rank then holds identical camera-side state and
+ * takes identical decisions, so each entry point below must be called by all
+ * ranks together (collective calls), with the same arguments' nullness.
+ * Exports that are per observation (residual vector, Jacobian, transpose
+ * plans, block diagonals, bae_solve_step) return BAE_ERR_UNSUPPORTED.
+ * Backends: NCCL (one process per GPU; rank 0 calls bae_nccl_unique_id and
+ * broadcasts the 128 bytes with its own launcher) or an in-process rank group
+ * (one host thread per rank, on one or several peer-enabled GPUs). */
+/* 128-byte NCCL unique id for bae_create_options.nccl_id (rank 0 creates it;
+ * NCCL is loaded at run time, BAE_ERR_NCCL if libnccl.so.2 is absent). */
 int bae_nccl_unique_id(void* out128);
+/* In-process rank group of `world` ranks (1..16) for bae_create_options.group;
+ * destroy it after every problem that uses it. */
+int bae_group_create(int32_t world, bae_group** out);
+void bae_group_destroy(bae_group* g);
 
 /* ---- problem (make_ba_problem, problems.hpp:87-136) ------------------------- */
 /* Validates like the reference (intrinsics count, empty observations,
@@ -207,6 +228,9 @@ int64_t bae_launch_count(const bae_problem* p);
  * [linearize, prep, assemble (direct), factor+solve (direct), pcg, trial,
  * commit]; reset != 0 clears after reading. */
 int bae_phase_times(bae_problem* p, double* ms7, int32_t reset);
+/* This handle's shard: rank, world, points and observations it owns. */
+int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32_t* local_points,
+                      int64_t* local_observations);
 /* Static sizes the roofline arithmetic needs: [N, P, C, tiles, tile-camera
  * entries, max obs per tile]. */
 int bae_problem_stats(const bae_problem* p, int64_t* out6);

@@ -3,9 +3,10 @@
 (include/bae_b200.h). See DESIGN.md."""
 from .api import (CheiralityError, DeviceError, IndexError, JacobianPair, LmConfig, LmIterationRecord, LmReport,
                   NotSpdError, NumericalBreakdownError, SolverChoice, TerminationReason, TracedProblem,
-                  UnsupportedOperationError, make_ba_problem, optimize, stop_on_plateau, write_csv)
+                  UnsupportedOperationError, RankGroup, make_ba_problem, nccl_unique_id, optimize,
+                  partition_points, stop_on_plateau, write_csv)
 from . import synthetic
 
 __all__ = ["CheiralityError", "DeviceError", "IndexError", "JacobianPair", "LmConfig", "LmIterationRecord", "LmReport",
            "NotSpdError", "NumericalBreakdownError", "SolverChoice", "TerminationReason", "TracedProblem",
-           "UnsupportedOperationError", "make_ba_problem", "optimize", "stop_on_plateau", "write_csv", "synthetic"]
+           "UnsupportedOperationError", "RankGroup", "make_ba_problem", "nccl_unique_id", "partition_points", "optimize", "stop_on_plateau", "write_csv", "synthetic"]

@@ -70,6 +70,7 @@ class CreateOptionsC(ctypes.Structure):
         ("world", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p),
+        ("group", ctypes.c_void_p),
     ]
 
 
@@ -81,6 +82,8 @@ SIGNATURES = {
     "bae_last_error": (ctypes.c_char_p, []),
     "bae_last_error_index": (ctypes.c_int64, []),
     "bae_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "bae_group_create": (ctypes.c_int, [ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_group_destroy": (None, [ctypes.c_void_p]),
     "bae_create_ba": (ctypes.c_int, [c_double_p, ctypes.c_int32, c_double_p, ctypes.c_int32, c_double_p,
                                      c_int32_p, c_int32_p, c_double_p, ctypes.c_int64,
                                      ctypes.POINTER(CreateOptionsC), ctypes.POINTER(ctypes.c_void_p)]),
@@ -111,6 +114,7 @@ SIGNATURES = {
     "bae_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
     "bae_phase_times": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int32]),
     "bae_problem_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
+    "bae_problem_shard": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p]),
 }
 
 _lib = None

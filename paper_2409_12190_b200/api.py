@@ -301,6 +301,14 @@ class TracedProblem:
     def launch_count(self) -> int:
         return int(_lib.load().bae_launch_count(self._h))
 
+    def shard(self):
+        """(rank, world, local points, local observations) of this handle."""
+        r, w, lp = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        lo = ctypes.c_int64()
+        _check(_lib.load().bae_problem_shard(self._h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(lp),
+                                             ctypes.byref(lo)))
+        return r.value, w.value, lp.value, lo.value
+
     def stats(self):
         out = np.empty(6, np.int64)
         _check(_lib.load().bae_problem_stats(self._h, ptr(out, ctypes.c_int64)))
@@ -308,13 +316,43 @@ class TracedProblem:
         return dict(zip(keys, (int(v) for v in out)))
 
 
-def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0, tile_obs: int = 0) -> TracedProblem:
+class RankGroup:
+    """In-process rank group: ``world`` ranks in one process, one host thread
+    per rank (bae_group_create). Keep it alive while its problems exist."""
+
+    def __init__(self, world: int):
+        self._h = ctypes.c_void_p()
+        _check(_lib.load().bae_group_create(int(world), ctypes.byref(self._h)))
+        self.world = int(world)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().bae_group_destroy(h)
+            self._h = None
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it and broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.load().bae_nccl_unique_id(buf))
+    return buf.raw
+
+
+def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0, tile_obs: int = 0,
+                    rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                    group: Optional[RankGroup] = None) -> TracedProblem:
     """make_ba_problem (problems.hpp:87-136) for BAL cameras.
 
     ``observations`` is ``(cam_idx, pt_idx, pixels)``. Raises ValueError for a
     wrong intrinsics count or no observations, IndexError(position) for an
     out-of-range index, CheiralityError(observation) when an initial point
-    lies on a camera plane (the reference's eager forward at construction)."""
+    lies on a camera plane (the reference's eager forward at construction).
+
+    Landmark-sharded: with ``world > 1`` and an ``nccl_id``
+    (one process per GPU) or a ``group`` (one thread per rank), every rank
+    passes the whole problem and keeps its point partition; all later calls
+    on the handle are collective."""
     cam_idx, pt_idx, pixels = observations
     p7 = _f64(poses).reshape(-1, 7)
     p3 = _f64(points).reshape(-1, 3)
@@ -331,6 +369,14 @@ def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0,
     lib.bae_create_options_default(ctypes.byref(opt))
     opt.device = device
     opt.tile_obs = tile_obs
+    opt.rank = rank
+    opt.world = world
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        opt.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    if group is not None:
+        opt.group = group._h
     h = ctypes.c_void_p()
     _check(lib.bae_create_ba(ptr(p7), C, ptr(p3), P, ptr(k3), ptr(ci, ctypes.c_int32), ptr(pi, ctypes.c_int32),
                              ptr(px), N, ctypes.byref(opt), ctypes.byref(h)))

@@ -74,10 +74,19 @@ int64_t bae_last_error_index(void) { return g_index; }
 
 int bae_nccl_unique_id(void* out128) {
   return guarded([&] {
-    (void)out128;
-    throw bae::Error(BAE_ERR_UNSUPPORTED, "built without NCCL");
+    if (!out128) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null output");
+    bae::nccl_unique_id(out128);
   });
 }
+
+int bae_group_create(int32_t world, bae_group** out) {
+  return guarded([&] {
+    if (!out) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null output handle");
+    *out = bae::group_create(world);
+  });
+}
+
+void bae_group_destroy(bae_group* g) { bae::group_destroy(g); }
 
 int bae_create_ba(const double* poses7, int32_t C, const double* points3, int32_t P, const double* intr3,
                   const int32_t* cam_idx, const int32_t* pt_idx, const double* px2, int64_t N,
@@ -92,7 +101,7 @@ int bae_create_ba(const double* poses7, int32_t C, const double* points3, int32_
     bae_create_options o;
     bae_create_options_default(&o);
     if (opts) o = *opts;
-    if (o.world != 1) throw bae::Error(BAE_ERR_UNSUPPORTED, "multi-rank problems need the NCCL build");
+    if (o.group && o.nccl_id) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "pass an NCCL id or a rank group, not both");
     auto h = std::make_unique<bae_problem>();
     h->impl = std::make_unique<bae::Problem>(poses7, C, points3, P, intr3, cam_idx, pt_idx, px2, N, o);
     *out = h.release();
@@ -120,6 +129,7 @@ int bae_evaluate(bae_problem* p, double* residuals2, double* cost) {
 int bae_jacobian(bae_problem* p, double* jpose, double* jpoint, int64_t* prp, int32_t* pcol, int64_t* lrp,
                  int32_t* lcol) {
   return guarded([&] {
+    if (p->impl->distributed()) throw bae::Error(BAE_ERR_UNSUPPORTED, "the Jacobian export needs a single-rank problem");
     if (jpose || jpoint) p->impl->jacobian(jpose, jpoint, nullptr);
     const bae::Plan& pl = p->impl->plan();
     const std::int64_t N = pl.N;
@@ -142,6 +152,8 @@ int bae_jacobian(bae_problem* p, double* jpose, double* jpoint, int64_t* prp, in
 
 int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t* col_idx, int64_t* src_block) {
   return guarded([&] {
+    if (p->impl->distributed())
+      throw bae::Error(BAE_ERR_UNSUPPORTED, "the transpose plans need a single-rank problem");
     const bae::Plan& pl = p->impl->plan();
     if (which == 0) {
       // camera segments: entries of each camera, observations re-listed in id order
@@ -261,6 +273,16 @@ int bae_problem_stats(const bae_problem* p, int64_t* out6) {
     out6[3] = pl.T;
     out6[4] = pl.E;
     out6[5] = pl.max_tile_obs;
+  });
+}
+
+int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32_t* local_points,
+                      int64_t* local_observations) {
+  return guarded([&] {
+    if (rank) *rank = p->impl->rank();
+    if (world) *world = p->impl->world();
+    if (local_points) *local_points = p->impl->local_points();
+    if (local_observations) *local_observations = p->impl->local_obs();
   });
 }
 

@@ -78,6 +78,11 @@ struct Dev {
   double* y;
   double* partial;    // E * 27
   double* tile_red;   // T * 2
+  // Sharded runs: per-rank camera-sized partial sums that the
+  // communicator sums in place between a tile pass and its camera pass;
+  // null on a single rank (the camera passes then read the entries directly).
+  double* cred;
+  double* cam_dot;    // 2C per-camera scalars for fixed-order totals
   double* block_red;  // grid-reduction scratch
   unsigned* tickets;  // grid-reduction tickets
   PcgDev* pcg;

@@ -424,41 +424,131 @@ __device__ __forceinline__ void warp_entry_sum(const Dev& d, int c, double (&acc
   for (int j = 0; j < W; ++j) acc[j] = warp_sum(acc[j]);
 }
 
-__global__ void k_cam_linearize(Dev d) {
-  __shared__ double red[32];
-  const int c = blockIdx.x * kWarpsPerCamBlock + (threadIdx.x >> 5);
-  const int lane = lane_id();
-  double gsq = 0.0;
-  if (c < d.C) {
-    double acc[27];
-    warp_entry_sum<27>(d, c, acc);
-    if (lane == 0) {
-#pragma unroll
-      for (int j = 0; j < 21; ++j) d.hcc[(long long)c * 21 + j] = acc[j];
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        d.gc[(long long)c * 6 + j] = acc[21 + j];
-        gsq += acc[21 + j] * acc[21 + j];
-      }
+// Block-wide sum of camera c's entries (W doubles each), fixed order. Entry
+// slot s = warp * G + lane / W (G = 32 / W slots per warp, S slots per
+// block) takes the camera's entries s, s + S, s + 2S, ... with four loads in
+// flight per lane and coalesced W-double rows; the S slot sums are then added
+// in slot order. out[0..W) (shared) is valid after the call.
+template <int W, int NT>
+__device__ __forceinline__ void block_entry_sum(const Dev& d, int c, double* red, double* out) {
+  constexpr int G = 32 / W, S = G * (NT / 32);
+  const int lane = lane_id(), warp = threadIdx.x >> 5;
+  const int slot = warp * G + lane / W, j = lane % W;
+  const bool active = lane < G * W;
+  const int e = d.cam_ent_ptr[c + 1];
+  double acc = 0.0;
+  if (active) {
+    int q = d.cam_ent_ptr[c] + slot;
+    for (; q + 3 * S < e; q += 4 * S) {
+      const int e0 = d.cam_ent[q], e1 = d.cam_ent[q + S], e2 = d.cam_ent[q + 2 * S], e3 = d.cam_ent[q + 3 * S];
+      const double v0 = d.partial[(long long)e0 * W + j], v1 = d.partial[(long long)e1 * W + j];
+      const double v2 = d.partial[(long long)e2 * W + j], v3 = d.partial[(long long)e3 * W + j];
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
     }
+    for (; q < e; q += S) acc += d.partial[(long long)d.cam_ent[q] * W + j];
+    red[slot * W + j] = acc;
   }
-  const double bs = block_sum(gsq, red);
-  const double vals[1] = {bs};
-  double tot[1];
-  if (grid_reduce<1>(vals, d.block_red, d.tickets + 0, tot)) {
-    // tile totals in tile order
-    double a = 0.0, b = 0.0;
+  __syncthreads();
+  if (threadIdx.x < W) {
+    double t = 0.0;
+    for (int k = 0; k < S; ++k) t += red[k * W + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
+// Camera c's W-vector: the rank-summed d.cred on sharded runs, else the
+// block entry sum.
+template <int W, int NT>
+__device__ __forceinline__ void cam_block_acc(const Dev& d, int c, double* red, double* out) {
+  if (d.cred) {
+    if (threadIdx.x < W) out[threadIdx.x] = d.cred[(long long)c * W + threadIdx.x];
+    __syncthreads();
+  } else {
+    block_entry_sum<W, NT>(d, c, red, out);
+  }
+}
+
+// Sharded runs: this rank's per-camera entry sums into d.cred (block per
+// camera), plus trailing scalars computed by one extra block:
+//   extra 1 (linearisation): [sum r^2, sum |g_p|^2] over this rank's tiles
+//   extra 2 (prep)          : [1 if a local point block was not SPD]
+// The W = 6 instance (PCG product) is skipped once the solve has finished,
+// like the other kernels of a PCG chunk.
+template <int W, int NT>
+__global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra) {
+  __shared__ double red[(32 / W) * (NT / 32) * W];
+  __shared__ double acc[W];
+  if (W == 6 && d.pcg->state >= kPcgDone) return;
+  if (blockIdx.x == gridDim.x - 1) {
+    if (extra == 1) {
+      double a = 0.0, b = 0.0;
+      for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) {
+        a += d.tile_red[tt * 2];
+        b += d.tile_red[tt * 2 + 1];
+      }
+      a = block_sum(a, red);
+      __syncthreads();
+      b = block_sum(b, red);
+      if (threadIdx.x == 0) {
+        d.cred[(long long)W * d.C] = a;
+        d.cred[(long long)W * d.C + 1] = b;
+      }
+    } else if (extra == 2 && threadIdx.x == 0) {
+      d.cred[(long long)W * d.C] = d.pcg->not_spd ? 1.0 : 0.0;
+    }
+    return;
+  }
+  const int c = blockIdx.x;
+  block_entry_sum<W, NT>(d, c, red, acc);
+  if (threadIdx.x < W) d.cred[(long long)c * W + threadIdx.x] = acc[threadIdx.x];
+}
+
+// Camera side of the linearisation (block per camera): H_cc (21) and g_c (6)
+// from the camera's entries; |g_c|^2 per camera for the totals.
+__global__ void __launch_bounds__(256) k_cam_linearize(Dev d) {
+  __shared__ double red[8 * 27];
+  __shared__ double acc[27];
+  const int c = blockIdx.x;
+  cam_block_acc<27, 256>(d, c, red, acc);
+  const int t = threadIdx.x;
+  if (t < 21) d.hcc[(long long)c * 21 + t] = acc[t];
+  else if (t < 27) d.gc[(long long)c * 6 + (t - 21)] = acc[t];
+  if (t == 0) {
+    double gsq = 0.0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) gsq += acc[21 + j] * acc[21 + j];
+    d.cam_dot[c] = gsq;
+  }
+}
+
+// Cost and ||J^T r||^2 of the linearisation (one block, fixed order): tile
+// totals in tile order (sharded: already summed over ranks) + camera |g_c|^2.
+__global__ void __launch_bounds__(1024) k_lin_totals(Dev d) {
+  __shared__ double red[32];
+  double a = 0.0, b = 0.0, g = 0.0;
+  if (!d.cred) {
     for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) {
       a += d.tile_red[tt * 2];
       b += d.tile_red[tt * 2 + 1];
     }
-    a = block_sum(a, red);
-    __syncthreads();
-    b = block_sum(b, red);
-    if (threadIdx.x == 0) {
-      d.lm->cost = a;
-      d.lm->grad_sq = b + tot[0];
+  }
+  for (int c = threadIdx.x; c < d.C; c += blockDim.x) g += d.cam_dot[c];
+  a = block_sum(a, red);
+  __syncthreads();
+  b = block_sum(b, red);
+  __syncthreads();
+  g = block_sum(g, red);
+  if (threadIdx.x == 0) {
+    if (d.cred) {
+      a = d.cred[27LL * d.C];
+      b = d.cred[27LL * d.C + 1];
     }
+    d.lm->cost = a;
+    d.lm->grad_sq = b + g;
   }
 }
 
@@ -468,11 +558,30 @@ __global__ void k_sum_tiles(Dev d, int trial) {
   double a = 0.0;
   for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) a += d.tile_red[tt * 2];
   a = block_sum(a, red);
+  if (d.cred) {  // sharded: [local cost, local trial failure] go to the cross-rank sum
+    if (threadIdx.x == 0) {
+      d.cred[0] = a;
+      d.cred[1] = (trial && d.lm->trial_bad) ? 1.0 : 0.0;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     if (trial)
       d.lm->new_cost = (d.lm->trial_bad || d.lm->retract_bad || !isfinite(a)) ? INFINITY : a;
     else
       d.lm->cost = a;
+  }
+}
+
+// Sharded runs: the cost (or trial cost) from the rank-summed [cost, failure].
+__global__ void k_finish_cost(Dev d, int trial) {
+  const double a = d.cred[0];
+  const bool bad = d.cred[1] > 0.0;
+  if (trial) {
+    d.lm->trial_bad = bad ? 1 : 0;
+    d.lm->new_cost = (bad || d.lm->retract_bad || !isfinite(a)) ? INFINITY : a;
+  } else {
+    d.lm->cost = a;
   }
 }
 
@@ -575,85 +684,90 @@ __global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, d
   BAE_TILE_DISPATCH(prep_tile, d, g, smem, slice, lambda, clo, chi);
 }
 
-// Camera side of the prep: damped H~_cc, block-Jacobi inverse of S_cc
-// (falls back to H~_cc^-1 when the 6x6 Schur block is not numerically SPD),
-// Schur RHS, and PCG initialisation x = 0, r = b, z = M^-1 r.
-__global__ void k_cam_prep(Dev d, double lambda, double clo, double chi, double tol, long long budget) {
-  __shared__ double red[32];
-  const int c = blockIdx.x * kWarpsPerCamBlock + (threadIdx.x >> 5);
-  const int lane = lane_id();
+// Camera side of the prep (block per camera): damped H~_cc, block-Jacobi
+// inverse of S_cc (falls back to H~_cc^-1 when the 6x6 Schur block is not
+// numerically SPD), Schur RHS, and PCG initialisation x = 0, r = b,
+// z = M^-1 r; per-camera r.r and r.z for the totals.
+__global__ void __launch_bounds__(256) k_cam_prep(Dev d, double lambda, double clo, double chi) {
+  __shared__ double red[8 * 27];
+  __shared__ double acc[27];
+  const int c = blockIdx.x;
+  cam_block_acc<27, 256>(d, c, red, acc);
+  if (threadIdx.x != 0) return;
+  double hd[21], s[21], m[36], b[6];
   double rr = 0.0, rz = 0.0;
-  int fail = 0;
-  if (c < d.C) {
-    double acc[27];
-    warp_entry_sum<27>(d, c, acc);
-    if (lane == 0) {
-      double hd[21], s[21], m[36], b[6];
 #pragma unroll
-      for (int j = 0; j < 21; ++j) hd[j] = d.hcc[(long long)c * 21 + j];
+  for (int j = 0; j < 21; ++j) hd[j] = d.hcc[(long long)c * 21 + j];
 #pragma unroll
-      for (int a = 0; a < 6; ++a) hd[sym6(a, a)] = damp_diag(hd[sym6(a, a)], lambda, clo, chi);
+  for (int a = 0; a < 6; ++a) hd[sym6(a, a)] = damp_diag(hd[sym6(a, a)], lambda, clo, chi);
 #pragma unroll
-      for (int j = 0; j < 21; ++j) {
-        d.hccd[(long long)c * 21 + j] = hd[j];
-        s[j] = hd[j] - acc[j];
-      }
-      if (!spd_inverse<6>(s, m)) {
-        if (!spd_inverse<6>(hd, m)) {
-          fail = 1;
+  for (int j = 0; j < 21; ++j) {
+    d.hccd[(long long)c * 21 + j] = hd[j];
+    s[j] = hd[j] - acc[j];
+  }
+  if (!spd_inverse<6>(s, m)) {
+    if (!spd_inverse<6>(hd, m)) {
+      atomicExch(&d.pcg->not_spd, 1);
 #pragma unroll
-          for (int j = 0; j < 36; ++j) m[j] = 0.0;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 36; ++j) d.minv[(long long)c * 36 + j] = m[j];
-#pragma unroll
-      for (int a = 0; a < 6; ++a) b[a] = -d.gc[(long long)c * 6 + a] + acc[21 + a];
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        double zz = 0.0;
-#pragma unroll
-        for (int j = 0; j < 6; ++j) zz += m[a * 6 + j] * b[j];
-        const long long o = (long long)c * 6 + a;
-        d.rhs[o] = b[a];
-        d.x[o] = 0.0;
-        d.r[o] = b[a];
-        d.z[o] = zz;
-        d.p[o] = 0.0;
-        rr += b[a] * b[a];
-        rz += b[a] * zz;
-      }
+      for (int j = 0; j < 36; ++j) m[j] = 0.0;
     }
   }
-  if (fail) atomicExch(&d.pcg->not_spd, 1);
-  const double v0 = block_sum(rr, red);
+#pragma unroll
+  for (int j = 0; j < 36; ++j) d.minv[(long long)c * 36 + j] = m[j];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) b[a] = -d.gc[(long long)c * 6 + a] + acc[21 + a];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    double zz = 0.0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) zz += m[a * 6 + j] * b[j];
+    const long long o = (long long)c * 6 + a;
+    d.rhs[o] = b[a];
+    d.x[o] = 0.0;
+    d.r[o] = b[a];
+    d.z[o] = zz;
+    d.p[o] = 0.0;
+    rr += b[a] * b[a];
+    rz += b[a] * zz;
+  }
+  d.cam_dot[2LL * c] = rr;
+  d.cam_dot[2LL * c + 1] = rz;
+}
+
+// PCG start state from the prep totals (one block, fixed order).
+__global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long long budget) {
+  __shared__ double red[32];
+  double rr = 0.0, rz = 0.0;
+  for (int c = threadIdx.x; c < d.C; c += blockDim.x) {
+    rr += d.cam_dot[2LL * c];
+    rz += d.cam_dot[2LL * c + 1];
+  }
+  rr = block_sum(rr, red);
   __syncthreads();
-  const double v1 = block_sum(rz, red);
-  const double vals[2] = {v0, v1};
-  double tot[2];
-  if (grid_reduce<2>(vals, d.block_red, d.tickets + 1, tot) && threadIdx.x == 0) {
-    PcgDev& s = *d.pcg;
-    // Tolerance semantics of the reference (pcg.hpp:85): ||r|| <= tol ||b|| with
-    // b the FULL right-hand side -J^T r. Back-substitution satisfies the point
-    // rows exactly, so the full residual equals the reduced one and the
-    // reference's test is applied unchanged to the reduced recurrence.
-    s.bnorm = sqrt(d.lm->grad_sq);
-    s.rz = tot[1];
-    s.tol = tol;
-    s.iters = 0;
-    s.budget = budget;
-    s.dir = kDirZ;
-    s.beta = 0.0;
-    s.converged = 0;
-    s.true_norm = sqrt(tot[0]);
-    if (s.not_spd) {
-      s.state = kPcgBreakdown;
-    } else if (s.bnorm == 0.0 || tot[0] == 0.0) {  // x = 0 solves the system exactly
-      s.state = kPcgDone;
-      s.converged = 1;
-    } else {
-      s.state = kPcgIter;
-    }
+  rz = block_sum(rz, red);
+  if (threadIdx.x != 0) return;
+  PcgDev& s = *d.pcg;
+  // Tolerance semantics of the reference (pcg.hpp:85): ||r|| <= tol ||b|| with
+  // b the FULL right-hand side -J^T r. Back-substitution satisfies the point
+  // rows exactly, so the full residual equals the reduced one and the
+  // reference's test is applied unchanged to the reduced recurrence.
+  s.bnorm = sqrt(d.lm->grad_sq);
+  s.rz = rz;
+  s.tol = tol;
+  s.iters = 0;
+  s.budget = budget;
+  s.dir = kDirZ;
+  s.beta = 0.0;
+  s.converged = 0;
+  s.true_norm = sqrt(rr);
+  if (d.cred && d.cred[27LL * d.C] > 0.0) s.not_spd = 1;  // a point block failed on some rank
+  if (s.not_spd) {
+    s.state = kPcgBreakdown;
+  } else if (s.bnorm == 0.0 || rr == 0.0) {  // x = 0 solves the system exactly
+    s.state = kPcgDone;
+    s.converged = 1;
+  } else {
+    s.state = kPcgIter;
   }
 }
 
@@ -697,10 +811,19 @@ __global__ void k_schur_dense(Dev d) {
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
         double v = -acc[r * 6 + c];
-        if (cc.x == cc.y) v += h[sym6(r, c)];
+        if (cc.x == cc.y && !d.cred) v += h[sym6(r, c)];  // sharded: added after the rank sum
         d.schur[(6LL * cc.y + c) * n + 6LL * cc.x + r] = v;
       }
   }
+}
+
+// Sharded direct solve: the damped camera blocks join the rank-summed S.
+__global__ void k_add_hccd(Dev d) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= 36LL * d.C) return;
+  const int c = (int)(idx / 36), r = (int)(idx % 36) / 6, col = (int)(idx % 6);
+  const long long n = 6LL * d.C;
+  d.schur[(6LL * c + col) * n + 6LL * c + r] += d.hccd[(long long)c * 21 + sym6(r, col)];
 }
 
 // ---------------------------------------------------------------------------
@@ -1105,8 +1228,8 @@ __device__ __forceinline__ void sx_pipelined(const Dev& d, const PcgDev& st, cha
   }
 }
 
-// K5 camera part for one camera (warp): y_c = H~_cc v_c - sum partial,
-// p <- v. Returns v.y (lane 0).
+// K5 camera part for one camera (warp; persistent single-rank PCG):
+// y_c = H~_cc v_c - sum partial, p <- v. Returns v.y (lane 0).
 __device__ __forceinline__ double sx_camera(const Dev& d, const PcgDev& st, int c) {
   double acc[6];
   warp_entry_sum<6>(d, c, acc);
@@ -1211,39 +1334,63 @@ __global__ void __launch_bounds__(256, 2) k_schur_tiles(Dev d, int slice) {
   sx_all_tiles(d, st, smem, blockIdx.x * wpb + (threadIdx.x >> 5), gridDim.x * wpb, ps);
 }
 
-__global__ void k_schur_cams(Dev d) {
-  __shared__ double red[32];
+// K5 camera part (block per camera): y_c = H~_cc v_c - sum of the camera's
+// entry partials (rank-summed on sharded runs), p <- v, and v.y per camera.
+__global__ void __launch_bounds__(128) k_schur_cams(Dev d) {
+  __shared__ double red[20 * 6];
+  __shared__ double acc[6];
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
-  const int c = blockIdx.x * kWarpsPerCamBlock + (threadIdx.x >> 5);
-  const double pap = c < d.C ? sx_camera(d, st, c) : 0.0;
-  const double bs = block_sum(pap, red);
-  const double vals[1] = {bs};
-  double tot[1];
-  if (grid_reduce<1>(vals, d.block_red, d.tickets + 2, tot) && threadIdx.x == 0) {
-    if (st.dir != kDirX) {
-      const double alpha = st.rz / tot[0];
-      d.pcg->alpha = alpha;
-      if (!isfinite(alpha)) d.pcg->state = kPcgBreakdown;  // pcg.hpp:77
-    }
+  const int c = blockIdx.x;
+  cam_block_acc<6, 128>(d, c, red, acc);
+  if (threadIdx.x != 0) return;
+  double v[6];
+  dir_vector(st, d, c, v);
+  const double* h = d.hccd + (long long)c * 21;
+  double pap = 0.0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    double hv = 0.0;
+#pragma unroll
+    for (int b = 0; b < 6; ++b) hv += h[sym6(a, b)] * v[b];
+    const double yy = hv - acc[a];
+    d.y[(long long)c * 6 + a] = yy;
+    if (st.dir != kDirX) d.p[(long long)c * 6 + a] = v[a];
+    pap += v[a] * yy;
   }
+  d.cam_dot[c] = pap;
 }
 
-__global__ void k_pcg_update(Dev d) {
+// PCG step on the camera vectors (one block, fixed-order sums): alpha from
+// p.Sp (pcg.hpp:73-77), x/r/z update and the recurrence / true-residual
+// decision (pcg.hpp:78-129).
+__global__ void __launch_bounds__(1024) k_pcg_update(Dev d) {
   __shared__ double red[32];
+  __shared__ double s_pap;
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  double rr = 0.0, rz = 0.0;
-  if (c < d.C) pcg_camera_update(d, st, st.alpha, c, rr, rz);
-  const double v0 = block_sum(rr, red);
+  double pap = 0.0;
+  for (int c = threadIdx.x; c < d.C; c += blockDim.x) pap += d.cam_dot[c];
+  pap = block_sum(pap, red);
+  if (threadIdx.x == 0) s_pap = pap;
   __syncthreads();
-  const double v1 = block_sum(rz, red);
-  const double vals[2] = {v0, v1};
-  double tot[2];
-  if (grid_reduce<2>(vals, d.block_red, d.tickets + 3, tot) && threadIdx.x == 0) {
+  double alpha = 0.0;
+  if (st.dir != kDirX) {
+    alpha = st.rz / s_pap;
+    if (!isfinite(alpha)) {  // pcg.hpp:77
+      if (threadIdx.x == 0) d.pcg->state = kPcgBreakdown;
+      return;
+    }
+  }
+  double rr = 0.0, rz = 0.0;
+  for (int c = threadIdx.x; c < d.C; c += blockDim.x) pcg_camera_update(d, st, alpha, c, rr, rz);
+  rr = block_sum(rr, red);
+  __syncthreads();
+  rz = block_sum(rz, red);
+  if (threadIdx.x == 0) {
     PcgDev o = st;
-    pcg_decide(o, tot[0], tot[1]);
+    o.alpha = alpha;
+    pcg_decide(o, rr, rz);
     *d.pcg = o;
   }
 }
@@ -1495,28 +1642,58 @@ static inline int elt_blocks(long long n, int bs) { return (int)((n + bs - 1) / 
 static inline int tile_blocks(int T, const TileLaunch& tl) { return (T + tl.wpb - 1) / tl.wpb; }
 static int schur_grid(const Dev& d, const SmemSizes& sm);
 
-void launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
+int launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
   k_camrec<<<elt_blocks(d.C, 128), 128, 0, s>>>(trial ? d.pose_t : d.pose, d.intr, trial ? d.camrec_t : d.camrec, d.C);
+  return 1;
 }
-void launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s) {
+// Sharded runs: this rank's camera partials -> cross-rank sum in d.cred.
+static int reduce_cams27(const Dev& d, int extra, int nextra, Comm* comm, cudaStream_t s) {
+  k_cam_entry_sums<27, 256><<<d.C + 1, 256, 0, s>>>(d, extra);
+  comm->allreduce_sum(d.cred, 27 * static_cast<std::size_t>(d.C) + nextra, s);
+  return 1;
+}
+int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm) {
+  int n = 3;
   k_linearize<<<tile_blocks(d.T, sm.lin), 32 * sm.lin.wpb, sm.lin.wpb * sm.lin.slice, s>>>(d, sm.lin.slice,
                                                                                          write_jac ? 1 : 0);
-  k_cam_linearize<<<cam_blocks(d.C), 32 * kWarpsPerCamBlock, 0, s>>>(d);
+  if (comm) {
+    n += reduce_cams27(d, 1, 2, comm, s);
+    comm->allreduce_min(&d.lm->err_obs, 1, s);
+  }
+  k_cam_linearize<<<d.C, 256, 0, s>>>(d);
+  k_lin_totals<<<1, 1024, 0, s>>>(d);
+  return n;
 }
-void launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
+int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   k_cost<<<tile_blocks(d.T, sm.cost), 32 * sm.cost.wpb, sm.cost.wpb * sm.cost.slice, s>>>(d, sm.cost.slice);
   k_sum_tiles<<<1, 1024, 0, s>>>(d, 0);
+  if (!comm) return 2;
+  comm->allreduce_sum(d.cred, 2, s);
+  comm->allreduce_min(&d.lm->err_obs, 1, s);
+  k_finish_cost<<<1, 1, 0, s>>>(d, 0);
+  return 3;
 }
-void launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
-                 long long budget, cudaStream_t s) {
+int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
+                long long budget, cudaStream_t s, Comm* comm) {
+  int n = 3;
   k_prep<<<tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s>>>(d, sm.prep.slice, lambda,
                                                                                          clo, chi);
-  k_cam_prep<<<cam_blocks(d.C), 32 * kWarpsPerCamBlock, 0, s>>>(d, lambda, clo, chi, tol, budget);
+  if (comm) n += reduce_cams27(d, 2, 1, comm, s);
+  k_cam_prep<<<d.C, 256, 0, s>>>(d, lambda, clo, chi);
+  k_prep_totals<<<1, 1024, 0, s>>>(d, tol, budget);
+  return n;
 }
-void launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
+int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
+  int n = 3;
   k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
-  k_schur_cams<<<cam_blocks(d.C), 32 * kWarpsPerCamBlock, 0, s>>>(d);
-  k_pcg_update<<<elt_blocks(d.C, 128), 128, 0, s>>>(d);
+  if (comm) {  // the one exchange per PCG iteration: 6C doubles
+    k_cam_entry_sums<6, 128><<<d.C + 1, 128, 0, s>>>(d, 0);
+    comm->allreduce_sum(d.cred, 6 * static_cast<std::size_t>(d.C), s);
+    ++n;
+  }
+  k_schur_cams<<<d.C, 128, 0, s>>>(d);
+  k_pcg_update<<<1, 1024, 0, s>>>(d);
+  return n;
 }
 static int resident_grid(const void* fn, int threads, int smem) {
   int per_sm = 0, dev = 0, nsm = 0;
@@ -1542,21 +1719,38 @@ cudaError_t launch_pcg_persistent(const Dev& d, const SmemSizes& sm, int grid, l
   return cudaLaunchCooperativeKernel((void*)k_pcg_persistent, dim3(grid), dim3(32 * sm.schur.wpb), args,
                                      sm.schur.wpb * sm.schur.slice, s);
 }
-void launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
+int launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
   k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
+  return 1;
 }
-void launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
+int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   k_cam_retract<<<elt_blocks(d.C, 128), 128, 0, s>>>(d);
   k_backsub_trial<<<tile_blocks(d.T, sm.trial), 32 * sm.trial.wpb, sm.trial.wpb * sm.trial.slice, s>>>(
       d, sm.trial.slice);
   k_sum_tiles<<<1, 1024, 0, s>>>(d, 1);
+  if (!comm) return 3;
+  comm->allreduce_sum(d.cred, 2, s);
+  k_finish_cost<<<1, 1, 0, s>>>(d, 1);
+  return 4;
 }
-void launch_schur_dense(const Dev& d, cudaStream_t s) {
-  if (d.nblk > 0) k_schur_dense<<<(d.nblk + 7) / 8, 256, 0, s>>>(d);
+int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
+  int n = 0;
+  if (d.nblk > 0) {
+    k_schur_dense<<<(d.nblk + 7) / 8, 256, 0, s>>>(d);
+    ++n;
+  }
+  if (comm) {  // the direct solve's exchange: the dense reduced matrix, once per LM iteration
+    const std::size_t nn = 6 * static_cast<std::size_t>(d.C);
+    comm->allreduce_sum(d.schur, nn * nn, s);
+    k_add_hccd<<<elt_blocks(36LL * d.C, 256), 256, 0, s>>>(d);
+    ++n;
+  }
+  return n;
 }
-void launch_commit(const Dev& d, cudaStream_t s) {
+int launch_commit(const Dev& d, cudaStream_t s) {
   const long long n = std::max<long long>((long long)d.P * 3, (long long)d.C * kCamRec);
   k_commit<<<elt_blocks(n, 256), 256, 0, s>>>(d);
+  return 1;
 }
 
 }  // namespace bae

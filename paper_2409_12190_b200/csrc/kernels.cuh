@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include "comm.hpp"
 #include "device.cuh"
 
 namespace bae {
@@ -21,22 +22,21 @@ struct SmemSizes {
 long long tile_ws_bytes(int kind, int ncam, int npts, int nobs);
 void set_smem_limits(int max_bytes);
 
-void launch_camrec(const Dev& d, bool trial, cudaStream_t s);
-void launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s);
-void launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s);
-void launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
-                 long long budget, cudaStream_t s);
-void launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s);
-// Cooperative persistent PCG (whole solve, grid barriers between phases).
+// Launch wrappers return the number of kernels they launched (the bench's
+// gpu_launches). `comm` is null on a single rank; on sharded runs the
+// wrapper inserts the cross-rank sums between the tile and camera passes.
+int launch_camrec(const Dev& d, bool trial, cudaStream_t s);
+int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm);
+int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
+int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
+                long long budget, cudaStream_t s, Comm* comm);
+int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
+// Cooperative persistent PCG (whole solve, grid barriers between phases; single rank only).
 int pcg_persistent_grid(const Dev& d, const SmemSizes& sm);
 cudaError_t launch_pcg_persistent(const Dev& d, const SmemSizes& sm, int grid, long long max_iters, cudaStream_t s);
-void launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s);
-void launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s);
-void launch_commit(const Dev& d, cudaStream_t s);
-void launch_schur_dense(const Dev& d, cudaStream_t s);
-
-// kernel launches issued per wrapper (for the bench's gpu_launches count)
-constexpr int kLaunchesLinearize = 2, kLaunchesCost = 2, kLaunchesPrep = 2, kLaunchesPcgIter = 3,
-              kLaunchesTrial = 3, kLaunchesCommit = 1, kLaunchesCamrec = 1;
+int launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s);
+int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
+int launch_commit(const Dev& d, cudaStream_t s);
+int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm);
 
 }  // namespace bae

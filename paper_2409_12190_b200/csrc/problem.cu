@@ -57,14 +57,77 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     throw Error(BAE_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
   if (opt.device < 0 || opt.device >= ndev) throw Error(BAE_ERR_INVALID_ARGUMENT, "bad device ordinal");
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
+  P_global_ = P;
+  N_global_ = N;
+
+  // Sharded run: every rank receives the whole problem, as the
+  // reference's make_ba_problem does, and keeps the points of its partition
+  // (bae_partition_points: contiguous ranges of the camera-sorted point order,
+  // balanced by observation count) with all their observations, in ascending
+  // observation order. Cameras are replicated.
+  const bool dist = opt.world > 1 || opt.nccl_id != nullptr || opt.group != nullptr;
+  std::vector<std::int32_t> lcam, lpt, gobs;
+  std::vector<double> lpx;
+  const std::int32_t* use_cam = cam_idx;
+  const std::int32_t* use_pt = pt_idx;
+  const double* use_px = px2;
+  int use_P = P;
+  std::int64_t use_N = N;
+  if (dist) {
+    if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world)
+      throw Error(BAE_ERR_INVALID_ARGUMENT, "sharded problem: rank must be in [0, world)");
+    if (!opt.group && !opt.nccl_id)
+      throw Error(BAE_ERR_INVALID_ARGUMENT, "sharded problem: needs an NCCL unique id or a rank group");
+    rank_of_point_.resize(static_cast<std::size_t>(P));
+    partition_points(C, P, cam_idx, pt_idx, N, opt.world, rank_of_point_.data());
+    std::vector<std::int32_t> owned(static_cast<std::size_t>(opt.world), 0);
+    for (int p = 0; p < P; ++p) ++owned[rank_of_point_[p]];
+    for (int r = 0; r < opt.world; ++r)
+      if (owned[r] == 0) throw Error(BAE_ERR_UNSUPPORTED, "sharded problem: more ranks than point partitions");
+    std::vector<std::int32_t> lp_of(static_cast<std::size_t>(P), -1);
+    for (int p = 0; p < P; ++p)
+      if (rank_of_point_[p] == opt.rank) {
+        lp_of[p] = static_cast<std::int32_t>(local_pts_.size());
+        local_pts_.push_back(p);
+      }
+    for (std::int64_t k = 0; k < N; ++k) {
+      const int lp = lp_of[pt_idx[k]];
+      if (lp < 0) continue;
+      lcam.push_back(cam_idx[k]);
+      lpt.push_back(lp);
+      lpx.push_back(px2[2 * k]);
+      lpx.push_back(px2[2 * k + 1]);
+      gobs.push_back(static_cast<std::int32_t>(k));
+    }
+    use_cam = lcam.data();
+    use_pt = lpt.data();
+    use_px = lpx.data();
+    use_P = static_cast<int>(local_pts_.size());
+    use_N = static_cast<std::int64_t>(gobs.size());
+    comm_ = opt.group ? make_group_comm(opt.group, opt.rank, opt.device)
+                      : make_nccl_comm(opt.nccl_id, opt.rank, opt.world, opt.device);
+  }
+  ck(cudaSetDevice(opt.device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : 64;
   if (const char* t = std::getenv("BAE_TILE_OBS")) tile_obs = std::max(8, std::atoi(t));
   int tile_cams = 32;
   if (const char* t = std::getenv("BAE_TILE_CAMS")) tile_cams = std::max(1, std::atoi(t));
   if (const char* m = std::getenv("BAE_PCG_MODE")) use_graph_pcg_ = std::string(m) != "persistent";
-  plan_ = build_plan(C, P, cam_idx, pt_idx, px2, N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
-                     kPipePts, 1 << 30);
+  if (comm_) use_graph_pcg_ = true;  // the persistent kernel has no place for the cross-rank sum
+  plan_ = build_plan(C, use_P, use_cam, use_pt, use_px, use_N, std::min(tile_obs, kPipeObs),
+                     std::min(tile_cams, kPipeCams), kPipePts, 1 << 30);
+  if (dist) {
+    // observation ids and the missing-diagonal checks refer to the whole problem
+    for (auto& k : plan_.obs_orig) k = gobs[k];
+    std::vector<char> cam_seen(static_cast<std::size_t>(C), 0), pt_seen(static_cast<std::size_t>(P), 0);
+    for (std::int64_t k = 0; k < N; ++k) {
+      cam_seen[cam_idx[k]] = 1;
+      pt_seen[pt_idx[k]] = 1;
+    }
+    plan_.has_empty_camera = std::find(cam_seen.begin(), cam_seen.end(), 0) != cam_seen.end();
+    plan_.has_empty_point = std::find(pt_seen.begin(), pt_seen.end(), 0) != pt_seen.end();
+  }
   intr_host_.assign(intr3, intr3 + 3 * static_cast<std::size_t>(C));
 
   // Tile classes. "Small" tiles (within the kPipe* caps) take the pipelined
@@ -130,10 +193,10 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
 
   Dev& d = d_;
   d.C = C;
-  d.P = P;
+  d.P = use_P;
   d.T = pl.T;
   d.E = pl.E;
-  d.N = static_cast<int>(N);
+  d.N = static_cast<int>(use_N);
   d.nbig = nbig;
   d.big_stride = big_stride;
   d.tile_obs_begin = upload(pl.tile_obs_begin);
@@ -160,14 +223,14 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.pose = dalloc<double>(7 * static_cast<std::size_t>(C));
   d.intr = upload(intr_host_);
   d.camrec = dalloc<double>(kCamRec * static_cast<std::size_t>(C));
-  d.pts = dalloc<double>(3 * static_cast<std::size_t>(P) + 2);  // +16 B: TMA point windows
+  d.pts = dalloc<double>(3 * static_cast<std::size_t>(use_P) + 2);  // +16 B: TMA point windows
   d.pose_t = dalloc<double>(7 * static_cast<std::size_t>(C));
   d.camrec_t = dalloc<double>(kCamRec * static_cast<std::size_t>(C));
-  d.pts_t = dalloc<double>(3 * static_cast<std::size_t>(P));
-  d.hpp = dalloc<double>(6 * static_cast<std::size_t>(P));
-  d.gp = dalloc<double>(3 * static_cast<std::size_t>(P));
-  d.hinv = dalloc<double>(6 * static_cast<std::size_t>(P));
-  d.dp = dalloc<double>(3 * static_cast<std::size_t>(P));
+  d.pts_t = dalloc<double>(3 * static_cast<std::size_t>(use_P));
+  d.hpp = dalloc<double>(6 * static_cast<std::size_t>(use_P));
+  d.gp = dalloc<double>(3 * static_cast<std::size_t>(use_P));
+  d.hinv = dalloc<double>(6 * static_cast<std::size_t>(use_P));
+  d.dp = dalloc<double>(3 * static_cast<std::size_t>(use_P));
   d.hcc = dalloc<double>(21 * static_cast<std::size_t>(C));
   d.gc = dalloc<double>(6 * static_cast<std::size_t>(C));
   d.hccd = dalloc<double>(21 * static_cast<std::size_t>(C));
@@ -180,6 +243,8 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.y = dalloc<double>(6 * static_cast<std::size_t>(C));
   d.partial = dalloc<double>(27 * static_cast<std::size_t>(std::max(pl.E, 1)));
   d.tile_red = dalloc<double>(2 * static_cast<std::size_t>(pl.T));
+  d.cred = dist ? dalloc<double>(27 * static_cast<std::size_t>(C) + 8) : nullptr;
+  d.cam_dot = dalloc<double>(2 * static_cast<std::size_t>(C));
   const int max_blocks = std::max((C + kWarpsPerCamBlock - 1) / kWarpsPerCamBlock, (C + 127) / 128) + 1;
   d.block_red = dalloc<double>(4 * static_cast<std::size_t>(std::max(max_blocks, 4096)));
   d.tickets = dalloc<unsigned>(16);
@@ -215,6 +280,11 @@ Problem::~Problem() {
   if (pcg_host_) cudaFreeHost(pcg_host_);
   if (lm_host_) cudaFreeHost(lm_host_);
   if (stream_) cudaStreamDestroy(stream_);
+  comm_.reset();
+}
+
+void Problem::require_single(const char* what) const {
+  if (comm_) throw Error(BAE_ERR_UNSUPPORTED, std::string(what) + " is not available on a sharded problem");
 }
 
 void Problem::activate() { ck(cudaSetDevice(opt_.device), "cudaSetDevice"); }
@@ -256,7 +326,7 @@ void Problem::set_parameters(const double* poses7, const double* points3) {
   const int C = d_.C, P = d_.P;
   std::vector<double> pts(points3 ? 3 * static_cast<std::size_t>(P) : 0);
   for (int i = 0; points3 && i < P; ++i) {
-    const int p = plan_.pt_of_internal[i];
+    const int p = comm_ ? local_pts_[plan_.pt_of_internal[i]] : plan_.pt_of_internal[i];
     pts[3 * i] = points3[3 * p];
     pts[3 * i + 1] = points3[3 * p + 1];
     pts[3 * i + 2] = points3[3 * p + 2];
@@ -266,8 +336,7 @@ void Problem::set_parameters(const double* poses7, const double* points3) {
   if (points3)
     ck(cudaMemcpyAsync(d_.pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, stream_),
        "H2D points");
-  launch_camrec(d_, false, stream_);
-  launches_ += kLaunchesCamrec;
+  launches_ += launch_camrec(d_, false, stream_);
   sync();
 }
 
@@ -275,7 +344,33 @@ void Problem::get_parameters(double* poses7, double* points3) {
   activate();
   const int C = d_.C, P = d_.P;
   if (poses7) ck(cudaMemcpy(poses7, d_.pose, 7 * sizeof(double) * C, cudaMemcpyDeviceToHost), "D2H poses");
-  if (points3) {
+  if (points3 && comm_) {
+    // every rank's points in ascending global id, gathered over the ranks
+    const int W = comm_->world();
+    std::vector<int> owned(static_cast<std::size_t>(W), 0);
+    for (int q : rank_of_point_) ++owned[q];
+    const std::size_t slot = 3 * static_cast<std::size_t>(*std::max_element(owned.begin(), owned.end()));
+    std::vector<double> pts(3 * static_cast<std::size_t>(P)), mine(slot, 0.0), all(slot * W);
+    ck(cudaMemcpy(pts.data(), d_.pts, pts.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H points");
+    for (int i = 0; i < P; ++i) {
+      const int lp = plan_.pt_of_internal[i];
+      for (int a = 0; a < 3; ++a) mine[3 * lp + a] = pts[3 * i + a];
+    }
+    double* dbuf = nullptr;
+    ck(cudaMalloc(&dbuf, sizeof(double) * slot * (W + 1)), "cudaMalloc");
+    ck(cudaMemcpyAsync(dbuf, mine.data(), sizeof(double) * slot, cudaMemcpyHostToDevice, stream_), "H2D gather");
+    comm_->allgather(dbuf, dbuf + slot, sizeof(double) * slot, stream_);
+    ck(cudaMemcpyAsync(all.data(), dbuf + slot, sizeof(double) * slot * W, cudaMemcpyDeviceToHost, stream_),
+       "D2H gather");
+    sync();
+    cudaFree(dbuf);
+    std::vector<std::size_t> next(static_cast<std::size_t>(W), 0);
+    for (int p = 0; p < P_global_; ++p) {
+      const int q = rank_of_point_[p];
+      const std::size_t at = q * slot + 3 * next[q]++;
+      for (int a = 0; a < 3; ++a) points3[3 * p + a] = all[at + a];
+    }
+  } else if (points3) {
     std::vector<double> pts(3 * static_cast<std::size_t>(P));
     ck(cudaMemcpy(pts.data(), d_.pts, pts.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H points");
     for (int i = 0; i < P; ++i) {
@@ -314,14 +409,14 @@ void Problem::unpermute_slots(const std::vector<double>& src, int comps, double*
 
 double Problem::evaluate(double* resid2) {
   activate();
+  if (resid2) require_single("the residual vector export");
   reset_lm_status();
   double* rbuf = nullptr;
   if (resid2) {
     ck(cudaMalloc(&rbuf, 2 * sizeof(double) * plan_.N), "cudaMalloc");
     d_.resid = rbuf;
   }
-  launch_cost(d_, sm_, stream_);
-  launches_ += kLaunchesCost;
+  launches_ += launch_cost(d_, sm_, stream_, comm_.get());
   d_.resid = nullptr;
   read_lm();
   if (lm_host_->err_obs != INT_MAX) {
@@ -340,9 +435,8 @@ double Problem::evaluate(double* resid2) {
 void Problem::linearize() {
   reset_lm_status();
   phase_begin(kPhLinearize);
-  launch_linearize(d_, sm_, false, stream_);
+  launches_ += launch_linearize(d_, sm_, false, stream_, comm_.get());
   phase_end();
-  launches_ += kLaunchesLinearize;
   read_lm();
   phase_collect();
   if (lm_host_->err_obs != INT_MAX)
@@ -351,6 +445,7 @@ void Problem::linearize() {
 
 void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
   activate();
+  require_single("the Jacobian export");
   const std::int64_t N = plan_.N;
   double* js = nullptr;
   double* rs = nullptr;
@@ -359,8 +454,7 @@ void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
   d_.jstore = js;
   d_.resid = rs;
   reset_lm_status();
-  launch_linearize(d_, sm_, true, stream_);
-  launches_ += kLaunchesLinearize;
+  launches_ += launch_linearize(d_, sm_, true, stream_, nullptr);
   d_.jstore = nullptr;
   d_.resid = nullptr;
   read_lm();
@@ -386,6 +480,7 @@ void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
 
 void Problem::block_diagonals(double* hcc36, double* gc6, double* hpp9, double* gp3) {
   activate();
+  require_single("the block-diagonal export");
   linearize();
   const int C = d_.C, P = d_.P;
   std::vector<double> h(21 * static_cast<std::size_t>(C)), g(6 * static_cast<std::size_t>(C));
@@ -414,7 +509,7 @@ void Problem::build_pcg_graph() {
   if (pcg_graph_) return;
   cudaGraph_t g;
   ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "begin capture");
-  for (int i = 0; i < kPcgChunk; ++i) launch_pcg_iteration(d_, sm_, stream_);
+  for (int i = 0; i < kPcgChunk; ++i) pcg_chunk_launches_ += launch_pcg_iteration(d_, sm_, stream_, comm_.get());
   ck(cudaStreamEndCapture(stream_, &g), "end capture");
   ck(cudaGraphInstantiate(&pcg_graph_, g, 0), "graph instantiate");
   cudaGraphDestroy(g);
@@ -503,14 +598,12 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
   if (!d_.wstore) d_.wstore = dalloc<double>(36 * static_cast<std::size_t>(plan_.N));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
-  launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_);
+  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get());
   phase_end();
-  launches_ += kLaunchesPrep;
   phase_begin(kPhAssemble);
   ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
-  launch_schur_dense(d_, stream_);
+  launches_ += launch_schur_dense(d_, stream_, comm_.get());
   phase_end();
-  launches_ += 1;
   ck(cudaMemcpyAsync(d_.x, d_.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_), "rhs copy");
   info.iters = 0;
   phase_begin(kPhFactor);
@@ -538,18 +631,25 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
 bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
   // budget as the reference computes it from the full system's block columns (lm.hpp:139-142)
   const long long budget =
-      cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * (d_.C + d_.P));
+      cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * (d_.C + P_global_));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
-  launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_);
+  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_, comm_.get());
   phase_end();
-  launches_ += kLaunchesPrep;
   phase_begin(kPhPcg);
-  if (use_graph_pcg_) {
+  if (comm_ && !comm_->capturable()) {
+    // in-process rank group: host-fenced collectives, plain launches
+    for (;;) {
+      for (int i = 0; i < kPcgChunk; ++i) launches_ += launch_pcg_iteration(d_, sm_, stream_, comm_.get());
+      ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+      sync();
+      if (pcg_host_->state >= kPcgDone) break;
+    }
+  } else if (use_graph_pcg_) {
     build_pcg_graph();
     for (;;) {
       ck(cudaGraphLaunch(pcg_graph_, stream_), "graph launch");
-      launches_ += kLaunchesPcgIter * kPcgChunk;
+      launches_ += pcg_chunk_launches_;
       ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
       sync();
       if (pcg_host_->state >= kPcgDone) break;
@@ -577,12 +677,12 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
 void Problem::solve_step(double lambda, const bae_lm_config& cfg, double* delta, std::int64_t* iters,
                          double* relres) {
   activate();
+  require_single("solve_step (a full-length step export)");
   linearize();
   SolveInfo info;
   if (!solve(lambda, cfg, info)) throw Error(BAE_ERR_NUMERICAL_BREAKDOWN, "damped system not SPD or PCG breakdown");
   reset_lm_status();
-  launch_trial(d_, sm_, stream_);
-  launches_ += kLaunchesTrial;
+  launches_ += launch_trial(d_, sm_, stream_, comm_.get());
   sync();
   const int C = d_.C, P = d_.P;
   ck(cudaMemcpy(delta, d_.x, 6 * sizeof(double) * C, cudaMemcpyDeviceToHost), "D2H dc");
@@ -624,7 +724,7 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   if (plan_.has_empty_camera || plan_.has_empty_point)
     throw Error(BAE_ERR_INVALID_ARGUMENT, "diagonal op: missing diagonal entry");  // csr.hpp:53
   if (poses7 || points3) set_parameters(poses7, points3);
-  const double n_obs = static_cast<double>(plan_.N);
+  const double n_obs = static_cast<double>(N_global_);
 
   cudaEvent_t ev0, ev1;
   ck(cudaEventCreate(&ev0), "event");
@@ -661,18 +761,16 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
     if (ok) {
       reset_lm_status();
       phase_begin(kPhTrial);
-      launch_trial(d_, sm_, stream_);
+      launches_ += launch_trial(d_, sm_, stream_, comm_.get());
       phase_end();
-      launches_ += kLaunchesTrial;
       read_lm();
       phase_collect();
       trial_cost = (lm_host_->retract_bad || lm_host_->trial_bad) ? std::numeric_limits<double>::infinity()
                                                                    : lm_host_->new_cost;
       if (trial_cost < cost) {
         phase_begin(kPhCommit);
-        launch_commit(d_, stream_);
+        launches_ += launch_commit(d_, stream_);
         phase_end();
-        launches_ += kLaunchesCommit;
         cost = trial_cost;
         history.push_back(cost);
         ++accepted_steps;
@@ -747,20 +845,16 @@ double Problem::time_kernel(int kind, int reps) {
   auto launch = [&]() {
     switch (kind) {
       case 0:
-        launch_linearize(d_, sm_, false, stream_);
-        launches_ += kLaunchesLinearize;
+        launches_ += launch_linearize(d_, sm_, false, stream_, comm_.get());
         break;
       case 1:
-        launch_schur_only(d_, sm_, stream_);
-        launches_ += 1;
+        launches_ += launch_schur_only(d_, sm_, stream_);
         break;
       case 2:
-        launch_pcg_iteration(d_, sm_, stream_);
-        launches_ += kLaunchesPcgIter;
+        launches_ += launch_pcg_iteration(d_, sm_, stream_, comm_.get());
         break;
       case 3:
-        launch_linearize(d_, sm_, true, stream_);
-        launches_ += kLaunchesLinearize;
+        launches_ += launch_linearize(d_, sm_, true, stream_, comm_.get());
         break;
       default:
         throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");

@@ -5,9 +5,11 @@
 #include <cusolverDn.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "bae_internal.hpp"
+#include "comm.hpp"
 #include "kernels.cuh"
 
 namespace bae {
@@ -43,8 +45,15 @@ class Problem {
   Problem& operator=(const Problem&) = delete;
 
   int num_cameras() const { return d_.C; }
-  int num_points() const { return d_.P; }
-  std::int64_t num_obs() const { return plan_.N; }
+  int num_points() const { return P_global_; }
+  std::int64_t num_obs() const { return N_global_; }
+  // Sharded problem: this rank owns a contiguous range of the
+  // points and all their observations; plan() / dev() describe that part.
+  bool distributed() const { return comm_ != nullptr; }
+  int rank() const { return comm_ ? comm_->rank() : 0; }
+  int world() const { return comm_ ? comm_->world() : 1; }
+  int local_points() const { return d_.P; }
+  std::int64_t local_obs() const { return plan_.N; }
   const Plan& plan() const { return plan_; }
   long long launches() const { return launches_; }
   const Dev& dev() const { return d_; }
@@ -74,6 +83,7 @@ class Problem {
   bool solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info);
   void build_direct();
   void build_pcg_graph();
+  void require_single(const char* what) const;
   void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
   void phase_begin(int ph);
   void phase_end();
@@ -94,6 +104,11 @@ class Problem {
   double phase_ms_[kPhases] = {0, 0, 0, 0, 0, 0, 0};
 
   bae_create_options opt_;
+  std::unique_ptr<Comm> comm_;       // null on a single rank
+  int P_global_ = 0;
+  std::int64_t N_global_ = 0;
+  std::vector<std::int32_t> rank_of_point_;  // sharded: owner of every global point
+  std::vector<std::int32_t> local_pts_;      // sharded: global ids of this rank's points, ascending
   Plan plan_;
   Dev d_{};
   SmemSizes sm_;
@@ -113,6 +128,7 @@ class Problem {
   int* dev_info_ = nullptr;
   int* host_info_ = nullptr;
   int pcg_grid_ = 0;
+  long long pcg_chunk_launches_ = 0;  // kernels in one captured PCG chunk
 };
 
 }  // namespace bae
