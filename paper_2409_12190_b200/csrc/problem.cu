@@ -29,21 +29,47 @@ constexpr int kSmemLimit = 200 * 1024;
 constexpr int kSliceLimit = 48 * 1024;    // per-warp tile workspace
 constexpr int kCtaSmemBudget = 100 * 1024; // two CTAs per SM
 constexpr int kPcgChunk = 8;
+
+// BAE_HOST_TIMING=1: host-side phase times on stderr (setup profiling).
+struct HostTimer {
+  bool on = std::getenv("BAE_HOST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bae host] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 }  // namespace
+
+// Device memory of a problem lives in a few large chunks carved by a bump
+// allocator (256-byte aligned, so TMA sources stay 16-byte aligned): one
+// cudaMalloc / cudaFree per chunk instead of one per array.
+constexpr std::size_t kArenaChunk = 32u << 20;
 
 template <class T>
 T* Problem::dalloc(std::size_t n) {
-  void* p = nullptr;
-  if (n == 0) n = 1;
-  ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
-  allocs_.push_back(p);
-  return static_cast<T*>(p);
+  const std::size_t bytes = (std::max<std::size_t>(n, 1) * sizeof(T) + 255) & ~std::size_t{255};
+  if (arena_used_ + bytes > arena_size_) {
+    const std::size_t sz = std::max(bytes, kArenaChunk);
+    void* p = nullptr;
+    ck(cudaMalloc(&p, sz), "cudaMalloc");
+    allocs_.push_back(p);
+    arena_base_ = static_cast<char*>(p);
+    arena_size_ = sz;
+    arena_used_ = 0;
+  }
+  T* r = reinterpret_cast<T*>(arena_base_ + arena_used_);
+  arena_used_ += bytes;
+  return r;
 }
 
 template <class T>
 T* Problem::upload(const std::vector<T>& v) {
   T* p = dalloc<T>(v.size());
-  if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  if (!v.empty())
+    ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream_), "upload");
   return p;
 }
 
@@ -51,6 +77,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
                  const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2, std::int64_t N,
                  const bae_create_options& opt)
     : opt_(opt) {
+  HostTimer ht;
   validate_inputs(C, P, cam_idx, pt_idx, N);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -109,6 +136,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   }
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  ht.mark("validate+partition");
   int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : 64;
   if (const char* t = std::getenv("BAE_TILE_OBS")) tile_obs = std::max(8, std::atoi(t));
   int tile_cams = 32;
@@ -117,6 +145,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (comm_) use_graph_pcg_ = true;  // the persistent kernel has no place for the cross-rank sum
   plan_ = build_plan(C, use_P, use_cam, use_pt, use_px, use_N, std::min(tile_obs, kPipeObs),
                      std::min(tile_cams, kPipeCams), kPipePts, 1 << 30);
+  ht.mark("build_plan");
   if (dist) {
     // observation ids and the missing-diagonal checks refer to the whole problem
     for (auto& k : plan_.obs_orig) k = gobs[k];
@@ -186,6 +215,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     // up to 8 warp-tiles per CTA, two CTAs per SM within the shared-memory budget
     tl.wpb = std::max(1, std::min(8, kCtaSmemBudget / tl.slice));
   }
+  ht.mark("tile blobs");
   sm_.schur.slice = kPipeWarpBytes;  // pipelined double buffer per warp
   sm_.schur.wpb = 4;
   big_stride = (big_stride + 255) / 256 * 256;
@@ -200,6 +230,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.nbig = nbig;
   d.big_stride = big_stride;
   d.tile_obs_begin = upload(pl.tile_obs_begin);
+  ht.mark("first chunk + upload");
   d.tile_pt_begin = upload(pl.tile_pt_begin);
   d.tile_ent_begin = upload(pl.tile_ent_begin);
   d.tile_ws = upload(pl.tile_ws);
@@ -217,6 +248,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.tile_blob = upload(blob);
   d.small_tiles = upload(small_tiles);
   d.big_tiles = upload(big_tiles);
+  ht.mark("uploads");
   d.n_small = static_cast<int>(small_tiles.size());
   d.n_big_tiles = static_cast<int>(big_tiles.size());
   d.bigws = nbig ? dalloc<char>(static_cast<std::size_t>(nbig) * big_stride) : nullptr;
@@ -260,14 +292,18 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.blk_cam = nullptr;
   d.nblk = 0;
   d.schur = nullptr;
+  ht.mark("allocs");
   ck(cudaMallocHost(&pcg_host_, sizeof(PcgDev)), "cudaMallocHost");
   ck(cudaMallocHost(&lm_host_, sizeof(LmDev)), "cudaMallocHost");
   ck(cudaMemset(d.pcg, 0, sizeof(PcgDev)), "memset");
 
+  ht.mark("device alloc+upload");
   set_parameters(poses7, points3);
+  ht.mark("set_parameters");
   // Eager forward at construction, as make_ba_problem's graph does
   // (trace.hpp:152,385): cheirality surfaces here with the observation id.
   evaluate(nullptr);
+  ht.mark("initial evaluate");
 }
 
 Problem::~Problem() {
@@ -530,54 +566,91 @@ constexpr long long kDirectMaxOrder = 32768;
 // block (two-pass stable counting sort), point-major inside a block.
 void Problem::build_direct() {
   if (direct_ready_) return;
+  HostTimer ht;
   const long long n = 6LL * d_.C;
   if (n > kDirectMaxOrder)
     throw Error(BAE_ERR_UNSUPPORTED, "solver=cholesky: reduced camera system too large for the dense direct solve; "
                                      "use solver=pcg");
   const Plan& pl = plan_;
+  const int C = d_.C;
   std::vector<int> cam_of_slot(static_cast<std::size_t>(pl.N));
   for (int t = 0; t < pl.T; ++t)
     for (int e = pl.tile_ent_begin[t]; e < pl.tile_ent_begin[t + 1]; ++e)
       for (int sl = pl.ent_obs_begin[e]; sl < pl.ent_obs_begin[e + 1]; ++sl) cam_of_slot[sl] = pl.ent_cam[e];
-  std::vector<int2> raw;
-  std::vector<int> slots;
-  for (int t = 0; t < pl.T; ++t) {
-    const int ob = pl.tile_obs_begin[t];
-    for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
-      slots.clear();
-      for (int q = pl.pt_ptr[i]; q < pl.pt_ptr[i + 1]; ++q) slots.push_back(ob + pl.ptobs[q]);
-      for (int k : slots)
-        for (int l : slots)
-          if (cam_of_slot[k] >= cam_of_slot[l]) raw.push_back(int2{k, l});
+  // Pairs in generation order (point, k, l), bucketed by c1 = camera(k) with a
+  // counting sort, then each c1 bucket stably by c2 = camera(l).
+  auto for_pairs = [&](auto&& emit) {
+    int kc[256], ks[256];
+    for (int t = 0; t < pl.T; ++t) {
+      const int ob = pl.tile_obs_begin[t];
+      for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
+        const int m = pl.pt_ptr[i + 1] - pl.pt_ptr[i];
+        for (int q = 0; q < m; ++q) {
+          const int sl = ob + pl.ptobs[pl.pt_ptr[i] + q];
+          if (q < 256) {
+            ks[q] = sl;
+            kc[q] = cam_of_slot[sl];
+          }
+        }
+        if (m <= 256) {
+          for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b)
+              if (kc[a] >= kc[b]) emit(kc[a], kc[b], ks[a], ks[b]);
+        } else {  // very long track
+          for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) {
+              const int sa = ob + pl.ptobs[pl.pt_ptr[i] + a], sb = ob + pl.ptobs[pl.pt_ptr[i] + b];
+              if (cam_of_slot[sa] >= cam_of_slot[sb]) emit(cam_of_slot[sa], cam_of_slot[sb], sa, sb);
+            }
+        }
+      }
     }
-  }
-  const std::size_t np = raw.size();
-  std::vector<int2> tmp(np), sorted(np);
-  std::vector<long long> cnt(static_cast<std::size_t>(d_.C) + 1);
-  auto pass = [&](const std::vector<int2>& in, std::vector<int2>& out, bool by_first) {
-    std::fill(cnt.begin(), cnt.end(), 0);
-    for (const int2& p : in) ++cnt[cam_of_slot[by_first ? p.x : p.y] + 1];
-    for (int c = 0; c < d_.C; ++c) cnt[c + 1] += cnt[c];
-    for (const int2& p : in) out[cnt[cam_of_slot[by_first ? p.x : p.y]]++] = p;
   };
-  pass(raw, tmp, false);
-  pass(tmp, sorted, true);
+  std::vector<long long> row(static_cast<std::size_t>(C) + 1, 0);
+  for_pairs([&](int c1, int, int, int) { ++row[c1 + 1]; });
+  for (int c = 0; c < C; ++c) row[c + 1] += row[c];
+  const std::size_t np = static_cast<std::size_t>(row[C]);
+  if (np >= (std::size_t{1} << 31)) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
+  std::vector<int2> bucket(np), sorted(np);
+  std::vector<int> bucket_c2(np);
+  {
+    std::vector<long long> cur(row.begin(), row.end() - 1);
+    for_pairs([&](int c1, int c2, int k, int l) {
+      const long long at = cur[c1]++;
+      bucket[at] = int2{k, l};
+      bucket_c2[at] = c2;
+    });
+  }
   std::vector<int> bptr{0};
   std::vector<int2> bcam;
-  for (std::size_t q = 0; q < np; ++q) {
-    const int c1 = cam_of_slot[sorted[q].x], c2 = cam_of_slot[sorted[q].y];
-    if (q == 0 || c1 != cam_of_slot[sorted[q - 1].x] || c2 != cam_of_slot[sorted[q - 1].y]) {
-      if (q) bptr.push_back(static_cast<int>(q));
+  std::vector<long long> cnt(static_cast<std::size_t>(C) + 1, 0);
+  std::vector<int> seen;
+  for (int c1 = 0; c1 < C; ++c1) {
+    const long long b = row[c1], e = row[c1 + 1];
+    seen.clear();
+    for (long long q = b; q < e; ++q)
+      if (cnt[bucket_c2[q]]++ == 0) seen.push_back(bucket_c2[q]);
+    std::sort(seen.begin(), seen.end());
+    long long at = b;
+    for (int c2 : seen) {
+      const long long m = cnt[c2];
+      cnt[c2] = at;  // becomes the write cursor
       bcam.push_back(int2{c1, c2});
+      bptr.push_back(static_cast<int>(at + m));
+      at += m;
     }
+    for (long long q = b; q < e; ++q) sorted[cnt[bucket_c2[q]]++] = bucket[q];
+    for (int c2 : seen) cnt[c2] = 0;
   }
-  bptr.push_back(static_cast<int>(np));
   d_.pairs = upload(sorted);
   d_.blk_ptr = upload(bptr);
   d_.blk_cam = upload(bcam);
   d_.nblk = static_cast<int>(bcam.size());
+  ht.mark("direct: pair list");
   d_.schur = dalloc<double>(static_cast<std::size_t>(n) * static_cast<std::size_t>(n));
+  ht.mark("direct: alloc S");
   if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw Error(BAE_ERR_CUDA, "cusolverDnCreate failed");
+  ht.mark("direct: cusolverDnCreate");
   cusolverDnSetStream(solver_, stream_);
   if (cusolverDnDpotrf_bufferSize(solver_, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), d_.schur,
                                   static_cast<int>(n), &potrf_lwork_) != CUSOLVER_STATUS_SUCCESS)
@@ -586,6 +659,7 @@ void Problem::build_direct() {
   dev_info_ = dalloc<int>(1);
   ck(cudaMallocHost(&host_info_, sizeof(int)), "cudaMallocHost");
   direct_ready_ = true;
+  ht.mark("direct: alloc+cusolver");
 }
 
 // Direct solve of the damped reduced camera system (the reference's default

@@ -114,7 +114,9 @@ class Problem {
   SmemSizes sm_;
   cudaStream_t stream_ = nullptr;
   cudaGraphExec_t pcg_graph_ = nullptr;
-  std::vector<void*> allocs_;
+  std::vector<void*> allocs_;  // arena chunks
+  char* arena_base_ = nullptr;
+  std::size_t arena_size_ = 0, arena_used_ = 0;
   std::vector<double> intr_host_;
   PcgDev* pcg_host_ = nullptr;
   LmDev* lm_host_ = nullptr;

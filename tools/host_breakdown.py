@@ -10,7 +10,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "trafalgar-257"
 solver = bae.SolverChoice[sys.argv[2] if len(sys.argv) > 2 else "cholesky"]
 s = bae.synthetic.config_scene(name)
 cfg = bae.LmConfig(max_iterations=50, solver=solver)
-for rep_i in range(3):
+for rep_i in range(5):
     t0 = time.perf_counter()
     g = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
     t1 = time.perf_counter()
