@@ -1,0 +1,78 @@
+// Tile-sparse Cholesky of the reduced camera system S (the direct solver,
+// SolverChoice::cholesky, lm.hpp:132-136; the reference factors the full
+// system with an AMD-ordered sparse Cholesky, cholesky.hpp:77-281).
+//
+// S (6C x 6C, camera order) is cut into kTB x kTB tiles (8 cameras per tile;
+// the last tile is padded with an identity). Only the tiles of L's fill
+// pattern are stored (column-major inside a tile). The pattern comes from a
+// tile-level symbolic factorisation done once per problem (plan_tile_chol).
+//
+// Numeric factorisation is ONE persistent kernel, left-looking by tile
+// column: CTA b owns columns b, b + G, ... and processes them in ascending
+// order. Column j first finishes its diagonal tile (the updates from every
+// column k with L(j,k) != 0, waiting on the epoch flag of that tile), factors
+// and inverts it and performs its step of the forward substitution L y = b;
+// then each tile below the diagonal gets its updates, is solved against
+// L(j,j)^-T and published with its own flag, so the next column starts as
+// soon as the one tile it needs exists. There is no grid-wide barrier:
+// independent parts of the elimination tree run concurrently. A second
+// dataflow kernel runs the backward substitution L^T x = y in descending
+// column order. Every sum runs in a fixed order: results are bitwise
+// reproducible.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace bae {
+
+constexpr int kTB = 48;              // tile edge (8 cameras)
+constexpr int kTT = kTB * kTB;       // doubles per tile
+constexpr int kCholThreads = 256;    // 16 x 16 threads, 3 x 3 outputs each
+
+// Host-side symbolic structure (plan_tile_chol).
+struct TileCholPlan {
+  int nt = 0;                       // tile columns
+  int n = 0;                        // true order (6C); rows >= n are padding
+  std::vector<int> colptr;          // nt+1: L tiles of column j, diagonal first, rows ascending
+  std::vector<int> rowidx;          // tile row of each stored tile (slot = position)
+  std::vector<int> rptr;            // nt+1: row structure of column j: k < j with L(j,k) != 0
+  std::vector<int> rk, rslot;       // k ascending, slot of L(j,k)
+  std::vector<int> uptr;            // per row-structure entry q: range of its tile updates
+  std::vector<int> usrc, udst;      // update: C(udst) -= L(usrc) L(rslot[q])^T
+  long long nnz_tiles() const { return static_cast<long long>(rowidx.size()); }
+};
+
+// Tile-level symbolic Cholesky from the lower-triangular tile pattern of S:
+// `lower_pairs` lists tile pairs (i, j), i >= j (duplicates allowed); every
+// diagonal tile is included automatically.
+TileCholPlan plan_tile_chol(int n, const std::vector<std::pair<int, int>>& lower_pairs);
+
+// Device view.
+struct TileChol {
+  int nt, n;
+  int nnz;              // stored tiles
+  const int* colptr;
+  const int* rowidx;
+  const int* rptr;
+  const int* rk;
+  const int* rslot;
+  const int* uptr;
+  const int* usrc;
+  const int* udst;
+  double* tiles;        // nnz_tiles * kTT; diagonal slots receive L(j,j)^-1 after the factorisation
+  const double* rhs;    // n (rows >= n read as 0)
+  double* y;            // nt * kTB forward-substitution result
+  double* x;            // n solution
+  unsigned* flags;      // nnz + nt epoch flags: one per stored tile (factor), one per column (backward)
+  int* fail;            // set when a pivot is not positive (NotSpdError, cholesky.hpp:229)
+  unsigned long long* trace;  // BAE_CHOL_TRACE: 8 globaltimer stamps per column, or null
+};
+
+// Factor + solve on stream s (two launches). `epoch` must increase by one per call.
+int launch_tile_chol(const TileChol& t, unsigned epoch, int grid, cudaStream_t s);
+int tile_chol_grid(int nt);
+
+}  // namespace bae

@@ -11,6 +11,7 @@ namespace bae {
 constexpr int kTileThreads = 256;  // CTA size of the tile kernels (8 warps)
 constexpr int kCamRec = 16;        // per camera: R[9] t[3] f k1 k2 pad
 constexpr int kWarpsPerCamBlock = 8;
+constexpr int kSTileElems = 48 * 48;  // one tile of the tile-sparse reduced matrix (chol.cuh kTT)
 
 // PCG state machine (implicit-Schur PCG, restating pcg.hpp:32-129 on the
 // reduced camera system).
@@ -97,7 +98,12 @@ struct Dev {
   const int* blk_ptr;      // nblk + 1
   const int2* blk_cam;     // (c1, c2), c1 >= c2
   int nblk;
-  double* schur;           // 6C x 6C, column-major (lower triangle used)
+  double* schur;           // 6C x 6C, column-major (lower triangle used; cuSOLVER path)
+  // tile-sparse storage of S (chol.cuh): per camera block the slot of the
+  // 48 x 48 tile holding it (8 cameras per tile), column-major tiles
+  const int* blk_tile;     // nblk slots, then one diagonal-tile slot per tile column
+  double* stiles;
+  long long stile_count;
   unsigned long long* trace;  // per-tile phase timestamps (BAE_TRACE) or null
   // pipelined small tiles: per-tile descriptor {blob offset / 16, blob bytes,
   // first point, point count} and the packed per-tile index blobs

@@ -806,13 +806,17 @@ __global__ void k_schur_dense(Dev d) {
   const long long n = 6LL * d.C;
   if (lane == 0) {
     const double* h = d.hccd + (long long)cc.x * 21;
+    // dense column-major S, or the block's place in its 48 x 48 tile
+    double* base = d.stiles ? d.stiles + (long long)d.blk_tile[blk] * kSTileElems + 6 * (cc.y & 7) * 48 + 6 * (cc.x & 7)
+                            : d.schur + 6LL * cc.y * n + 6LL * cc.x;
+    const long long ld = d.stiles ? 48 : n;
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
         double v = -acc[r * 6 + c];
         if (cc.x == cc.y && !d.cred) v += h[sym6(r, c)];  // sharded: added after the rank sum
-        d.schur[(6LL * cc.y + c) * n + 6LL * cc.x + r] = v;
+        base[c * ld + r] = v;
       }
   }
 }
@@ -823,7 +827,11 @@ __global__ void k_add_hccd(Dev d) {
   if (idx >= 36LL * d.C) return;
   const int c = (int)(idx / 36), r = (int)(idx % 36) / 6, col = (int)(idx % 6);
   const long long n = 6LL * d.C;
-  d.schur[(6LL * c + col) * n + 6LL * c + r] += d.hccd[(long long)c * 21 + sym6(r, col)];
+  const double h = d.hccd[(long long)c * 21 + sym6(r, col)];
+  if (d.stiles)  // diag_tile[c / 8] holds camera c's diagonal block
+    d.stiles[(long long)d.blk_tile[d.nblk + c / 8] * kSTileElems + (6 * (c & 7) + col) * 48 + 6 * (c & 7) + r] += h;
+  else
+    d.schur[(6LL * c + col) * n + 6LL * c + r] += h;
 }
 
 // ---------------------------------------------------------------------------
@@ -1739,9 +1747,12 @@ int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
     k_schur_dense<<<(d.nblk + 7) / 8, 256, 0, s>>>(d);
     ++n;
   }
-  if (comm) {  // the direct solve's exchange: the dense reduced matrix, once per LM iteration
+  if (comm) {  // the direct solve's exchange: the reduced matrix, once per LM iteration
     const std::size_t nn = 6 * static_cast<std::size_t>(d.C);
-    comm->allreduce_sum(d.schur, nn * nn, s);
+    if (d.stiles)
+      comm->allreduce_sum(d.stiles, static_cast<std::size_t>(d.stile_count) * kSTileElems, s);
+    else
+      comm->allreduce_sum(d.schur, nn * nn, s);
     k_add_hccd<<<elt_blocks(36LL * d.C, 256), 256, 0, s>>>(d);
     ++n;
   }

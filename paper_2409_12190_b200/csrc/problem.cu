@@ -568,7 +568,8 @@ void Problem::build_direct() {
   if (direct_ready_) return;
   HostTimer ht;
   const long long n = 6LL * d_.C;
-  if (n > kDirectMaxOrder)
+  if (const char* m = std::getenv("BAE_DIRECT")) use_tiles_ = std::string(m) != "cusolver";
+  if (!use_tiles_ && n > kDirectMaxOrder)
     throw Error(BAE_ERR_UNSUPPORTED, "solver=cholesky: reduced camera system too large for the dense direct solve; "
                                      "use solver=pcg");
   const Plan& pl = plan_;
@@ -647,6 +648,12 @@ void Problem::build_direct() {
   d_.blk_cam = upload(bcam);
   d_.nblk = static_cast<int>(bcam.size());
   ht.mark("direct: pair list");
+  if (use_tiles_) {
+    build_tile_chol(bcam);
+    ht.mark("direct: tile symbolic");
+    direct_ready_ = true;
+    return;
+  }
   d_.schur = dalloc<double>(static_cast<std::size_t>(n) * static_cast<std::size_t>(n));
   ht.mark("direct: alloc S");
   if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw Error(BAE_ERR_CUDA, "cusolverDnCreate failed");
@@ -662,6 +669,71 @@ void Problem::build_direct() {
   ht.mark("direct: alloc+cusolver");
 }
 
+// Tile pattern of S (camera blocks -> 48 x 48 tiles, the union over ranks on
+// sharded runs), its symbolic factorisation and the device structures.
+void Problem::build_tile_chol(const std::vector<int2>& bcam) {
+  const int C = d_.C;
+  const int n = 6 * C;
+  const int nt = (n + kTB - 1) / kTB;
+  std::vector<std::pair<int, int>> tp;
+  if (comm_) {
+    // union of the ranks' patterns: 0 = present, 1 = absent, min over ranks
+    const std::size_t ntri = static_cast<std::size_t>(nt) * (nt + 1) / 2;
+    std::vector<int> tri(ntri, 1);
+    for (const int2& b : bcam) tri[static_cast<std::size_t>(b.x / 8) * (b.x / 8 + 1) / 2 + b.y / 8] = 0;
+    int* dtri = nullptr;
+    ck(cudaMalloc(&dtri, ntri * sizeof(int)), "cudaMalloc");
+    ck(cudaMemcpyAsync(dtri, tri.data(), ntri * sizeof(int), cudaMemcpyHostToDevice, stream_), "H2D pattern");
+    comm_->allreduce_min(dtri, ntri, stream_);
+    ck(cudaMemcpyAsync(tri.data(), dtri, ntri * sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H pattern");
+    sync();
+    cudaFree(dtri);
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j)
+        if (tri[static_cast<std::size_t>(i) * (i + 1) / 2 + j] == 0) tp.emplace_back(i, j);
+  } else {
+    tp.reserve(bcam.size());
+    for (const int2& b : bcam) tp.emplace_back(b.x / 8, b.y / 8);
+  }
+  const TileCholPlan pl = plan_tile_chol(n, tp);
+  // slot of every camera block's tile, then the diagonal slot of each tile column
+  std::vector<int> blk_tile;
+  blk_tile.reserve(bcam.size() + static_cast<std::size_t>(nt));
+  for (const int2& b : bcam) {
+    const int ti = b.x / 8, tj = b.y / 8;
+    const auto first = pl.rowidx.begin() + pl.colptr[tj], last = pl.rowidx.begin() + pl.colptr[tj + 1];
+    blk_tile.push_back(static_cast<int>(std::lower_bound(first, last, ti) - pl.rowidx.begin()));
+  }
+  for (int j = 0; j < nt; ++j) blk_tile.push_back(pl.colptr[j]);
+  d_.blk_tile = upload(blk_tile);
+  d_.stile_count = pl.nnz_tiles();
+  d_.stiles = dalloc<double>(static_cast<std::size_t>(pl.nnz_tiles()) * kTT);
+  TileChol& t = tchol_;
+  t.nt = nt;
+  t.n = n;
+  t.colptr = upload(pl.colptr);
+  t.rowidx = upload(pl.rowidx);
+  t.rptr = upload(pl.rptr);
+  t.rk = upload(pl.rk);
+  t.rslot = upload(pl.rslot);
+  t.uptr = upload(pl.uptr);
+  t.usrc = upload(pl.usrc);
+  t.udst = upload(pl.udst);
+  t.tiles = d_.stiles;
+  t.rhs = d_.rhs;
+  t.y = dalloc<double>(static_cast<std::size_t>(nt) * kTB);
+  t.x = d_.x;
+  t.nnz = static_cast<int>(pl.nnz_tiles());
+  t.flags = dalloc<unsigned>(static_cast<std::size_t>(t.nnz) + nt);
+  ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (static_cast<std::size_t>(t.nnz) + nt), stream_),
+     "memset flags");
+  t.fail = dalloc<int>(1);
+  chol_epoch_ = 0;
+  chol_grid_ = tile_chol_grid(nt);
+  chol_updates_ = static_cast<long long>(pl.usrc.size());
+  if (!host_info_) ck(cudaMallocHost(&host_info_, sizeof(int)), "cudaMallocHost");
+}
+
 // Direct solve of the damped reduced camera system (the reference's default
 // Cholesky solver on the Schur complement instead of the full system):
 // dense S from per-observation W, W H~^-1 (my kernels), LL^T factor and
@@ -675,9 +747,70 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
   launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get());
   phase_end();
   phase_begin(kPhAssemble);
-  ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
+  if (use_tiles_)
+    ck(cudaMemsetAsync(d_.stiles, 0, sizeof(double) * kTT * d_.stile_count, stream_), "memset S tiles");
+  else
+    ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
   launches_ += launch_schur_dense(d_, stream_, comm_.get());
   phase_end();
+  if (use_tiles_) {
+    // tile-sparse Cholesky + both substitutions: x = S^-1 rhs straight into d_.x
+    info.iters = 0;
+    phase_begin(kPhFactor);
+    ck(cudaMemsetAsync(tchol_.fail, 0, sizeof(int), stream_), "memset fail");
+    std::vector<unsigned long long> trace;
+    if (std::getenv("BAE_CHOL_TRACE")) {
+      ck(cudaMalloc(&tchol_.trace, 8 * sizeof(unsigned long long) * tchol_.nt), "cudaMalloc");
+      ck(cudaMemsetAsync(tchol_.trace, 0, 8 * sizeof(unsigned long long) * tchol_.nt, stream_), "memset");
+    }
+    launches_ += launch_tile_chol(tchol_, ++chol_epoch_, chol_grid_, stream_);
+    phase_end();
+    if (tchol_.trace) {
+      trace.resize(8 * static_cast<std::size_t>(tchol_.nt));
+      ck(cudaMemcpyAsync(trace.data(), tchol_.trace, trace.size() * 8, cudaMemcpyDeviceToHost, stream_), "D2H");
+      sync();
+      cudaFree(tchol_.trace);
+      tchol_.trace = nullptr;
+      unsigned long long t0 = ~0ull, t1 = 0, tb0 = ~0ull;
+      double upd = 0, pot = 0, inv = 0, trs = 0, fwd = 0, bwd = 0;
+      for (int j = 0; j < tchol_.nt; ++j) {
+        const unsigned long long* r = &trace[8 * static_cast<std::size_t>(j)];
+        t0 = std::min(t0, r[0]);
+        t1 = std::max(t1, r[5]);
+        tb0 = std::min(tb0, r[6]);
+        upd += r[1] - r[0];
+        pot += r[2] - r[1];
+        inv += r[3] - r[2];
+        trs += r[4] - r[3];
+        fwd += r[5] - r[4];
+        bwd += r[7] - r[6];
+      }
+      unsigned long long tb1 = 0;
+      for (int j = 0; j < tchol_.nt; ++j) tb1 = std::max(tb1, trace[8 * static_cast<std::size_t>(j) + 7]);
+      const double nt = tchol_.nt;
+      std::fprintf(stderr,
+                   "[bae chol] nt %d tiles %lld updates %lld: factor span %.1f us, backward span %.1f us; per column "
+                   "mean: wait+update %.2f potrf %.2f trinv %.2f trsm %.2f fwd+publish %.2f backward %.2f us\n",
+                   tchol_.nt, static_cast<long long>(d_.stile_count), chol_updates_, (t1 - t0) * 1e-3,
+                   (tb1 - tb0) * 1e-3, upd / nt * 1e-3, pot / nt * 1e-3, inv / nt * 1e-3, trs / nt * 1e-3,
+                   fwd / nt * 1e-3, bwd / nt * 1e-3);
+      if (std::getenv("BAE_CHOL_TRACE")[0] == '2')
+        for (int j = 0; j < tchol_.nt; ++j) {
+          const unsigned long long* r = &trace[8 * static_cast<std::size_t>(j)];
+          std::fprintf(stderr, "  col %4d: start %8.1f upd %7.1f potrf %6.1f inv %6.1f trsm %6.1f pub %6.1f\n", j,
+                       (r[0] - t0) * 1e-3, (r[1] - r[0]) * 1e-3, (r[2] - r[1]) * 1e-3, (r[3] - r[2]) * 1e-3,
+                       (r[4] - r[3]) * 1e-3, (r[5] - r[4]) * 1e-3);
+        }
+    }
+    ck(cudaMemcpyAsync(host_info_, tchol_.fail, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H fail");
+    ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+    sync();
+    phase_collect();
+    if (*host_info_ != 0 || pcg_host_->not_spd) return false;  // NotSpdError (cholesky.hpp:229)
+    info.converged = true;
+    info.rel_residual = 0.0;
+    return true;
+  }
   ck(cudaMemcpyAsync(d_.x, d_.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_), "rhs copy");
   info.iters = 0;
   phase_begin(kPhFactor);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "bae_internal.hpp"
+#include "chol.cuh"
 #include "comm.hpp"
 #include "kernels.cuh"
 
@@ -83,6 +84,7 @@ class Problem {
   bool solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info);
   void build_direct();
   void build_pcg_graph();
+  void build_tile_chol(const std::vector<int2>& bcam);
   void require_single(const char* what) const;
   void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
   void phase_begin(int ph);
@@ -130,6 +132,12 @@ class Problem {
   int* dev_info_ = nullptr;
   int* host_info_ = nullptr;
   int pcg_grid_ = 0;
+  // tile-sparse Cholesky (default direct solver; BAE_DIRECT=cusolver: dense cuSOLVER)
+  bool use_tiles_ = true;
+  TileChol tchol_{};
+  unsigned chol_epoch_ = 0;
+  int chol_grid_ = 0;
+  long long chol_updates_ = 0;
   long long pcg_chunk_launches_ = 0;  // kernels in one captured PCG chunk
 };
 

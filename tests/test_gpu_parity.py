@@ -188,3 +188,29 @@ def test_default_config_trajectory_matches_oracle(oracle):
     p7, p3 = gpu.get_parameters()
     assert np.abs(p3 - oref["points"]).max() <= 1e-7
     assert np.abs(p7 - oref["poses"]).max() <= 1e-7
+
+
+@pytest.mark.parametrize("lmbda", [1e-6, 1e-1])
+def test_tile_cholesky_step_many_tiles(oracle, lmbda):
+    """Tile-sparse Cholesky with a banded, ring-closed tile pattern (C = 64
+    cameras -> 8 tile columns, fill in the closing corner) against the
+    oracle's damped full system."""
+    s = _scene(C=64, P=500, N=2500, seed=12)
+    gpu, ref = _pair(s, oracle)
+    dg, iters, _ = gpu.solve_step(lmbda, bae.LmConfig())
+    assert iters == 0
+    A, b = ref.normal_dense(lmbda)
+    assert np.linalg.norm(A @ dg - b) <= 1e-9 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("C,P,N", [(100, 2000, 9000), (257, 3000, 15000)])
+def test_tile_cholesky_matches_dense_cusolver(monkeypatch, C, P, N):
+    """The tile-sparse factorisation (default) and the dense cuSOLVER
+    factorisation (BAE_DIRECT=cusolver) of the same reduced system agree."""
+    s = _scene(C=C, P=P, N=N, seed=C)
+    tile = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+    d_tile, _, _ = tile.solve_step(1e-4, bae.LmConfig())
+    monkeypatch.setenv("BAE_DIRECT", "cusolver")
+    dense = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+    d_dense, _, _ = dense.solve_step(1e-4, bae.LmConfig())
+    assert np.linalg.norm(d_tile - d_dense) <= 1e-8 * np.linalg.norm(d_dense)
