@@ -45,6 +45,16 @@ struct TileCholPlan {
   long long nnz_tiles() const { return static_cast<long long>(rowidx.size()); }
 };
 
+// Fill-reducing order of the camera graph (cameras joined when they see a
+// common point): nested dissection by BFS level sets -- a pseudo-peripheral
+// start, the middle level as separator, the two sides recursively, the
+// separator last. Groups are returned in elimination order; every group is
+// later padded to whole tiles, so independent subtrees never share a tile
+// and the elimination tree's height drops from O(C) to O(log C) separator
+// levels for banded / sequential camera graphs. Small or dense subgraphs
+// stay one group (BFS order).
+std::vector<std::vector<int>> nd_camera_groups(int C, const std::vector<std::pair<int, int>>& edges, int leaf);
+
 // Tile-level symbolic Cholesky from the lower-triangular tile pattern of S:
 // `lower_pairs` lists tile pairs (i, j), i >= j (duplicates allowed); every
 // diagonal tile is included automatically.
@@ -52,7 +62,7 @@ TileCholPlan plan_tile_chol(int n, const std::vector<std::pair<int, int>>& lower
 
 // Device view.
 struct TileChol {
-  int nt, n;
+  int nt, n;            // n = 6 * positions (padded, tile-aligned groups)
   int nnz;              // stored tiles
   const int* colptr;
   const int* rowidx;
@@ -63,9 +73,11 @@ struct TileChol {
   const int* usrc;
   const int* udst;
   double* tiles;        // nnz_tiles * kTT; diagonal slots receive L(j,j)^-1 after the factorisation
-  const double* rhs;    // n (rows >= n read as 0)
+  const double* rhs;    // right-hand side, camera order (6 per camera)
   double* y;            // nt * kTB forward-substitution result
-  double* x;            // n solution
+  double* x;            // solution, camera order (6 per camera)
+  const int* pos_cam;   // camera at each position (n / 6), -1 for a padding slot
+  const unsigned long long* padmask;  // per tile: bit r set when row r is padding (unit pivot)
   unsigned* flags;      // nnz + nt epoch flags: one per stored tile (factor), one per column (backward)
   int* fail;            // set when a pivot is not positive (NotSpdError, cholesky.hpp:229)
   unsigned long long* trace;  // BAE_CHOL_TRACE: 8 globaltimer stamps per column, or null

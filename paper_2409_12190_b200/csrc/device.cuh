@@ -101,7 +101,9 @@ struct Dev {
   double* schur;           // 6C x 6C, column-major (lower triangle used; cuSOLVER path)
   // tile-sparse storage of S (chol.cuh): per camera block the slot of the
   // 48 x 48 tile holding it (8 cameras per tile), column-major tiles
-  const int* blk_tile;     // nblk slots, then one diagonal-tile slot per tile column
+  // per camera block {tile slot, row offset | col offset << 8 | transposed << 16},
+  // then per camera {diagonal tile slot, offset}
+  const int2* blk_tile;
   double* stiles;
   long long stile_count;
   unsigned long long* trace;  // per-tile phase timestamps (BAE_TRACE) or null

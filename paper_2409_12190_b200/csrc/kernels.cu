@@ -806,17 +806,29 @@ __global__ void k_schur_dense(Dev d) {
   const long long n = 6LL * d.C;
   if (lane == 0) {
     const double* h = d.hccd + (long long)cc.x * 21;
-    // dense column-major S, or the block's place in its 48 x 48 tile
-    double* base = d.stiles ? d.stiles + (long long)d.blk_tile[blk] * kSTileElems + 6 * (cc.y & 7) * 48 + 6 * (cc.x & 7)
-                            : d.schur + 6LL * cc.y * n + 6LL * cc.x;
-    const long long ld = d.stiles ? 48 : n;
+    // dense column-major S, or the block's place in its 48 x 48 tile (the
+    // camera order of the tile factorisation may put it transposed)
+    double* base;
+    long long ldr, ldc;  // element (r, c) of the block at base[r * ldr + c * ldc]
+    if (d.stiles) {
+      const int2 bt = d.blk_tile[blk];
+      const int ro = bt.y & 0xff, co = (bt.y >> 8) & 0xff;
+      base = d.stiles + (long long)bt.x * kSTileElems + co * 48 + ro;
+      const bool tr = (bt.y >> 16) & 1;
+      ldr = tr ? 48 : 1;
+      ldc = tr ? 1 : 48;
+    } else {
+      base = d.schur + 6LL * cc.y * n + 6LL * cc.x;
+      ldr = 1;
+      ldc = n;
+    }
 #pragma unroll
     for (int r = 0; r < 6; ++r)
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
         double v = -acc[r * 6 + c];
         if (cc.x == cc.y && !d.cred) v += h[sym6(r, c)];  // sharded: added after the rank sum
-        base[c * ld + r] = v;
+        base[r * ldr + c * ldc] = v;
       }
   }
 }
@@ -828,8 +840,10 @@ __global__ void k_add_hccd(Dev d) {
   const int c = (int)(idx / 36), r = (int)(idx % 36) / 6, col = (int)(idx % 6);
   const long long n = 6LL * d.C;
   const double h = d.hccd[(long long)c * 21 + sym6(r, col)];
-  if (d.stiles)  // diag_tile[c / 8] holds camera c's diagonal block
-    d.stiles[(long long)d.blk_tile[d.nblk + c / 8] * kSTileElems + (6 * (c & 7) + col) * 48 + 6 * (c & 7) + r] += h;
+  if (d.stiles) {  // camera c's diagonal block inside its diagonal tile
+    const int2 bt = d.blk_tile[d.nblk + c];
+    d.stiles[(long long)bt.x * kSTileElems + (bt.y + col) * 48 + bt.y + r] += h;
+  }
   else
     d.schur[(6LL * c + col) * n + 6LL * c + r] += h;
 }

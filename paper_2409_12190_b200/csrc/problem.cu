@@ -673,38 +673,93 @@ void Problem::build_direct() {
 // sharded runs), its symbolic factorisation and the device structures.
 void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   const int C = d_.C;
-  const int n = 6 * C;
-  const int nt = (n + kTB - 1) / kTB;
-  std::vector<std::pair<int, int>> tp;
+  // camera graph: pairs of distinct cameras that share a point (the union
+  // over ranks on sharded runs, so that every rank derives the same order)
+  std::vector<long long> keys;
+  keys.reserve(bcam.size());
+  for (const int2& b : bcam)
+    if (b.x != b.y) keys.push_back(static_cast<long long>(b.x) * C + b.y);
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
   if (comm_) {
-    // union of the ranks' patterns: 0 = present, 1 = absent, min over ranks
-    const std::size_t ntri = static_cast<std::size_t>(nt) * (nt + 1) / 2;
-    std::vector<int> tri(ntri, 1);
-    for (const int2& b : bcam) tri[static_cast<std::size_t>(b.x / 8) * (b.x / 8 + 1) / 2 + b.y / 8] = 0;
-    int* dtri = nullptr;
-    ck(cudaMalloc(&dtri, ntri * sizeof(int)), "cudaMalloc");
-    ck(cudaMemcpyAsync(dtri, tri.data(), ntri * sizeof(int), cudaMemcpyHostToDevice, stream_), "H2D pattern");
-    comm_->allreduce_min(dtri, ntri, stream_);
-    ck(cudaMemcpyAsync(tri.data(), dtri, ntri * sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H pattern");
+    int* dcnt = nullptr;
+    ck(cudaMalloc(&dcnt, sizeof(int)), "cudaMalloc");
+    const int neg = -static_cast<int>(keys.size());
+    ck(cudaMemcpyAsync(dcnt, &neg, sizeof(int), cudaMemcpyHostToDevice, stream_), "H2D");
+    comm_->allreduce_min(dcnt, 1, stream_);  // -max count
+    int mx = 0;
+    ck(cudaMemcpyAsync(&mx, dcnt, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
     sync();
-    cudaFree(dtri);
-    for (int i = 0; i < nt; ++i)
-      for (int j = 0; j <= i; ++j)
-        if (tri[static_cast<std::size_t>(i) * (i + 1) / 2 + j] == 0) tp.emplace_back(i, j);
+    cudaFree(dcnt);
+    const std::size_t slot = static_cast<std::size_t>(std::max(-mx, 1));
+    std::vector<long long> mine(slot, -1), all(slot * comm_->world());
+    std::copy(keys.begin(), keys.end(), mine.begin());
+    long long* dbuf = nullptr;
+    ck(cudaMalloc(&dbuf, sizeof(long long) * slot * (comm_->world() + 1)), "cudaMalloc");
+    ck(cudaMemcpyAsync(dbuf, mine.data(), sizeof(long long) * slot, cudaMemcpyHostToDevice, stream_), "H2D");
+    comm_->allgather(dbuf, dbuf + slot, sizeof(long long) * slot, stream_);
+    ck(cudaMemcpyAsync(all.data(), dbuf + slot, sizeof(long long) * all.size(), cudaMemcpyDeviceToHost, stream_),
+       "D2H");
+    sync();
+    cudaFree(dbuf);
+    keys.clear();
+    for (long long k : all)
+      if (k >= 0) keys.push_back(k);
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  }
+  std::vector<std::pair<int, int>> edges;
+  edges.reserve(keys.size());
+  for (long long k : keys) edges.emplace_back(static_cast<int>(k / C), static_cast<int>(k % C));
+  // elimination order: nested dissection (BAE_ORDER=natural: camera order)
+  std::vector<std::vector<int>> groups;
+  const char* ord = std::getenv("BAE_ORDER");
+  if (ord && std::string(ord) == "natural") {
+    groups.emplace_back(C);
+    for (int c = 0; c < C; ++c) groups[0][c] = c;
   } else {
-    tp.reserve(bcam.size());
-    for (const int2& b : bcam) tp.emplace_back(b.x / 8, b.y / 8);
+    groups = nd_camera_groups(C, edges, 24);
+  }
+  // positions: groups in order, each padded to whole tiles (8 cameras)
+  std::vector<int> pos(static_cast<std::size_t>(C), -1), pos_cam;
+  for (const auto& g : groups) {
+    for (int c : g) {
+      pos[c] = static_cast<int>(pos_cam.size());
+      pos_cam.push_back(c);
+    }
+    while (pos_cam.size() % 8) pos_cam.push_back(-1);
+  }
+  const int npos = static_cast<int>(pos_cam.size());
+  const int n = 6 * npos;
+  const int nt = npos / 8;
+  chol_groups_ = static_cast<int>(groups.size());
+  std::vector<std::pair<int, int>> tp;
+  tp.reserve(edges.size());
+  for (const auto& e : edges) {
+    const int a = pos[e.first] / 8, b = pos[e.second] / 8;
+    tp.emplace_back(std::max(a, b), std::min(a, b));
   }
   const TileCholPlan pl = plan_tile_chol(n, tp);
-  // slot of every camera block's tile, then the diagonal slot of each tile column
-  std::vector<int> blk_tile;
-  blk_tile.reserve(bcam.size() + static_cast<std::size_t>(nt));
-  for (const int2& b : bcam) {
-    const int ti = b.x / 8, tj = b.y / 8;
+  auto slot_of = [&](int ti, int tj) {
     const auto first = pl.rowidx.begin() + pl.colptr[tj], last = pl.rowidx.begin() + pl.colptr[tj + 1];
-    blk_tile.push_back(static_cast<int>(std::lower_bound(first, last, ti) - pl.rowidx.begin()));
+    const auto it = std::lower_bound(first, last, ti);
+    if (it == last || *it != ti) throw Error(BAE_ERR_INVALID_ARGUMENT, "tile pattern misses a camera block");
+    return static_cast<int>(it - pl.rowidx.begin());
+  };
+  // per camera block: its tile slot and where it sits (transposed when the
+  // ordering puts camera(k) before camera(l)); then per camera its diagonal slot
+  std::vector<int2> blk_tile;
+  blk_tile.reserve(bcam.size() + static_cast<std::size_t>(C));
+  for (const int2& b : bcam) {
+    int p1 = pos[b.x], p2 = pos[b.y];
+    const int trans = p1 < p2 ? 1 : 0;
+    if (trans) std::swap(p1, p2);
+    blk_tile.push_back(int2{slot_of(p1 / 8, p2 / 8), 6 * (p1 % 8) | (6 * (p2 % 8)) << 8 | trans << 16});
   }
-  for (int j = 0; j < nt; ++j) blk_tile.push_back(pl.colptr[j]);
+  for (int c = 0; c < C; ++c) blk_tile.push_back(int2{slot_of(pos[c] / 8, pos[c] / 8), 6 * (pos[c] % 8)});
+  std::vector<unsigned long long> padmask(static_cast<std::size_t>(nt), 0ull);
+  for (int q = 0; q < npos; ++q)
+    if (pos_cam[q] < 0) padmask[q / 8] |= 0x3full << (6 * (q % 8));
   d_.blk_tile = upload(blk_tile);
   d_.stile_count = pl.nnz_tiles();
   d_.stiles = dalloc<double>(static_cast<std::size_t>(pl.nnz_tiles()) * kTT);
@@ -723,6 +778,8 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.rhs = d_.rhs;
   t.y = dalloc<double>(static_cast<std::size_t>(nt) * kTB);
   t.x = d_.x;
+  t.pos_cam = upload(pos_cam);
+  t.padmask = upload(padmask);
   t.nnz = static_cast<int>(pl.nnz_tiles());
   t.flags = dalloc<unsigned>(static_cast<std::size_t>(t.nnz) + nt);
   ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (static_cast<std::size_t>(t.nnz) + nt), stream_),
@@ -789,9 +846,9 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
       for (int j = 0; j < tchol_.nt; ++j) tb1 = std::max(tb1, trace[8 * static_cast<std::size_t>(j) + 7]);
       const double nt = tchol_.nt;
       std::fprintf(stderr,
-                   "[bae chol] nt %d tiles %lld updates %lld: factor span %.1f us, backward span %.1f us; per column "
+                   "[bae chol] groups %d nt %d tiles %lld updates %lld: factor span %.1f us, backward span %.1f us; per column "
                    "mean: wait+update %.2f potrf %.2f trinv %.2f trsm %.2f fwd+publish %.2f backward %.2f us\n",
-                   tchol_.nt, static_cast<long long>(d_.stile_count), chol_updates_, (t1 - t0) * 1e-3,
+                   chol_groups_, tchol_.nt, static_cast<long long>(d_.stile_count), chol_updates_, (t1 - t0) * 1e-3,
                    (tb1 - tb0) * 1e-3, upd / nt * 1e-3, pot / nt * 1e-3, inv / nt * 1e-3, trs / nt * 1e-3,
                    fwd / nt * 1e-3, bwd / nt * 1e-3);
       if (std::getenv("BAE_CHOL_TRACE")[0] == '2')

@@ -138,6 +138,7 @@ class Problem {
   unsigned chol_epoch_ = 0;
   int chol_grid_ = 0;
   long long chol_updates_ = 0;
+  int chol_groups_ = 0;
   long long pcg_chunk_launches_ = 0;  // kernels in one captured PCG chunk
 };
 
