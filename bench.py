@@ -8,13 +8,16 @@ defaults, max_iterations = 50, cli.hpp:25) and the reference's default
 solver (SolverChoice::cholesky, lm.hpp:34): on the GPU that is the dense
 reduced-camera-system direct solve. value = LM iterations per second over
 the K timed solves (device time, CUDA events on the solver stream), max over
-ranks; time_to_converge_s = mean device time per solve. With --gpus N > 1
+ranks; time_to_converge_s = mean device time per solve. The direct solve is
+the tile-sparse Cholesky of the reduced camera system (chol.cu). The larger
+BASELINE.json configs (Venice-1778, Final-13682) are solved the same way and
+reported under "configs". With --gpus N > 1
 (torchrun, one process per GPU) the same problem is sharded by landmark over
 the N GPUs (NCCL allreduce of the camera-sized sums), so the
 scaling is strong: value = LM iterations of the one joint solve / the max over
 ranks of the device time. The north-star
 implicit-Schur PCG path (solver = pcg) is measured the same way and
-reported under "pcg", with the roofline of its dominant kernel.
+reported under "pcg"; per-kernel rooflines under "kernels".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config NAME]
 
@@ -174,8 +177,32 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+# B200 FP64 datasheet figure: MEASURED_PEAKS.json has no FP64 number, so the
+# FP64 roofline of the Cholesky kernel is against this nominal peak.
+FP64_NOMINAL_TFLOPS = 40.0
+
+
+def _alg_bytes(kernel, st):
+    """Algorithmic HBM bytes per launch (each logically required array element
+    once): fused linearisation (K1 + camera pass) and
+    the implicit Schur tile pass (K5)."""
+    N, P, C, T, E = st["observations"], st["points"], st["cameras"], st["tiles"], st["entries"]
+    if kernel == "linearize":  # obs idx+px 22, points 24 + H_pp/g_p 72, entry partials 216 w + 216 r, cameras
+        return 22 * N + 96 * P + 432 * E + 368 * C + 16 * T
+    if kernel == "schur_tiles":  # blob 6/obs, points 24 + H~pp^-1 48, camera record+direction 176 + partial 48
+        return 6 * N + 72 * P + 224 * E + 32 * T
+    raise ValueError(kernel)
+
+
+def _chol_flops(ds):
+    """FP64 flops of one tile Cholesky factorisation (48 x 48 tiles): tile
+    updates and triangular solves (2 * 48^3 each) + per column factor and
+    inverse (~2 * 48^3 / 3)."""
+    g = 2 * 48 ** 3
+    return ds["tile_updates"] * g + (ds["tiles"] - ds["tile_columns"]) * g + ds["tile_columns"] * (g // 3)
+
+
 def run_b200(args):
-    import numpy as np
     import torch
     rank, world, dist = _dist_init(args.gpus)
     local = _env_int("LOCAL_RANK", 0)
@@ -183,89 +210,97 @@ def run_b200(args):
     import paper_2409_12190_b200 as bae
     from paper_2409_12190_b200.api import LmConfig, SolverChoice
 
-    C, P, N = bae.synthetic.CONFIGS[args.config]
-    # One problem for the whole job. N > 1: landmark-sharded over the ranks
-    # -- each rank owns a point partition and its observations,
-    # cameras are replicated, camera-sized partial sums are allreduced with
-    # NCCL (per LM phase, and once per PCG iteration).
-    scene = bae.synthetic.bal_shaped(C, P, N, seed=C)
-    cfg = LmConfig(max_iterations=50)  # reference defaults: solver = cholesky
-    cfg_pcg = LmConfig(max_iterations=50, solver=SolverChoice.pcg)
+    peak_hbm, peak_kind = _peaks()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
     def fresh_id():
+        # One problem for the whole job. N > 1: landmark-sharded over the ranks
+        # -- each rank owns a point partition and its
+        # observations, cameras are replicated, camera-sized partial sums are
+        # allreduced with NCCL (per LM phase, and once per PCG iteration).
         if world == 1:
             return {}
         obj = [bae.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return dict(rank=rank, world=world, nccl_id=obj[0])
 
-    prob = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local,
-                               **fresh_id())
-    stats = prob.stats()
-    shard_max_pts = int(_max_over_ranks(dist, prob.shard()[2]))
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    def make(scene):
+        return bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local,
+                                   **fresh_id())
 
-    def one_solve(c=None):
+    def one_solve(prob, scene, cfg):
         prob.set_parameters(scene.poses, scene.points)  # untimed: inputs resident before the timed solve
         flush.zero_()  # L2 flush between timed steps (L2 = 126 MB; 256 MB written)
         torch.cuda.synchronize()
-        rep = bae.optimize(prob, None, None, c or cfg)
-        return rep
+        return bae.optimize(prob, None, None, cfg)
 
-    for _ in range(args.warmup):
-        one_solve()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = prob.launch_count()
-    prob.phase_times(reset=True)
-    dev_s, iters, pcg = 0.0, 0, 0
-    reports = []
+    def series(prob, scene, cfg, steps, warmup, clk=None):
+        for _ in range(warmup):
+            one_solve(prob, scene, cfg)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = prob.launch_count()
+        prob.phase_times(reset=True)
+        dev, its, inner, reps = 0.0, 0, 0, []
+        for _ in range(steps):
+            r = one_solve(prob, scene, cfg)
+            reps.append(r)
+            dev += r.device_seconds
+            its += r.iterations
+            inner += r.total_pcg_iters
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ph = prob.phase_times(reset=True)
+        dev_max = _max_over_ranks(dist, dev)
+        return dict(value=its / dev_max, dev_max=dev_max, iterations=its, inner=inner, reports=reps,
+                    phases={k: v / steps for k, v in ph.items()}, launches=prob.launch_count() - l0)
+
+    C, P, N = bae.synthetic.CONFIGS[args.config]
+    scene = bae.synthetic.bal_shaped(C, P, N, seed=C)
+    cfg = LmConfig(max_iterations=50)  # reference defaults: solver = cholesky (here: tile-sparse Cholesky)
+    cfg_pcg = LmConfig(max_iterations=50, solver=SolverChoice.pcg)
+    prob = make(scene)
+    stats = prob.stats()
+    shard_max_pts = int(_max_over_ranks(dist, prob.shard()[2]))
+
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            rep = one_solve()
-            reports.append(rep)
-            dev_s += rep.device_seconds
-            iters += rep.iterations
-            pcg += rep.total_pcg_iters
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    launches = prob.launch_count() - launches0
-    phases = prob.phase_times(reset=True)
-    dev_max = _max_over_ranks(dist, dev_s)
-    value = iters / dev_max  # whole-job LM iterations / s (one jointly solved problem)
+        head = series(prob, scene, cfg, args.steps, args.warmup)
+    last = head["reports"][-1]
+    ds = prob.direct_stats()
 
-    # --- north-star PCG path, same protocol ---
-    for _ in range(max(1, args.warmup // 2)):
-        one_solve(cfg_pcg)
-    prob.phase_times(reset=True)
-    pcg_dev, pcg_it, pcg_inner = 0.0, 0, 0
-    pcg_steps = max(1, min(args.steps, 3))
-    for _ in range(pcg_steps):
-        r = one_solve(cfg_pcg)
-        pcg_dev += r.device_seconds
-        pcg_it += r.iterations
-        pcg_inner += r.total_pcg_iters
-    pcg_phases = prob.phase_times(reset=True)
-    pcg_dev = _max_over_ranks(dist, pcg_dev)
-    pcg_value = pcg_it / pcg_dev
+    # --- north-star implicit-Schur PCG path, same protocol ---
+    pcg = series(prob, scene, cfg_pcg, max(1, min(args.steps, 3)), max(1, args.warmup // 2))
 
-    # --- kernel-level measurements (device events on the solver stream) ---
+    # --- kernel-level device times (CUDA events on the solver stream) ---
     ms_lin = prob.time_kernel(0, 20)
     ms_sx = prob.time_kernel(1, 50)
     ms_pcg = prob.time_kernel(2, 50)
-    peak, peak_kind = _peaks()
-    # SURVEY.md 8(d) algorithmic bytes per unit: K5 (S*p per PCG iteration)
-    alg_sx = 280 * N + 48 * P + 800 * C
-    achieved = alg_sx / (ms_sx * 1e-3) / 1e9
+    ms_chol = prob.time_kernel(4, 20)
+    lin_b, sx_b, chol_f = _alg_bytes("linearize", stats), _alg_bytes("schur_tiles", stats), _chol_flops(ds)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get("k_schur_tiles")
+            traffic = json.load(open(tpath)).get(args.config, {}).get("k_tile_chol_factor")
         except Exception:
             traffic = None
+    solve_ms = 1e3 * head["dev_max"] / args.steps
+    chol_share = head["phases"].get("factor", 0.0) / solve_ms if solve_ms else None
+    kernels = [
+        {"kernel": "k_tile_chol_factor + k_tile_chol_backward (direct solve, per LM iteration)", "us": 1e3 * ms_chol,
+         "bound": "fp64 pipe / latency", "achieved": chol_f / (ms_chol * 1e-3) / 1e12, "unit": "TFLOP/s",
+         "peak": FP64_NOMINAL_TFLOPS, "peak_source": "nominal FP64",
+         "frac": chol_f / (ms_chol * 1e-3) / 1e12 / FP64_NOMINAL_TFLOPS},
+        {"kernel": "k_linearize + k_cam_linearize + k_lin_totals (fused residual + Jacobian + J^T J / J^T r blocks)",
+         "us": 1e3 * ms_lin, "bound": "hbm", "achieved": lin_b / (ms_lin * 1e-3) / 1e9, "unit": "GB/s",
+         "peak": peak_hbm, "frac": lin_b / (ms_lin * 1e-3) / 1e9 / peak_hbm, "obs_per_s": N / (ms_lin * 1e-3)},
+        {"kernel": "k_schur_tiles (implicit Schur S*p tile pass, per PCG iteration)", "us": 1e3 * ms_sx,
+         "bound": "hbm", "achieved": sx_b / (ms_sx * 1e-3) / 1e9, "unit": "GB/s", "peak": peak_hbm,
+         "frac": sx_b / (ms_sx * 1e-3) / 1e9 / peak_hbm},
+        {"kernel": "one PCG iteration (tile pass + camera pass + update)", "us": 1e3 * ms_pcg},
+    ]
 
     # --- end to end through the C ABI with host buffers (create + solve + read back) ---
     e2e_iters, e2e_s = 0, 0.0
@@ -277,18 +312,42 @@ def run_b200(args):
         t0 = time.perf_counter()
         p2 = bae.make_ba_problem(scene.poses, scene.points, scene.intrinsics, scene.observations, device=local,
                                  **ids)
-        st = {}
-        r2 = bae.optimize(p2, scene.poses, scene.points, cfg, final_state=st)
+        r2 = bae.optimize(p2, scene.poses, scene.points, cfg, final_state={})
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
         del p2
-        if i > 0:  # first one warms host allocations
+        if i > 0:  # the first one warms host allocations
             e2e_iters += r2.iterations
             e2e_s += el
     e2e_max = _max_over_ranks(dist, e2e_s)
     e2e_value = e2e_iters / e2e_max
     h2d = 56 * C + 24 * P + 24 * C + 24 * N + 56 * C + 24 * P  # create inputs + optimize init params
     d2h = 56 * C + 24 * P
+
+    # --- the larger BASELINE.json configs: time-to-converge with the reference defaults ---
+    extra = {}
+    if not args.no_extra:
+        for name in ("venice-1778", "final-13682"):
+            c2, p2_, n2 = bae.synthetic.CONFIGS[name]
+            sc = bae.synthetic.config_scene(name)
+            t0 = time.perf_counter()
+            pr = make(sc)
+            t_create = _max_over_ranks(dist, time.perf_counter() - t0)
+            ser = series(pr, sc, cfg, 2, 1)
+            r = ser["reports"][-1]
+            ms_l = pr.time_kernel(0, 5)
+            st2 = pr.stats()
+            extra[name] = {
+                "workload": f"{name} BA (C={c2}, P={p2_}, N={n2}), LmConfig defaults (direct solve)",
+                "lm_iters_per_s": ser["value"], "time_to_converge_s": ser["dev_max"] / 2,
+                "lm_iterations": r.iterations, "termination": r.reason.name, "final_mse": r.final_mse,
+                "ms_per_lm_iteration": 1e3 * ser["dev_max"] / max(1, ser["iterations"]),
+                "phase_ms_per_solve": ser["phases"], "create_s": t_create,
+                "obs_per_s_residual_jacobian": n2 / (_max_over_ranks(dist, ms_l) * 1e-3),
+                "linearize_hbm_frac": _alg_bytes("linearize", st2) / (ms_l * 1e-3) / 1e9 / peak_hbm,
+                "direct": pr.direct_stats(),
+            }
+            del pr
 
     clocks = clk.summary()
     if rank == 0:
@@ -298,34 +357,40 @@ def run_b200(args):
             cpu = {"value": v, "unit": "LM iter/s", "cores": os.cpu_count() or 1, "kind": "port",
                    "sample": f"2 LM iterations of the reference algorithm (oracle port, Cholesky) on "
                              f"{args.config}, {el:.1f} s"}
-        last = reports[-1]
+        chol_ach = chol_f / (ms_chol * 1e-3) / 1e12
         line = {
-            "metric": "lm_iters_per_s", "value": value, "unit": "LM iter/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 * dev_max / args.steps, "higher_is_better": True,
+            "metric": "lm_iters_per_s", "value": head["value"], "unit": "LM iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": solve_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic BAL-shaped (SURVEY.md 8d generator, seed = camera count)",
             "config": {"workload": f"{args.config} BA (C={C}, P={P}, N={N}), LM with LmConfig defaults "
-                                   f"(solver=cholesky, max_iterations=50) from the same initial state each step",
+                                   f"(solver=cholesky: tile-sparse Cholesky of the reduced camera system, "
+                                   f"max_iterations=50) from the same initial state each step",
                        "parallelism": (f"landmark-sharded over {world} GPUs (NCCL allreduce of camera vectors)"
                                        if world > 1 else "single GPU"),
                        "points_per_rank_max": shard_max_pts,
                        "l2": "flushed (256 MB write) between steps",
-                       "tiles": stats["tiles"], "tile_camera_entries": stats["entries"]},
-            "time_to_converge_s": dev_max / args.steps,
-            "lm_iterations_per_solve": last.iterations, "pcg_iterations_per_solve": last.total_pcg_iters,
-            "final_mse": last.final_mse, "termination": last.reason.name,
+                       "tiles": stats["tiles"], "tile_camera_entries": stats["entries"], "direct": ds},
+            "time_to_converge_s": head["dev_max"] / args.steps,
+            "lm_iterations_per_solve": last.iterations, "final_mse": last.final_mse,
+            "termination": last.reason.name,
             "obs_per_s_residual_jacobian": N / (ms_lin * 1e-3),
-            "kernel_us": {"linearize": ms_lin * 1e3, "schur_tiles": ms_sx * 1e3, "pcg_iteration": ms_pcg * 1e3},
-            "phase_ms_per_solve": {k: v / args.steps for k, v in phases.items()},
-            "pcg": {"lm_iters_per_s": pcg_value, "phase_ms_per_solve": {k: v / pcg_steps for k, v in pcg_phases.items()}, "time_to_converge_s": pcg_dev / pcg_steps,
-                    "pcg_iterations_per_solve": pcg_inner / pcg_steps,
+            "phase_ms_per_solve": head["phases"],
+            "pcg": {"lm_iters_per_s": pcg["value"], "time_to_converge_s": pcg["dev_max"] / len(pcg["reports"]),
+                    "pcg_iterations_per_solve": pcg["inner"] / len(pcg["reports"]),
+                    "phase_ms_per_solve": pcg["phases"],
                     "config": "same workload, solver=pcg (implicit-Schur PCG, block-Jacobi), pcg_tol=1e-8"},
-            "roofline": {"bound": "hbm", "kernel": "k_schur_tiles (implicit Schur S*p, per PCG iteration)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_kind,
-                         "algorithmic_bytes": "SURVEY 8(d) K5: 280 N + 48 P + 800 C per launch"},
+            "roofline": {"bound": "tensor", "kernel": "k_tile_chol_factor + k_tile_chol_backward",
+                         "achieved": chol_ach, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s",
+                         "frac": chol_ach / FP64_NOMINAL_TFLOPS, "traffic": traffic,
+                         "peak_source": "nominal B200 FP64 (FMA pipe, not tcgen05; no measured FP64 peak)",
+                         "share_of_step": chol_share,
+                         "limiter": "latency: the dependent pivot chain along the nested-dissection tree",
+                         "algorithmic_flops": "2*48^3 per tile update / solve + 2*48^3/3 per tile column"},
+            "kernels": kernels,
+            "configs": extra,
             "e2e": {"value": e2e_value, "unit": "LM iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches,
+            "gpu_launches": head["launches"],
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
@@ -340,6 +405,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=BASE_CFG)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the Venice / Final time-to-converge lines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -220,7 +220,9 @@ int bae_partition_points(int32_t num_cameras, int32_t num_points, const int32_t*
  * launches: kind 0 = linearisation (fused residual + Jacobian + block
  * reductions), 1 = one implicit Schur S*x product (one PCG iteration's
  * operator), 2 = one full PCG iteration, 3 = fused residual+Jacobian to HBM
- * (stored J). ms receives the mean milliseconds per launch. */
+ * (stored J), 4 = tile-sparse Cholesky factorisation + forward/backward
+ * substitution of the reduced camera system (direct solver). ms receives the
+ * mean milliseconds per launch. */
 int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms);
 /* Number of kernel launches issued by this handle since creation. */
 int64_t bae_launch_count(const bae_problem* p);
@@ -231,6 +233,9 @@ int bae_phase_times(bae_problem* p, double* ms7, int32_t reset);
 /* This handle's shard: rank, world, points and observations it owns. */
 int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32_t* local_points,
                       int64_t* local_observations);
+/* Direct solver structure (after its first use): [tile columns, stored
+ * 48x48 tiles, tile updates, nested-dissection groups, camera positions]. */
+int bae_direct_stats(const bae_problem* p, int64_t* out5);
 /* Static sizes the roofline arithmetic needs: [N, P, C, tiles, tile-camera
  * entries, max obs per tile]. */
 int bae_problem_stats(const bae_problem* p, int64_t* out6);

@@ -115,6 +115,7 @@ SIGNATURES = {
     "bae_phase_times": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int32]),
     "bae_problem_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
     "bae_problem_shard": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p]),
+    "bae_direct_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
 }
 
 _lib = None

@@ -309,6 +309,13 @@ class TracedProblem:
                                              ctypes.byref(lo)))
         return r.value, w.value, lp.value, lo.value
 
+    def direct_stats(self):
+        """Tile Cholesky structure of the direct solver (zeros before its first use)."""
+        out = np.zeros(5, np.int64)
+        _check(_lib.load().bae_direct_stats(self._h, ptr(out, ctypes.c_int64)))
+        keys = ("tile_columns", "tiles", "tile_updates", "nd_groups", "positions")
+        return dict(zip(keys, (int(v) for v in out)))
+
     def stats(self):
         out = np.empty(6, np.int64)
         _check(_lib.load().bae_problem_stats(self._h, ptr(out, ctypes.c_int64)))

@@ -264,6 +264,14 @@ int bae_phase_times(bae_problem* p, double* ms7, int32_t reset) {
   });
 }
 
+int bae_direct_stats(const bae_problem* p, int64_t* out5) {
+  return guarded([&] {
+    long long v[5];
+    p->impl->direct_stats(v);
+    for (int i = 0; i < 5; ++i) out5[i] = v[i];
+  });
+}
+
 int bae_problem_stats(const bae_problem* p, int64_t* out6) {
   return guarded([&] {
     const bae::Plan& pl = p->impl->plan();

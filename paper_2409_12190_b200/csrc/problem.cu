@@ -1101,6 +1101,14 @@ double Problem::time_kernel(int kind, int reps) {
     s.tol = 0.0;
     ck(cudaMemcpy(d_.pcg, &s, sizeof(PcgDev), cudaMemcpyHostToDevice), "H2D pcg");
   }
+  if (kind == 4) {  // one damped direct solve first: S assembled, plan built
+    linearize();
+    SolveInfo info;
+    bae_lm_config c2 = cfg;
+    c2.solver = BAE_SOLVER_CHOLESKY;
+    solve(1e-4, c2, info);
+    if (!use_tiles_) throw Error(BAE_ERR_UNSUPPORTED, "time_kernel 4 needs the tile solver");
+  }
   double* js = nullptr;
   if (kind == 3) {
     ck(cudaMalloc(&js, 18 * sizeof(double) * plan_.N), "cudaMalloc");
@@ -1119,6 +1127,9 @@ double Problem::time_kernel(int kind, int reps) {
         break;
       case 3:
         launches_ += launch_linearize(d_, sm_, true, stream_, comm_.get());
+        break;
+      case 4:  // tile Cholesky factor + both substitutions (re-factors the factor: same work)
+        launches_ += launch_tile_chol(tchol_, ++chol_epoch_, chol_grid_, stream_);
         break;
       default:
         throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");

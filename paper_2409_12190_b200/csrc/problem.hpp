@@ -69,6 +69,14 @@ class Problem {
   void optimize(const double* poses7, const double* points3, const bae_lm_config& cfg,
                 std::vector<bae_iter_record>& traj, bae_lm_report& rep);
   double time_kernel(int kind, int reps);
+  // [tile columns, stored tiles, tile updates, ordering groups, positions] of the tile Cholesky (0 before use)
+  void direct_stats(long long* out5) const {
+    out5[0] = tchol_.nt;
+    out5[1] = tchol_.nnz;
+    out5[2] = chol_updates_;
+    out5[3] = chol_groups_;
+    out5[4] = tchol_.n / 6;
+  }
 
  private:
   template <class T>
