@@ -321,6 +321,22 @@ def run_b200(args):
             e2e_s += el
     e2e_max = _max_over_ranks(dist, e2e_s)
     e2e_value = e2e_iters / e2e_max
+    # warm variant: optimize on the existing problem through the public API
+    # (initial parameters H2D, solve, final parameters D2H) -- what the
+    # reference arm times (its problem is built outside the timed region)
+    w_iters, w_s = 0, 0.0
+    for i in range(max(1, min(args.steps, 3)) + 1):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r3 = bae.optimize(prob, scene.poses, scene.points, cfg, final_state={})
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if i > 0:
+            w_iters += r3.iterations
+            w_s += el
+    e2e_warm = w_iters / _max_over_ranks(dist, w_s)
     h2d = 56 * C + 24 * P + 24 * C + 24 * N + 56 * C + 24 * P  # create inputs + optimize init params
     d2h = 56 * C + 24 * P
 
@@ -389,7 +405,11 @@ def run_b200(args):
                          "algorithmic_flops": "2*48^3 per tile update / solve + 2*48^3/3 per tile column"},
             "kernels": kernels,
             "configs": extra,
-            "e2e": {"value": e2e_value, "unit": "LM iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_value, "unit": "LM iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "includes": "make_ba_problem (planning, upload) + optimize + parameter read-back, every step",
+                    "warm": {"value": e2e_warm, "unit": "LM iter/s", "h2d_bytes_per_step": 56 * C + 24 * P,
+                             "d2h_bytes_per_step": d2h,
+                             "includes": "optimize(init params from host) + read-back on an existing problem"}},
             "gpu_launches": head["launches"],
             "clocks": clocks,
             "cpu_baseline": cpu,

@@ -2,8 +2,11 @@
 // and the C ABI.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "bae_b200.h"
@@ -61,6 +64,28 @@ struct Plan {
   int n_big = 0, big_obs = 0, big_cams = 0, big_pts = 0;
   bool has_empty_camera = false, has_empty_point = false;
 };
+
+// Host worker count for the setup passes: BAE_HOST_THREADS, else the
+// hardware concurrency, capped at 16.
+inline int host_threads() {
+  if (const char* e = std::getenv("BAE_HOST_THREADS")) return std::max(1, std::atoi(e));
+  return static_cast<int>(std::clamp(std::thread::hardware_concurrency(), 1u, 16u));
+}
+
+// f(chunk, begin, end) over `chunks` contiguous ranges of [0, n) (chunk 0 on
+// the calling thread). Chunk boundaries depend only on n and chunks, so a
+// caller that combines per-chunk results in chunk order is deterministic.
+template <class F>
+void parallel_chunks(std::int64_t n, int chunks, F&& f) {
+  if (chunks <= 1 || n < 2) {
+    f(0, std::int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int c = 1; c < chunks; ++c) th.emplace_back([&, c] { f(c, n * c / chunks, n * (c + 1) / chunks); });
+  f(0, std::int64_t{0}, n / chunks);
+  for (auto& t : th) t.join();
+}
 
 // Validation follows make_ba_problem (problems.hpp:90-110): per observation,
 // camera index before point index, IndexError carries the position.

@@ -10,12 +10,29 @@
 // (see Plan in bae_internal.hpp). Everything here is O(N + P + C) counting
 // sorts.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
 #include "bae_internal.hpp"
 
 namespace bae {
+
+namespace {
+// BAE_HOST_TIMING=1: planner stage times on stderr.
+struct StageTimer {
+  bool on = std::getenv("BAE_HOST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bae plan] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
 
 void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N) {
   if (N <= 0) throw Error(BAE_ERR_INVALID_ARGUMENT, "make_ba_problem: no observations");
@@ -30,6 +47,7 @@ void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32
 
 Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2,
                 std::int64_t N, int tile_obs_target, int tile_cam_cap, int tile_pts_cap, int smem_tile_obs_cap) {
+  StageTimer st;
   Plan pl;
   pl.C = C;
   pl.P = P;
@@ -54,7 +72,14 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
     std::vector<std::int32_t> cur(pcnt.begin(), pcnt.end() - 1);
     for (std::int64_t k = 0; k < N; ++k) pobs[cur[pt_idx[k]]++] = static_cast<std::int32_t>(k);
   }
+  const int nth = N >= (1 << 16) ? host_threads() : 1;
+  // camera of each observation in point order (one gather instead of one per pass)
+  std::vector<std::int32_t> pcam(static_cast<std::size_t>(N));
+  parallel_chunks(N, nth, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t j = b; j < e; ++j) pcam[j] = cam_idx[pobs[j]];
+  });
 
+  st.mark("point lists");
   // Internal point order: stable counting sort by the lowest observing camera,
   // so consecutive points share cameras and a tile touches few of them.
   std::vector<std::int32_t> mincam(static_cast<std::size_t>(P), C);
@@ -72,6 +97,7 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
     }
   }
 
+  st.mark("internal order");
   // Greedy tile packing over internal points.
   std::vector<std::int32_t> stamp(static_cast<std::size_t>(C), -1), seen(static_cast<std::size_t>(C), -1);
   std::vector<std::vector<std::int32_t>> tile_cams;
@@ -82,13 +108,13 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
   auto distinct_new = [&](int p, int tile) {
     int n = 0;
     for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
-      const int c = cam_idx[pobs[j]];
+      const int c = pcam[j];
       if (stamp[c] != tile && seen[c] != p) {
         seen[c] = p;
         ++n;
       }
     }
-    for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) seen[cam_idx[pobs[j]]] = -1;
+    for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) seen[pcam[j]] = -1;
     return n;
   };
   for (int i = 0; i < P; ++i) {
@@ -107,7 +133,7 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
       newc = distinct_new(p, t);
     }
     for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
-      const int c = cam_idx[pobs[j]];
+      const int c = pcam[j];
       if (stamp[c] != t) {
         stamp[c] = t;
         cur_cams.push_back(c);
@@ -121,54 +147,69 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
   pl.tile_obs_begin.push_back(pl.tile_obs_begin.back() + t_obs);
   pl.T = t + 1;
 
+  st.mark("tile packing");
   // Per-tile slot order: (local camera, internal point, observation id).
+  // Tiles are independent once their entry offsets are known: sort the
+  // camera lists and fill the slots in parallel chunks of tiles.
   pl.obs_lcpt.resize(static_cast<std::size_t>(N));
   pl.obs_orig.resize(static_cast<std::size_t>(N));
   pl.obs_px.resize(static_cast<std::size_t>(N) * 2);
   pl.pt_ptr.assign(static_cast<std::size_t>(P) + 1, 0);
   pl.ptobs.resize(static_cast<std::size_t>(N));
-  pl.tile_ent_begin.push_back(0);
   pl.tile_ws.assign(static_cast<std::size_t>(pl.T), -1);
-  std::vector<std::int32_t> lcam_of(static_cast<std::size_t>(C), -1);
-  std::vector<std::int32_t> seg;
+  pl.tile_ent_begin.assign(static_cast<std::size_t>(pl.T) + 1, 0);
   for (int tt = 0; tt < pl.T; ++tt) {
-    auto& cams = tile_cams[tt];
-    std::sort(cams.begin(), cams.end());
-    const int nc = static_cast<int>(cams.size());
-    for (int l = 0; l < nc; ++l) lcam_of[cams[l]] = l;
-    const std::int32_t ob = pl.tile_obs_begin[tt], oe = pl.tile_obs_begin[tt + 1];
-    const std::int32_t pb = pl.tile_pt_begin[tt], pe = pl.tile_pt_begin[tt + 1];
-    const int nobs = oe - ob, npts = pe - pb;
-    if (nobs > 65536) throw Error(BAE_ERR_UNSUPPORTED, "tile exceeds 65536 observations");
-    seg.assign(static_cast<std::size_t>(nc) + 1, 0);
-    for (int i = pb; i < pe; ++i) {
-      const int p = pl.pt_of_internal[i];
-      for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) ++seg[lcam_of[cam_idx[pobs[j]]] + 1];
-    }
-    std::partial_sum(seg.begin(), seg.end(), seg.begin());
-    for (int l = 0; l < nc; ++l) {
-      pl.ent_cam.push_back(cams[l]);
-      pl.ent_obs_begin.push_back(ob + seg[l]);
-    }
-    pl.E += nc;
-    pl.tile_ent_begin.push_back(pl.E);
-    std::int32_t pcur = ob;
-    for (int i = pb; i < pe; ++i) {
-      const int p = pl.pt_of_internal[i];
-      pl.pt_ptr[i] = pcur;
-      for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
-        const std::int32_t k = pobs[j];
-        const int l = lcam_of[cam_idx[k]];
-        const std::int32_t local = seg[l]++;
-        const std::int32_t slot = ob + local;
-        pl.obs_lcpt[slot] = static_cast<std::uint32_t>(l) | (static_cast<std::uint32_t>(i - pb) << 16);
-        pl.obs_orig[slot] = k;
-        pl.obs_px[2 * static_cast<std::size_t>(slot)] = px2[2 * k];
-        pl.obs_px[2 * static_cast<std::size_t>(slot) + 1] = px2[2 * k + 1];
-        pl.ptobs[pcur++] = static_cast<std::uint16_t>(local);
+    if (pl.tile_obs_begin[tt + 1] - pl.tile_obs_begin[tt] > 65536)
+      throw Error(BAE_ERR_UNSUPPORTED, "tile exceeds 65536 observations");
+    pl.tile_ent_begin[tt + 1] = pl.tile_ent_begin[tt] + static_cast<std::int32_t>(tile_cams[tt].size());
+  }
+  pl.E = pl.tile_ent_begin[pl.T];
+  pl.ent_cam.resize(static_cast<std::size_t>(pl.E));
+  pl.ent_obs_begin.resize(static_cast<std::size_t>(pl.E) + 1);
+  parallel_chunks(pl.T, pl.T >= 256 ? nth : 1, [&](int, std::int64_t t0, std::int64_t t1) {
+    std::vector<std::int32_t> lcam_of(static_cast<std::size_t>(C), -1);
+    std::vector<std::int32_t> seg;
+    for (std::int64_t tt = t0; tt < t1; ++tt) {
+      auto& cams = tile_cams[tt];
+      std::sort(cams.begin(), cams.end());
+      const int nc = static_cast<int>(cams.size());
+      for (int l = 0; l < nc; ++l) lcam_of[cams[l]] = l;
+      const std::int32_t ob = pl.tile_obs_begin[tt];
+      const std::int32_t pb = pl.tile_pt_begin[tt], pe = pl.tile_pt_begin[tt + 1];
+      seg.assign(static_cast<std::size_t>(nc) + 1, 0);
+      for (int i = pb; i < pe; ++i) {
+        const int p = pl.pt_of_internal[i];
+        for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) ++seg[lcam_of[pcam[j]] + 1];
       }
+      std::partial_sum(seg.begin(), seg.end(), seg.begin());
+      const std::int32_t eb = pl.tile_ent_begin[tt];
+      for (int l = 0; l < nc; ++l) {
+        pl.ent_cam[eb + l] = cams[l];
+        pl.ent_obs_begin[eb + l] = ob + seg[l];
+      }
+      std::int32_t pcur = ob;
+      for (int i = pb; i < pe; ++i) {
+        const int p = pl.pt_of_internal[i];
+        pl.pt_ptr[i] = pcur;
+        for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
+          const std::int32_t k = pobs[j];
+          const int l = lcam_of[pcam[j]];
+          const std::int32_t local = seg[l]++;
+          const std::int32_t slot = ob + local;
+          pl.obs_lcpt[slot] = static_cast<std::uint32_t>(l) | (static_cast<std::uint32_t>(i - pb) << 16);
+          pl.obs_orig[slot] = k;
+          pl.obs_px[2 * static_cast<std::size_t>(slot)] = px2[2 * k];
+          pl.obs_px[2 * static_cast<std::size_t>(slot) + 1] = px2[2 * k + 1];
+          pl.ptobs[pcur++] = static_cast<std::uint16_t>(local);
+        }
+      }
+      for (int l = 0; l < nc; ++l) lcam_of[cams[l]] = -1;
     }
-    for (int l = 0; l < nc; ++l) lcam_of[cams[l]] = -1;
+  });
+  for (int tt = 0; tt < pl.T; ++tt) {
+    const int nobs = pl.tile_obs_begin[tt + 1] - pl.tile_obs_begin[tt];
+    const int npts = pl.tile_pt_begin[tt + 1] - pl.tile_pt_begin[tt];
+    const int nc = pl.tile_ent_begin[tt + 1] - pl.tile_ent_begin[tt];
     pl.max_tile_obs = std::max(pl.max_tile_obs, nobs);
     pl.max_tile_cams = std::max(pl.max_tile_cams, nc);
     pl.max_tile_pts = std::max(pl.max_tile_pts, npts);
@@ -180,8 +221,9 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
     }
   }
   pl.pt_ptr[P] = static_cast<std::int32_t>(N);
-  pl.ent_obs_begin.push_back(static_cast<std::int32_t>(N));
+  pl.ent_obs_begin[pl.E] = static_cast<std::int32_t>(N);
 
+  st.mark("slot order");
   // Entries of each camera in ascending entry (= tile) order.
   pl.cam_ent_ptr.assign(static_cast<std::size_t>(C) + 1, 0);
   for (int e = 0; e < pl.E; ++e) ++pl.cam_ent_ptr[pl.ent_cam[e] + 1];
@@ -191,6 +233,7 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
     std::vector<std::int32_t> cur(pl.cam_ent_ptr.begin(), pl.cam_ent_ptr.end() - 1);
     for (int e = 0; e < pl.E; ++e) pl.cam_ent[cur[pl.ent_cam[e]]++] = e;
   }
+  st.mark("camera entries");
   return pl;
 }
 

@@ -578,20 +578,20 @@ void Problem::build_direct() {
   for (int t = 0; t < pl.T; ++t)
     for (int e = pl.tile_ent_begin[t]; e < pl.tile_ent_begin[t + 1]; ++e)
       for (int sl = pl.ent_obs_begin[e]; sl < pl.ent_obs_begin[e + 1]; ++sl) cam_of_slot[sl] = pl.ent_cam[e];
-  // Pairs in generation order (point, k, l), bucketed by c1 = camera(k) with a
-  // counting sort, then each c1 bucket stably by c2 = camera(l).
-  auto for_pairs = [&](auto&& emit) {
+  // Pairs in generation order (tile, point, k, l), bucketed by c1 = camera(k)
+  // with a counting sort, then each c1 bucket stably by c2 = camera(l). Both
+  // passes run over contiguous chunks of tiles (chunk-ordered offsets keep the
+  // sequential order), the per-c1 sorts over chunks of c1.
+  auto for_pairs = [&](int t0, int t1, auto&& emit) {
     int kc[256], ks[256];
-    for (int t = 0; t < pl.T; ++t) {
+    for (int t = t0; t < t1; ++t) {
       const int ob = pl.tile_obs_begin[t];
       for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
         const int m = pl.pt_ptr[i + 1] - pl.pt_ptr[i];
-        for (int q = 0; q < m; ++q) {
+        for (int q = 0; q < m && q < 256; ++q) {
           const int sl = ob + pl.ptobs[pl.pt_ptr[i] + q];
-          if (q < 256) {
-            ks[q] = sl;
-            kc[q] = cam_of_slot[sl];
-          }
+          ks[q] = sl;
+          kc[q] = cam_of_slot[sl];
         }
         if (m <= 256) {
           for (int a = 0; a < m; ++a)
@@ -607,42 +607,63 @@ void Problem::build_direct() {
       }
     }
   };
+  const int nch = pl.T >= 256 ? host_threads() : 1;
+  std::vector<std::vector<long long>> ccnt(static_cast<std::size_t>(nch),
+                                           std::vector<long long>(static_cast<std::size_t>(C), 0));
+  parallel_chunks(pl.T, nch, [&](int ch, std::int64_t t0, std::int64_t t1) {
+    auto& cc = ccnt[ch];
+    for_pairs(static_cast<int>(t0), static_cast<int>(t1), [&](int c1, int, int, int) { ++cc[c1]; });
+  });
   std::vector<long long> row(static_cast<std::size_t>(C) + 1, 0);
-  for_pairs([&](int c1, int, int, int) { ++row[c1 + 1]; });
-  for (int c = 0; c < C; ++c) row[c + 1] += row[c];
+  for (int c = 0; c < C; ++c) {  // bucket c1: chunk 0's pairs, then chunk 1's, ... (= tile order)
+    long long at = row[c];
+    for (int ch = 0; ch < nch; ++ch) {
+      const long long m = ccnt[ch][c];
+      ccnt[ch][c] = at;
+      at += m;
+    }
+    row[c + 1] = at;
+  }
   const std::size_t np = static_cast<std::size_t>(row[C]);
   if (np >= (std::size_t{1} << 31)) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
   std::vector<int2> bucket(np), sorted(np);
   std::vector<int> bucket_c2(np);
-  {
-    std::vector<long long> cur(row.begin(), row.end() - 1);
-    for_pairs([&](int c1, int c2, int k, int l) {
+  parallel_chunks(pl.T, nch, [&](int ch, std::int64_t t0, std::int64_t t1) {
+    auto& cur = ccnt[ch];
+    for_pairs(static_cast<int>(t0), static_cast<int>(t1), [&](int c1, int c2, int k, int l) {
       const long long at = cur[c1]++;
       bucket[at] = int2{k, l};
       bucket_c2[at] = c2;
     });
-  }
+  });
+  std::vector<std::vector<int2>> blocks(static_cast<std::size_t>(C));  // per c1: (c2, pairs)
+  parallel_chunks(C, C >= 64 ? nch : 1, [&](int, std::int64_t cb, std::int64_t ce) {
+    std::vector<long long> cnt(static_cast<std::size_t>(C), 0);
+    std::vector<int> seen;
+    for (std::int64_t c1 = cb; c1 < ce; ++c1) {
+      const long long b = row[c1], e = row[c1 + 1];
+      seen.clear();
+      for (long long q = b; q < e; ++q)
+        if (cnt[bucket_c2[q]]++ == 0) seen.push_back(bucket_c2[q]);
+      std::sort(seen.begin(), seen.end());
+      long long at = b;
+      for (int c2 : seen) {
+        const long long m = cnt[c2];
+        cnt[c2] = at;  // becomes the write cursor
+        blocks[c1].push_back(int2{c2, static_cast<int>(m)});
+        at += m;
+      }
+      for (long long q = b; q < e; ++q) sorted[cnt[bucket_c2[q]]++] = bucket[q];
+      for (int c2 : seen) cnt[c2] = 0;
+    }
+  });
   std::vector<int> bptr{0};
   std::vector<int2> bcam;
-  std::vector<long long> cnt(static_cast<std::size_t>(C) + 1, 0);
-  std::vector<int> seen;
-  for (int c1 = 0; c1 < C; ++c1) {
-    const long long b = row[c1], e = row[c1 + 1];
-    seen.clear();
-    for (long long q = b; q < e; ++q)
-      if (cnt[bucket_c2[q]]++ == 0) seen.push_back(bucket_c2[q]);
-    std::sort(seen.begin(), seen.end());
-    long long at = b;
-    for (int c2 : seen) {
-      const long long m = cnt[c2];
-      cnt[c2] = at;  // becomes the write cursor
-      bcam.push_back(int2{c1, c2});
-      bptr.push_back(static_cast<int>(at + m));
-      at += m;
+  for (int c1 = 0; c1 < C; ++c1)
+    for (const int2& bl : blocks[c1]) {
+      bcam.push_back(int2{c1, bl.x});
+      bptr.push_back(bptr.back() + bl.y);
     }
-    for (long long q = b; q < e; ++q) sorted[cnt[bucket_c2[q]]++] = bucket[q];
-    for (int c2 : seen) cnt[c2] = 0;
-  }
   d_.pairs = upload(sorted);
   d_.blk_ptr = upload(bptr);
   d_.blk_cam = upload(bcam);
