@@ -41,6 +41,8 @@ extern "C" {
 #define BAE_ERR_UNSUPPORTED 6         /* UnsupportedOperationError                 */
 #define BAE_ERR_CUDA 7                /* CUDA runtime failure (no device, OOM ...) */
 #define BAE_ERR_NCCL 8                /* NCCL failure                              */
+#define BAE_ERR_PARSE 9               /* ParseError(line)       errors.hpp:60-69    */
+#define BAE_ERR_IO 10                 /* a file cannot be opened / written         */
 
 /* LmConfig::solver (lm.hpp:20). */
 #define BAE_SOLVER_CHOLESKY 0
@@ -208,6 +210,36 @@ int bae_synth_bal_shaped(int32_t num_cameras, int32_t num_points, int64_t num_ob
                          double point_sigma, double* poses7, double* points3,
                          double* intrinsics3, int32_t* cam_idx, int32_t* pt_idx,
                          double* pixels2, double* true_poses7, double* true_points3);
+
+/* ---- BAL files, the reference's synthetic scene, the CLI - */
+typedef struct bae_bal bae_bal;
+/* parse_bal (io/bal.hpp:103-142) of a file / a text buffer. ParseError ->
+ * BAE_ERR_PARSE with bae_last_error_index() = line (the reference's messages
+ * and line numbers); an unopenable file -> BAE_ERR_IO. */
+int bae_bal_read(const char* path, bae_bal** out);
+int bae_bal_parse(const char* text, int64_t len, bae_bal** out);
+/* synth_ba (io/synthetic.hpp:46-91): every camera sees every point. */
+int bae_bal_synthetic(int32_t num_cameras, int32_t num_points, double pixel_noise, double pose_noise,
+                      uint64_t seed, bae_bal** out);
+/* A BalProblem from arrays; cameras9 = C x [rodrigues3, translation3, f, k1, k2]. */
+int bae_bal_from_arrays(int32_t num_cameras, int32_t num_points, int64_t num_observations, const double* cameras9,
+                        const double* points3, const int32_t* cam_idx, const int32_t* pt_idx, const double* pixels2,
+                        bae_bal** out);
+int bae_bal_counts(const bae_bal* b, int32_t* num_cameras, int32_t* num_points, int64_t* num_observations);
+/* Arrays of the problem (any may be NULL): poses7 / intrinsics3 through
+ * BalCamera::pose / intrinsics (io/bal.hpp:24-27), points, observations, and
+ * the raw 9-scalar camera records. */
+int bae_bal_arrays(const bae_bal* b, double* poses7, double* intrinsics3, double* points3, int32_t* cam_idx,
+                   int32_t* pt_idx, double* pixels2, double* cameras9);
+/* serialize_bal (io/bal.hpp:145-157): %.17g, round-trips doubles exactly. */
+int bae_bal_write(const bae_bal* b, const char* path);
+void bae_bal_free(bae_bal* b);
+/* write_csv (cli.hpp:69-79): iter,cost,mse,lambda,accepted,cum_time_s. */
+int bae_write_csv(const char* path, const bae_iter_record* traj, int32_t n);
+/* cli_main (cli.hpp:116-200): `ba` / `pgo` subcommands, the reference's flags
+ * (+ --device), summary line and exit codes (0 ok, 1 usage, 2 data error,
+ * 3 solver failure). paper_2409_12190_b200/traceopt_bench wraps it. */
+int bae_cli_main(int argc, const char* const* argv);
 
 /* ---- multi-GPU landmark partition, host only ----------------- */
 /* Contiguous ranges of the internal point order balanced by observation

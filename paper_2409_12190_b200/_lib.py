@@ -116,6 +116,19 @@ SIGNATURES = {
     "bae_problem_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
     "bae_problem_shard": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p]),
     "bae_direct_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
+    "bae_bal_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_bal_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_bal_synthetic": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_bal_from_arrays": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, c_double_p, c_double_p,
+                                           c_int32_p, c_int32_p, c_double_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_bal_counts": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int64_p]),
+    "bae_bal_arrays": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, c_double_p, c_int32_p, c_int32_p,
+                                      c_double_p, c_double_p]),
+    "bae_bal_write": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
+    "bae_bal_free": (None, [ctypes.c_void_p]),
+    "bae_write_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(IterRecordC), ctypes.c_int32]),
+    "bae_cli_main": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p)]),
 }
 
 _lib = None

@@ -57,6 +57,12 @@ class UnsupportedOperationError(RuntimeError):
     pass
 
 
+class ParseError(RuntimeError):  # mirrors traceopt::ParseError (errors.hpp:60-69)
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
+
+
 class DeviceError(RuntimeError):
     """CUDA / NCCL failure (no reference counterpart)."""
 
@@ -77,6 +83,10 @@ def _raise(code: int):
         raise NumericalBreakdownError(msg)
     if code == 6:
         raise UnsupportedOperationError(msg)
+    if code == 9:
+        raise ParseError(msg, idx)
+    if code == 10:
+        raise OSError(msg)
     raise DeviceError(f"[{code}] {msg}")
 
 
@@ -436,9 +446,85 @@ def partition_points(num_cameras: int, num_points: int, observations, world: int
 
 
 def write_csv(path: str, report: LmReport):
-    """CSV trajectory with the reference CLI's schema (cli.hpp:69-79)."""
-    with open(path, "w") as f:
-        f.write("iter,cost,mse,lambda,accepted,cum_time_s\n")
-        for r in report.trajectory:
-            f.write("%d,%.17g,%.17g,%.17g,%d,%.6f\n" % (r.iteration, r.cost, r.mse, r.lmbda, 1 if r.accepted else 0,
-                                                      r.cum_time_s))
+    """CSV trajectory with the reference CLI's schema (cli.hpp:69-79), written by the library."""
+    recs = (IterRecordC * len(report.trajectory))()
+    for i, r in enumerate(report.trajectory):
+        recs[i].iteration, recs[i].cost, recs[i].mse = r.iteration, r.cost, r.mse
+        recs[i].lmbda, recs[i].accepted, recs[i].cum_time_s = r.lmbda, 1 if r.accepted else 0, r.cum_time_s
+    _check(_lib.load().bae_write_csv(path.encode(), recs, len(recs)))
+
+
+@dataclasses.dataclass
+class BalProblem:
+    """BalProblem (io/bal.hpp:29-47): cameras as the 9 BAL scalars
+    [rodrigues3, translation3, f, k1, k2]; poses / intrinsics through
+    BalCamera::pose / intrinsics (io/bal.hpp:24-27)."""
+    cameras: np.ndarray
+    points: np.ndarray
+    cam_idx: np.ndarray
+    pt_idx: np.ndarray
+    pixels: np.ndarray
+    poses: np.ndarray
+    intrinsics: np.ndarray
+
+    @property
+    def observations(self):
+        return self.cam_idx, self.pt_idx, self.pixels
+
+
+def _bal_from_handle(h) -> BalProblem:
+    lib = _lib.load()
+    C, P, N = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    try:
+        _check(lib.bae_bal_counts(h, ctypes.byref(C), ctypes.byref(P), ctypes.byref(N)))
+        C, P, N = C.value, P.value, N.value
+        cams, pts, px = np.empty((C, 9)), np.empty((P, 3)), np.empty((N, 2))
+        poses, intr = np.empty((C, 7)), np.empty((C, 3))
+        ci, pi = np.empty(N, np.int32), np.empty(N, np.int32)
+        _check(lib.bae_bal_arrays(h, ptr(poses), ptr(intr), ptr(pts), ptr(ci, ctypes.c_int32),
+                                  ptr(pi, ctypes.c_int32), ptr(px), ptr(cams)))
+    finally:
+        lib.bae_bal_free(h)
+    return BalProblem(cams, pts, ci, pi, px, poses, intr)
+
+
+def read_bal(path: str) -> BalProblem:
+    """parse_bal (io/bal.hpp:103-142) of a file; ParseError carries the line (ParseError.line)."""
+    h = ctypes.c_void_p()
+    _check(_lib.load().bae_bal_read(str(path).encode(), ctypes.byref(h)))
+    return _bal_from_handle(h)
+
+
+def parse_bal(text) -> BalProblem:
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = ctypes.c_void_p()
+    _check(_lib.load().bae_bal_parse(data, len(data), ctypes.byref(h)))
+    return _bal_from_handle(h)
+
+
+def synth_ba(num_cameras: int, num_points: int, pixel_noise: float, pose_noise: float, seed: int) -> BalProblem:
+    """synth_ba (io/synthetic.hpp:46-91): every camera sees every point."""
+    h = ctypes.c_void_p()
+    _check(_lib.load().bae_bal_synthetic(num_cameras, num_points, pixel_noise, pose_noise, seed, ctypes.byref(h)))
+    return _bal_from_handle(h)
+
+
+def write_bal(path: str, problem: BalProblem):
+    """serialize_bal (io/bal.hpp:145-157), %.17g."""
+    lib = _lib.load()
+    cams, pts = _f64(problem.cameras).reshape(-1, 9), _f64(problem.points).reshape(-1, 3)
+    ci, pi, px = _i32(problem.cam_idx), _i32(problem.pt_idx), _f64(problem.pixels).reshape(-1, 2)
+    h = ctypes.c_void_p()
+    _check(lib.bae_bal_from_arrays(cams.shape[0], pts.shape[0], ci.size, ptr(cams), ptr(pts), ptr(ci, ctypes.c_int32),
+                                   ptr(pi, ctypes.c_int32), ptr(px), ctypes.byref(h)))
+    try:
+        _check(lib.bae_bal_write(h, str(path).encode()))
+    finally:
+        lib.bae_bal_free(h)
+
+
+def cli_main(argv) -> int:
+    """cli_main (cli.hpp:116-200) in-process; argv without the program name."""
+    args = [b"traceopt_bench"] + [str(a).encode() for a in argv]
+    arr = (ctypes.c_char_p * len(args))(*args)
+    return int(_lib.load().bae_cli_main(len(args), arr))

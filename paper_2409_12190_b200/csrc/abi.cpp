@@ -3,6 +3,7 @@
 // return codes and records the message / index for bae_last_error*().
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -11,10 +12,15 @@
 
 #include "bae_b200.h"
 #include "bae_internal.hpp"
+#include "bal_io.hpp"
 #include "problem.hpp"
 
 struct bae_problem {
   std::unique_ptr<bae::Problem> impl;
+};
+
+struct bae_bal {
+  bae::BalData d;
 };
 
 namespace {
@@ -291,6 +297,94 @@ int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32
     if (world) *world = p->impl->world();
     if (local_points) *local_points = p->impl->local_points();
     if (local_observations) *local_observations = p->impl->local_obs();
+  });
+}
+
+// ---- BAL files, the reference's synthetic scene, the CSV trajectory ---------
+int bae_bal_read(const char* path, bae_bal** out) {
+  return guarded([&] {
+    if (!path || !out) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null argument");
+    auto h = std::make_unique<bae_bal>();
+    h->d = bae::parse_bal_file(path);
+    *out = h.release();
+  });
+}
+
+int bae_bal_parse(const char* text, int64_t len, bae_bal** out) {
+  return guarded([&] {
+    if (!text || !out || len < 0) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null argument");
+    auto h = std::make_unique<bae_bal>();
+    h->d = bae::parse_bal_text(text, text + len);
+    *out = h.release();
+  });
+}
+
+int bae_bal_synthetic(int32_t C, int32_t P, double pixel_noise, double pose_noise, uint64_t seed, bae_bal** out) {
+  return guarded([&] {
+    if (!out) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null argument");
+    auto h = std::make_unique<bae_bal>();
+    h->d = bae::synth_ba_dense(C, P, pixel_noise, pose_noise, seed);
+    *out = h.release();
+  });
+}
+
+int bae_bal_from_arrays(int32_t C, int32_t P, int64_t N, const double* cameras9, const double* points3,
+                        const int32_t* cam_idx, const int32_t* pt_idx, const double* px2, bae_bal** out) {
+  return guarded([&] {
+    if (!out || C < 1 || P < 1 || N < 1 || !cameras9 || !points3 || !cam_idx || !pt_idx || !px2)
+      throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "bad BAL arrays");
+    auto h = std::make_unique<bae_bal>();
+    bae::BalData& d = h->d;
+    d.C = C;
+    d.P = P;
+    d.N = N;
+    d.cameras.assign(cameras9, cameras9 + 9 * static_cast<std::size_t>(C));
+    d.points.assign(points3, points3 + 3 * static_cast<std::size_t>(P));
+    d.cam_idx.assign(cam_idx, cam_idx + N);
+    d.pt_idx.assign(pt_idx, pt_idx + N);
+    d.px.assign(px2, px2 + 2 * N);
+    *out = h.release();
+  });
+}
+
+int bae_bal_counts(const bae_bal* b, int32_t* C, int32_t* P, int64_t* N) {
+  return guarded([&] {
+    if (C) *C = b->d.C;
+    if (P) *P = b->d.P;
+    if (N) *N = b->d.N;
+  });
+}
+
+int bae_bal_arrays(const bae_bal* b, double* poses7, double* intr3, double* points3, int32_t* cam_idx,
+                   int32_t* pt_idx, double* px2, double* cameras9) {
+  return guarded([&] {
+    const bae::BalData& d = b->d;
+    bae::bal_poses(d, poses7, intr3);
+    if (points3) std::memcpy(points3, d.points.data(), d.points.size() * sizeof(double));
+    if (cam_idx) std::memcpy(cam_idx, d.cam_idx.data(), d.cam_idx.size() * sizeof(int32_t));
+    if (pt_idx) std::memcpy(pt_idx, d.pt_idx.data(), d.pt_idx.size() * sizeof(int32_t));
+    if (px2) std::memcpy(px2, d.px.data(), d.px.size() * sizeof(double));
+    if (cameras9) std::memcpy(cameras9, d.cameras.data(), d.cameras.size() * sizeof(double));
+  });
+}
+
+int bae_bal_write(const bae_bal* b, const char* path) {
+  return guarded([&] { bae::write_bal_file(b->d, path); });
+}
+
+void bae_bal_free(bae_bal* b) { delete b; }
+
+int bae_write_csv(const char* path, const bae_iter_record* traj, int32_t n) {  // cli.hpp:69-79
+  return guarded([&] {
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) throw bae::Error(BAE_ERR_IO, std::string("cannot open CSV output '") + path + "'");
+    std::fputs("iter,cost,mse,lambda,accepted,cum_time_s\n", f);
+    for (int32_t i = 0; i < n; ++i) {
+      const bae_iter_record& r = traj[i];
+      std::fprintf(f, "%d,%.17g,%.17g,%.17g,%d,%.6f\n", r.iteration, r.cost, r.mse, r.lambda, r.accepted ? 1 : 0,
+                   r.cum_time_s);
+    }
+    if (std::fclose(f) != 0) throw bae::Error(BAE_ERR_IO, std::string("cannot write CSV output '") + path + "'");
   });
 }
 

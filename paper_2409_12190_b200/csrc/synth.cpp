@@ -19,11 +19,10 @@
 
 #include "bae/rng.hpp"
 #include "bae_internal.hpp"
+#include "bal_io.hpp"
 #include "lie.cuh"
 
 namespace bae {
-
-namespace {
 
 // look_at_origin (io/synthetic.hpp:26-38) including Eigen's matrix ->
 // quaternion conversion.
@@ -62,8 +61,6 @@ void look_at_origin(const P3& pos, Q4& q, P3& t) {
   t = {-(m[0] * pos.x + m[1] * pos.y + m[2] * pos.z), -(m[3] * pos.x + m[4] * pos.y + m[5] * pos.z),
        -(m[6] * pos.x + m[7] * pos.y + m[8] * pos.z)};
 }
-
-}  // namespace
 
 void synth_bal_shaped(int C, int P, std::int64_t N, std::uint64_t seed, double pixel_sigma, double pose_sigma,
                       double point_sigma, double* poses7, double* points3, double* intr3, std::int32_t* cam_idx,
