@@ -241,6 +241,18 @@ int bae_write_csv(const char* path, const bae_iter_record* traj, int32_t n);
  * 3 solver failure). paper_2409_12190_b200/traceopt_bench wraps it. */
 int bae_cli_main(int argc, const char* const* argv);
 
+/* ---- direct-solver host logic, exposed for tests ---------------------------- */
+/* Nested-dissection order of a camera graph (edges2 = pairs of cameras):
+ * order (C) lists the cameras group by group in elimination order,
+ * group_ptr (C + 1) the group boundaries. */
+int bae_nd_order(int32_t num_cameras, int64_t num_edges, const int32_t* edges2, int32_t leaf, int32_t* order,
+                 int32_t* group_ptr, int32_t* num_groups);
+/* Tile-level symbolic Cholesky of an nt x nt tile pattern (pairs2 = lower
+ * tile pairs (i, j), i >= j): colptr (nt + 1) and rowidx (nnz, diagonal first,
+ * rows ascending) of L's tiles. */
+int bae_tile_symbolic(int32_t nt, int64_t num_pairs, const int32_t* pairs2, int32_t* colptr, int32_t* rowidx,
+                      int64_t capacity, int64_t* nnz);
+
 /* ---- multi-GPU landmark partition, host only ----------------- */
 /* Contiguous ranges of the internal point order balanced by observation
  * count: rank_of_point[p] in [0, world). Cameras are replicated. */

@@ -116,6 +116,10 @@ SIGNATURES = {
     "bae_problem_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
     "bae_problem_shard": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p]),
     "bae_direct_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
+    "bae_nd_order": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, c_int32_p, ctypes.c_int32, c_int32_p, c_int32_p,
+                                     c_int32_p]),
+    "bae_tile_symbolic": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, c_int32_p, c_int32_p, c_int32_p,
+                                          ctypes.c_int64, c_int64_p]),
     "bae_bal_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     "bae_bal_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
     "bae_bal_synthetic": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_double,

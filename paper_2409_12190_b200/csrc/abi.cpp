@@ -13,6 +13,7 @@
 #include "bae_b200.h"
 #include "bae_internal.hpp"
 #include "bal_io.hpp"
+#include "chol.cuh"
 #include "problem.hpp"
 
 struct bae_problem {
@@ -297,6 +298,40 @@ int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32
     if (world) *world = p->impl->world();
     if (local_points) *local_points = p->impl->local_points();
     if (local_observations) *local_observations = p->impl->local_obs();
+  });
+}
+
+// ---- host-logic hooks of the tile Cholesky (tests) ---------------------------
+int bae_nd_order(int32_t C, int64_t nedges, const int32_t* edges2, int32_t leaf, int32_t* order, int32_t* group_ptr,
+                 int32_t* ngroups) {
+  return guarded([&] {
+    std::vector<std::pair<int, int>> e(static_cast<std::size_t>(nedges));
+    for (int64_t i = 0; i < nedges; ++i) {
+      if (edges2[2 * i] < 0 || edges2[2 * i] >= C || edges2[2 * i + 1] < 0 || edges2[2 * i + 1] >= C)
+        throw bae::Error(BAE_ERR_INDEX, "edge out of range", i);
+      e[i] = {edges2[2 * i], edges2[2 * i + 1]};
+    }
+    const auto groups = bae::nd_camera_groups(C, e, leaf);
+    int at = 0, g = 0;
+    group_ptr[0] = 0;
+    for (const auto& gr : groups) {
+      for (int c : gr) order[at++] = c;
+      group_ptr[++g] = at;
+    }
+    *ngroups = g;
+  });
+}
+
+int bae_tile_symbolic(int32_t nt, int64_t npairs, const int32_t* pairs2, int32_t* colptr, int32_t* rowidx,
+                      int64_t cap, int64_t* nnz) {
+  return guarded([&] {
+    std::vector<std::pair<int, int>> tp(static_cast<std::size_t>(npairs));
+    for (int64_t i = 0; i < npairs; ++i) tp[i] = {pairs2[2 * i], pairs2[2 * i + 1]};
+    const bae::TileCholPlan pl = bae::plan_tile_chol(nt * bae::kTB, tp);
+    *nnz = pl.nnz_tiles();
+    if (pl.nnz_tiles() > cap) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "rowidx capacity too small");
+    std::memcpy(colptr, pl.colptr.data(), pl.colptr.size() * sizeof(int32_t));
+    std::memcpy(rowidx, pl.rowidx.data(), pl.rowidx.size() * sizeof(int32_t));
   });
 }
 

@@ -1,0 +1,120 @@
+"""Host logic of the direct solver, on CPU: the nested-
+dissection camera order and the tile-level symbolic Cholesky, against an
+independent dense symbolic factorisation and numeric fill."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2409_12190_b200 import _lib
+from paper_2409_12190_b200._lib import ptr
+
+
+def nd_order(C, edges, leaf=24):
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+    order, gptr, ng = np.empty(C, np.int32), np.empty(C + 1, np.int32), ctypes.c_int32()
+    assert _lib.load().bae_nd_order(C, e.shape[0], ptr(e, ctypes.c_int32), leaf, ptr(order, ctypes.c_int32),
+                                    ptr(gptr, ctypes.c_int32), ctypes.byref(ng)) == 0
+    return order, gptr[:ng.value + 1]
+
+
+def tile_symbolic(nt, pairs):
+    pr = np.ascontiguousarray(np.asarray(pairs, np.int32).reshape(-1, 2))
+    colptr, rowidx, nnz = np.empty(nt + 1, np.int32), np.empty(nt * nt, np.int32), ctypes.c_int64()
+    assert _lib.load().bae_tile_symbolic(nt, pr.shape[0], ptr(pr, ctypes.c_int32), ptr(colptr, ctypes.c_int32),
+                                         ptr(rowidx, ctypes.c_int32), nt * nt, ctypes.byref(nnz)) == 0
+    return colptr, rowidx[:nnz.value]
+
+
+def dense_symbolic(nt, pairs):
+    """Boolean right-looking elimination: L's pattern."""
+    a = np.eye(nt, dtype=bool)
+    for i, j in pairs:
+        a[i, j] = a[j, i] = True
+    for k in range(nt):
+        rows = np.flatnonzero(a[k + 1:, k]) + k + 1
+        for i in rows:
+            a[rows, i] = True
+            a[i, rows] = True
+    return np.tril(a)
+
+
+def ring_edges(C, band):
+    return [(max(c, (c + d) % C), min(c, (c + d) % C)) for c in range(C) for d in range(1, band + 1)]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tile_symbolic_matches_dense_elimination(seed):
+    rng = np.random.default_rng(seed)
+    nt = int(rng.integers(3, 40))
+    pairs = {(i, j) for i, j in zip(rng.integers(0, nt, 2 * nt), rng.integers(0, nt, 2 * nt)) if i != j}
+    pairs = [(max(i, j), min(i, j)) for i, j in pairs]
+    colptr, rowidx = tile_symbolic(nt, pairs)
+    ref = dense_symbolic(nt, pairs)
+    for j in range(nt):
+        rows = rowidx[colptr[j]:colptr[j + 1]]
+        assert rows[0] == j and np.all(np.diff(rows) > 0)  # diagonal first, ascending
+        assert np.array_equal(rows, np.flatnonzero(ref[:, j])), j
+
+
+def test_tile_symbolic_covers_numeric_fill():
+    """Numeric Cholesky of a random SPD matrix with the tile pattern never
+    puts a nonzero outside the symbolic tiles."""
+    rng = np.random.default_rng(7)
+    nt, tb = 12, 4
+    pairs = [(i, j) for i in range(nt) for j in range(i) if rng.random() < 0.2]
+    m = np.zeros((nt * tb, nt * tb))
+    for i, j in pairs + [(k, k) for k in range(nt)]:
+        blk = rng.standard_normal((tb, tb))
+        m[i * tb:(i + 1) * tb, j * tb:(j + 1) * tb] = blk
+        m[j * tb:(j + 1) * tb, i * tb:(i + 1) * tb] = blk.T
+    m = m @ m.T * 0 + m + nt * tb * 4 * np.eye(nt * tb)  # symmetric, diagonally dominant
+    L = np.linalg.cholesky(m)
+    colptr, rowidx = tile_symbolic(nt, pairs)
+    allowed = np.zeros((nt, nt), bool)
+    for j in range(nt):
+        allowed[rowidx[colptr[j]:colptr[j + 1]], j] = True
+    for i in range(nt):
+        for j in range(i + 1):
+            if np.abs(L[i * tb:(i + 1) * tb, j * tb:(j + 1) * tb]).max() > 1e-12:
+                assert allowed[i, j], (i, j)
+
+
+def test_nd_order_is_a_permutation_and_shortens_the_ring_chain():
+    C, band = 257, 15
+    edges = ring_edges(C, band)
+    order, gptr = nd_order(C, edges)
+    assert np.array_equal(np.sort(order), np.arange(C))
+    assert gptr[0] == 0 and gptr[-1] == C and np.all(np.diff(gptr) > 0)
+    # tile pattern in the padded group layout, then the elimination-tree height
+    pos, at = np.empty(C, int), 0
+    for g in range(len(gptr) - 1):
+        for c in order[gptr[g]:gptr[g + 1]]:
+            pos[c] = at
+            at += 1
+        at = (at + 7) // 8 * 8
+    nt = at // 8
+    tp = {(max(pos[a] // 8, pos[b] // 8), min(pos[a] // 8, pos[b] // 8)) for a, b in edges}
+    tp = [p for p in tp if p[0] != p[1]]
+    colptr, rowidx = tile_symbolic(nt, tp)
+    parent = [rowidx[colptr[j] + 1] if colptr[j + 1] - colptr[j] > 1 else -1 for j in range(nt)]
+    depth = [0] * nt
+    for j in range(nt):  # parents come later in the order
+        if parent[j] >= 0:
+            depth[parent[j]] = max(depth[parent[j]], depth[j] + 1)
+    height = max(depth) + 1
+    natural_nt = (C + 7) // 8
+    assert height <= natural_nt // 2, (height, natural_nt)
+
+
+def test_nd_order_dense_graph_is_one_group():
+    C = 20
+    edges = [(i, j) for i in range(C) for j in range(i)]
+    order, gptr = nd_order(C, edges)
+    assert len(gptr) == 2 and np.array_equal(np.sort(order), np.arange(C))
+
+
+def test_nd_order_disconnected_components():
+    edges = ring_edges(30, 2) + [(a + 30, b + 30) for a, b in ring_edges(30, 2)]
+    order, gptr = nd_order(60, edges)
+    assert np.array_equal(np.sort(order), np.arange(60))
