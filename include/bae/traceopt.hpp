@@ -13,6 +13,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <variant>
 #include <vector>
 
 #include "bae_b200.h"
@@ -32,9 +33,13 @@ struct PoseSE3 {  // world -> camera (lie.hpp:119-136)
   QuatRotation rotation;
   Vec3 translation;
 };
+struct PinholeIntrinsics {  // camera.hpp:17-19
+  double fx = 0, fy = 0, cx = 0, cy = 0;
+};
 struct BalIntrinsics {  // camera.hpp:23-25
   double f = 0, k1 = 0, k2 = 0;
 };
+using CameraIntrinsics = std::variant<PinholeIntrinsics, BalIntrinsics>;  // camera.hpp:27
 struct Observation {  // problems.hpp:19-23
   std::int32_t camera_index = 0;
   std::int32_t point_index = 0;
@@ -213,21 +218,36 @@ class TracedProblem {
   std::unique_ptr<bae_problem, void (*)(bae_problem*)> h_;
 };
 
-// make_ba_problem (problems.hpp:87-136) for BAL cameras.
+// make_ba_problem (problems.hpp:87-136): one camera variant per problem,
+// mixed variants are rejected like the reference (problems.hpp:94-98).
 inline TracedProblem make_ba_problem(std::span<const PoseSE3> poses, std::span<const Vec3> points,
-                                     std::span<const BalIntrinsics> intrinsics,
+                                     std::span<const CameraIntrinsics> intrinsics,
                                      std::span<const Observation> observations, int device = 0) {
   if (intrinsics.size() != poses.size())
     throw std::invalid_argument("make_ba_problem: one intrinsics entry per camera required");
   if (observations.empty()) throw std::invalid_argument("make_ba_problem: no observations");
-  std::vector<double> p7, p3, k3(intrinsics.size() * 3), px(observations.size() * 2);
+  const bool pinhole = std::holds_alternative<PinholeIntrinsics>(intrinsics[0]);
+  for (const auto& k : intrinsics)
+    if (std::holds_alternative<PinholeIntrinsics>(k) != pinhole)
+      throw std::invalid_argument("make_ba_problem: mixed camera variants are not supported");
+  const std::size_t kw = pinhole ? 4 : 3;
+  std::vector<double> p7, p3, kk(intrinsics.size() * kw), px(observations.size() * 2);
   std::vector<std::int32_t> ci(observations.size()), pi(observations.size());
   detail::pack_poses(poses, p7);
   detail::pack_points(points, p3);
   for (std::size_t i = 0; i < intrinsics.size(); ++i) {
-    k3[i * 3] = intrinsics[i].f;
-    k3[i * 3 + 1] = intrinsics[i].k1;
-    k3[i * 3 + 2] = intrinsics[i].k2;
+    if (pinhole) {
+      const auto& k = std::get<PinholeIntrinsics>(intrinsics[i]);
+      kk[i * 4] = k.fx;
+      kk[i * 4 + 1] = k.fy;
+      kk[i * 4 + 2] = k.cx;
+      kk[i * 4 + 3] = k.cy;
+    } else {
+      const auto& k = std::get<BalIntrinsics>(intrinsics[i]);
+      kk[i * 3] = k.f;
+      kk[i * 3 + 1] = k.k1;
+      kk[i * 3 + 2] = k.k2;
+    }
   }
   for (std::size_t k = 0; k < observations.size(); ++k) {
     ci[k] = observations[k].camera_index;
@@ -238,11 +258,20 @@ inline TracedProblem make_ba_problem(std::span<const PoseSE3> poses, std::span<c
   bae_create_options opt;
   bae_create_options_default(&opt);
   opt.device = device;
+  opt.camera_model = pinhole ? BAE_CAMERA_PINHOLE : BAE_CAMERA_BAL;
   bae_problem* h = nullptr;
   detail::check(bae_create_ba(p7.data(), static_cast<int32_t>(poses.size()), p3.data(),
-                              static_cast<int32_t>(points.size()), k3.data(), ci.data(), pi.data(), px.data(),
+                              static_cast<int32_t>(points.size()), kk.data(), ci.data(), pi.data(), px.data(),
                               static_cast<int64_t>(observations.size()), &opt, &h));
   return TracedProblem(h);
+}
+
+// BAL-only convenience overload (the BalProblem path, io/bal.hpp:159-161).
+inline TracedProblem make_ba_problem(std::span<const PoseSE3> poses, std::span<const Vec3> points,
+                                     std::span<const BalIntrinsics> intrinsics,
+                                     std::span<const Observation> observations, int device = 0) {
+  std::vector<CameraIntrinsics> v(intrinsics.begin(), intrinsics.end());
+  return make_ba_problem(poses, points, std::span<const CameraIntrinsics>(v), observations, device);
 }
 
 // optimize (lm.hpp:205-255); the model keeps the optimised parameters.

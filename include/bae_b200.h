@@ -18,7 +18,9 @@
  *            (trace.hpp:318-326 write_pose). Quaternions are taken as-is
  *            (read_pose uses QuatRotation::from_unit, trace.hpp:329-333).
  *   point  : 3 doubles [x, y, z]
- *   intr   : 3 doubles [f, k1, k2] (BalIntrinsics, camera.hpp:23-25)
+ *   intr   : 3 doubles [f, k1, k2] (BalIntrinsics, camera.hpp:23-25), or with
+ *            camera_model = BAE_CAMERA_PINHOLE 4 doubles [fx, fy, cx, cy]
+ *            (PinholeIntrinsics, camera.hpp:17-19)
  *   pixel  : 2 doubles per observation
  *   indices: int32 camera / point index per observation (problems.hpp:19-23)
  */
@@ -47,6 +49,10 @@ extern "C" {
 /* LmConfig::solver (lm.hpp:20). */
 #define BAE_SOLVER_CHOLESKY 0
 #define BAE_SOLVER_PCG 1
+
+/* CameraIntrinsics variant of a problem (camera.hpp:17-27; one per problem, problems.hpp:94-98). */
+#define BAE_CAMERA_BAL 0
+#define BAE_CAMERA_PINHOLE 1
 
 /* TerminationReason (lm.hpp:21). */
 #define BAE_TERM_PLATEAU 0
@@ -105,7 +111,8 @@ typedef struct bae_create_options {
   int32_t jacobian;    /* 0 = recompute blocks in every pass, 1 = store J in HBM  */
   int32_t rank;        /* distributed: this rank (default 0)                      */
   int32_t world;       /* distributed: number of ranks (default 1)                */
-  int32_t reserved;
+  int32_t camera_model; /* BAE_CAMERA_BAL (default; intrinsics C x [f, k1, k2]) or
+                           BAE_CAMERA_PINHOLE (C x [fx, fy, cx, cy]); camera.hpp:17-27 */
   const void* nccl_id; /* distributed: 128-byte ncclUniqueId from rank 0 (one process per GPU) */
   struct bae_group* group; /* distributed: in-process rank group (one host thread per rank) */
 } bae_create_options;

@@ -68,7 +68,7 @@ class CreateOptionsC(ctypes.Structure):
         ("jacobian", ctypes.c_int32),
         ("rank", ctypes.c_int32),
         ("world", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("camera_model", ctypes.c_int32),
         ("nccl_id", ctypes.c_void_p),
         ("group", ctypes.c_void_p),
     ]

@@ -361,7 +361,8 @@ def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0,
                     group: Optional[RankGroup] = None) -> TracedProblem:
     """make_ba_problem (problems.hpp:87-136) for BAL cameras.
 
-    ``observations`` is ``(cam_idx, pt_idx, pixels)``. Raises ValueError for a
+    ``observations`` is ``(cam_idx, pt_idx, pixels)``; ``intrinsics`` is C x 3
+    (BAL: f, k1, k2) or C x 4 (pinhole: fx, fy, cx, cy). Raises ValueError for a
     wrong intrinsics count or no observations, IndexError(position) for an
     out-of-range index, CheiralityError(observation) when an initial point
     lies on a camera plane (the reference's eager forward at construction).
@@ -373,7 +374,11 @@ def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0,
     cam_idx, pt_idx, pixels = observations
     p7 = _f64(poses).reshape(-1, 7)
     p3 = _f64(points).reshape(-1, 3)
-    k3 = _f64(intrinsics).reshape(-1, 3)
+    kk = _f64(intrinsics)
+    # the CameraIntrinsics variant (camera.hpp:17-27): rows of 3 = BalIntrinsics
+    # [f, k1, k2], rows of 4 = PinholeIntrinsics [fx, fy, cx, cy]
+    pinhole = kk.ndim == 2 and kk.shape[1] == 4
+    k3 = kk.reshape(-1, 4 if pinhole else 3)
     ci, pi = _i32(cam_idx), _i32(pt_idx)
     px = _f64(pixels).reshape(-1, 2)
     C, P, N = p7.shape[0], p3.shape[0], ci.shape[0]
@@ -386,6 +391,7 @@ def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0,
     lib.bae_create_options_default(ctypes.byref(opt))
     opt.device = device
     opt.tile_obs = tile_obs
+    opt.camera_model = 1 if pinhole else 0
     opt.rank = rank
     opt.world = world
     idbuf = None

@@ -9,7 +9,7 @@
 namespace bae {
 
 constexpr int kTileThreads = 256;  // CTA size of the tile kernels (8 warps)
-constexpr int kCamRec = 16;        // per camera: R[9] t[3] f k1 k2 pad
+constexpr int kCamRec = 16;        // per camera: R[9] t[3] intrinsics[4] (BAL f k1 k2 0 | pinhole fx fy cx cy)
 constexpr int kWarpsPerCamBlock = 8;
 constexpr int kSTileElems = 48 * 48;  // one tile of the tile-sparse reduced matrix (chol.cuh kTT)
 
@@ -37,6 +37,7 @@ struct LmDev {
 // Everything a kernel needs, passed by value.
 struct Dev {
   int C, P, T, E, N;
+  int pinhole;  // camera variant of the whole problem (problems.hpp:94-98)
   int nbig;
   long long big_stride;  // bytes per big-tile workspace
   const int* tile_obs_begin;
@@ -55,7 +56,7 @@ struct Dev {
   char* bigws;
   // parameters
   double* pose;    // 7C  [t q]
-  double* intr;    // 3C  [f k1 k2]
+  double* intr;    // 4C  [f k1 k2 0] or [fx fy cx cy]
   double* camrec;  // 16C
   double* pts;     // 3P internal order
   double* pose_t;

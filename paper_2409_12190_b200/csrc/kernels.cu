@@ -30,14 +30,14 @@ namespace bae {
 // per-observation math
 // ---------------------------------------------------------------------------
 
-// y = R p + t and D for one observation from a 15-double camera record
-// (R[9] t[3] f k1 k2).
-__device__ __forceinline__ void obs_geometry(const double* cam, const double* pt, P3& y, double* D) {
+// y = R p + t and D for one observation from a camera record
+// (R[9] t[3] intrinsics[4]).
+__device__ __forceinline__ void obs_geometry(bool pin, const double* cam, const double* pt, P3& y, double* D) {
   const double* R = cam;
   y.x = R[0] * pt[0] + R[1] * pt[1] + R[2] * pt[2] + cam[9];
   y.y = R[3] * pt[0] + R[4] * pt[1] + R[5] * pt[2] + cam[10];
   y.z = R[6] * pt[0] + R[7] * pt[1] + R[8] * pt[2] + cam[11];
-  bal_dproj(y, cam[12], cam[13], cam[14], D);
+  cam_dproj(pin, y, cam + 12, D);
 }
 
 // J_c = D [I | -[y]x] (trace.hpp:612-629 with up = D), row-major 2x6.
@@ -96,14 +96,15 @@ __device__ __forceinline__ void jct_jp_t(const double* D, const P3& y, const dou
 }
 
 // Forward residual exactly as the reference evaluates it: quaternion rotate
-// (trace.hpp:439-452, lie.hpp:88-93), bal_project_cam (camera.hpp:50-57),
-// sub as p0 + (-1) p1 (trace.hpp:488-497). cam: [t3 q4 f k1 k2].
-__device__ __forceinline__ bool residual(const double* cam, const double* pt, double2 px, double& r0, double& r1,
-                                         P3& y) {
+// (trace.hpp:439-452, lie.hpp:88-93), bal_project_cam / pinhole_project_cam
+// (camera.hpp:33-57), sub as p0 + (-1) p1 (trace.hpp:488-497).
+// cam: [t3 q4 intrinsics4].
+__device__ __forceinline__ bool residual(bool pin, const double* cam, const double* pt, double2 px, double& r0,
+                                         double& r1, P3& y) {
   const P3 yr = quat_rotate({cam[3], cam[4], cam[5], cam[6]}, {pt[0], pt[1], pt[2]});
   y = {yr.x + cam[0], yr.y + cam[1], yr.z + cam[2]};
   double u, w;
-  if (!bal_project(y, cam[7], cam[8], cam[9], u, w)) return false;
+  if (!cam_project(pin, y, cam + 7, u, w)) return false;
   r0 = u + -1.0 * px.x;
   r1 = w + -1.0 * px.y;
   return true;
@@ -231,10 +232,10 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
   o[9] = s[0];
   o[10] = s[1];
   o[11] = s[2];
-  o[12] = intr[c * 3];
-  o[13] = intr[c * 3 + 1];
-  o[14] = intr[c * 3 + 2];
-  o[15] = 0.0;
+  o[12] = intr[c * 4];
+  o[13] = intr[c * 4 + 1];
+  o[14] = intr[c * 4 + 2];
+  o[15] = intr[c * 4 + 3];
 }
 
 // ---------------------------------------------------------------------------
@@ -246,9 +247,9 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
 //   per tile  : sum r^2, sum |g_p|^2       -> tile_red
 // The forward residual follows the reference (quaternion rotate); its
 // Jacobian uses that forward value y (trace.hpp:612-629).
-// cam: [t3 q4 f k1 k2 R9] (19) ; pt: p3 ; stage: Jc12 Jp6 r2 (20)
+// cam: [t3 q4 k4 R9] (20) ; pt: p3 ; stage: Jc12 Jp6 r2 (20)
 // ---------------------------------------------------------------------------
-constexpr WsDims kLinWs{19, 3, 20, 0};
+constexpr WsDims kLinWs{20, 3, 20, 0};
 
 template <bool kShared>
 __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t,
@@ -258,25 +259,25 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
   load_point_fields<3>(ws, 3, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
   __syncwarp();
-  load_cam_fields<7>(ws, g.ncam, 19, 0, d.pose, 7);
-  load_cam_fields<3>(ws, g.ncam, 19, 7, d.intr, 3);
-  load_cam_fields<9>(ws, g.ncam, 19, 10, d.camrec, kCamRec);
+  load_cam_fields<7>(ws, g.ncam, 20, 0, d.pose, 7);
+  load_cam_fields<4>(ws, g.ncam, 20, 7, d.intr, 4);
+  load_cam_fields<9>(ws, g.ncam, 20, 11, d.camrec, kCamRec);
   __syncwarp();
   double cost = 0.0;
   int bad = INT_MAX;
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
-    const double* cam = ws.cam + (lcpt & 0xffff) * 19;
+    const double* cam = ws.cam + (lcpt & 0xffff) * 20;
     const double* pt = ws.pt + (lcpt >> 16) * 3;
     const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
     double* st = ws.stage + s * 20;
     double r0 = 0.0, r1 = 0.0;
     P3 y;
-    if (residual(cam, pt, px, r0, r1, y)) {
+    if (residual(d.pinhole, cam, pt, px, r0, r1, y)) {
       double D[6];
-      bal_dproj(y, cam[7], cam[8], cam[9], D);
+      cam_dproj(d.pinhole, y, cam + 7, D);
       jac_cam(D, y, st);
-      jac_pt(D, cam + 10, st + 12);
+      jac_pt(D, cam + 11, st + 12);
       st[18] = r0;
       st[19] = r1;
       cost += r0 * r0 + r1 * r1;
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_j
 
 // Residual only (evaluate + squared_norm, problems.hpp:66, lm.hpp:81-85) at
 // the current parameters; writes resid when requested.
-constexpr WsDims kCostWs{10, 3, 0, 0};
+constexpr WsDims kCostWs{11, 3, 0, 0};
 
 template <bool kShared>
 __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t) {
@@ -372,8 +373,8 @@ __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char*
   load_point_fields<3>(ws, 3, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
   __syncwarp();
-  load_cam_fields<7>(ws, g.ncam, 10, 0, d.pose, 7);
-  load_cam_fields<3>(ws, g.ncam, 10, 7, d.intr, 3);
+  load_cam_fields<7>(ws, g.ncam, 11, 0, d.pose, 7);
+  load_cam_fields<4>(ws, g.ncam, 11, 7, d.intr, 4);
   __syncwarp();
   double cost = 0.0;
   int bad = INT_MAX;
@@ -382,7 +383,7 @@ __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char*
     const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
     double r0, r1;
     P3 y;
-    if (residual(ws.cam + (lcpt & 0xffff) * 10, ws.pt + (lcpt >> 16) * 3, px, r0, r1, y)) {
+    if (residual(d.pinhole, ws.cam + (lcpt & 0xffff) * 11, ws.pt + (lcpt >> 16) * 3, px, r0, r1, y)) {
       if (d.resid) {
         d.resid[g.ob + s] = r0;
         d.resid[(long long)d.N + g.ob + s] = r1;
@@ -589,9 +590,9 @@ __global__ void k_finish_cost(Dev d, int trial) {
 // K3/K4 prep for one damping value: per point H~_pp^-1 and v = H~_pp^-1 g_p;
 // per entry the Schur right-hand side (J_c^T J_p v) and the block-Jacobi
 // blocks (W H~_pp^-1 W^T, W = J_c^T J_p) of S's diagonal.
-// cam: R9 t3 f k1 k2 (15) ; pt: p3 hinv6 v3 (12) ; stage 27
+// cam: R9 t3 k4 (16) ; pt: p3 hinv6 v3 (12) ; stage 27
 // ---------------------------------------------------------------------------
-constexpr WsDims kPrepWs{15, 12, 27, 0};
+constexpr WsDims kPrepWs{16, 12, 27, 0};
 
 template <bool kShared>
 __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char* smem, int slice, double lambda,
@@ -601,7 +602,7 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
   load_point_fields<3>(ws, 12, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
   __syncwarp();
-  load_cam_fields<15>(ws, g.ncam, 15, 0, d.camrec, kCamRec);
+  load_cam_fields<16>(ws, g.ncam, 16, 0, d.camrec, kCamRec);
   int fail = 0;
   for (int lp = lane; lp < g.npts; lp += 32) {
     const long long ip = g.pb + lp;
@@ -632,11 +633,11 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
   __syncwarp();
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
-    const double* cam = ws.cam + (lcpt & 0xffff) * 15;
+    const double* cam = ws.cam + (lcpt & 0xffff) * 16;
     const double* sp = ws.pt + (lcpt >> 16) * 12;
     P3 y;
     double D[6], Jc[12], Jp[6];
-    obs_geometry(cam, sp, y, D);
+    obs_geometry(d.pinhole, cam, sp, y, D);
     jac_cam(D, y, Jc);
     jac_pt(D, cam, Jp);
     double W[18];  // 6x3
@@ -972,7 +973,7 @@ __device__ __forceinline__ void sx_tile_impl(const Dev& d, const PcgDev& st, con
     const int s = r * 32 + lane;
     if (s < nobs) {
       const double* cam = ws.cam + (lc[r] & 0xffff) * 24;
-      obs_geometry(cam, px[r], cy[r], cD[r]);
+      obs_geometry(d.pinhole, cam, px[r], cy[r], cD[r]);
       double sv[3];
       jpt_jc_v(cD[r], cy[r], cam, cam + 16, sv);
       ws.stage[s] = sv[0];
@@ -987,7 +988,7 @@ __device__ __forceinline__ void sx_tile_impl(const Dev& d, const PcgDev& st, con
     const double pp[3] = {p[0], p[1], p[2]};
     P3 y;
     double D[6], sv[3];
-    obs_geometry(cam, pp, y, D);
+    obs_geometry(d.pinhole, cam, pp, y, D);
     jpt_jc_v(D, y, cam, cam + 16, sv);
     ws.stage[s] = sv[0];
     ws.stage[nobs + s] = sv[1];
@@ -1033,7 +1034,7 @@ __device__ __forceinline__ void sx_tile_impl(const Dev& d, const PcgDev& st, con
     const double pp[3] = {p[0], p[1], p[2]};
     P3 y;
     double D[6], z[6];
-    obs_geometry(cam, pp, y, D);
+    obs_geometry(d.pinhole, cam, pp, y, D);
     jct_jp_t(D, y, cam, ws.pt + (l >> 16) * 3, z);
 #pragma unroll
     for (int j = 0; j < 6; ++j) ws.stage[j * nobs + s] = z[j];
@@ -1142,7 +1143,7 @@ __device__ __forceinline__ void sx_pipe_tile(const Dev& d, const PcgDev& st, cha
     if (s < nobs) {
       const int l = lc[r] & 0xffff;
       const double* cam = cams + l * 16;
-      obs_geometry(cam, pts + (lc[r] >> 16) * 3, cy[r], cD[r]);
+      obs_geometry(d.pinhole, cam, pts + (lc[r] >> 16) * 3, cy[r], cD[r]);
       double sv[3];
       jpt_jc_v(cD[r], cy[r], cam, vz + l * 6, sv);
       stage[s] = sv[0];
@@ -1536,14 +1537,14 @@ __global__ void k_cam_retract(Dev d) {
   rec[9] = t.x;
   rec[10] = t.y;
   rec[11] = t.z;
-  rec[12] = d.intr[c * 3];
-  rec[13] = d.intr[c * 3 + 1];
-  rec[14] = d.intr[c * 3 + 2];
-  rec[15] = 0.0;
+  rec[12] = d.intr[c * 4];
+  rec[13] = d.intr[c * 4 + 1];
+  rec[14] = d.intr[c * 4 + 2];
+  rec[15] = d.intr[c * 4 + 3];
 }
 
-// cam: R9 t3 f k1 k2 dc6 | trial t3 q4 (28), intr at 12..14 ; pt: p3 ptrial3 ; stage 3
-constexpr WsDims kTrialWs{28, 6, 3, 0};
+// cam: R9 t3 k4 dc6 | trial t3 q4 (29), intrinsics at 12..15 ; pt: p3 ptrial3 ; stage 3
+constexpr WsDims kTrialWs{29, 6, 3, 0};
 
 template <bool kShared>
 __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t) {
@@ -1552,17 +1553,17 @@ __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char
   load_point_fields<3>(ws, 6, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
   __syncwarp();
-  load_cam_fields<15>(ws, g.ncam, 28, 0, d.camrec, kCamRec);
-  load_cam_fields<6>(ws, g.ncam, 28, 15, d.x, 6);
-  load_cam_fields<7>(ws, g.ncam, 28, 21, d.pose_t, 7);
+  load_cam_fields<16>(ws, g.ncam, 29, 0, d.camrec, kCamRec);
+  load_cam_fields<6>(ws, g.ncam, 29, 16, d.x, 6);
+  load_cam_fields<7>(ws, g.ncam, 29, 22, d.pose_t, 7);
   __syncwarp();
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
-    const double* cam = ws.cam + (lcpt & 0xffff) * 28;
+    const double* cam = ws.cam + (lcpt & 0xffff) * 29;
     P3 y;
     double D[6];
-    obs_geometry(cam, ws.pt + (lcpt >> 16) * 6, y, D);
-    jpt_jc_v(D, y, cam, cam + 15, ws.stage + s * 3);
+    obs_geometry(d.pinhole, cam, ws.pt + (lcpt >> 16) * 6, y, D);
+    jpt_jc_v(D, y, cam, cam + 16, ws.stage + s * 3);
   }
   __syncwarp();
   // Delta p = H~_pp^-1 (-g_p - sum_k J_p^T J_c dc), p_trial = p + Delta p
@@ -1597,14 +1598,15 @@ __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char
   int bad = 0;
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
-    const double* cam = ws.cam + (lcpt & 0xffff) * 28;
+    const double* cam = ws.cam + (lcpt & 0xffff) * 29;
     const double* pt = ws.pt + (lcpt >> 16) * 6 + 3;
-    // trial camera in the [t3 q4 f k1 k2] layout of residual()
-    const double tc[10] = {cam[21], cam[22], cam[23], cam[24], cam[25], cam[26], cam[27], cam[12], cam[13], cam[14]};
+    // trial camera in the [t3 q4 k4] layout of residual()
+    const double tc[11] = {cam[22], cam[23], cam[24], cam[25], cam[26], cam[27], cam[28],
+                           cam[12], cam[13], cam[14], cam[15]};
     const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
     double r0, r1;
     P3 y;
-    if (residual(tc, pt, px, r0, r1, y))
+    if (residual(d.pinhole, tc, pt, px, r0, r1, y))
       cost += r0 * r0 + r1 * r1;
     else
       bad = 1;  // CheiralityError in the trial evaluate -> cost = inf (lm.hpp:176-181)

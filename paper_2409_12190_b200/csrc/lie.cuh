@@ -148,4 +148,39 @@ BAE_HD void bal_dproj(const P3& p, double f, double k1, double k2, double* D) {
   D[5] = f * (d * dq12 + qy * a2);
 }
 
+constexpr double kPinholeDepthEps = 1e-9;  // camera.hpp:30
+
+// pinhole_project_cam forward (camera.hpp:33-38): false unless the point is
+// in front of the camera (CheiralityError in the reference).
+BAE_HD bool pinhole_project(const P3& p, double fx, double fy, double cx, double cy, double& u, double& v) {
+  if (!(p.z > kPinholeDepthEps)) return false;
+  u = fx * p.x / p.z + cx;
+  v = fy * p.y / p.z + cy;
+  return true;
+}
+
+// pinhole_project_cam_jacobian (camera.hpp:40-46).
+BAE_HD void pinhole_dproj(const P3& p, double fx, double fy, double* D) {
+  const double iz = 1.0 / p.z;
+  D[0] = fx * iz;
+  D[1] = 0.0;
+  D[2] = -fx * p.x * iz * iz;
+  D[3] = 0.0;
+  D[4] = fy * iz;
+  D[5] = -fy * p.y * iz * iz;
+}
+
+// The camera variant of a problem (make_ba_problem, problems.hpp:94-98: one
+// variant per problem) on a 4-double intrinsics record: BAL [f k1 k2 0],
+// pinhole [fx fy cx cy].
+BAE_HD bool cam_project(bool pinhole, const P3& p, const double* k, double& u, double& v) {
+  return pinhole ? pinhole_project(p, k[0], k[1], k[2], k[3], u, v) : bal_project(p, k[0], k[1], k[2], u, v);
+}
+BAE_HD void cam_dproj(bool pinhole, const P3& p, const double* k, double* D) {
+  if (pinhole)
+    pinhole_dproj(p, k[0], k[1], D);
+  else
+    bal_dproj(p, k[0], k[1], k[2], D);
+}
+
 }  // namespace bae

@@ -157,7 +157,13 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     plan_.has_empty_camera = std::find(cam_seen.begin(), cam_seen.end(), 0) != cam_seen.end();
     plan_.has_empty_point = std::find(pt_seen.begin(), pt_seen.end(), 0) != pt_seen.end();
   }
-  intr_host_.assign(intr3, intr3 + 3 * static_cast<std::size_t>(C));
+  // intrinsics as 4 doubles per camera: BAL [f k1 k2 0], pinhole [fx fy cx cy]
+  const bool pinhole = opt.camera_model == BAE_CAMERA_PINHOLE;
+  if (opt.camera_model != BAE_CAMERA_BAL && !pinhole) throw Error(BAE_ERR_INVALID_ARGUMENT, "unknown camera model");
+  const int kw = pinhole ? 4 : 3;
+  intr_host_.assign(4 * static_cast<std::size_t>(C), 0.0);
+  for (int c = 0; c < C; ++c)
+    for (int j = 0; j < kw; ++j) intr_host_[4 * static_cast<std::size_t>(c) + j] = intr3[kw * static_cast<std::size_t>(c) + j];
 
   // Tile classes. "Small" tiles (within the kPipe* caps) take the pipelined
   // TMA path of the Schur product and a per-warp shared-memory slice in the
@@ -223,6 +229,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
 
   Dev& d = d_;
   d.C = C;
+  d.pinhole = pinhole ? 1 : 0;
   d.P = use_P;
   d.T = pl.T;
   d.E = pl.E;
@@ -317,6 +324,11 @@ Problem::~Problem() {
   if (lm_host_) cudaFreeHost(lm_host_);
   if (stream_) cudaStreamDestroy(stream_);
   comm_.reset();
+}
+
+// CheiralityError messages of the two camera models (camera.hpp:36, 52).
+const char* Problem::cheirality_msg() const {
+  return d_.pinhole ? "pinhole projection: point behind camera" : "bal projection: point on camera plane";
 }
 
 void Problem::require_single(const char* what) const {
@@ -457,7 +469,7 @@ double Problem::evaluate(double* resid2) {
   read_lm();
   if (lm_host_->err_obs != INT_MAX) {
     if (rbuf) cudaFree(rbuf);
-    throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
+    throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
   }
   if (rbuf) {
     std::vector<double> h(2 * static_cast<std::size_t>(plan_.N));
@@ -476,7 +488,7 @@ void Problem::linearize() {
   read_lm();
   phase_collect();
   if (lm_host_->err_obs != INT_MAX)
-    throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
+    throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
 }
 
 void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
@@ -500,7 +512,7 @@ void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
   cudaFree(js);
   cudaFree(rs);
   if (lm_host_->err_obs != INT_MAX)
-    throw Error(BAE_ERR_CHEIRALITY, "bal projection: point on camera plane", lm_host_->err_obs);
+    throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
   for (std::int64_t s = 0; s < N; ++s) {
     const std::int64_t k = plan_.obs_orig[s];
     if (jpose)

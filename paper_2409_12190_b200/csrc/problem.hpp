@@ -94,6 +94,7 @@ class Problem {
   void build_pcg_graph();
   void build_tile_chol(const std::vector<int2>& bcam);
   void require_single(const char* what) const;
+  const char* cheirality_msg() const;
   void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
   void phase_begin(int ph);
   void phase_end();
