@@ -480,10 +480,10 @@ __device__ __forceinline__ void cam_block_acc(const Dev& d, int c, double* red, 
 // The W = 6 instance (PCG product) is skipped once the solve has finished,
 // like the other kernels of a PCG chunk.
 template <int W, int NT>
-__global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra) {
+__global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg_gated) {
   __shared__ double red[(32 / W) * (NT / 32) * W];
   __shared__ double acc[W];
-  if (W == 6 && d.pcg->state >= kPcgDone) return;
+  if (pcg_gated && d.pcg->state >= kPcgDone) return;
   if (blockIdx.x == gridDim.x - 1) {
     if (extra == 1) {
       double a = 0.0, b = 0.0;
@@ -591,13 +591,17 @@ __global__ void k_finish_cost(Dev d, int trial) {
 // per entry the Schur right-hand side (J_c^T J_p v) and the block-Jacobi
 // blocks (W H~_pp^-1 W^T, W = J_c^T J_p) of S's diagonal.
 // cam: R9 t3 k4 (16) ; pt: p3 hinv6 v3 (12) ; stage 27
+// Direct solver (kDirect): no block-Jacobi blocks (PCG only), stage 6 (the
+// RHS), and W, W H~_pp^-1 of every slot kept for the assembly of S.
 // ---------------------------------------------------------------------------
 constexpr WsDims kPrepWs{16, 12, 27, 0};
+constexpr WsDims kPrepDirWs{16, 12, 6, 0};
 
-template <bool kShared>
+template <bool kShared, bool kDirect>
 __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char* smem, int slice, double lambda,
                                           double clo, double chi) {
-  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kPrepWs, g.ncam, g.npts, g.nobs);
+  constexpr int SW = kDirect ? 6 : 27;
+  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kDirect ? kPrepDirWs : kPrepWs, g.ncam, g.npts, g.nobs);
   const int lane = lane_id();
   load_point_fields<3>(ws, 12, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
@@ -653,17 +657,19 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
 #pragma unroll
       for (int j = 0; j < 3; ++j)
         WH[a * 3 + j] = W[a * 3] * H[j] + W[a * 3 + 1] * H[3 + j] + W[a * 3 + 2] * H[6 + j];
-    double* st = ws.stage + s * 27;
-    int q = 0;
+    double* st = ws.stage + s * SW;
+    if (!kDirect) {
+      int q = 0;
 #pragma unroll
-    for (int a = 0; a < 6; ++a)
+      for (int a = 0; a < 6; ++a)
 #pragma unroll
-      for (int b = a; b < 6; ++b)
-        st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
+        for (int b = a; b < 6; ++b)
+          st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
+    }
     const double* vp = sp + 9;
 #pragma unroll
-    for (int a = 0; a < 6; ++a) st[21 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
-    if (d.wstore) {  // direct solver: keep W and W H~^-1 of this slot
+    for (int a = 0; a < 6; ++a) st[SW - 6 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
+    if (kDirect) {  // direct solver: keep W and W H~^-1 of this slot
       double* w = d.wstore + (long long)(g.ob + s) * 36;
 #pragma unroll
       for (int j = 0; j < 18; ++j) {
@@ -673,16 +679,42 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     }
   }
   __syncwarp();
-  entries_from_stage<27, 27>(ws, g.ncam, g.eb, d.partial);
+  entries_from_stage<SW, SW>(ws, g.ncam, g.eb, d.partial);
   __syncwarp();
 }
 
+template <bool kDirect>
 __global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, double clo, double chi) {
   extern __shared__ __align__(16) char smem[];
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
   const TileGeom g = tile_geom(d, t);
-  BAE_TILE_DISPATCH(prep_tile, d, g, smem, slice, lambda, clo, chi);
+  if (g.big >= 0)
+    prep_tile<false, kDirect>(d, g, smem, slice, lambda, clo, chi);
+  else
+    prep_tile<true, kDirect>(d, g, smem, slice, lambda, clo, chi);
+}
+
+// Camera side of the direct solver's prep (block per camera): damped H~_cc
+// and the Schur RHS b = -g_c + sum_k J_c^T J_p H~_pp^-1 g_p.
+__global__ void __launch_bounds__(128) k_cam_prep_direct(Dev d, double lambda, double clo, double chi) {
+  __shared__ double red[20 * 6];
+  __shared__ double acc[6];
+  const int c = blockIdx.x;
+  cam_block_acc<6, 128>(d, c, red, acc);
+  if (threadIdx.x == 0 && c == 0 && d.cred && d.cred[6LL * d.C] > 0.0)
+    atomicExch(&d.pcg->not_spd, 1);  // a point block failed on some rank
+  if (threadIdx.x < 21) {
+    const int t = threadIdx.x;
+    double h = d.hcc[(long long)c * 21 + t];
+    if (t == sym6(0, 0) || t == sym6(1, 1) || t == sym6(2, 2) || t == sym6(3, 3) || t == sym6(4, 4) ||
+        t == sym6(5, 5))
+      h = damp_diag(h, lambda, clo, chi);
+    d.hccd[(long long)c * 21 + t] = h;
+  } else if (threadIdx.x >= 32 && threadIdx.x < 38) {
+    const int a = threadIdx.x - 32;
+    d.rhs[(long long)c * 6 + a] = -d.gc[(long long)c * 6 + a] + acc[a];
+  }
 }
 
 // Camera side of the prep (block per camera): damped H~_cc, block-Jacobi
@@ -779,33 +811,44 @@ __global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long lo
 // (W_k H~_pp^-1) W_l^T, pairs in (point, k, l) order, lanes strided over the
 // block's pairs, fixed xor tree; column-major lower triangle for potrf.
 // ---------------------------------------------------------------------------
-__global__ void k_schur_dense(Dev d) {
+__global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
+  // Warp per camera block; lane = 4 * slot + part: 8 pairs in flight, each
+  // pair's 6x6 product split in four 3x3 corners (rows 3 (part & 1), columns
+  // 3 (part >> 1)), so a lane loads two contiguous 9-double row bands
+  // (W_k H~^-1 and W_l) and keeps 9 accumulators. The 8 slot sums are then
+  // combined by a fixed shuffle tree: the order depends only on the block.
   const int blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= d.nblk) return;
-  const int lane = lane_id();
-  double acc[36];
+  const int lane = lane_id(), slot = lane >> 2, part = lane & 3;
+  const int r0 = 3 * (part & 1), c0 = 3 * (part >> 1);
+  double acc[9];
 #pragma unroll
-  for (int j = 0; j < 36; ++j) acc[j] = 0.0;
-  for (int q = d.blk_ptr[blk] + lane; q < d.blk_ptr[blk + 1]; q += 32) {
+  for (int j = 0; j < 9; ++j) acc[j] = 0.0;
+  const int qe = d.blk_ptr[blk + 1];
+#pragma unroll 2
+  for (int q = d.blk_ptr[blk] + slot; q < qe; q += 8) {
     const int2 pr = d.pairs[q];
-    const double* wh = d.wstore + (long long)pr.x * 36 + 18;  // W_k H~^-1 (6x3)
-    const double* w = d.wstore + (long long)pr.y * 36;        // W_l (6x3)
-    double a[18], b[18];
+    const double* wh = d.wstore + (long long)pr.x * 36 + 18 + 3 * r0;  // W_k H~^-1 rows r0..r0+2
+    const double* w = d.wstore + (long long)pr.y * 36 + 3 * c0;        // W_l rows c0..c0+2
+    double a[9], b[9];
 #pragma unroll
-    for (int j = 0; j < 18; ++j) {
+    for (int j = 0; j < 9; ++j) {
       a[j] = wh[j];
       b[j] = w[j];
     }
 #pragma unroll
-    for (int r = 0; r < 6; ++r)
+    for (int x = 0; x < 3; ++x)
 #pragma unroll
-      for (int c = 0; c < 6; ++c) acc[r * 6 + c] += a[r * 3] * b[c * 3] + a[r * 3 + 1] * b[c * 3 + 1] + a[r * 3 + 2] * b[c * 3 + 2];
+      for (int y = 0; y < 3; ++y)
+        acc[x * 3 + y] += a[x * 3] * b[y * 3] + a[x * 3 + 1] * b[y * 3 + 1] + a[x * 3 + 2] * b[y * 3 + 2];
   }
 #pragma unroll
-  for (int j = 0; j < 36; ++j) acc[j] = warp_sum(acc[j]);
+  for (int j = 0; j < 9; ++j)
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
   const int2 cc = d.blk_cam[blk];
   const long long n = 6LL * d.C;
-  if (lane == 0) {
+  if (slot == 0) {  // lanes 0..3: one 3x3 corner each
     const double* h = d.hccd + (long long)cc.x * 21;
     // dense column-major S, or the block's place in its 48 x 48 tile (the
     // camera order of the tile factorisation may put it transposed)
@@ -824,10 +867,11 @@ __global__ void k_schur_dense(Dev d) {
       ldc = n;
     }
 #pragma unroll
-    for (int r = 0; r < 6; ++r)
+    for (int x = 0; x < 3; ++x)
 #pragma unroll
-      for (int c = 0; c < 6; ++c) {
-        double v = -acc[r * 6 + c];
+      for (int y = 0; y < 3; ++y) {
+        const int r = r0 + x, c = c0 + y;
+        double v = -acc[x * 3 + y];
         if (cc.x == cc.y && !d.cred) v += h[sym6(r, c)];  // sharded: added after the rank sum
         base[r * ldr + c * ldc] = v;
       }
@@ -1644,6 +1688,8 @@ long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) {
       return ws_bytes(kCostWs, ncam, npts, nobs);
     case kWsPrep:
       return ws_bytes(kPrepWs, ncam, npts, nobs);
+    case kWsPrepDir:
+      return ws_bytes(kPrepDirWs, ncam, npts, nobs);
     case kWsSchur:
       return ws_bytes(kSxWs, ncam, npts, nobs);
     case kWsTrial:
@@ -1655,7 +1701,8 @@ long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) {
 void set_smem_limits(int max_bytes) {
   cudaFuncSetAttribute(k_linearize, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
-  cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+  cudaFuncSetAttribute(k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+  cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_schur_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_backsub_trial, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_pcg_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
@@ -1672,7 +1719,7 @@ int launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
 }
 // Sharded runs: this rank's camera partials -> cross-rank sum in d.cred.
 static int reduce_cams27(const Dev& d, int extra, int nextra, Comm* comm, cudaStream_t s) {
-  k_cam_entry_sums<27, 256><<<d.C + 1, 256, 0, s>>>(d, extra);
+  k_cam_entry_sums<27, 256><<<d.C + 1, 256, 0, s>>>(d, extra, 0);
   comm->allreduce_sum(d.cred, 27 * static_cast<std::size_t>(d.C) + nextra, s);
   return 1;
 }
@@ -1698,10 +1745,22 @@ int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   return 3;
 }
 int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
-                long long budget, cudaStream_t s, Comm* comm) {
+                long long budget, cudaStream_t s, Comm* comm, bool direct) {
+  if (direct) {  // RHS, damped H_cc and the per-slot W / W H~^-1 only
+    k_prep<true><<<tile_blocks(d.T, sm.prepd), 32 * sm.prepd.wpb, sm.prepd.wpb * sm.prepd.slice, s>>>(
+        d, sm.prepd.slice, lambda, clo, chi);
+    int n = 2;
+    if (comm) {
+      k_cam_entry_sums<6, 128><<<d.C + 1, 128, 0, s>>>(d, 2, 0);
+      comm->allreduce_sum(d.cred, 6 * static_cast<std::size_t>(d.C) + 1, s);
+      ++n;
+    }
+    k_cam_prep_direct<<<d.C, 128, 0, s>>>(d, lambda, clo, chi);
+    return n;
+  }
   int n = 3;
-  k_prep<<<tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s>>>(d, sm.prep.slice, lambda,
-                                                                                         clo, chi);
+  k_prep<false><<<tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s>>>(
+      d, sm.prep.slice, lambda, clo, chi);
   if (comm) n += reduce_cams27(d, 2, 1, comm, s);
   k_cam_prep<<<d.C, 256, 0, s>>>(d, lambda, clo, chi);
   k_prep_totals<<<1, 1024, 0, s>>>(d, tol, budget);
@@ -1711,7 +1770,7 @@ int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm
   int n = 3;
   k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
   if (comm) {  // the one exchange per PCG iteration: 6C doubles
-    k_cam_entry_sums<6, 128><<<d.C + 1, 128, 0, s>>>(d, 0);
+    k_cam_entry_sums<6, 128><<<d.C + 1, 128, 0, s>>>(d, 0, 1);
     comm->allreduce_sum(d.cred, 6 * static_cast<std::size_t>(d.C), s);
     ++n;
   }

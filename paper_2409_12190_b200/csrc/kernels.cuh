@@ -8,7 +8,7 @@
 
 namespace bae {
 
-enum WsKind { kWsLin = 0, kWsCost = 1, kWsPrep = 2, kWsSchur = 3, kWsTrial = 4, kWsKinds = 5 };
+enum WsKind { kWsLin = 0, kWsCost = 1, kWsPrep = 2, kWsSchur = 3, kWsTrial = 4, kWsPrepDir = 5, kWsKinds = 6 };
 
 // Launch shape of one warp-tile kernel: `slice` bytes of shared memory per
 // warp (largest small tile of that kind) and `wpb` warps (tiles) per CTA.
@@ -16,7 +16,7 @@ struct TileLaunch {
   int slice = 0, wpb = 1;
 };
 struct SmemSizes {
-  TileLaunch lin, cost, prep, schur, trial;
+  TileLaunch lin, cost, prep, schur, trial, prepd;
 };
 
 long long tile_ws_bytes(int kind, int ncam, int npts, int nobs);
@@ -28,8 +28,10 @@ void set_smem_limits(int max_bytes);
 int launch_camrec(const Dev& d, bool trial, cudaStream_t s);
 int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm);
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
+// direct = true: the direct solver's prep (RHS, damped H_cc, per-slot W and
+// W H~_pp^-1; no block-Jacobi preconditioner and no PCG start state).
 int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
-                long long budget, cudaStream_t s, Comm* comm);
+                long long budget, cudaStream_t s, Comm* comm, bool direct);
 int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
 // Cooperative persistent PCG (whole solve, grid barriers between phases; single rank only).
 int pcg_persistent_grid(const Dev& d, const SmemSizes& sm);

@@ -172,7 +172,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   Plan& pl = plan_;
   long long big_stride = 0;
   int nbig = 0;
-  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial};
+  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial, &sm_.prepd};
   std::vector<int4> desc(static_cast<std::size_t>(pl.T), int4{0, 0, 0, 0});
   std::vector<char> blob;
   std::vector<int> small_tiles, big_tiles;
@@ -834,7 +834,8 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
   if (!d_.wstore) d_.wstore = dalloc<double>(36 * static_cast<std::size_t>(plan_.N));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
-  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get());
+  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
+                           true);
   phase_end();
   phase_begin(kPhAssemble);
   if (use_tiles_)
@@ -931,7 +932,8 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
       cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * (d_.C + P_global_));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
-  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_, comm_.get());
+  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_, comm_.get(),
+                           false);
   phase_end();
   phase_begin(kPhPcg);
   if (comm_ && !comm_->capturable()) {
