@@ -8,8 +8,10 @@
 // tile-level symbolic factorisation done once per problem (plan_tile_chol).
 //
 // Numeric factorisation is ONE persistent kernel, left-looking by tile
-// column: CTA b owns columns b, b + G, ... and processes them in ascending
-// order. Column j first finishes its diagonal tile (the updates from every
+// column: CTAs claim columns in ascending (topological) order from an atomic
+// work counter, so a column that waits for its subtree never holds back
+// columns that are ready (list scheduling; every lower column is already
+// claimed, hence no deadlock). Column j first finishes its diagonal tile (the updates from every
 // column k with L(j,k) != 0, waiting on the epoch flag of that tile), factors
 // and inverts it and performs its step of the forward substitution L y = b;
 // then each tile below the diagonal gets its updates, is solved against
@@ -79,6 +81,7 @@ struct TileChol {
   const int* pos_cam;   // camera at each position (n / 6), -1 for a padding slot
   const unsigned long long* padmask;  // per tile: bit r set when row r is padding (unit pivot)
   unsigned* flags;      // nnz + nt epoch flags: one per stored tile (factor), one per column (backward)
+  unsigned* next;       // 2 work counters (factor, backward): CTAs claim columns in topological order
   int* fail;            // set when a pivot is not positive (NotSpdError, cholesky.hpp:229)
   unsigned long long* trace;  // BAE_CHOL_TRACE: 8 globaltimer stamps per column, or null
 };

@@ -818,6 +818,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (static_cast<std::size_t>(t.nnz) + nt), stream_),
      "memset flags");
   t.fail = dalloc<int>(1);
+  t.next = dalloc<unsigned>(2);
   chol_epoch_ = 0;
   chol_grid_ = tile_chol_grid(nt);
   chol_updates_ = static_cast<long long>(pl.usrc.size());
