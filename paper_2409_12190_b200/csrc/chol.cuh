@@ -44,6 +44,10 @@ struct TileCholPlan {
   std::vector<int> rk, rslot;       // k ascending, slot of L(j,k)
   std::vector<int> uptr;            // per row-structure entry q: range of its tile updates
   std::vector<int> usrc, udst;      // update: C(udst) -= L(usrc) L(rslot[q])^T
+  // per column, its off-diagonal updates ordered by (target tile, k):
+  // {target position in the column, source slot L(i,k), slot of L(j,k)}
+  std::vector<int> bptr;            // nt+1
+  std::vector<int> bop;             // 3 per update
   long long nnz_tiles() const { return static_cast<long long>(rowidx.size()); }
 };
 
@@ -74,6 +78,8 @@ struct TileChol {
   const int* uptr;
   const int* usrc;
   const int* udst;
+  const int* bptr;
+  const int* bop;
   double* tiles;        // nnz_tiles * kTT; diagonal slots receive L(j,j)^-1 after the factorisation
   const double* rhs;    // right-hand side, camera order (6 per camera)
   double* y;            // nt * kTB forward-substitution result

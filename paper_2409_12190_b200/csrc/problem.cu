@@ -751,7 +751,9 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
     groups.emplace_back(C);
     for (int c = 0; c < C; ++c) groups[0][c] = c;
   } else {
-    groups = nd_camera_groups(C, edges, 24);
+    int leaf = 24;  // cameras per nested-dissection leaf (3 tiles)
+    if (const char* l = std::getenv("BAE_ND_LEAF")) leaf = std::max(1, std::atoi(l));
+    groups = nd_camera_groups(C, edges, leaf);
   }
   // positions: groups in order, each padded to whole tiles (8 cameras)
   std::vector<int> pos(static_cast<std::size_t>(C), -1), pos_cam;
@@ -807,6 +809,8 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.uptr = upload(pl.uptr);
   t.usrc = upload(pl.usrc);
   t.udst = upload(pl.udst);
+  t.bptr = upload(pl.bptr);
+  t.bop = upload(pl.bop);
   t.tiles = d_.stiles;
   t.rhs = d_.rhs;
   t.y = dalloc<double>(static_cast<std::size_t>(nt) * kTB);
