@@ -149,6 +149,22 @@ int bae_nccl_unique_id(void* out128);
 int bae_group_create(int32_t world, bae_group** out);
 void bae_group_destroy(bae_group* g);
 
+/* ---- pose graph (make_pgo_problem, problems.hpp:141-188) -- */
+/* Edges (i, j, measurement T as a pose7) with the residual
+ * Log(z_i^-1 z_j T^-1) (trace.hpp:475-487); information36 (nullable) holds a
+ * row-major 6x6 information matrix per edge, used where has_information[k]
+ * != 0 (NULL = every edge): residual rows are whitened by L^T of its Cholesky
+ * factor (problems.hpp:169-184). anchor_first holds pose 0 fixed. The
+ * handle works with bae_optimize (poses only; points NULL; solver =
+ * cholesky), bae_evaluate (6 residuals per edge), bae_set/get_parameters,
+ * bae_num_poses, bae_residual_rows (= edges). */
+int bae_create_pgo(const double* poses7, int32_t num_poses, const int32_t* edge_i, const int32_t* edge_j,
+                   const double* measurements7, const double* information36, const int32_t* has_information,
+                   int64_t num_edges, int32_t anchor_first, const bae_create_options* opts, bae_problem** out);
+/* Per edge d r_w / d pose_i and d r_w / d pose_j (row-major 6x6 each; the
+ * reverse pass of trace.hpp:657-671), for parity tests. */
+int bae_pgo_jacobian(bae_problem* p, double* jacobian_i36, double* jacobian_j36);
+
 /* ---- problem (make_ba_problem, problems.hpp:87-136) ------------------------- */
 /* Validates like the reference (intrinsics count, empty observations,
  * IndexError with the observation position, camera index checked first) and

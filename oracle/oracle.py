@@ -53,6 +53,10 @@ _SIG = {
     "or_ba_problem_new": (VP, [ctypes.c_int, ctypes.c_int, D, ctypes.c_int, D, D, ctypes.c_int64, I32, I32, D,
                                ctypes.POINTER(ctypes.c_int)]),
     "or_scalar_problem_new": (VP, [ctypes.c_int, D]),
+    "or_pgo_problem_new": (VP, [D, ctypes.c_int, I32, I32, D, D, I32, ctypes.c_int64, ctypes.c_int]),
+    "or_make_random_pgo": (ctypes.c_int, [VP, ctypes.c_int, ctypes.c_int, ctypes.c_double, D, I32, I32, D, D, I32,
+                                          I64]),
+    "or_problem_jacobian_dense": (ctypes.c_int, [VP, D, ctypes.c_int64, ctypes.c_int64]),
     "or_problem_free": (None, [VP]),
     "or_problem_evaluate": (ctypes.c_int, [VP, D, D, D, D]),
     "or_problem_jacobian": (ctypes.c_int, [VP, D, D, I64, I32, I64, I32]),
@@ -250,6 +254,59 @@ class Problem:
         return dict(final_cost=rep.final_cost, final_mse=rep.final_mse, iterations=rep.iterations,
                     reason=rep.reason, trajectory=traj, poses=o7, points=o3, solve_seconds=rep.solve_seconds,
                     accepted_steps=rep.accepted_steps, rejected_steps=rep.rejected_steps)
+
+
+def make_random_pgo(rng: Rng, n: int, with_information: bool, noise: float = 0.05):
+    """tests/oracles.hpp:120-152: a chain of poses plus n/2 random extra edges."""
+    cap = n - 1 + n // 2
+    poses = np.empty((n, 7))
+    ei, ej = np.empty(cap, np.int32), np.empty(cap, np.int32)
+    meas, info = np.empty((cap, 7)), np.zeros((cap, 6, 6))
+    has = np.zeros(cap, np.int32)
+    m = ctypes.c_int64()
+    _chk(lib().or_make_random_pgo(rng.h, n, 1 if with_information else 0, noise, p(poses), p(ei, ctypes.c_int32),
+                                  p(ej, ctypes.c_int32), p(meas), p(info), p(has, ctypes.c_int32), ctypes.byref(m)))
+    k = m.value
+    return dict(poses=poses, edge_i=ei[:k].copy(), edge_j=ej[:k].copy(), measurements=meas[:k].copy(),
+                information=info[:k].copy(), has_information=has[:k].copy())
+
+
+class PgoProblem(Problem):
+    """make_pgo_problem restated (problems.hpp:141-188) + the generic LM driver."""
+
+    def __init__(self, poses, edge_i, edge_j, measurements, information=None, has_information=None,
+                 anchor_first=True):
+        self.poses = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 7)
+        self.points = np.zeros((0, 3))
+        ei = np.ascontiguousarray(edge_i, dtype=np.int32)
+        ej = np.ascontiguousarray(edge_j, dtype=np.int32)
+        meas = np.ascontiguousarray(measurements, dtype=np.float64).reshape(-1, 7)
+        self.C, self.P, self.M = self.poses.shape[0], 0, ei.shape[0]
+        self.anchor = bool(anchor_first)
+        info = None if information is None else np.ascontiguousarray(information, dtype=np.float64).reshape(-1, 36)
+        has = None if has_information is None else np.ascontiguousarray(has_information, dtype=np.int32)
+        self.h = lib().or_pgo_problem_new(p(self.poses), self.C, p(ei, ctypes.c_int32), p(ej, ctypes.c_int32),
+                                          p(meas), p(info), p(has, ctypes.c_int32), self.M, 1 if anchor_first else 0)
+        if not self.h:
+            _chk(7 if not lib().or_last_error() else 1)
+
+    @classmethod
+    def from_dict(cls, d, anchor_first=True):
+        return cls(d["poses"], d["edge_i"], d["edge_j"], d["measurements"], d["information"], d["has_information"],
+                   anchor_first)
+
+    def evaluate(self, poses=None, points=None):
+        r = np.empty(6 * self.M)
+        c = ctypes.c_double()
+        p7 = None if poses is None else np.ascontiguousarray(poses, dtype=np.float64)
+        _chk(lib().or_problem_evaluate(self.h, p(p7), None, p(r), ctypes.byref(c)))
+        return r, c.value
+
+    def jacobian_dense(self):
+        cols = 6 * (self.C - (1 if self.anchor else 0))
+        out = np.empty((6 * self.M, cols))
+        _chk(lib().or_problem_jacobian_dense(self.h, p(out), out.shape[0], cols))
+        return out
 
 
 class ScalarProblem:

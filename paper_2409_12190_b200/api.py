@@ -333,6 +333,55 @@ class TracedProblem:
         return dict(zip(keys, (int(v) for v in out)))
 
 
+class PoseGraphProblem(TracedProblem):
+    """make_pgo_problem (problems.hpp:141-188): one 6-row residual per edge,
+    Log(z_i^-1 z_j T^-1) whitened by L^T of the edge information."""
+
+    def residual_width(self) -> int:
+        return 6
+
+    def evaluate(self) -> np.ndarray:
+        r = np.empty(6 * self._N)
+        cost = ctypes.c_double()
+        _check(_lib.load().bae_evaluate(self._h, ptr(r), ctypes.byref(cost)))
+        return r
+
+    def get_parameters(self):
+        p7 = np.empty((self._C, 7))
+        _check(_lib.load().bae_get_parameters(self._h, ptr(p7), None))
+        return p7, np.zeros((0, 3))
+
+    def set_parameters(self, poses, points=None):
+        p7 = _f64(poses, (self._C, 7))
+        _check(_lib.load().bae_set_parameters(self._h, ptr(p7), None))
+
+    def edge_jacobians(self):
+        """Per edge d r_w / d pose_i and d r_w / d pose_j (6 x 6 each)."""
+        ji, jj = np.empty((self._N, 6, 6)), np.empty((self._N, 6, 6))
+        _check(_lib.load().bae_pgo_jacobian(self._h, ptr(ji), ptr(jj)))
+        return ji, jj
+
+
+def make_pgo_problem(poses, edge_i, edge_j, measurements, information=None, has_information=None,
+                     anchor_first: bool = True, *, device: int = 0) -> PoseGraphProblem:
+    """make_pgo_problem (problems.hpp:141-188). ``information`` is E x 6 x 6
+    (or None: unwhitened), ``has_information`` flags the edges that carry one."""
+    p7 = _f64(poses).reshape(-1, 7)
+    ei, ej = _i32(edge_i), _i32(edge_j)
+    meas = _f64(measurements).reshape(-1, 7)
+    info = None if information is None else _f64(information).reshape(-1, 36)
+    has = None if has_information is None else _i32(has_information)
+    lib = _lib.load()
+    opt = CreateOptionsC()
+    lib.bae_create_options_default(ctypes.byref(opt))
+    opt.device = device
+    h = ctypes.c_void_p()
+    _check(lib.bae_create_pgo(ptr(p7), p7.shape[0], ptr(ei, ctypes.c_int32), ptr(ej, ctypes.c_int32), ptr(meas),
+                              ptr(info), ptr(has, ctypes.c_int32), ei.size, 1 if anchor_first else 0,
+                              ctypes.byref(opt), ctypes.byref(h)))
+    return PoseGraphProblem(h, p7.shape[0], 0, ei.size)
+
+
 class RankGroup:
     """In-process rank group: ``world`` ranks in one process, one host thread
     per rank (bae_group_create). Keep it alive while its problems exist."""

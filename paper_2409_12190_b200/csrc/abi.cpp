@@ -14,11 +14,22 @@
 #include "bae_internal.hpp"
 #include "bal_io.hpp"
 #include "chol.cuh"
+#include "pgo.hpp"
 #include "problem.hpp"
 
 struct bae_problem {
-  std::unique_ptr<bae::Problem> impl;
+  std::unique_ptr<bae::Problem> impl;    // bundle adjustment
+  std::unique_ptr<bae::PgoProblem> pgo;  // pose graph (make_pgo_problem)
 };
+
+namespace {
+// The BA problem behind a handle (entry points that only BA supports).
+bae::Problem* ba(const bae_problem* p) {
+  if (!p) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null problem handle");
+  if (!p->impl) throw bae::Error(BAE_ERR_UNSUPPORTED, "not available on a pose-graph problem");
+  return p->impl.get();
+}
+}  // namespace
 
 struct bae_bal {
   bae::BalData d;
@@ -117,28 +128,71 @@ int bae_create_ba(const double* poses7, int32_t C, const double* points3, int32_
 
 void bae_destroy(bae_problem* p) { delete p; }
 
-int32_t bae_num_poses(const bae_problem* p) { return p ? p->impl->num_cameras() : 0; }
-int32_t bae_num_points(const bae_problem* p) { return p ? p->impl->num_points() : 0; }
-int64_t bae_residual_rows(const bae_problem* p) { return p ? p->impl->num_obs() : 0; }
+int bae_create_pgo(const double* poses7, int32_t num_poses, const int32_t* edge_i, const int32_t* edge_j,
+                   const double* measurements7, const double* information36, const int32_t* has_information,
+                   int64_t num_edges, int32_t anchor_first, const bae_create_options* opts, bae_problem** out) {
+  return guarded([&] {
+    if (!out) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null output handle");
+    *out = nullptr;
+    if ((num_poses > 0 && !poses7) || (num_edges > 0 && (!edge_i || !edge_j || !measurements7)))
+      throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null pose-graph arrays");
+    bae_create_options o;
+    bae_create_options_default(&o);
+    if (opts) o = *opts;
+    if (o.world != 1 || o.group || o.nccl_id)
+      throw bae::Error(BAE_ERR_UNSUPPORTED, "pose graphs run on a single rank");
+    auto h = std::make_unique<bae_problem>();
+    h->pgo = std::make_unique<bae::PgoProblem>(poses7, num_poses, edge_i, edge_j, measurements7, information36,
+                                               has_information, num_edges, anchor_first != 0, o);
+    *out = h.release();
+  });
+}
+
+int bae_pgo_jacobian(bae_problem* p, double* ji36, double* jj36) {
+  return guarded([&] {
+    if (!p || !p->pgo) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "not a pose-graph problem");
+    p->pgo->jacobian(ji36, jj36);
+  });
+}
+
+int32_t bae_num_poses(const bae_problem* p) {
+  return !p ? 0 : p->pgo ? p->pgo->num_poses() : p->impl->num_cameras();
+}
+int32_t bae_num_points(const bae_problem* p) { return !p || p->pgo ? 0 : p->impl->num_points(); }
+int64_t bae_residual_rows(const bae_problem* p) {
+  return !p ? 0 : p->pgo ? p->pgo->num_edges() : p->impl->num_obs();
+}
 
 int bae_set_parameters(bae_problem* p, const double* poses7, const double* points3) {
-  return guarded([&] { p->impl->set_parameters(poses7, points3); });
+  return guarded([&] {
+    if (p && p->pgo) {
+      if (poses7) p->pgo->set_parameters(poses7);
+      return;
+    }
+    ba(p)->set_parameters(poses7, points3);
+  });
 }
 int bae_get_parameters(bae_problem* p, double* poses7, double* points3) {
-  return guarded([&] { p->impl->get_parameters(poses7, points3); });
+  return guarded([&] {
+    if (p && p->pgo) {
+      if (poses7) p->pgo->get_parameters(poses7);
+      return;
+    }
+    ba(p)->get_parameters(poses7, points3);
+  });
 }
 int bae_evaluate(bae_problem* p, double* residuals2, double* cost) {
   return guarded([&] {
-    const double c = p->impl->evaluate(residuals2);
+    const double c = (p && p->pgo) ? p->pgo->evaluate(residuals2) : ba(p)->evaluate(residuals2);
     if (cost) *cost = c;
   });
 }
 int bae_jacobian(bae_problem* p, double* jpose, double* jpoint, int64_t* prp, int32_t* pcol, int64_t* lrp,
                  int32_t* lcol) {
   return guarded([&] {
-    if (p->impl->distributed()) throw bae::Error(BAE_ERR_UNSUPPORTED, "the Jacobian export needs a single-rank problem");
-    if (jpose || jpoint) p->impl->jacobian(jpose, jpoint, nullptr);
-    const bae::Plan& pl = p->impl->plan();
+    if (ba(p)->distributed()) throw bae::Error(BAE_ERR_UNSUPPORTED, "the Jacobian export needs a single-rank problem");
+    if (jpose || jpoint) ba(p)->jacobian(jpose, jpoint, nullptr);
+    const bae::Plan& pl = ba(p)->plan();
     const std::int64_t N = pl.N;
     std::vector<std::int32_t> cam(static_cast<std::size_t>(N)), pt(static_cast<std::size_t>(N));
     // gather columns from the device-side decomposition (entry camera, tile point)
@@ -159,9 +213,9 @@ int bae_jacobian(bae_problem* p, double* jpose, double* jpoint, int64_t* prp, in
 
 int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t* col_idx, int64_t* src_block) {
   return guarded([&] {
-    if (p->impl->distributed())
+    if (ba(p)->distributed())
       throw bae::Error(BAE_ERR_UNSUPPORTED, "the transpose plans need a single-rank problem");
-    const bae::Plan& pl = p->impl->plan();
+    const bae::Plan& pl = ba(p)->plan();
     if (which == 0) {
       // camera segments: entries of each camera, observations re-listed in id order
       std::vector<std::int64_t> rp(static_cast<std::size_t>(pl.C) + 1, 0);
@@ -200,7 +254,7 @@ int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t*
 }
 
 int bae_block_diagonals(bae_problem* p, double* hcc36, double* gc6, double* hpp9, double* gp3) {
-  return guarded([&] { p->impl->block_diagonals(hcc36, gc6, hpp9, gp3); });
+  return guarded([&] { ba(p)->block_diagonals(hcc36, gc6, hpp9, gp3); });
 }
 
 int bae_optimize(bae_problem* p, const double* init_poses7, const double* init_points3, const bae_lm_config* cfg,
@@ -212,11 +266,18 @@ int bae_optimize(bae_problem* p, const double* init_poses7, const double* init_p
     if (cfg) c = *cfg;
     std::vector<bae_iter_record> t;
     bae_lm_report r{};
-    p->impl->optimize(init_poses7, init_points3, c, t, r);
+    if (p && p->pgo)
+      p->pgo->optimize(init_poses7, c, t, r);
+    else
+      ba(p)->optimize(init_poses7, init_points3, c, t, r);
     if (traj)
       for (int i = 0; i < std::min<int>(traj_cap, static_cast<int>(t.size())); ++i) traj[i] = t[i];
     if (report) *report = r;
-    if (poses_out || points_out) p->impl->get_parameters(poses_out, points_out);
+    if (p->pgo) {
+      if (poses_out) p->pgo->get_parameters(poses_out);
+    } else if (poses_out || points_out) {
+      ba(p)->get_parameters(poses_out, points_out);
+    }
   });
 }
 
@@ -226,7 +287,7 @@ int bae_solve_step(bae_problem* p, double lambda, const bae_lm_config* cfg, doub
     bae_lm_config c;
     bae_lm_config_default(&c);
     if (cfg) c = *cfg;
-    p->impl->solve_step(lambda, c, delta, iters, relres);
+    ba(p)->solve_step(lambda, c, delta, iters, relres);
   });
 }
 
@@ -259,29 +320,31 @@ int bae_partition_points(int32_t C, int32_t P, const int32_t* cam_idx, const int
 }
 
 int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms) {
-  return guarded([&] { *ms = p->impl->time_kernel(kind, reps); });
+  return guarded([&] { *ms = ba(p)->time_kernel(kind, reps); });
 }
 
-int64_t bae_launch_count(const bae_problem* p) { return p ? p->impl->launches() : 0; }
+int64_t bae_launch_count(const bae_problem* p) {
+  return !p ? 0 : p->pgo ? p->pgo->launches() : p->impl->launches();
+}
 
 int bae_phase_times(bae_problem* p, double* ms7, int32_t reset) {
   return guarded([&] {
-    if (ms7) p->impl->phase_times(ms7);
-    if (reset) p->impl->phase_reset();
+    if (ms7) ba(p)->phase_times(ms7);
+    if (reset) ba(p)->phase_reset();
   });
 }
 
 int bae_direct_stats(const bae_problem* p, int64_t* out5) {
   return guarded([&] {
     long long v[5];
-    p->impl->direct_stats(v);
+    ba(p)->direct_stats(v);
     for (int i = 0; i < 5; ++i) out5[i] = v[i];
   });
 }
 
 int bae_problem_stats(const bae_problem* p, int64_t* out6) {
   return guarded([&] {
-    const bae::Plan& pl = p->impl->plan();
+    const bae::Plan& pl = ba(p)->plan();
     out6[0] = pl.N;
     out6[1] = pl.P;
     out6[2] = pl.C;
@@ -294,10 +357,10 @@ int bae_problem_stats(const bae_problem* p, int64_t* out6) {
 int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32_t* local_points,
                       int64_t* local_observations) {
   return guarded([&] {
-    if (rank) *rank = p->impl->rank();
-    if (world) *world = p->impl->world();
-    if (local_points) *local_points = p->impl->local_points();
-    if (local_observations) *local_observations = p->impl->local_obs();
+    if (rank) *rank = ba(p)->rank();
+    if (world) *world = ba(p)->world();
+    if (local_points) *local_points = ba(p)->local_points();
+    if (local_observations) *local_observations = ba(p)->local_obs();
   });
 }
 
