@@ -257,6 +257,18 @@ int bae_bal_arrays(const bae_bal* b, double* poses7, double* intrinsics3, double
 /* serialize_bal (io/bal.hpp:145-157): %.17g, round-trips doubles exactly. */
 int bae_bal_write(const bae_bal* b, const char* path);
 void bae_bal_free(bae_bal* b);
+/* parse_g2o (io/g2o.hpp:30-80): VERTEX_SE3:QUAT / EDGE_SE3:QUAT, edge
+ * endpoints remapped to vertex positions, identity information elided
+ * (has_information = 0), unknown tags kept as warnings; ParseError ->
+ * BAE_ERR_PARSE with the line. */
+typedef struct bae_g2o bae_g2o;
+int bae_g2o_read(const char* path, bae_g2o** out);
+int bae_g2o_parse(const char* text, int64_t len, bae_g2o** out);
+int bae_g2o_counts(const bae_g2o* g, int32_t* num_vertices, int64_t* num_edges, int32_t* num_warnings);
+int bae_g2o_arrays(const bae_g2o* g, double* poses7, int64_t* vertex_ids, int32_t* edge_i, int32_t* edge_j,
+                   double* measurements7, double* information36, int32_t* has_information);
+const char* bae_g2o_warning(const bae_g2o* g, int32_t k);
+void bae_g2o_free(bae_g2o* g);
 /* write_csv (cli.hpp:69-79): iter,cost,mse,lambda,accepted,cum_time_s. */
 int bae_write_csv(const char* path, const bae_iter_record* traj, int32_t n);
 /* cli_main (cli.hpp:116-200): `ba` / `pgo` subcommands, the reference's flags

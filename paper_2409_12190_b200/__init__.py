@@ -5,10 +5,12 @@ from .api import (CheiralityError, DeviceError, IndexError, JacobianPair, LmConf
                   NotSpdError, NumericalBreakdownError, SolverChoice, TerminationReason, TracedProblem,
                   UnsupportedOperationError, RankGroup, make_ba_problem, nccl_unique_id, optimize,
                   partition_points, stop_on_plateau, write_csv, BalProblem, ParseError, read_bal, parse_bal,
-                  synth_ba, write_bal, cli_main, PoseGraphProblem, make_pgo_problem)
+                  synth_ba, write_bal, cli_main, PoseGraphProblem, make_pgo_problem,
+                  PoseGraph, read_g2o, parse_g2o)
 from . import synthetic
 
 __all__ = ["CheiralityError", "DeviceError", "IndexError", "JacobianPair", "LmConfig", "LmIterationRecord", "LmReport",
            "NotSpdError", "NumericalBreakdownError", "SolverChoice", "TerminationReason", "TracedProblem",
            "UnsupportedOperationError", "RankGroup", "make_ba_problem", "nccl_unique_id", "partition_points", "optimize", "BalProblem",
-           "ParseError", "read_bal", "parse_bal", "synth_ba", "write_bal", "cli_main", "PoseGraphProblem", "make_pgo_problem", "stop_on_plateau", "write_csv", "synthetic"]
+           "ParseError", "read_bal", "parse_bal", "synth_ba", "write_bal", "cli_main", "PoseGraphProblem", "make_pgo_problem", "PoseGraph", "read_g2o",
+           "parse_g2o", "stop_on_plateau", "write_csv", "synthetic"]

@@ -135,6 +135,13 @@ SIGNATURES = {
                                       c_double_p, c_double_p]),
     "bae_bal_write": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
     "bae_bal_free": (None, [ctypes.c_void_p]),
+    "bae_g2o_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_g2o_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "bae_g2o_counts": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int64_p, c_int32_p]),
+    "bae_g2o_arrays": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_int64_p, c_int32_p, c_int32_p, c_double_p,
+                                      c_double_p, c_int32_p]),
+    "bae_g2o_warning": (ctypes.c_char_p, [ctypes.c_void_p, ctypes.c_int32]),
+    "bae_g2o_free": (None, [ctypes.c_void_p]),
     "bae_write_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(IterRecordC), ctypes.c_int32]),
     "bae_cli_main": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p)]),
 }

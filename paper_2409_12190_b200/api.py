@@ -362,10 +362,15 @@ class PoseGraphProblem(TracedProblem):
         return ji, jj
 
 
-def make_pgo_problem(poses, edge_i, edge_j, measurements, information=None, has_information=None,
+def make_pgo_problem(poses, edge_i=None, edge_j=None, measurements=None, information=None, has_information=None,
                      anchor_first: bool = True, *, device: int = 0) -> PoseGraphProblem:
     """make_pgo_problem (problems.hpp:141-188). ``information`` is E x 6 x 6
-    (or None: unwhitened), ``has_information`` flags the edges that carry one."""
+    (or None: unwhitened), ``has_information`` flags the edges that carry one.
+    ``make_pgo_problem(graph)`` takes a PoseGraph (io/g2o.hpp:82-84)."""
+    if isinstance(poses, PoseGraph):
+        g = poses
+        return make_pgo_problem(g.vertices, g.edge_i, g.edge_j, g.measurements, g.information,
+                                g.has_information, anchor_first if edge_i is None else bool(edge_i), device=device)
     p7 = _f64(poses).reshape(-1, 7)
     ei, ej = _i32(edge_i), _i32(edge_j)
     meas = _f64(measurements).reshape(-1, 7)
@@ -555,6 +560,52 @@ def parse_bal(text) -> BalProblem:
     h = ctypes.c_void_p()
     _check(_lib.load().bae_bal_parse(data, len(data), ctypes.byref(h)))
     return _bal_from_handle(h)
+
+
+@dataclasses.dataclass
+class PoseGraph:
+    """PoseGraph (io/g2o.hpp:16-23): vertices as pose7 [t, q(x,y,z,w)] in file
+    order with their g2o ids; edges remapped to vertex positions; identity
+    information elided (has_information 0); skipped-tag warnings."""
+    vertex_ids: np.ndarray
+    vertices: np.ndarray
+    edge_i: np.ndarray
+    edge_j: np.ndarray
+    measurements: np.ndarray
+    information: np.ndarray
+    has_information: np.ndarray
+    warnings: list
+
+
+def _g2o_from_handle(h) -> PoseGraph:
+    lib = _lib.load()
+    n, m, w = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int32()
+    try:
+        _check(lib.bae_g2o_counts(h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(w)))
+        n, m = n.value, m.value
+        ids, poses = np.empty(n, np.int64), np.empty((n, 7))
+        ei, ej, has = np.empty(m, np.int32), np.empty(m, np.int32), np.empty(m, np.int32)
+        meas, info = np.empty((m, 7)), np.empty((m, 6, 6))
+        _check(lib.bae_g2o_arrays(h, ptr(poses), ptr(ids, ctypes.c_int64), ptr(ei, ctypes.c_int32),
+                                  ptr(ej, ctypes.c_int32), ptr(meas), ptr(info), ptr(has, ctypes.c_int32)))
+        warnings = [lib.bae_g2o_warning(h, k).decode() for k in range(w.value)]
+    finally:
+        lib.bae_g2o_free(h)
+    return PoseGraph(ids, poses, ei, ej, meas, info, has, warnings)
+
+
+def read_g2o(path: str) -> PoseGraph:
+    """parse_g2o (io/g2o.hpp:30-80) of a file; ParseError carries the line."""
+    h = ctypes.c_void_p()
+    _check(_lib.load().bae_g2o_read(str(path).encode(), ctypes.byref(h)))
+    return _g2o_from_handle(h)
+
+
+def parse_g2o(text) -> PoseGraph:
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = ctypes.c_void_p()
+    _check(_lib.load().bae_g2o_parse(data, len(data), ctypes.byref(h)))
+    return _g2o_from_handle(h)
 
 
 def synth_ba(num_cameras: int, num_points: int, pixel_noise: float, pose_noise: float, seed: int) -> BalProblem:

@@ -35,6 +35,10 @@ struct bae_bal {
   bae::BalData d;
 };
 
+struct bae_g2o {
+  bae::G2oData d;
+};
+
 namespace {
 thread_local std::string g_msg;
 thread_local std::int64_t g_index = -1;
@@ -471,6 +475,55 @@ int bae_bal_write(const bae_bal* b, const char* path) {
 }
 
 void bae_bal_free(bae_bal* b) { delete b; }
+
+int bae_g2o_read(const char* path, bae_g2o** out) {
+  return guarded([&] {
+    if (!path || !out) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null argument");
+    auto h = std::make_unique<bae_g2o>();
+    h->d = bae::parse_g2o_file(path);
+    *out = h.release();
+  });
+}
+
+int bae_g2o_parse(const char* text, int64_t len, bae_g2o** out) {
+  return guarded([&] {
+    if (!text || !out || len < 0) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "null argument");
+    auto h = std::make_unique<bae_g2o>();
+    h->d = bae::parse_g2o_text(text, text + len);
+    *out = h.release();
+  });
+}
+
+int bae_g2o_counts(const bae_g2o* g, int32_t* num_vertices, int64_t* num_edges, int32_t* num_warnings) {
+  return guarded([&] {
+    if (num_vertices) *num_vertices = static_cast<int32_t>(g->d.ids.size());
+    if (num_edges) *num_edges = static_cast<int64_t>(g->d.ei.size());
+    if (num_warnings) *num_warnings = static_cast<int32_t>(g->d.warnings.size());
+  });
+}
+
+int bae_g2o_arrays(const bae_g2o* g, double* poses7, int64_t* vertex_ids, int32_t* edge_i, int32_t* edge_j,
+                   double* measurements7, double* information36, int32_t* has_information) {
+  return guarded([&] {
+    const bae::G2oData& d = g->d;
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(poses7, d.poses);
+    cp(vertex_ids, d.ids);
+    cp(edge_i, d.ei);
+    cp(edge_j, d.ej);
+    cp(measurements7, d.meas);
+    cp(information36, d.info);
+    cp(has_information, d.has_info);
+  });
+}
+
+const char* bae_g2o_warning(const bae_g2o* g, int32_t k) {
+  return (g && k >= 0 && k < static_cast<int32_t>(g->d.warnings.size())) ? g->d.warnings[k].c_str() : nullptr;
+}
+
+void bae_g2o_free(bae_g2o* g) { delete g; }
 
 int bae_write_csv(const char* path, const bae_iter_record* traj, int32_t n) {  // cli.hpp:69-79
   return guarded([&] {

@@ -10,8 +10,10 @@
 #include <charconv>
 #include <cmath>
 #include <cstdio>
+#include <cctype>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "bae/rng.hpp"
@@ -192,6 +194,113 @@ void bal_poses(const BalData& d, double* poses7, double* intr3) {
       intr3[3 * c + 2] = cam[8];
     }
   }
+}
+
+namespace {
+// QuatRotation(x, y, z, w) (lie.hpp:33-45): normalise, w >= 0; invalid_argument otherwise.
+void quat_ctor(double x, double y, double z, double w, double* out4) {
+  if (!std::isfinite(x) || !std::isfinite(y) || !std::isfinite(z) || !std::isfinite(w))
+    throw Error(BAE_ERR_INVALID_ARGUMENT, "QuatRotation: non-finite component");
+  Q4 q;
+  if (!quat_normalize(x, y, z, w, q)) throw Error(BAE_ERR_INVALID_ARGUMENT, "QuatRotation: zero quaternion");
+  out4[0] = q.x;
+  out4[1] = q.y;
+  out4[2] = q.z;
+  out4[3] = q.w;
+}
+bool parse_num(const std::string& t, double& v) {
+  const auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+  return r.ec == std::errc{} && r.ptr == t.data() + t.size();
+}
+bool parse_num(const std::string& t, std::int64_t& v) {
+  const auto r = std::from_chars(t.data(), t.data() + t.size(), v);
+  return r.ec == std::errc{} && r.ptr == t.data() + t.size();
+}
+}  // namespace
+
+G2oData parse_g2o_text(const char* b, const char* e) {
+  G2oData g;
+  std::unordered_map<std::int64_t, std::int32_t> index;
+  std::size_t line_no = 0;
+  std::vector<std::string> tok;
+  const char* p = b;
+  while (p < e) {
+    const char* le = p;
+    while (le < e && *le != '\n') ++le;
+    ++line_no;
+    tok.clear();
+    for (const char* q = p; q < le;) {  // whitespace tokens of the line
+      while (q < le && std::isspace(static_cast<unsigned char>(*q))) ++q;
+      const char* t0 = q;
+      while (q < le && !std::isspace(static_cast<unsigned char>(*q))) ++q;
+      if (q > t0) tok.emplace_back(t0, q);
+    }
+    p = le < e ? le + 1 : le;
+    if (tok.empty() || tok[0][0] == '#') continue;
+    const std::string& tag = tok[0];
+    if (tag == "VERTEX_SE3:QUAT") {
+      std::int64_t id = 0;
+      double v[7];
+      bool ok = tok.size() >= 9 && parse_num(tok[1], id);
+      for (int i = 0; ok && i < 7; ++i) ok = parse_num(tok[2 + i], v[i]);
+      if (!ok) throw Error(BAE_ERR_PARSE, "malformed VERTEX_SE3:QUAT line", static_cast<std::int64_t>(line_no));
+      if (index.count(id)) throw Error(BAE_ERR_PARSE, "duplicate vertex id", static_cast<std::int64_t>(line_no));
+      index[id] = static_cast<std::int32_t>(g.ids.size());
+      g.ids.push_back(id);
+      double q[4];
+      quat_ctor(v[3], v[4], v[5], v[6], q);
+      g.poses.insert(g.poses.end(), {v[0], v[1], v[2], q[0], q[1], q[2], q[3]});
+    } else if (tag == "EDGE_SE3:QUAT") {
+      std::int64_t i = 0, j = 0;
+      double v[7];
+      bool ok = tok.size() >= 10 && parse_num(tok[1], i) && parse_num(tok[2], j);
+      for (int k = 0; ok && k < 7; ++k) ok = parse_num(tok[3 + k], v[k]);
+      if (!ok) throw Error(BAE_ERR_PARSE, "malformed EDGE_SE3:QUAT line", static_cast<std::int64_t>(line_no));
+      double info[36];
+      std::size_t at = 10;
+      for (int r = 0; r < 6; ++r)
+        for (int c = r; c < 6; ++c) {
+          double x = 0;
+          if (at >= tok.size() || !parse_num(tok[at], x))
+            throw Error(BAE_ERR_PARSE, "missing information entries on edge", static_cast<std::int64_t>(line_no));
+          ++at;
+          info[r * 6 + c] = x;
+          info[c * 6 + r] = x;
+        }
+      const auto it_i = index.find(i), it_j = index.find(j);
+      if (it_i == index.end() || it_j == index.end())
+        throw Error(BAE_ERR_PARSE, "edge references undeclared vertex", static_cast<std::int64_t>(line_no));
+      g.ei.push_back(it_i->second);
+      g.ej.push_back(it_j->second);
+      double q[4];
+      quat_ctor(v[3], v[4], v[5], v[6], q);
+      g.meas.insert(g.meas.end(), {v[0], v[1], v[2], q[0], q[1], q[2], q[3]});
+      // Eigen isApprox(Identity): ||info - I||_F <= 1e-12 min(||info||_F, ||I||_F)
+      double dn = 0.0, an = 0.0;
+      for (int r = 0; r < 36; ++r) {
+        const double id = (r % 7 == 0) ? 1.0 : 0.0;
+        dn += (info[r] - id) * (info[r] - id);
+        an += info[r] * info[r];
+      }
+      const bool identity = std::sqrt(dn) <= 1e-12 * std::min(std::sqrt(an), std::sqrt(6.0));
+      g.has_info.push_back(identity ? 0 : 1);
+      g.info.insert(g.info.end(), info, info + 36);
+    } else {
+      g.warnings.push_back("line " + std::to_string(line_no) + ": skipped unknown tag '" + tag + "'");
+    }
+  }
+  return g;
+}
+
+G2oData parse_g2o_file(const char* path) {
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) throw Error(BAE_ERR_IO, std::string("cannot open '") + path + "'");
+  std::string buf;
+  char chunk[1 << 16];
+  std::size_t n;
+  while ((n = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.append(chunk, n);
+  std::fclose(f);
+  return parse_g2o_text(buf.data(), buf.data() + buf.size());
 }
 
 BalData synth_ba_dense(int C, int P, double pixel_sigma, double pose_sigma, std::uint64_t seed) {

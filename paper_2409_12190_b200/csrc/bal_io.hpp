@@ -28,4 +28,18 @@ void bal_poses(const BalData& d, double* poses7, double* intr3);  // BalCamera::
 BalData synth_ba_dense(int C, int P, double pixel_sigma, double pose_sigma, std::uint64_t seed);  // synth_ba
 void look_at_origin(const P3& pos, Q4& q, P3& t);  // io/synthetic.hpp:26-38 (synth.cpp)
 
+// PoseGraph (io/g2o.hpp:16-23): vertices as pose7 in file order (ids kept),
+// edges with endpoints remapped to vertex positions, information matrices
+// (36 row-major, has_info = not the identity), skipped-tag warnings.
+struct G2oData {
+  std::vector<std::int64_t> ids;
+  std::vector<double> poses;  // 7 n
+  std::vector<std::int32_t> ei, ej, has_info;
+  std::vector<double> meas;   // 7 m
+  std::vector<double> info;   // 36 m
+  std::vector<std::string> warnings;
+};
+G2oData parse_g2o_text(const char* begin, const char* end);  // parse_g2o, io/g2o.hpp:30-80
+G2oData parse_g2o_file(const char* path);
+
 }  // namespace bae

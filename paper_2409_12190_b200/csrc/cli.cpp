@@ -38,7 +38,7 @@ const char* kHelp =
     "Usage: traceopt_bench SUBCOMMAND [OPTIONS]\n\n"
     "Subcommands:\n"
     "  ba     Bundle adjustment on a BAL file or synthetic scene\n"
-    "  pgo    Pose graph optimization on a g2o file (not part of the B200 path)\n\n"
+    "  pgo    Pose graph optimization on a g2o file\n\n"
     "ba options:\n"
     "  --input FILE          BAL problem file\n"
     "  --synthetic CxP       Synthetic scene CxP, e.g. 3x50\n"
@@ -166,6 +166,42 @@ int report_error(int code) {
   }
 }
 
+// run_and_report (cli.hpp:89-106): optimise, print the summary line, write
+// the CSV; exit 3 on solver failure. Destroys the problem.
+int run_and_report(bae_problem* prob, const double* poses, const double* points, const CliOptions& o,
+                   const std::string& dataset) {
+  bae_lm_config cfg;  // config_from (cli.hpp:47-54)
+  bae_lm_config_default(&cfg);
+  cfg.initial_damping = o.damping;
+  cfg.max_iterations = o.max_iters;
+  cfg.solver = o.solver == "pcg" ? BAE_SOLVER_PCG : BAE_SOLVER_CHOLESKY;
+  cfg.pcg_tol = o.pcg_tol;
+  std::vector<bae_iter_record> traj(static_cast<std::size_t>(std::max(o.max_iters, 0)) + 1);
+  bae_lm_report rep;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = bae_optimize(prob, poses, points, &cfg, traj.data(), static_cast<int32_t>(traj.size()),
+                              &rep, nullptr, nullptr);
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rc) {
+    const int code = report_error(rc);
+    bae_destroy(prob);
+    return code;
+  }
+  bae_destroy(prob);
+  std::printf("dataset=%s solver=%s iterations=%d final_cost=%.9g final_mse=%.9g termination=%s time_s=%.3f\n",
+              dataset.c_str(), o.solver.c_str(), rep.iterations, rep.final_cost, rep.final_mse,
+              reason_name(rep.reason), wall);
+  std::fflush(stdout);
+  if (!o.csv_path.empty()) {
+    const int n = std::min(rep.iterations + 1, static_cast<int>(traj.size()));
+    if (int wc = bae_write_csv(o.csv_path.c_str(), traj.data(), n)) {
+      std::fprintf(stderr, "error: %s\n", bae_last_error());
+      return wc == BAE_ERR_IO ? 3 : 3;
+    }
+  }
+  return rep.reason == BAE_TERM_SOLVER_FAILURE ? 3 : 0;
+}
+
 }  // namespace
 }  // namespace bae
 
@@ -186,15 +222,27 @@ extern "C" int bae_cli_main(int argc, const char* const* argv) {
     const std::string t = std::to_string(o.threads);
     setenv("BAE_HOST_THREADS", t.c_str(), 1);  // set_num_threads (cli.hpp:174)
   }
-  if (sub == "pgo") {
-    std::FILE* f = std::fopen(o.input.c_str(), "rb");
-    if (!f) {
-      std::fprintf(stderr, "cannot open '%s'\n", o.input.c_str());
-      return 2;
-    }
-    std::fclose(f);
-    std::fprintf(stderr, "pgo: pose-graph optimisation is not part of the B200 path (DESIGN.md section 9)\n");
-    return 1;
+  if (sub == "pgo") {  // cli.hpp:179-185
+    bae_g2o* g = nullptr;
+    if (int rc = bae_g2o_read(o.input.c_str(), &g)) return report_error(rc);
+    int32_t nv = 0, nw = 0;
+    int64_t ne = 0;
+    bae_g2o_counts(g, &nv, &ne, &nw);
+    for (int32_t k = 0; k < nw; ++k) std::fprintf(stderr, "warning: %s\n", bae_g2o_warning(g, k));
+    std::vector<double> poses(7 * static_cast<std::size_t>(nv)), meas(7 * static_cast<std::size_t>(ne)),
+        info(36 * static_cast<std::size_t>(ne));
+    std::vector<int32_t> ei(static_cast<std::size_t>(ne)), ej(static_cast<std::size_t>(ne)),
+        has(static_cast<std::size_t>(ne));
+    bae_g2o_arrays(g, poses.data(), nullptr, ei.data(), ej.data(), meas.data(), info.data(), has.data());
+    bae_g2o_free(g);
+    bae_create_options opt;
+    bae_create_options_default(&opt);
+    opt.device = o.device;
+    bae_problem* prob = nullptr;
+    if (int rc = bae_create_pgo(poses.data(), nv, ei.data(), ej.data(), meas.data(), info.data(), has.data(), ne, 1,
+                                &opt, &prob))
+      return report_error(rc);
+    return run_and_report(prob, poses.data(), nullptr, o, o.input);
   }
   bae_bal* bal = nullptr;
   std::string dataset;
@@ -228,34 +276,5 @@ extern "C" int bae_cli_main(int argc, const char* const* argv) {
   if (int rc = bae_create_ba(poses.data(), C, pts.data(), P, intr.data(), ci.data(), pi.data(), px.data(), N, &opt,
                              &prob))
     return report_error(rc);
-  bae_lm_config cfg;  // config_from (cli.hpp:47-54)
-  bae_lm_config_default(&cfg);
-  cfg.initial_damping = o.damping;
-  cfg.max_iterations = o.max_iters;
-  cfg.solver = o.solver == "pcg" ? BAE_SOLVER_PCG : BAE_SOLVER_CHOLESKY;
-  cfg.pcg_tol = o.pcg_tol;
-  std::vector<bae_iter_record> traj(static_cast<std::size_t>(std::max(o.max_iters, 0)) + 1);
-  bae_lm_report rep;
-  const auto t0 = std::chrono::steady_clock::now();
-  const int rc = bae_optimize(prob, poses.data(), pts.data(), &cfg, traj.data(), static_cast<int32_t>(traj.size()),
-                              &rep, nullptr, nullptr);
-  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  if (rc) {
-    const int code = report_error(rc);
-    bae_destroy(prob);
-    return code;
-  }
-  bae_destroy(prob);
-  std::printf("dataset=%s solver=%s iterations=%d final_cost=%.9g final_mse=%.9g termination=%s time_s=%.3f\n",
-              dataset.c_str(), o.solver.c_str(), rep.iterations, rep.final_cost, rep.final_mse,
-              reason_name(rep.reason), wall);
-  std::fflush(stdout);
-  if (!o.csv_path.empty()) {
-    const int n = std::min(rep.iterations + 1, static_cast<int>(traj.size()));
-    if (int wc = bae_write_csv(o.csv_path.c_str(), traj.data(), n)) {
-      std::fprintf(stderr, "error: %s\n", bae_last_error());
-      return wc == BAE_ERR_IO ? 3 : 3;
-    }
-  }
-  return rep.reason == BAE_TERM_SOLVER_FAILURE ? 3 : 0;
+  return run_and_report(prob, poses.data(), pts.data(), o, dataset);
 }
