@@ -44,10 +44,10 @@ struct TileCholPlan {
   std::vector<int> rk, rslot;       // k ascending, slot of L(j,k)
   std::vector<int> uptr;            // per row-structure entry q: range of its tile updates
   std::vector<int> usrc, udst;      // update: C(udst) -= L(usrc) L(rslot[q])^T
-  // per column, its off-diagonal updates ordered by (target tile, k):
-  // {target position in the column, source slot L(i,k), slot of L(j,k)}
+  // per column, all its updates ordered by (k, target tile):
+  // {target position in the column (0 = diagonal), source slot L(i,k), slot of L(j,k), q}
   std::vector<int> bptr;            // nt+1
-  std::vector<int> bop;             // 3 per update
+  std::vector<int> bop;             // 4 per update
   long long nnz_tiles() const { return static_cast<long long>(rowidx.size()); }
 };
 

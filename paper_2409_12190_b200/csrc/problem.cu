@@ -867,35 +867,33 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
       sync();
       cudaFree(tchol_.trace);
       tchol_.trace = nullptr;
-      unsigned long long t0 = ~0ull, t1 = 0, tb0 = ~0ull;
-      double upd = 0, pot = 0, inv = 0, trs = 0, fwd = 0, bwd = 0;
+      unsigned long long t0 = ~0ull, t1 = 0, tb0 = ~0ull, tb1 = 0;
+      double upd = 0, pot = 0, trs = 0, bwd = 0;
       for (int j = 0; j < tchol_.nt; ++j) {
         const unsigned long long* r = &trace[8 * static_cast<std::size_t>(j)];
         t0 = std::min(t0, r[0]);
-        t1 = std::max(t1, r[5]);
+        t1 = std::max(t1, r[4]);
         tb0 = std::min(tb0, r[6]);
+        tb1 = std::max(tb1, r[7]);
         upd += r[1] - r[0];
         pot += r[2] - r[1];
-        inv += r[3] - r[2];
-        trs += r[4] - r[3];
-        fwd += r[5] - r[4];
+        trs += r[4] - r[2];
         bwd += r[7] - r[6];
       }
-      unsigned long long tb1 = 0;
-      for (int j = 0; j < tchol_.nt; ++j) tb1 = std::max(tb1, trace[8 * static_cast<std::size_t>(j) + 7]);
       const double nt = tchol_.nt;
       std::fprintf(stderr,
                    "[bae chol] groups %d nt %d tiles %lld updates %lld: factor span %.1f us, backward span %.1f us; per column "
-                   "mean: wait+update %.2f potrf %.2f trinv %.2f trsm %.2f fwd+publish %.2f backward %.2f us\n",
+                   "mean: wait+update %.2f potrf %.2f below-diagonal %.2f backward %.2f us\n",
                    chol_groups_, tchol_.nt, static_cast<long long>(d_.stile_count), chol_updates_, (t1 - t0) * 1e-3,
-                   (tb1 - tb0) * 1e-3, upd / nt * 1e-3, pot / nt * 1e-3, inv / nt * 1e-3, trs / nt * 1e-3,
-                   fwd / nt * 1e-3, bwd / nt * 1e-3);
-      if (std::getenv("BAE_CHOL_TRACE")[0] == '2')
+                   (tb1 - tb0) * 1e-3, upd / nt * 1e-3, pot / nt * 1e-3, trs / nt * 1e-3, bwd / nt * 1e-3);
+      if (std::getenv("BAE_CHOL_TRACE")[0] == '2')  // fast-path columns: absolute times from the first start
         for (int j = 0; j < tchol_.nt; ++j) {
           const unsigned long long* r = &trace[8 * static_cast<std::size_t>(j)];
-          std::fprintf(stderr, "  col %4d: start %8.1f upd %7.1f potrf %6.1f inv %6.1f trsm %6.1f pub %6.1f\n", j,
-                       (r[0] - t0) * 1e-3, (r[1] - r[0]) * 1e-3, (r[2] - r[1]) * 1e-3, (r[3] - r[2]) * 1e-3,
-                       (r[4] - r[3]) * 1e-3, (r[5] - r[4]) * 1e-3);
+          auto at = [&](int k) { return r[k] ? (r[k] - t0) * 1e-3 : -1.0; };
+          std::fprintf(stderr,
+                       "  col %4d: start %7.1f last-k seen %7.1f potrf %7.1f..%7.1f first pub %7.1f done %7.1f "
+                       "bwd %7.1f..%7.1f\n",
+                       j, at(0), at(3), at(1), at(2), at(5), at(4), at(6), at(7));
         }
     }
     ck(cudaMemcpyAsync(host_info_, tchol_.fail, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H fail");
