@@ -6,6 +6,10 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -72,19 +76,73 @@ inline int host_threads() {
   return static_cast<int>(std::clamp(std::thread::hardware_concurrency(), 1u, 16u));
 }
 
+// Persistent host worker pool behind parallel_chunks: spawning threads per
+// call cost more than the planning passes themselves at BAL sizes. Workers
+// are created once (leaked at exit, never joined); any number of caller
+// threads may submit concurrently; a call made from inside a worker runs
+// serially (no nested waits on the pool).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool(15);
+    return *p;
+  }
+  static bool in_worker() { return worker_flag(); }
+  void submit(std::function<void()> job) {
+    {
+      std::lock_guard<std::mutex> l(m_);
+      q_.push_back(std::move(job));
+    }
+    cv_.notify_one();
+  }
+
+ private:
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i)
+      std::thread([this] {
+        worker_flag() = true;
+        for (;;) {
+          std::function<void()> job;
+          {
+            std::unique_lock<std::mutex> l(m_);
+            cv_.wait(l, [this] { return !q_.empty(); });
+            job = std::move(q_.front());
+            q_.pop_front();
+          }
+          job();
+        }
+      }).detach();
+  }
+  static bool& worker_flag() {
+    static thread_local bool w = false;
+    return w;
+  }
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+};
+
 // f(chunk, begin, end) over `chunks` contiguous ranges of [0, n) (chunk 0 on
 // the calling thread). Chunk boundaries depend only on n and chunks, so a
 // caller that combines per-chunk results in chunk order is deterministic.
 template <class F>
 void parallel_chunks(std::int64_t n, int chunks, F&& f) {
-  if (chunks <= 1 || n < 2) {
-    f(0, std::int64_t{0}, n);
+  if (chunks <= 1 || n < 2 || HostPool::in_worker()) {
+    for (int c = 0; c < std::max(chunks, 1); ++c) f(c, n * c / std::max(chunks, 1), n * (c + 1) / std::max(chunks, 1));
     return;
   }
-  std::vector<std::thread> th;
-  for (int c = 1; c < chunks; ++c) th.emplace_back([&, c] { f(c, n * c / chunks, n * (c + 1) / chunks); });
+  std::mutex dm;
+  std::condition_variable dcv;
+  int left = chunks - 1;
+  for (int c = 1; c < chunks; ++c)
+    HostPool::get().submit([&, c] {
+      f(c, n * c / chunks, n * (c + 1) / chunks);
+      std::lock_guard<std::mutex> l(dm);  // the waiter cannot return before this unlocks
+      if (--left == 0) dcv.notify_all();
+    });
   f(0, std::int64_t{0}, n / chunks);
-  for (auto& t : th) t.join();
+  std::unique_lock<std::mutex> l(dm);
+  dcv.wait(l, [&] { return left == 0; });
 }
 
 // Validation follows make_ba_problem (problems.hpp:90-110): per observation,

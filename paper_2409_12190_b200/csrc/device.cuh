@@ -94,7 +94,7 @@ struct Dev {
   double* resid;   // 2 * N or null
   // direct solver (dense reduced camera system): per-slot W = J_c^T J_p and
   // W H~_pp^-1 (36 doubles, slot order), pair list grouped by camera block
-  double* wstore;
+  double* wstore;           // direct solver: V = W L^-T per slot (18 doubles)
   const int2* pairs;       // (slot k, slot l), c(k) >= c(l), grouped by block
   const int* blk_ptr;      // nblk + 1
   const int2* blk_cam;     // (c1, c2), c1 >= c2
@@ -104,6 +104,7 @@ struct Dev {
   // 48 x 48 tile holding it (8 cameras per tile), column-major tiles
   // per camera block {tile slot, row offset | col offset << 8 | transposed << 16},
   // then per camera {diagonal tile slot, offset}
+  const int* blk_ord;       // direct solver: blocks by descending pair count (k_schur_dense order)
   const int2* blk_tile;
   double* stiles;
   long long stile_count;

@@ -616,7 +616,8 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     h[0] = damp_diag(h[0], lambda, clo, chi);
     h[3] = damp_diag(h[3], lambda, clo, chi);
     h[5] = damp_diag(h[5], lambda, clo, chi);
-    if (!spd_inverse<3>(h, inv)) {
+    const bool pfail = !spd_inverse<3>(h, inv);
+    if (pfail) {
       fail = 1;
 #pragma unroll
       for (int j = 0; j < 9; ++j) inv[j] = 0.0;
@@ -624,9 +625,25 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     double* sp = ws.pt + lp * 12;
     const double hi[6] = {inv[0], inv[1], inv[2], inv[4], inv[5], inv[8]};
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      sp[3 + j] = hi[j];
-      d.hinv[ip * 6 + j] = hi[j];
+    for (int j = 0; j < 6; ++j) d.hinv[ip * 6 + j] = hi[j];
+    if (kDirect) {  // the Cholesky factor L of H~_pp instead (1/l00, l10, l20, 1/l11, l21, 1/l22)
+      double lf[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (!pfail) {
+        const double l00 = sqrt(h[0]), l10 = h[1] / l00, l20 = h[2] / l00;
+        const double l11 = sqrt(h[3] - l10 * l10), l21 = (h[4] - l20 * l10) / l11;
+        const double l22 = sqrt(h[5] - l20 * l20 - l21 * l21);
+        lf[0] = 1.0 / l00;
+        lf[1] = l10;
+        lf[2] = l20;
+        lf[3] = 1.0 / l11;
+        lf[4] = l21;
+        lf[5] = 1.0 / l22;
+      }
+#pragma unroll
+      for (int j = 0; j < 6; ++j) sp[3 + j] = lf[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) sp[3 + j] = hi[j];
     }
     const double g0 = d.gp[ip * 3], g1 = d.gp[ip * 3 + 1], g2 = d.gp[ip * 3 + 2];
     sp[9] = inv[0] * g0 + inv[1] * g1 + inv[2] * g2;
@@ -649,34 +666,38 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     for (int a = 0; a < 6; ++a)
 #pragma unroll
       for (int j = 0; j < 3; ++j) W[a * 3 + j] = Jc[a] * Jp[j] + Jc[6 + a] * Jp[3 + j];
-    const double* hi = sp + 3;  // packed xx xy xz yy yz zz
-    const double H[9] = {hi[0], hi[1], hi[2], hi[1], hi[3], hi[4], hi[2], hi[4], hi[5]};
-    double WH[18];
-#pragma unroll
-    for (int a = 0; a < 6; ++a)
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        WH[a * 3 + j] = W[a * 3] * H[j] + W[a * 3 + 1] * H[3 + j] + W[a * 3 + 2] * H[6 + j];
     double* st = ws.stage + s * SW;
     if (!kDirect) {
+      const double* hi = sp + 3;  // packed xx xy xz yy yz zz
+      const double H[9] = {hi[0], hi[1], hi[2], hi[1], hi[3], hi[4], hi[2], hi[4], hi[5]};
+      double WH[18];
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          WH[a * 3 + j] = W[a * 3] * H[j] + W[a * 3 + 1] * H[3 + j] + W[a * 3 + 2] * H[6 + j];
       int q = 0;
 #pragma unroll
       for (int a = 0; a < 6; ++a)
 #pragma unroll
         for (int b = a; b < 6; ++b)
           st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
+    } else {  // direct solver: keep V = W L^-T (V V^T = W H~^-1 W^T) of this slot
+      const double* lf = sp + 3;
+      double* vo = d.wstore + (long long)(g.ob + s) * 18;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        const double v0 = W[a * 3] * lf[0];
+        const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
+        const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
+        vo[a * 3] = v0;
+        vo[a * 3 + 1] = v1;
+        vo[a * 3 + 2] = v2;
+      }
     }
     const double* vp = sp + 9;
 #pragma unroll
     for (int a = 0; a < 6; ++a) st[SW - 6 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
-    if (kDirect) {  // direct solver: keep W and W H~^-1 of this slot
-      double* w = d.wstore + (long long)(g.ob + s) * 36;
-#pragma unroll
-      for (int j = 0; j < 18; ++j) {
-        w[j] = W[j];
-        w[18 + j] = WH[j];
-      }
-    }
   }
   __syncwarp();
   entries_from_stage<SW, SW>(ws, g.ncam, g.eb, d.partial);
@@ -808,17 +829,20 @@ __global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long lo
 // F2: dense reduced camera system for the direct solver (the reference's
 // default SolverChoice::cholesky, lm.hpp:132-136). One warp per camera block
 // (c1 >= c2):  S[c1,c2] = delta(c1,c2) H~_cc - sum_{points} sum_{k in c1, l in c2}
-// (W_k H~_pp^-1) W_l^T, pairs in (point, k, l) order, lanes strided over the
-// block's pairs, fixed xor tree; column-major lower triangle for potrf.
+// V_k V_l^T with V = W L^-T (H~_pp = L L^T, so V_k V_l^T = W_k H~_pp^-1 W_l^T
+// from half the bytes of W and W H~^-1), pairs in (point, k, l) order, lanes
+// strided over the block's pairs, fixed xor tree; column-major lower
+// triangle for potrf.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
   // Warp per camera block; lane = 4 * slot + part: 8 pairs in flight, each
   // pair's 6x6 product split in four 3x3 corners (rows 3 (part & 1), columns
   // 3 (part >> 1)), so a lane loads two contiguous 9-double row bands
-  // (W_k H~^-1 and W_l) and keeps 9 accumulators. The 8 slot sums are then
+  // (V_k and V_l) and keeps 9 accumulators. The 8 slot sums are then
   // combined by a fixed shuffle tree: the order depends only on the block.
-  const int blk = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (blk >= d.nblk) return;
+  const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= d.nblk) return;
+  const int blk = d.blk_ord[wid];  // diagonal blocks first, then row by row
   const int lane = lane_id(), slot = lane >> 2, part = lane & 3;
   const int r0 = 3 * (part & 1), c0 = 3 * (part >> 1);
   double acc[9];
@@ -828,8 +852,8 @@ __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
 #pragma unroll 2
   for (int q = d.blk_ptr[blk] + slot; q < qe; q += 8) {
     const int2 pr = d.pairs[q];
-    const double* wh = d.wstore + (long long)pr.x * 36 + 18 + 3 * r0;  // W_k H~^-1 rows r0..r0+2
-    const double* w = d.wstore + (long long)pr.y * 36 + 3 * c0;        // W_l rows c0..c0+2
+    const double* wh = d.wstore + (long long)pr.x * 18 + 3 * r0;  // V_k rows r0..r0+2
+    const double* w = d.wstore + (long long)pr.y * 18 + 3 * c0;   // V_l rows c0..c0+2
     double a[9], b[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) {

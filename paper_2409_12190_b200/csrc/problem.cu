@@ -297,6 +297,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.pairs = nullptr;
   d.blk_ptr = nullptr;
   d.blk_cam = nullptr;
+  d.blk_ord = nullptr;
   d.nblk = 0;
   d.schur = nullptr;
   ht.mark("allocs");
@@ -679,6 +680,17 @@ void Problem::build_direct() {
   d_.pairs = upload(sorted);
   d_.blk_ptr = upload(bptr);
   d_.blk_cam = upload(bcam);
+  {  // diagonal blocks first (the heaviest: every observation of the camera),
+     // then the rest row by row: a CTA's warps get blocks of similar length
+     // and neighbouring rows, which keeps the V_k they share in L2
+    std::vector<int> ord;
+    ord.reserve(bcam.size());
+    for (std::size_t b = 0; b < bcam.size(); ++b)
+      if (bcam[b].x == bcam[b].y) ord.push_back(static_cast<int>(b));
+    for (std::size_t b = 0; b < bcam.size(); ++b)
+      if (bcam[b].x != bcam[b].y) ord.push_back(static_cast<int>(b));
+    d_.blk_ord = upload(ord);
+  }
   d_.nblk = static_cast<int>(bcam.size());
   ht.mark("direct: pair list");
   if (use_tiles_) {
@@ -836,7 +848,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
 bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
   build_direct();
   const long long n = 6LL * d_.C;
-  if (!d_.wstore) d_.wstore = dalloc<double>(36 * static_cast<std::size_t>(plan_.N));
+  if (!d_.wstore) d_.wstore = dalloc<double>(18 * static_cast<std::size_t>(plan_.N));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
   launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
