@@ -179,7 +179,11 @@ def run_reference(args):
 
 # B200 FP64 datasheet figure: MEASURED_PEAKS.json has no FP64 number, so the
 # FP64 roofline of the Cholesky kernel is against this nominal peak.
-FP64_NOMINAL_TFLOPS = 40.0
+# FP64 peak measured on this pool's B200 by tools/lat/dmma.cu (profiles/r01b_fp64_peak.txt):
+# 63.8 FMA/clk/SM (mma.sync m8n8k4 f64; DFMA 58.5) x 148 SMs x 1.965 GHz x 2 = 37.1 TFLOP/s
+# (NVIDIA's nominal figure is 40). MEASURED_PEAKS.json carries no FP64 number.
+FP64_PEAK_TFLOPS = 37.1
+FP64_PEAK_SOURCE = "measured FP64 peak (tools/lat/dmma.cu, profiles/r01b_fp64_peak.txt; nominal 40)"
 
 
 def _alg_bytes(kernel, st):
@@ -291,8 +295,8 @@ def run_b200(args):
     kernels = [
         {"kernel": "k_tile_chol_factor + k_tile_chol_backward (direct solve, per LM iteration)", "us": 1e3 * ms_chol,
          "bound": "fp64 pipe / latency", "achieved": chol_f / (ms_chol * 1e-3) / 1e12, "unit": "TFLOP/s",
-         "peak": FP64_NOMINAL_TFLOPS, "peak_source": "nominal FP64",
-         "frac": chol_f / (ms_chol * 1e-3) / 1e12 / FP64_NOMINAL_TFLOPS},
+         "peak": FP64_PEAK_TFLOPS, "peak_source": FP64_PEAK_SOURCE,
+         "frac": chol_f / (ms_chol * 1e-3) / 1e12 / FP64_PEAK_TFLOPS},
         {"kernel": "k_linearize + k_cam_linearize + k_lin_totals (fused residual + Jacobian + J^T J / J^T r blocks)",
          "us": 1e3 * ms_lin, "bound": "hbm", "achieved": lin_b / (ms_lin * 1e-3) / 1e9, "unit": "GB/s",
          "peak": peak_hbm, "frac": lin_b / (ms_lin * 1e-3) / 1e9 / peak_hbm, "obs_per_s": N / (ms_lin * 1e-3)},
@@ -397,9 +401,9 @@ def run_b200(args):
                     "phase_ms_per_solve": pcg["phases"],
                     "config": "same workload, solver=pcg (implicit-Schur PCG, block-Jacobi), pcg_tol=1e-8"},
             "roofline": {"bound": "tensor", "kernel": "k_tile_chol_factor + k_tile_chol_backward",
-                         "achieved": chol_ach, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s",
-                         "frac": chol_ach / FP64_NOMINAL_TFLOPS, "traffic": traffic,
-                         "peak_source": "nominal B200 FP64 (FMA pipe, not tcgen05; no measured FP64 peak)",
+                         "achieved": chol_ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": chol_ach / FP64_PEAK_TFLOPS, "traffic": traffic,
+                         "peak_source": FP64_PEAK_SOURCE,
                          "share_of_step": chol_share,
                          "limiter": "latency: the dependent pivot chain along the nested-dissection tree",
                          "algorithmic_flops": "2*48^3 per tile update / solve + 2*48^3/3 per tile column"},
