@@ -1737,6 +1737,26 @@ static inline int elt_blocks(long long n, int bs) { return (int)((n + bs - 1) / 
 static inline int tile_blocks(int T, const TileLaunch& tl) { return (T + tl.wpb - 1) / tl.wpb; }
 static int schur_grid(const Dev& d, const SmemSizes& sm);
 
+// Points between the caller's order and the internal (camera-sorted) order:
+// internal point i is caller point src[i].
+__global__ void k_points_permute(const double* __restrict__ in, const int* __restrict__ src, double* __restrict__ out,
+                                 int P, int to_internal) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const long long u = 3LL * src[i], v = 3LL * i;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (to_internal)
+      out[v + a] = in[u + a];
+    else
+      out[u + a] = in[v + a];
+  }
+}
+int launch_points_permute(const double* in, const int* src, double* out, int P, bool to_internal, cudaStream_t s) {
+  k_points_permute<<<elt_blocks(P, 256), 256, 0, s>>>(in, src, out, P, to_internal ? 1 : 0);
+  return 1;
+}
+
 int launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
   k_camrec<<<elt_blocks(d.C, 128), 128, 0, s>>>(trial ? d.pose_t : d.pose, d.intr, trial ? d.camrec_t : d.camrec, d.C);
   return 1;

@@ -1,0 +1,22 @@
+// Device construction of the direct solver's pair list (pairs.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "device.cuh"
+
+namespace bae {
+
+// Per internal point the number of its (k, l) pairs with c(k) >= c(l),
+// exclusive-scanned into off[0..P]; returns the total (synchronises s).
+long long count_pairs(const Dev& d, long long* off, cudaStream_t s);
+
+// The pairs grouped by camera block (c1, c2) ascending, generation order
+// inside a block, into pairs[0..np); the blocks' cameras and pair offsets to
+// the host (synchronises s).
+void build_pairs(const Dev& d, const long long* off, long long np, int2* pairs, std::vector<int2>& bcam,
+                 std::vector<int>& bptr, cudaStream_t s);
+
+}  // namespace bae

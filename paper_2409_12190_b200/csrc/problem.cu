@@ -17,6 +17,7 @@
 #include <string>
 #include <limits>
 
+#include "pairs.cuh"
 #include "problem.hpp"
 
 namespace bae {
@@ -373,20 +374,35 @@ void Problem::sync() { ck(cudaStreamSynchronize(stream_), "kernel execution"); }
 void Problem::set_parameters(const double* poses7, const double* points3) {
   activate();
   const int C = d_.C, P = d_.P;
-  std::vector<double> pts(points3 ? 3 * static_cast<std::size_t>(P) : 0);
-  for (int i = 0; points3 && i < P; ++i) {
-    const int p = comm_ ? local_pts_[plan_.pt_of_internal[i]] : plan_.pt_of_internal[i];
-    pts[3 * i] = points3[3 * p];
-    pts[3 * i + 1] = points3[3 * p + 1];
-    pts[3 * i + 2] = points3[3 * p + 2];
-  }
   if (poses7)
     ck(cudaMemcpyAsync(d_.pose, poses7, 7 * sizeof(double) * C, cudaMemcpyHostToDevice, stream_), "H2D poses");
-  if (points3)
+  if (points3 && !comm_) {  // caller order up, permuted into the internal order on the device
+    ensure_point_staging();
+    ck(cudaMemcpyAsync(pts_user_, points3, 3 * sizeof(double) * P, cudaMemcpyHostToDevice, stream_), "H2D points");
+    launches_ += launch_points_permute(pts_user_, src_of_internal_, d_.pts, P, true, stream_);
+  } else if (points3) {
+    std::vector<double> pts(3 * static_cast<std::size_t>(P));
+    for (int i = 0; i < P; ++i) {
+      const int p = local_pts_[plan_.pt_of_internal[i]];
+      pts[3 * i] = points3[3 * p];
+      pts[3 * i + 1] = points3[3 * p + 1];
+      pts[3 * i + 2] = points3[3 * p + 2];
+    }
     ck(cudaMemcpyAsync(d_.pts, pts.data(), pts.size() * sizeof(double), cudaMemcpyHostToDevice, stream_),
        "H2D points");
+    sync();
+  }
   launches_ += launch_camrec(d_, false, stream_);
   sync();
+}
+
+// Device staging of the caller-ordered points (single rank): the order
+// permutation runs as a kernel instead of a host loop over P.
+void Problem::ensure_point_staging() {
+  if (pts_user_) return;
+  std::vector<int> src(plan_.pt_of_internal.begin(), plan_.pt_of_internal.end());
+  src_of_internal_ = upload(src);
+  pts_user_ = dalloc<double>(3 * static_cast<std::size_t>(d_.P));
 }
 
 void Problem::get_parameters(double* poses7, double* points3) {
@@ -419,15 +435,11 @@ void Problem::get_parameters(double* poses7, double* points3) {
       const std::size_t at = q * slot + 3 * next[q]++;
       for (int a = 0; a < 3; ++a) points3[3 * p + a] = all[at + a];
     }
-  } else if (points3) {
-    std::vector<double> pts(3 * static_cast<std::size_t>(P));
-    ck(cudaMemcpy(pts.data(), d_.pts, pts.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H points");
-    for (int i = 0; i < P; ++i) {
-      const int p = plan_.pt_of_internal[i];
-      points3[3 * p] = pts[3 * i];
-      points3[3 * p + 1] = pts[3 * i + 1];
-      points3[3 * p + 2] = pts[3 * i + 2];
-    }
+  } else if (points3) {  // permuted back to the caller's order on the device
+    ensure_point_staging();
+    launches_ += launch_points_permute(d_.pts, src_of_internal_, pts_user_, P, false, stream_);
+    ck(cudaMemcpyAsync(points3, pts_user_, 3 * sizeof(double) * P, cudaMemcpyDeviceToHost, stream_), "D2H points");
+    sync();
   }
 }
 
@@ -585,99 +597,26 @@ void Problem::build_direct() {
   if (!use_tiles_ && n > kDirectMaxOrder)
     throw Error(BAE_ERR_UNSUPPORTED, "solver=cholesky: reduced camera system too large for the dense direct solve; "
                                      "use solver=pcg");
-  const Plan& pl = plan_;
-  const int C = d_.C;
-  std::vector<int> cam_of_slot(static_cast<std::size_t>(pl.N));
-  for (int t = 0; t < pl.T; ++t)
-    for (int e = pl.tile_ent_begin[t]; e < pl.tile_ent_begin[t + 1]; ++e)
-      for (int sl = pl.ent_obs_begin[e]; sl < pl.ent_obs_begin[e + 1]; ++sl) cam_of_slot[sl] = pl.ent_cam[e];
-  // Pairs in generation order (tile, point, k, l), bucketed by c1 = camera(k)
-  // with a counting sort, then each c1 bucket stably by c2 = camera(l). Both
-  // passes run over contiguous chunks of tiles (chunk-ordered offsets keep the
-  // sequential order), the per-c1 sorts over chunks of c1.
-  auto for_pairs = [&](int t0, int t1, auto&& emit) {
-    int kc[256], ks[256];
-    for (int t = t0; t < t1; ++t) {
-      const int ob = pl.tile_obs_begin[t];
-      for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
-        const int m = pl.pt_ptr[i + 1] - pl.pt_ptr[i];
-        for (int q = 0; q < m && q < 256; ++q) {
-          const int sl = ob + pl.ptobs[pl.pt_ptr[i] + q];
-          ks[q] = sl;
-          kc[q] = cam_of_slot[sl];
-        }
-        if (m <= 256) {
-          for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b)
-              if (kc[a] >= kc[b]) emit(kc[a], kc[b], ks[a], ks[b]);
-        } else {  // very long track
-          for (int a = 0; a < m; ++a)
-            for (int b = 0; b < m; ++b) {
-              const int sa = ob + pl.ptobs[pl.pt_ptr[i] + a], sb = ob + pl.ptobs[pl.pt_ptr[i] + b];
-              if (cam_of_slot[sa] >= cam_of_slot[sb]) emit(cam_of_slot[sa], cam_of_slot[sb], sa, sb);
-            }
-        }
-      }
-    }
-  };
-  const int nch = pl.T >= 256 ? host_threads() : 1;
-  std::vector<std::vector<long long>> ccnt(static_cast<std::size_t>(nch),
-                                           std::vector<long long>(static_cast<std::size_t>(C), 0));
-  parallel_chunks(pl.T, nch, [&](int ch, std::int64_t t0, std::int64_t t1) {
-    auto& cc = ccnt[ch];
-    for_pairs(static_cast<int>(t0), static_cast<int>(t1), [&](int c1, int, int, int) { ++cc[c1]; });
-  });
-  std::vector<long long> row(static_cast<std::size_t>(C) + 1, 0);
-  for (int c = 0; c < C; ++c) {  // bucket c1: chunk 0's pairs, then chunk 1's, ... (= tile order)
-    long long at = row[c];
-    for (int ch = 0; ch < nch; ++ch) {
-      const long long m = ccnt[ch][c];
-      ccnt[ch][c] = at;
-      at += m;
-    }
-    row[c + 1] = at;
-  }
-  const std::size_t np = static_cast<std::size_t>(row[C]);
-  if (np >= (std::size_t{1} << 31)) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
-  std::vector<int2> bucket(np), sorted(np);
-  std::vector<int> bucket_c2(np);
-  parallel_chunks(pl.T, nch, [&](int ch, std::int64_t t0, std::int64_t t1) {
-    auto& cur = ccnt[ch];
-    for_pairs(static_cast<int>(t0), static_cast<int>(t1), [&](int c1, int c2, int k, int l) {
-      const long long at = cur[c1]++;
-      bucket[at] = int2{k, l};
-      bucket_c2[at] = c2;
-    });
-  });
-  std::vector<std::vector<int2>> blocks(static_cast<std::size_t>(C));  // per c1: (c2, pairs)
-  parallel_chunks(C, C >= 64 ? nch : 1, [&](int, std::int64_t cb, std::int64_t ce) {
-    std::vector<long long> cnt(static_cast<std::size_t>(C), 0);
-    std::vector<int> seen;
-    for (std::int64_t c1 = cb; c1 < ce; ++c1) {
-      const long long b = row[c1], e = row[c1 + 1];
-      seen.clear();
-      for (long long q = b; q < e; ++q)
-        if (cnt[bucket_c2[q]]++ == 0) seen.push_back(bucket_c2[q]);
-      std::sort(seen.begin(), seen.end());
-      long long at = b;
-      for (int c2 : seen) {
-        const long long m = cnt[c2];
-        cnt[c2] = at;  // becomes the write cursor
-        blocks[c1].push_back(int2{c2, static_cast<int>(m)});
-        at += m;
-      }
-      for (long long q = b; q < e; ++q) sorted[cnt[bucket_c2[q]]++] = bucket[q];
-      for (int c2 : seen) cnt[c2] = 0;
-    }
-  });
-  std::vector<int> bptr{0};
+  // the pair list on the device (pairs.cu): count, scan, generate, sort by block
   std::vector<int2> bcam;
-  for (int c1 = 0; c1 < C; ++c1)
-    for (const int2& bl : blocks[c1]) {
-      bcam.push_back(int2{c1, bl.x});
-      bptr.push_back(bptr.back() + bl.y);
+  std::vector<int> bptr;
+  {
+    long long* off = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&off), (static_cast<std::size_t>(d_.P) + 1) * sizeof(long long),
+                       stream_),
+       "cudaMallocAsync pair offsets");
+    try {
+      const long long np = count_pairs(d_, off, stream_);
+      if (np >= (1LL << 31) - 1) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
+      int2* pairs = dalloc<int2>(static_cast<std::size_t>(std::max(np, 1LL)));
+      build_pairs(d_, off, np, pairs, bcam, bptr, stream_);
+      d_.pairs = pairs;
+    } catch (...) {
+      cudaFreeAsync(off, stream_);
+      throw;
     }
-  d_.pairs = upload(sorted);
+    cudaFreeAsync(off, stream_);
+  }
   d_.blk_ptr = upload(bptr);
   d_.blk_cam = upload(bcam);
   {  // diagonal blocks first (the heaviest: every observation of the camera),

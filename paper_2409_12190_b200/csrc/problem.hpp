@@ -84,6 +84,7 @@ class Problem {
   template <class T>
   T* upload(const std::vector<T>& v);
   void sync();
+  void ensure_point_staging();
   void reset_lm_status();
   void read_lm();
   void linearize();
@@ -120,6 +121,8 @@ class Problem {
   std::int64_t N_global_ = 0;
   std::vector<std::int32_t> rank_of_point_;  // sharded: owner of every global point
   std::vector<std::int32_t> local_pts_;      // sharded: global ids of this rank's points, ascending
+  int* src_of_internal_ = nullptr;           // single rank: caller id of each internal point (device)
+  double* pts_user_ = nullptr;               // single rank: caller-ordered points (device staging)
   Plan plan_;
   Dev d_{};
   SmemSizes sm_;
