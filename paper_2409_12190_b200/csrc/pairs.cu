@@ -9,7 +9,11 @@
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+#include <cstdint>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "bae_internal.hpp"
 #include "pairs.cuh"
@@ -114,7 +118,27 @@ void sort_and_encode(const Dev& d, const long long* off, long long np, int2* pai
     cudaFreeAsync(q, s);
 }
 
+// The stream-ordered scratch comes from the device's default pool; keep what
+// it grows to (the default release threshold of 0 hands it back to the
+// driver at every synchronisation, and the next problem maps it again).
+void keep_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static std::mutex m;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> l(m);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    std::uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
 }  // namespace
+
+void pairs_pool_setup() { keep_pool(); }
 
 long long count_pairs(const Dev& d, long long* off, cudaStream_t s) {
   // off: P + 1 entries; counts per internal point, then an exclusive scan

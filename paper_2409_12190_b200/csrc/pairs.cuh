@@ -9,6 +9,10 @@
 
 namespace bae {
 
+// Keeps the device's default memory pool from returning its memory at every
+// synchronisation (the pair list's stream-ordered scratch).
+void pairs_pool_setup();
+
 // Per internal point the number of its (k, l) pairs with c(k) >= c(l),
 // exclusive-scanned into off[0..P]; returns the total (synchronises s).
 long long count_pairs(const Dev& d, long long* off, cudaStream_t s);

@@ -8,6 +8,8 @@
 // iteration the host reads back one small status record.
 #include <algorithm>
 #include <chrono>
+#include <mutex>
+#include <map>
 #include <climits>
 #include <cstddef>
 #include <cmath>
@@ -46,19 +48,82 @@ struct HostTimer {
 
 // Device memory of a problem lives in a few large chunks carved by a bump
 // allocator (256-byte aligned, so TMA sources stay 16-byte aligned): one
-// cudaMalloc / cudaFree per chunk instead of one per array.
+// cudaMalloc / cudaFree per chunk instead of one per array. Chunks of a
+// destroyed problem (and the small pinned host words) go to a process-wide
+// cache for the next problem on the same device, so a create -> optimise ->
+// destroy loop does not pay cudaMalloc / cudaMallocHost each time (bounded;
+// the rest is freed).
 constexpr std::size_t kArenaChunk = 32u << 20;
+constexpr std::size_t kChunkCacheLimit = 8ull << 30;
+constexpr std::size_t kPinnedWord = 4096;
+
+namespace {
+struct MemCache {
+  std::mutex m;
+  std::map<int, std::multimap<std::size_t, void*>> chunks;  // device -> (bytes, chunk)
+  std::size_t cached = 0;
+  std::vector<void*> pinned;  // kPinnedWord-byte pinned host blocks
+};
+MemCache& mem_cache() {
+  static MemCache* c = new MemCache;  // leaked: never torn down under a live CUDA context
+  return *c;
+}
+void* chunk_take(int device, std::size_t want, std::size_t& got) {
+  MemCache& c = mem_cache();
+  std::lock_guard<std::mutex> l(c.m);
+  auto& mm = c.chunks[device];
+  const auto it = mm.lower_bound(want);
+  if (it == mm.end() || it->first > 2 * want) return nullptr;
+  got = it->first;
+  void* p = it->second;
+  c.cached -= got;
+  mm.erase(it);
+  return p;
+}
+void chunk_give(int device, void* p, std::size_t bytes) {  // the device is current
+  MemCache& c = mem_cache();
+  std::lock_guard<std::mutex> l(c.m);
+  if (c.cached + bytes > kChunkCacheLimit) {
+    cudaFree(p);
+    return;
+  }
+  c.chunks[device].emplace(bytes, p);
+  c.cached += bytes;
+}
+void* pinned_take() {
+  MemCache& c = mem_cache();
+  {
+    std::lock_guard<std::mutex> l(c.m);
+    if (!c.pinned.empty()) {
+      void* p = c.pinned.back();
+      c.pinned.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  ck(cudaMallocHost(&p, kPinnedWord), "cudaMallocHost");
+  return p;
+}
+void pinned_give(void* p) {
+  if (!p) return;
+  MemCache& c = mem_cache();
+  std::lock_guard<std::mutex> l(c.m);
+  c.pinned.push_back(p);
+}
+}  // namespace
 
 template <class T>
 T* Problem::dalloc(std::size_t n) {
   const std::size_t bytes = (std::max<std::size_t>(n, 1) * sizeof(T) + 255) & ~std::size_t{255};
   if (arena_used_ + bytes > arena_size_) {
     const std::size_t sz = std::max(bytes, kArenaChunk);
-    void* p = nullptr;
-    ck(cudaMalloc(&p, sz), "cudaMalloc");
+    std::size_t got = sz;
+    void* p = chunk_take(opt_.device, sz, got);
+    if (!p) ck(cudaMalloc(&p, sz), "cudaMalloc");
     allocs_.push_back(p);
+    alloc_bytes_.push_back(got);
     arena_base_ = static_cast<char*>(p);
-    arena_size_ = sz;
+    arena_size_ = got;
     arena_used_ = 0;
   }
   T* r = reinterpret_cast<T*>(arena_base_ + arena_used_);
@@ -302,8 +367,9 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.nblk = 0;
   d.schur = nullptr;
   ht.mark("allocs");
-  ck(cudaMallocHost(&pcg_host_, sizeof(PcgDev)), "cudaMallocHost");
-  ck(cudaMallocHost(&lm_host_, sizeof(LmDev)), "cudaMallocHost");
+  static_assert(sizeof(PcgDev) <= kPinnedWord && sizeof(LmDev) <= kPinnedWord, "pinned word");
+  pcg_host_ = static_cast<PcgDev*>(pinned_take());
+  lm_host_ = static_cast<LmDev*>(pinned_take());
   ck(cudaMemset(d.pcg, 0, sizeof(PcgDev)), "memset");
 
   ht.mark("device alloc+upload");
@@ -319,11 +385,12 @@ Problem::~Problem() {
   cudaSetDevice(opt_.device);
   for (auto& e : ev_pool_) cudaEventDestroy(e);
   if (solver_) cusolverDnDestroy(solver_);
-  if (host_info_) cudaFreeHost(host_info_);
+  if (stream_) cudaStreamSynchronize(stream_);  // the chunks are reused by the next problem
+  pinned_give(host_info_);
   if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
-  for (void* p : allocs_) cudaFree(p);
-  if (pcg_host_) cudaFreeHost(pcg_host_);
-  if (lm_host_) cudaFreeHost(lm_host_);
+  for (std::size_t i = 0; i < allocs_.size(); ++i) chunk_give(opt_.device, allocs_[i], alloc_bytes_[i]);
+  pinned_give(pcg_host_);
+  pinned_give(lm_host_);
   if (stream_) cudaStreamDestroy(stream_);
   comm_.reset();
 }
@@ -602,6 +669,7 @@ void Problem::build_direct() {
   std::vector<int> bptr;
   {
     long long* off = nullptr;
+    pairs_pool_setup();
     ck(cudaMallocAsync(reinterpret_cast<void**>(&off), (static_cast<std::size_t>(d_.P) + 1) * sizeof(long long),
                        stream_),
        "cudaMallocAsync pair offsets");
@@ -648,7 +716,7 @@ void Problem::build_direct() {
     throw Error(BAE_ERR_CUDA, "potrf workspace query failed");
   potrf_work_ = dalloc<double>(static_cast<std::size_t>(std::max(potrf_lwork_, 1)));
   dev_info_ = dalloc<int>(1);
-  ck(cudaMallocHost(&host_info_, sizeof(int)), "cudaMallocHost");
+  host_info_ = static_cast<int*>(pinned_take());
   direct_ready_ = true;
   ht.mark("direct: alloc+cusolver");
 }
@@ -777,7 +845,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   chol_epoch_ = 0;
   chol_grid_ = tile_chol_grid(nt);
   chol_updates_ = static_cast<long long>(pl.usrc.size());
-  if (!host_info_) ck(cudaMallocHost(&host_info_, sizeof(int)), "cudaMallocHost");
+  if (!host_info_) host_info_ = static_cast<int*>(pinned_take());
 }
 
 // Direct solve of the damped reduced camera system (the reference's default

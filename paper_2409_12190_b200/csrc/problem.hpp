@@ -129,6 +129,7 @@ class Problem {
   cudaStream_t stream_ = nullptr;
   cudaGraphExec_t pcg_graph_ = nullptr;
   std::vector<void*> allocs_;  // arena chunks
+  std::vector<std::size_t> alloc_bytes_;
   char* arena_base_ = nullptr;
   std::size_t arena_size_ = 0, arena_used_ = 0;
   std::vector<double> intr_host_;
