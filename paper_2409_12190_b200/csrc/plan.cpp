@@ -55,24 +55,59 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
   pl.tile_obs_target = tile_obs_target;
   pl.tile_cam_cap = tile_cam_cap;
 
-  // Observations of each original point, ascending id (point transpose plan).
+  // Observations of each original point, ascending id (point transpose plan):
+  // per-chunk histograms over contiguous observation ranges, chunk-ordered
+  // offsets, a parallel scatter -- the order inside a point is ascending k
+  // whatever the chunking.
+  const int nth = N >= (1 << 16) ? host_threads() : 1;
+  const int nch = std::min(nth, 8);
+  std::vector<std::vector<std::int32_t>> ccnt(static_cast<std::size_t>(nch));
+  std::vector<std::vector<std::int32_t>> ccam(static_cast<std::size_t>(nch));
+  parallel_chunks(N, nch, [&](int c, std::int64_t b, std::int64_t e) {
+    ccnt[c].assign(static_cast<std::size_t>(P), 0);
+    ccam[c].assign(static_cast<std::size_t>(C), 0);
+    auto& h = ccnt[c];
+    auto& hc = ccam[c];
+    for (std::int64_t k = b; k < e; ++k) {
+      ++h[pt_idx[k]];
+      ++hc[cam_idx[k]];
+    }
+  });
+  for (int c = 0; c < C; ++c) {
+    std::int32_t n = 0;
+    for (int ch = 0; ch < nch; ++ch) n += ccam[ch][c];
+    if (n == 0) pl.has_empty_camera = true;
+  }
   std::vector<std::int32_t> pcnt(static_cast<std::size_t>(P) + 1, 0);
-  for (std::int64_t k = 0; k < N; ++k) ++pcnt[pt_idx[k] + 1];
-  std::vector<std::int32_t> camcnt(static_cast<std::size_t>(C), 0);
-  for (std::int64_t k = 0; k < N; ++k) ++camcnt[cam_idx[k]];
-  for (int c = 0; c < C; ++c)
-    if (camcnt[c] == 0) pl.has_empty_camera = true;
+  parallel_chunks(P, nth, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t p = b; p < e; ++p) {
+      std::int32_t n = 0;
+      for (int ch = 0; ch < nch; ++ch) n += ccnt[ch][p];
+      pcnt[p + 1] = n;
+    }
+  });
   for (int p = 0; p < P; ++p) {
     if (pcnt[p + 1] == 0) pl.has_empty_point = true;
     if (pcnt[p + 1] > 65535) throw Error(BAE_ERR_UNSUPPORTED, "a point has more than 65535 observations");
   }
   std::partial_sum(pcnt.begin(), pcnt.end(), pcnt.begin());
+  parallel_chunks(P, nth, [&](int, std::int64_t b, std::int64_t e) {  // chunk write cursors
+    for (std::int64_t p = b; p < e; ++p) {
+      std::int32_t run = pcnt[p];
+      for (int ch = 0; ch < nch; ++ch) {
+        const std::int32_t m = ccnt[ch][p];
+        ccnt[ch][p] = run;
+        run += m;
+      }
+    }
+  });
   std::vector<std::int32_t> pobs(static_cast<std::size_t>(N));
-  {
-    std::vector<std::int32_t> cur(pcnt.begin(), pcnt.end() - 1);
-    for (std::int64_t k = 0; k < N; ++k) pobs[cur[pt_idx[k]]++] = static_cast<std::int32_t>(k);
-  }
-  const int nth = N >= (1 << 16) ? host_threads() : 1;
+  parallel_chunks(N, nch, [&](int c, std::int64_t b, std::int64_t e) {
+    auto& cur = ccnt[c];
+    for (std::int64_t k = b; k < e; ++k) pobs[cur[pt_idx[k]]++] = static_cast<std::int32_t>(k);
+  });
+  ccnt.clear();
+  ccnt.shrink_to_fit();
   // camera of each observation in point order (one gather instead of one per pass)
   std::vector<std::int32_t> pcam(static_cast<std::size_t>(N));
   parallel_chunks(N, nth, [&](int, std::int64_t b, std::int64_t e) {
@@ -83,69 +118,112 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
   // Internal point order: stable counting sort by the lowest observing camera,
   // so consecutive points share cameras and a tile touches few of them.
   std::vector<std::int32_t> mincam(static_cast<std::size_t>(P), C);
-  for (std::int64_t k = 0; k < N; ++k) mincam[pt_idx[k]] = std::min(mincam[pt_idx[k]], cam_idx[k]);
+  parallel_chunks(P, nth, [&](int, std::int64_t b, std::int64_t e) {
+    for (std::int64_t p = b; p < e; ++p) {
+      std::int32_t m = C;
+      for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) m = std::min(m, pcam[j]);
+      mincam[p] = m;
+    }
+  });
   {
-    std::vector<std::int32_t> bucket(static_cast<std::size_t>(C) + 2, 0);
-    for (int p = 0; p < P; ++p) ++bucket[mincam[p] + 1];
-    std::partial_sum(bucket.begin(), bucket.end(), bucket.begin());
+    const int pch = P >= (1 << 16) ? nch : 1;
+    std::vector<std::vector<std::int32_t>> bucket(static_cast<std::size_t>(pch));
+    parallel_chunks(P, pch, [&](int c, std::int64_t b, std::int64_t e) {
+      bucket[c].assign(static_cast<std::size_t>(C) + 1, 0);
+      for (std::int64_t p = b; p < e; ++p) ++bucket[c][mincam[p]];
+    });
+    std::int32_t run = 0;  // bucket-major, chunk-minor offsets: stable in p
+    for (int m = 0; m <= C; ++m)
+      for (int c = 0; c < pch; ++c) {
+        const std::int32_t n = bucket[c][m];
+        bucket[c][m] = run;
+        run += n;
+      }
     pl.pt_of_internal.resize(static_cast<std::size_t>(P));
     pl.internal_of_pt.resize(static_cast<std::size_t>(P));
-    for (int p = 0; p < P; ++p) {
-      const std::int32_t i = bucket[mincam[p]]++;
-      pl.pt_of_internal[i] = p;
-      pl.internal_of_pt[p] = i;
-    }
+    parallel_chunks(P, pch, [&](int c, std::int64_t b, std::int64_t e) {
+      auto& cur = bucket[c];
+      for (std::int64_t p = b; p < e; ++p) {
+        const std::int32_t i = cur[mincam[p]]++;
+        pl.pt_of_internal[i] = static_cast<std::int32_t>(p);
+        pl.internal_of_pt[p] = i;
+      }
+    });
   }
 
   st.mark("internal order");
-  // Greedy tile packing over internal points.
-  std::vector<std::int32_t> stamp(static_cast<std::size_t>(C), -1), seen(static_cast<std::size_t>(C), -1);
-  std::vector<std::vector<std::int32_t>> tile_cams;
-  pl.tile_pt_begin.push_back(0);
-  pl.tile_obs_begin.push_back(0);
-  int t = 0, t_obs = 0, t_pts = 0;
-  std::vector<std::int32_t> cur_cams;
-  auto distinct_new = [&](int p, int tile) {
-    int n = 0;
-    for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
-      const int c = pcam[j];
-      if (stamp[c] != tile && seen[c] != p) {
-        seen[c] = p;
-        ++n;
-      }
-    }
-    for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) seen[pcam[j]] = -1;
-    return n;
+  // Greedy tile packing over internal points, in a fixed number of segments
+  // (a function of P only, so the tiling does not depend on the thread
+  // count); each segment starts a fresh tile and is packed independently.
+  const int nseg = std::clamp(P / 8192, 1, 64);
+  struct Seg {
+    std::vector<std::int32_t> pt_begin, obs_count;  // per tile
+    std::vector<std::vector<std::int32_t>> cams;
   };
-  for (int i = 0; i < P; ++i) {
-    const int p = pl.pt_of_internal[i];
-    const int m = pcnt[p + 1] - pcnt[p];
-    int newc = distinct_new(p, t);
-    if (t_pts > 0 && (t_obs + m > tile_obs_target || static_cast<int>(cur_cams.size()) + newc > tile_cam_cap ||
-                      t_pts + 1 > tile_pts_cap)) {
-      tile_cams.push_back(cur_cams);
-      cur_cams.clear();
-      pl.tile_pt_begin.push_back(i);
-      pl.tile_obs_begin.push_back(pl.tile_obs_begin.back() + t_obs);
+  std::vector<Seg> segs(static_cast<std::size_t>(nseg));
+  parallel_chunks(nseg, std::min(nth, nseg), [&](int, std::int64_t s0, std::int64_t s1) {
+    std::vector<std::int32_t> stamp(static_cast<std::size_t>(C), -1), seen(static_cast<std::size_t>(C), -1);
+    int t = 0;  // running stamp over this thread's segments
+    for (std::int64_t sg = s0; sg < s1; ++sg) {
+      Seg& S = segs[sg];
+      const int i0 = static_cast<int>(static_cast<std::int64_t>(P) * sg / nseg);
+      const int i1 = static_cast<int>(static_cast<std::int64_t>(P) * (sg + 1) / nseg);
+      if (i1 <= i0) continue;
       ++t;
-      t_obs = 0;
-      t_pts = 0;
-      newc = distinct_new(p, t);
-    }
-    for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
-      const int c = pcam[j];
-      if (stamp[c] != t) {
-        stamp[c] = t;
-        cur_cams.push_back(c);
+      int t_obs = 0, t_pts = 0;
+      std::vector<std::int32_t> cur_cams;
+      S.pt_begin.push_back(i0);
+      auto distinct_new = [&](int p) {
+        int n = 0;
+        for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
+          const int c = pcam[j];
+          if (stamp[c] != t && seen[c] != p) {
+            seen[c] = p;
+            ++n;
+          }
+        }
+        for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) seen[pcam[j]] = -1;
+        return n;
+      };
+      for (int i = i0; i < i1; ++i) {
+        const int p = pl.pt_of_internal[i];
+        const int m = pcnt[p + 1] - pcnt[p];
+        const int newc = distinct_new(p);
+        if (t_pts > 0 && (t_obs + m > tile_obs_target || static_cast<int>(cur_cams.size()) + newc > tile_cam_cap ||
+                          t_pts + 1 > tile_pts_cap)) {
+          S.cams.push_back(std::move(cur_cams));
+          cur_cams.clear();
+          S.obs_count.push_back(t_obs);
+          S.pt_begin.push_back(i);
+          ++t;
+          t_obs = 0;
+          t_pts = 0;
+        }
+        for (std::int32_t j = pcnt[p]; j < pcnt[p + 1]; ++j) {
+          const int c = pcam[j];
+          if (stamp[c] != t) {
+            stamp[c] = t;
+            cur_cams.push_back(c);
+          }
+        }
+        t_obs += m;
+        ++t_pts;
       }
+      S.cams.push_back(std::move(cur_cams));
+      S.obs_count.push_back(t_obs);
     }
-    t_obs += m;
-    ++t_pts;
-  }
-  tile_cams.push_back(cur_cams);
+  });
+  std::vector<std::vector<std::int32_t>> tile_cams;
+  pl.tile_pt_begin.clear();
+  pl.tile_obs_begin.assign(1, 0);
+  for (Seg& S : segs)
+    for (std::size_t k = 0; k < S.pt_begin.size(); ++k) {
+      pl.tile_pt_begin.push_back(S.pt_begin[k]);
+      pl.tile_obs_begin.push_back(pl.tile_obs_begin.back() + S.obs_count[k]);
+      tile_cams.push_back(std::move(S.cams[k]));
+    }
   pl.tile_pt_begin.push_back(P);
-  pl.tile_obs_begin.push_back(pl.tile_obs_begin.back() + t_obs);
-  pl.T = t + 1;
+  pl.T = static_cast<int>(tile_cams.size());
 
   st.mark("tile packing");
   // Per-tile slot order: (local camera, internal point, observation id).

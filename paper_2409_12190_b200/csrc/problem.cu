@@ -242,6 +242,9 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   std::vector<int4> desc(static_cast<std::size_t>(pl.T), int4{0, 0, 0, 0});
   std::vector<char> blob;
   std::vector<int> small_tiles, big_tiles;
+  // sizes and offsets first (serial, per-tile arithmetic), then the index
+  // blobs filled in parallel chunks of tiles
+  std::size_t blob_bytes = 0;
   for (int t = 0; t < pl.T; ++t) {
     const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
     const int nobs = pl.tile_obs_begin[t + 1] - ob;
@@ -260,27 +263,37 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     for (int k = 0; k < kWsKinds; ++k)
       kinds[k]->slice = std::max<int>(kinds[k]->slice, static_cast<int>(tile_ws_bytes(k, ncam, npts, nobs)));
     // index blob: hdr | camid | ent | pptr | lcpt | ptl, padded to 16 bytes
-    const std::size_t off = blob.size();
     const int bytes = (32 + 4 * ncam + 4 * (ncam + 1) + 4 * (npts + 1) + 6 * nobs + 15) / 16 * 16;
-    blob.resize(off + static_cast<std::size_t>(bytes), 0);
-    int* w = reinterpret_cast<int*>(blob.data() + off);
-    w[0] = ob;
-    w[1] = nobs;
-    w[2] = pb;
-    w[3] = npts;
-    w[4] = eb;
-    w[5] = ncam;
-    int* q = w + 8;
-    for (int l = 0; l < ncam; ++l) *q++ = pl.ent_cam[eb + l];
-    for (int l = 0; l <= ncam; ++l) *q++ = pl.ent_obs_begin[eb + l] - ob;
-    for (int i = 0; i <= npts; ++i) *q++ = pl.pt_ptr[pb + i] - ob;
-    std::uint32_t* lc = reinterpret_cast<std::uint32_t*>(q);
-    for (int i = 0; i < nobs; ++i) lc[i] = pl.obs_lcpt[ob + i];
-    std::uint16_t* ptl = reinterpret_cast<std::uint16_t*>(lc + nobs);
-    for (int i = 0; i < nobs; ++i) ptl[i] = pl.ptobs[ob + i];
-    desc[t] = int4{static_cast<int>(off / 16), bytes, pb, npts};
+    desc[t] = int4{static_cast<int>(blob_bytes / 16), bytes, pb, npts};
+    blob_bytes += static_cast<std::size_t>(bytes);
     small_tiles.push_back(t);
   }
+  blob.assign(blob_bytes, 0);
+  parallel_chunks(static_cast<std::int64_t>(small_tiles.size()), small_tiles.size() >= 1024 ? host_threads() : 1,
+                  [&](int, std::int64_t i0, std::int64_t i1) {
+    for (std::int64_t ii = i0; ii < i1; ++ii) {
+      const int t = small_tiles[ii];
+      const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
+      const int nobs = pl.tile_obs_begin[t + 1] - ob;
+      const int npts = pl.tile_pt_begin[t + 1] - pb;
+      const int ncam = pl.tile_ent_begin[t + 1] - eb;
+      int* w = reinterpret_cast<int*>(blob.data() + 16 * static_cast<std::size_t>(desc[t].x));
+      w[0] = ob;
+      w[1] = nobs;
+      w[2] = pb;
+      w[3] = npts;
+      w[4] = eb;
+      w[5] = ncam;
+      int* q = w + 8;
+      for (int l = 0; l < ncam; ++l) *q++ = pl.ent_cam[eb + l];
+      for (int l = 0; l <= ncam; ++l) *q++ = pl.ent_obs_begin[eb + l] - ob;
+      for (int i = 0; i <= npts; ++i) *q++ = pl.pt_ptr[pb + i] - ob;
+      std::uint32_t* lc = reinterpret_cast<std::uint32_t*>(q);
+      for (int i = 0; i < nobs; ++i) lc[i] = pl.obs_lcpt[ob + i];
+      std::uint16_t* ptl = reinterpret_cast<std::uint16_t*>(lc + nobs);
+      for (int i = 0; i < nobs; ++i) ptl[i] = pl.ptobs[ob + i];
+    }
+  });
   for (int k = 0; k < kWsKinds; ++k) {
     TileLaunch& tl = *kinds[k];
     tl.slice = std::max(16, (tl.slice + 15) / 16 * 16);
