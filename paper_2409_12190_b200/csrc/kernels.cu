@@ -1757,6 +1757,18 @@ int launch_points_permute(const double* in, const int* src, double* out, int P, 
   return 1;
 }
 
+// Observation pixels from the caller's order into slot order.
+__global__ void k_gather_pixels(const double2* __restrict__ raw, const int* __restrict__ orig, double2* __restrict__ px,
+                                long long N) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < N) px[i] = raw[orig[i]];
+}
+int launch_gather_pixels(const double* raw, const int* orig, double* px, long long N, cudaStream_t s) {
+  k_gather_pixels<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(reinterpret_cast<const double2*>(raw), orig,
+                                                                      reinterpret_cast<double2*>(px), N);
+  return 1;
+}
+
 int launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
   k_camrec<<<elt_blocks(d.C, 128), 128, 0, s>>>(trial ? d.pose_t : d.pose, d.intr, trial ? d.camrec_t : d.camrec, d.C);
   return 1;

@@ -26,6 +26,7 @@ void set_smem_limits(int max_bytes);
 // gpu_launches). `comm` is null on a single rank; on sharded runs the
 // wrapper inserts the cross-rank sums between the tile and camera passes.
 int launch_camrec(const Dev& d, bool trial, cudaStream_t s);
+int launch_gather_pixels(const double* raw, const int* orig, double* px, long long N, cudaStream_t s);
 int launch_points_permute(const double* in, const int* src, double* out, int P, bool to_internal, cudaStream_t s);
 int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm);
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);

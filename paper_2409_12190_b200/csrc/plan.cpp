@@ -231,7 +231,7 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
   // camera lists and fill the slots in parallel chunks of tiles.
   pl.obs_lcpt.resize(static_cast<std::size_t>(N));
   pl.obs_orig.resize(static_cast<std::size_t>(N));
-  pl.obs_px.resize(static_cast<std::size_t>(N) * 2);
+  if (px2) pl.obs_px.resize(static_cast<std::size_t>(N) * 2);  // null: the caller gathers them on the device
   pl.pt_ptr.assign(static_cast<std::size_t>(P) + 1, 0);
   pl.ptobs.resize(static_cast<std::size_t>(N));
   pl.tile_ws.assign(static_cast<std::size_t>(pl.T), -1);
@@ -276,8 +276,10 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
           const std::int32_t slot = ob + local;
           pl.obs_lcpt[slot] = static_cast<std::uint32_t>(l) | (static_cast<std::uint32_t>(i - pb) << 16);
           pl.obs_orig[slot] = k;
-          pl.obs_px[2 * static_cast<std::size_t>(slot)] = px2[2 * k];
-          pl.obs_px[2 * static_cast<std::size_t>(slot) + 1] = px2[2 * k + 1];
+          if (px2) {
+            pl.obs_px[2 * static_cast<std::size_t>(slot)] = px2[2 * k];
+            pl.obs_px[2 * static_cast<std::size_t>(slot) + 1] = px2[2 * k + 1];
+          }
           pl.ptobs[pcur++] = static_cast<std::uint16_t>(local);
         }
       }

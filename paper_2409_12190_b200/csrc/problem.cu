@@ -209,7 +209,9 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (const char* t = std::getenv("BAE_TILE_CAMS")) tile_cams = std::max(1, std::atoi(t));
   if (const char* m = std::getenv("BAE_PCG_MODE")) use_graph_pcg_ = std::string(m) != "persistent";
   if (comm_) use_graph_pcg_ = true;  // the persistent kernel has no place for the cross-rank sum
-  plan_ = build_plan(C, use_P, use_cam, use_pt, use_px, use_N, std::min(tile_obs, kPipeObs),
+  // single rank: the pixels go up in the caller's order and are gathered into
+  // slot order on the device (a random gather over N on the host otherwise)
+  plan_ = build_plan(C, use_P, use_cam, use_pt, dist ? use_px : nullptr, use_N, std::min(tile_obs, kPipeObs),
                      std::min(tile_cams, kPipeCams), kPipePts, 1 << 30);
   ht.mark("build_plan");
   if (dist) {
@@ -322,7 +324,17 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.tile_ws = upload(pl.tile_ws);
   d.obs_lcpt = upload(pl.obs_lcpt);
   d.obs_orig = upload(pl.obs_orig);
-  d.obs_px = upload(pl.obs_px);
+  if (dist) {
+    d.obs_px = upload(pl.obs_px);
+  } else {
+    double* px = dalloc<double>(2 * static_cast<std::size_t>(use_N));
+    double* raw = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&raw), 2 * sizeof(double) * use_N, stream_), "cudaMallocAsync");
+    ck(cudaMemcpyAsync(raw, px2, 2 * sizeof(double) * use_N, cudaMemcpyHostToDevice, stream_), "H2D pixels");
+    launches_ += launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_);
+    ck(cudaFreeAsync(raw, stream_), "cudaFreeAsync");
+    d.obs_px = px;
+  }
   d.ent_cam = upload(pl.ent_cam);
   d.ent_obs_begin = upload(pl.ent_obs_begin);
   d.cam_ent_ptr = upload(pl.cam_ent_ptr);
