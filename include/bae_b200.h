@@ -236,7 +236,8 @@ int bae_synth_bal_shaped(int32_t num_cameras, int32_t num_points, int64_t num_ob
 
 /* ---- BAL files, the reference's synthetic scene, the CLI - */
 typedef struct bae_bal bae_bal;
-/* parse_bal (io/bal.hpp:103-142) of a file / a text buffer. ParseError ->
+/* parse_bal (io/bal.hpp:103-142) of a file / a text buffer (a file may also
+ * be the binary cache of bae_bal_write_binary). ParseError ->
  * BAE_ERR_PARSE with bae_last_error_index() = line (the reference's messages
  * and line numbers); an unopenable file -> BAE_ERR_IO. */
 int bae_bal_read(const char* path, bae_bal** out);
@@ -256,6 +257,10 @@ int bae_bal_arrays(const bae_bal* b, double* poses7, double* intrinsics3, double
                    int32_t* pt_idx, double* pixels2, double* cameras9);
 /* serialize_bal (io/bal.hpp:145-157): %.17g, round-trips doubles exactly. */
 int bae_bal_write(const bae_bal* b, const char* path);
+/* Binary problem cache (no reference counterpart): the
+ * parsed arrays with a magic header. bae_bal_read (and so the CLI's --input)
+ * recognises the format and loads it without the text scanner. */
+int bae_bal_write_binary(const bae_bal* b, const char* path);
 void bae_bal_free(bae_bal* b);
 /* parse_g2o (io/g2o.hpp:30-80): VERTEX_SE3:QUAT / EDGE_SE3:QUAT, edge
  * endpoints remapped to vertex positions, identity information elided

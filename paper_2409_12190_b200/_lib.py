@@ -134,6 +134,7 @@ SIGNATURES = {
     "bae_bal_arrays": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, c_double_p, c_int32_p, c_int32_p,
                                       c_double_p, c_double_p]),
     "bae_bal_write": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
+    "bae_bal_write_binary": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
     "bae_bal_free": (None, [ctypes.c_void_p]),
     "bae_g2o_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     "bae_g2o_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),

@@ -615,8 +615,9 @@ def synth_ba(num_cameras: int, num_points: int, pixel_noise: float, pose_noise: 
     return _bal_from_handle(h)
 
 
-def write_bal(path: str, problem: BalProblem):
-    """serialize_bal (io/bal.hpp:145-157), %.17g."""
+def write_bal(path: str, problem: BalProblem, binary: bool = False):
+    """serialize_bal (io/bal.hpp:145-157), %.17g; ``binary=True`` writes the
+    binary problem cache instead (read back by read_bal and the CLI)."""
     lib = _lib.load()
     cams, pts = _f64(problem.cameras).reshape(-1, 9), _f64(problem.points).reshape(-1, 3)
     ci, pi, px = _i32(problem.cam_idx), _i32(problem.pt_idx), _f64(problem.pixels).reshape(-1, 2)
@@ -624,7 +625,7 @@ def write_bal(path: str, problem: BalProblem):
     _check(lib.bae_bal_from_arrays(cams.shape[0], pts.shape[0], ci.size, ptr(cams), ptr(pts), ptr(ci, ctypes.c_int32),
                                    ptr(pi, ctypes.c_int32), ptr(px), ctypes.byref(h)))
     try:
-        _check(lib.bae_bal_write(h, str(path).encode()))
+        _check((lib.bae_bal_write_binary if binary else lib.bae_bal_write)(h, str(path).encode()))
     finally:
         lib.bae_bal_free(h)
 

@@ -474,6 +474,10 @@ int bae_bal_write(const bae_bal* b, const char* path) {
   return guarded([&] { bae::write_bal_file(b->d, path); });
 }
 
+int bae_bal_write_binary(const bae_bal* b, const char* path) {
+  return guarded([&] { bae::write_bal_binary(b->d, path); });
+}
+
 void bae_bal_free(bae_bal* b) { delete b; }
 
 int bae_g2o_read(const char* path, bae_g2o** out) {

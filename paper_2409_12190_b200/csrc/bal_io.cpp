@@ -125,6 +125,72 @@ BalData parse_bal_text(const char* b, const char* e) {
   return d;
 }
 
+// Binary problem cache: the parsed arrays as they
+// are in memory, so a large synthetic or converted problem loads at disk
+// speed instead of through the text scanner. Layout (little endian):
+// "BAEBAL\0\1" | int32 C | int32 P | int64 N | cameras 9C f64 | points 3P f64 |
+// cam_idx N i32 | pt_idx N i32 | pixels 2N f64. parse_bal_file recognises it
+// by the magic; indices are validated like the text parser's.
+namespace {
+constexpr char kBinMagic[8] = {'B', 'A', 'E', 'B', 'A', 'L', '\0', '\1'};
+
+BalData decode_bal_binary(const char* b, std::size_t len) {
+  auto need = [&](std::size_t at, std::size_t n) {
+    if (at + n > len) throw Error(BAE_ERR_PARSE, "binary BAL: truncated file", 0);
+  };
+  std::size_t at = 8;
+  std::int32_t C = 0, P = 0;
+  std::int64_t N = 0;
+  need(at, 16);
+  std::memcpy(&C, b + at, 4);
+  std::memcpy(&P, b + at + 4, 4);
+  std::memcpy(&N, b + at + 8, 8);
+  at += 16;
+  if (C < 1 || P < 1 || N < 1) throw Error(BAE_ERR_PARSE, "binary BAL: non-positive counts in header", 0);
+  if (N >= (std::int64_t{1} << 31) - 1) throw Error(BAE_ERR_UNSUPPORTED, "binary BAL: counts exceed the 32-bit range", 0);
+  const std::size_t total = 8 + 16 + 8 * (9 * static_cast<std::size_t>(C) + 3 * static_cast<std::size_t>(P)) +
+                            static_cast<std::size_t>(N) * (4 + 4 + 16);
+  if (len != total) throw Error(BAE_ERR_PARSE, "binary BAL: size does not match the header", 0);
+  BalData d;
+  d.C = C;
+  d.P = P;
+  d.N = N;
+  auto take = [&](auto& v, std::size_t n) {
+    v.resize(n);
+    std::memcpy(v.data(), b + at, n * sizeof(v[0]));
+    at += n * sizeof(v[0]);
+  };
+  take(d.cameras, 9 * static_cast<std::size_t>(C));
+  take(d.points, 3 * static_cast<std::size_t>(P));
+  take(d.cam_idx, static_cast<std::size_t>(N));
+  take(d.pt_idx, static_cast<std::size_t>(N));
+  take(d.px, 2 * static_cast<std::size_t>(N));
+  for (std::int64_t k = 0; k < N; ++k) {
+    if (d.cam_idx[k] < 0 || d.cam_idx[k] >= C) throw Error(BAE_ERR_PARSE, "camera index out of range", k);
+    if (d.pt_idx[k] < 0 || d.pt_idx[k] >= P) throw Error(BAE_ERR_PARSE, "point index out of range", k);
+  }
+  return d;
+}
+}  // namespace
+
+void write_bal_binary(const BalData& d, const char* path) {
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) throw Error(BAE_ERR_IO, std::string("cannot open '") + path + "' for writing");
+  const std::int32_t C = d.C, P = d.P;
+  const std::int64_t N = d.N;
+  bool ok = std::fwrite(kBinMagic, 1, 8, f) == 8 && std::fwrite(&C, 4, 1, f) == 1 && std::fwrite(&P, 4, 1, f) == 1 &&
+            std::fwrite(&N, 8, 1, f) == 1;
+  auto put = [&](const auto& v) {
+    if (ok && !v.empty()) ok = std::fwrite(v.data(), sizeof(v[0]), v.size(), f) == v.size();
+  };
+  put(d.cameras);
+  put(d.points);
+  put(d.cam_idx);
+  put(d.pt_idx);
+  put(d.px);
+  if (std::fclose(f) != 0 || !ok) throw Error(BAE_ERR_IO, std::string("cannot write '") + path + "'");
+}
+
 BalData parse_bal_file(const char* path) {
   std::FILE* f = std::fopen(path, "rb");
   if (!f) throw Error(BAE_ERR_IO, std::string("cannot open '") + path + "'");
@@ -133,6 +199,7 @@ BalData parse_bal_file(const char* path) {
   std::size_t n;
   while ((n = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.append(chunk, n);
   std::fclose(f);
+  if (buf.size() >= 8 && std::memcmp(buf.data(), kBinMagic, 8) == 0) return decode_bal_binary(buf.data(), buf.size());
   return parse_bal_text(buf.data(), buf.data() + buf.size());
 }
 

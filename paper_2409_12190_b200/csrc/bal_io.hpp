@@ -24,6 +24,7 @@ BalData parse_bal_text(const char* begin, const char* end);  // parse_bal, io/ba
 BalData parse_bal_file(const char* path);
 std::string serialize_bal_text(const BalData& d);             // serialize_bal, io/bal.hpp:145-157
 void write_bal_file(const BalData& d, const char* path);
+void write_bal_binary(const BalData& d, const char* path);  // binary cache (row f4); parse_bal_file reads both
 void bal_poses(const BalData& d, double* poses7, double* intr3);  // BalCamera::pose, io/bal.hpp:24-26
 BalData synth_ba_dense(int C, int P, double pixel_sigma, double pose_sigma, std::uint64_t seed);  // synth_ba
 void look_at_origin(const P3& pos, Q4& q, P3& t);  // io/synthetic.hpp:26-38 (synth.cpp)

@@ -185,3 +185,54 @@ def test_synth_ba_noise_floor():  # test_io.cpp:211-220
     p = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
     rep = bae.optimize(p, s.poses, s.points, bae.LmConfig(max_iterations=50))
     assert 0.5 <= rep.final_mse <= 2.0
+
+
+def test_binary_cache_round_trip(tmp_path):
+    """Row f4: the binary problem cache holds exactly the parsed arrays and
+    read_bal / the CLI recognise it."""
+    s = bae.synth_ba(4, 25, 0.5, 0.05, 13)
+    txt, binf = tmp_path / "s.bal", tmp_path / "s.baeb"
+    bae.write_bal(txt, s)
+    p = bae.read_bal(txt)
+    bae.write_bal(binf, p, binary=True)
+    q = bae.read_bal(binf)
+    for f in ("cameras", "points", "cam_idx", "pt_idx", "pixels", "poses", "intrinsics"):
+        assert np.array_equal(getattr(p, f), getattr(q, f)), f
+    assert binf.stat().st_size == 24 + 8 * (9 * 4 + 3 * 25) + 24 * p.cam_idx.size
+
+
+@pytest.mark.parametrize("mutate,err", [
+    (lambda b: b[:-8], "truncated|size"),                      # short file
+    (lambda b: b[:8] + (0).to_bytes(4, "little") + b[12:], "non-positive"),
+])
+def test_binary_cache_errors(tmp_path, mutate, err):
+    s = bae.synth_ba(2, 5, 0.0, 0.0, 1)
+    f = tmp_path / "s.baeb"
+    bae.write_bal(f, s, binary=True)
+    f.write_bytes(mutate(f.read_bytes()))
+    with pytest.raises(bae.ParseError, match=err):
+        bae.read_bal(f)
+
+
+def test_binary_cache_index_validation(tmp_path):
+    s = bae.synth_ba(2, 5, 0.0, 0.0, 1)
+    f = tmp_path / "s.baeb"
+    bae.write_bal(f, s, binary=True)
+    raw = bytearray(f.read_bytes())
+    off = 24 + 8 * (9 * 2 + 3 * 5)  # first camera index
+    raw[off:off + 4] = (7).to_bytes(4, "little")
+    f.write_bytes(bytes(raw))
+    with pytest.raises(bae.ParseError, match="camera index out of range"):
+        bae.read_bal(f)
+
+
+@pytest.mark.gpu
+def test_cli_binary_cache_same_solve(tmp_path):
+    s = bae.synth_ba(3, 30, 1.0, 0.05, 21)
+    txt, binf = tmp_path / "s.bal", tmp_path / "s.baeb"
+    bae.write_bal(txt, s)
+    bae.write_bal(binf, bae.read_bal(txt), binary=True)
+    a, b = _cli("ba", "--input", str(txt), "--max-iters", "10"), _cli("ba", "--input", str(binf), "--max-iters", "10")
+    assert a[0] == 0 and b[0] == 0, (a[2], b[2])
+    strip = lambda out: out.split("final_cost=")[1].split(" time_s=")[0]  # noqa: E731
+    assert strip(a[1]) == strip(b[1])
