@@ -233,6 +233,16 @@ int bae_synth_bal_shaped(int32_t num_cameras, int32_t num_points, int64_t num_ob
                          double point_sigma, double* poses7, double* points3,
                          double* intrinsics3, int32_t* cam_idx, int32_t* pt_idx,
                          double* pixels2, double* true_poses7, double* true_points3);
+/* The same scene family generated on the device (row f4): every value from
+ * Philox4x32-10 keyed by the seed, counter = (stream, entity, draw), one
+ * thread per point / camera / observation (csrc/synth_device.cu documents the
+ * streams). Not the host generator's values (that one follows the reference
+ * Rng stream); the oracle restates this one for the tests. */
+int bae_synth_bal_shaped_device(int32_t num_cameras, int32_t num_points, int64_t num_observations,
+                                uint64_t seed, double pixel_sigma, double pose_sigma, double point_sigma,
+                                int32_t device, double* poses7, double* points3, double* intrinsics3,
+                                int32_t* cam_idx, int32_t* pt_idx, double* pixels2, double* true_poses7,
+                                double* true_points3);
 
 /* ---- BAL files, the reference's synthetic scene, the CLI - */
 typedef struct bae_bal bae_bal;

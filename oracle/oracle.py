@@ -50,6 +50,11 @@ _SIG = {
                                          I32, D, I64]),
     "or_synth_ba": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, D,
                                    D, D, I32, I32, D, D]),
+    "or_synth_bal_shaped_philox": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
+                                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, D, D, D, I32, I32,
+                                                  D, D, D]),
+    "or_philox4x32_10": (ctypes.c_uint32, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
+                                           ctypes.POINTER(ctypes.c_uint32)]),
     "or_ba_problem_new": (VP, [ctypes.c_int, ctypes.c_int, D, ctypes.c_int, D, D, ctypes.c_int64, I32, I32, D,
                                ctypes.POINTER(ctypes.c_int)]),
     "or_scalar_problem_new": (VP, [ctypes.c_int, D]),
@@ -161,6 +166,26 @@ def synth_ba(C, P, pix_sigma, pose_sigma, seed):
                            p(pi, ctypes.c_int32), p(px), p(tp)))
     return dict(poses=poses, points=pts, intrinsics=intr, cam_idx=ci, pt_idx=pi, pixels=px, true_poses=tp,
                 pinhole=False)
+
+
+def synth_bal_shaped_philox(C, P, N, seed, pixel_sigma=1.0, pose_sigma=0.05, point_sigma=0.01):
+    """The on-device generator's algorithm (row f4) restated on the host."""
+    out = dict(poses=np.empty((C, 7)), points=np.empty((P, 3)), intrinsics=np.empty((C, 3)),
+               cam_idx=np.empty(N, np.int32), pt_idx=np.empty(N, np.int32), pixels=np.empty((N, 2)),
+               true_poses=np.empty((C, 7)), true_points=np.empty((P, 3)))
+    _chk(lib().or_synth_bal_shaped_philox(C, P, N, seed, pixel_sigma, pose_sigma, point_sigma, p(out["poses"]),
+                                          p(out["points"]), p(out["intrinsics"]), p(out["cam_idx"], ctypes.c_int32),
+                                          p(out["pt_idx"], ctypes.c_int32), p(out["pixels"]), p(out["true_poses"]),
+                                          p(out["true_points"])))
+    return out
+
+
+def philox4x32_10(ctr, key):
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    lib().or_philox4x32_10(c, k, o)
+    return list(o)
 
 
 class Problem:

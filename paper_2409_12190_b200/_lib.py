@@ -108,6 +108,10 @@ SIGNATURES = {
                                             ctypes.c_double, ctypes.c_double, ctypes.c_double, c_double_p,
                                             c_double_p, c_double_p, c_int32_p, c_int32_p, c_double_p,
                                             c_double_p, c_double_p]),
+    "bae_synth_bal_shaped_device": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int32, c_double_p,
+                                            c_double_p, c_double_p, c_int32_p, c_int32_p, c_double_p,
+                                            c_double_p, c_double_p]),
     "bae_partition_points": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, c_int32_p, c_int32_p, ctypes.c_int64,
                                             ctypes.c_int32, c_int32_p]),
     "bae_time_kernel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, c_double_p]),

@@ -318,6 +318,16 @@ int bae_synth_bal_shaped(int32_t C, int32_t P, int64_t N, uint64_t seed, double 
   });
 }
 
+int bae_synth_bal_shaped_device(int32_t C, int32_t P, int64_t N, uint64_t seed, double pixel_sigma,
+                                double pose_sigma, double point_sigma, int32_t device, double* poses7, double* points3,
+                                double* intr3, int32_t* cam_idx, int32_t* pt_idx, double* px2, double* true_poses7,
+                                double* true_points3) {
+  return guarded([&] {
+    bae::synth_bal_shaped_device(C, P, N, seed, pixel_sigma, pose_sigma, point_sigma, device, poses7, points3, intr3,
+                                 cam_idx, pt_idx, px2, true_poses7, true_points3);
+  });
+}
+
 int bae_partition_points(int32_t C, int32_t P, const int32_t* cam_idx, const int32_t* pt_idx, int64_t N,
                          int32_t world, int32_t* rank_of_point) {
   return guarded([&] { bae::partition_points(C, P, cam_idx, pt_idx, N, world, rank_of_point); });

@@ -155,6 +155,11 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
 void partition_points(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N,
                       int world, std::int32_t* rank_of_point);
 
+void synth_bal_shaped_device(int C, int P, std::int64_t N, std::uint64_t seed, double pixel_sigma, double pose_sigma,
+                             double point_sigma, int device, double* poses7, double* points3, double* intr3,
+                             std::int32_t* cam_idx, std::int32_t* pt_idx, double* px2, double* true_poses7,
+                             double* true_points3);
+
 void synth_bal_shaped(int C, int P, std::int64_t N, std::uint64_t seed, double pixel_sigma, double pose_sigma,
                       double point_sigma, double* poses7, double* points3, double* intr3, std::int32_t* cam_idx,
                       std::int32_t* pt_idx, double* px2, double* true_poses7, double* true_points3);

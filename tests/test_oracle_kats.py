@@ -306,3 +306,35 @@ def test_acceptance_synthetic_ba(oracle):
     d = oracle.synth_ba(3, 50, 1.0, 0.05, 9)
     rep = oracle.Problem.from_dict(d).optimize(LmConfig(max_iterations=50))
     assert 0.5 <= rep["final_mse"] <= 2.0
+
+
+# --- Philox4x32-10 (row f4's on-device generator) ------------------------------
+# Known answers of the published algorithm (Random123 kat_vectors).
+@pytest.mark.parametrize("ctr,key,want", [
+    ([0, 0, 0, 0], [0, 0], [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]),
+    ([0xffffffff] * 4, [0xffffffff] * 2, [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]),
+    ([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0],
+     [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]),
+])
+def test_philox_known_answers(oracle, ctr, key, want):
+    assert oracle.philox4x32_10(ctr, key) == want
+
+
+def test_philox_scene_shape(oracle):
+    """The restated device generator: exactly N observations, camera-major
+    with points ascending, no duplicate (camera, point), every point's
+    cameras inside a window of min(C, 16), BAL-shaped counts."""
+    C, P, N = 40, 300, 1237
+    s = oracle.synth_bal_shaped_philox(C, P, N, 40)
+    ci, pi = s["cam_idx"], s["pt_idx"]
+    key = ci.astype(np.int64) * P + pi
+    assert np.all(np.diff(key) > 0)  # camera-major, points ascending, no duplicates
+    counts = np.bincount(pi, minlength=P)
+    assert counts.sum() == N and counts.min() == N // P and counts.max() == N // P + 1
+    for j in range(P):
+        cams = ci[pi == j]
+        assert any(max((c - a) % C for c in cams) < 16 for a in cams)  # inside some window of 16
+    assert np.all(np.abs(s["true_points"]) <= 0.5)
+    assert np.all(np.abs(s["intrinsics"][:, 1]) <= 0.1) and np.all(np.abs(s["intrinsics"][:, 2]) <= 0.01)
+    b = oracle.synth_bal_shaped_philox(C, P, N, 40)
+    assert all(np.array_equal(s[k], b[k]) for k in s)  # deterministic
