@@ -104,7 +104,12 @@ struct Dev {
   // 48 x 48 tile holding it (8 cameras per tile), column-major tiles
   // per camera block {tile slot, row offset | col offset << 8 | transposed << 16},
   // then per camera {diagonal tile slot, offset}
-  const int* blk_ord;       // direct solver: blocks by descending pair count (k_schur_dense order)
+  const int* blk_ord;       // direct solver: diagonal blocks first, then row by row
+  const int4* chunks;       // k_schur_dense work: (block, first pair, end pair, block's first chunk), blk_ord order
+  int nchunk;
+  const int* blk_nchunk;    // chunks per block
+  unsigned* blk_ticket;     // per block: chunks done (reset before every assembly)
+  double* schur_part;       // 36 per chunk: partial 6x6 sums of multi-chunk blocks
   const int2* blk_tile;
   double* stiles;
   long long stile_count;

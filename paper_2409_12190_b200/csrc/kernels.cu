@@ -835,22 +835,28 @@ __global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long lo
 // triangle for potrf.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
-  // Warp per camera block; lane = 4 * slot + part: 8 pairs in flight, each
-  // pair's 6x6 product split in four 3x3 corners (rows 3 (part & 1), columns
-  // 3 (part >> 1)), so a lane loads two contiguous 9-double row bands
-  // (V_k and V_l) and keeps 9 accumulators. The 8 slot sums are then
-  // combined by a fixed shuffle tree: the order depends only on the block.
+  // Warp per chunk of at most kSchurChunk pairs of one camera block (a long
+  // block -- a diagonal one holds every observation of its camera -- is cut
+  // into several, so no warp walks a whole camera's observations alone).
+  // Lane = 4 * slot + part: 8 pairs in flight, each pair's 6x6 product split
+  // in four 3x3 corners (rows 3 (part & 1), columns 3 (part >> 1)), so a lane
+  // loads two contiguous 9-double row bands (V_k and V_l) and keeps 9
+  // accumulators; the 8 slot sums are combined by a fixed shuffle tree. A
+  // block of one chunk is written at once; otherwise each chunk stores its
+  // 6x6 partial and the block's last chunk to finish (ticket) adds the
+  // partials in chunk order. Every order depends only on the block.
   const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (wid >= d.nblk) return;
-  const int blk = d.blk_ord[wid];  // diagonal blocks first, then row by row
+  if (wid >= d.nchunk) return;
+  const int4 ch = d.chunks[wid];  // block, first pair, end pair, index of the block's first chunk
+  const int blk = ch.x;
   const int lane = lane_id(), slot = lane >> 2, part = lane & 3;
   const int r0 = 3 * (part & 1), c0 = 3 * (part >> 1);
   double acc[9];
 #pragma unroll
   for (int j = 0; j < 9; ++j) acc[j] = 0.0;
-  const int qe = d.blk_ptr[blk + 1];
+  const int qe = ch.z;
 #pragma unroll 2
-  for (int q = d.blk_ptr[blk] + slot; q < qe; q += 8) {
+  for (int q = ch.y + slot; q < qe; q += 8) {
     const int2 pr = d.pairs[q];
     const double* wh = d.wstore + (long long)pr.x * 18 + 3 * r0;  // V_k rows r0..r0+2
     const double* w = d.wstore + (long long)pr.y * 18 + 3 * c0;   // V_l rows c0..c0+2
@@ -870,35 +876,77 @@ __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
   for (int j = 0; j < 9; ++j)
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+  const int first = ch.w, count = d.blk_nchunk[blk];
+  bool writer = true;
+  double v36 = 0.0;  // multi-chunk: entry (lane / 6, lane % 6) of the block sum, lanes 0..35 -> 0..31 + 4 below
+  double v36b = 0.0;
+  if (count > 1) {
+    double* mine = d.schur_part + 36LL * wid;
+    if (slot == 0) {
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) mine[(r0 + x) * 6 + c0 + y] = acc[x * 3 + y];
+    }
+    __threadfence();
+    __syncwarp();
+    int t = 0;
+    if (lane == 0) t = static_cast<int>(atomicAdd(d.blk_ticket + blk, 1u));
+    t = __shfl_sync(0xffffffffu, t, 0);
+    writer = t == count - 1;
+    if (!writer) return;
+    __threadfence();  // the other chunks' partials, published before their tickets
+    for (int i = 0; i < count; ++i) {  // chunk order
+      const double* pp = d.schur_part + 36LL * (first + i);
+      v36 += __ldcg(pp + lane);
+      if (lane < 4) v36b += __ldcg(pp + 32 + lane);
+    }
+  }
   const int2 cc = d.blk_cam[blk];
   const long long n = 6LL * d.C;
-  if (slot == 0) {  // lanes 0..3: one 3x3 corner each
-    const double* h = d.hccd + (long long)cc.x * 21;
-    // dense column-major S, or the block's place in its 48 x 48 tile (the
-    // camera order of the tile factorisation may put it transposed)
-    double* base;
-    long long ldr, ldc;  // element (r, c) of the block at base[r * ldr + c * ldc]
-    if (d.stiles) {
-      const int2 bt = d.blk_tile[blk];
-      const int ro = bt.y & 0xff, co = (bt.y >> 8) & 0xff;
-      base = d.stiles + (long long)bt.x * kSTileElems + co * 48 + ro;
-      const bool tr = (bt.y >> 16) & 1;
-      ldr = tr ? 48 : 1;
-      ldc = tr ? 1 : 48;
-    } else {
-      base = d.schur + 6LL * cc.y * n + 6LL * cc.x;
-      ldr = 1;
-      ldc = n;
+  const double* h = d.hccd + (long long)cc.x * 21;
+  // dense column-major S, or the block's place in its 48 x 48 tile (the
+  // camera order of the tile factorisation may put it transposed)
+  double* base;
+  long long ldr, ldc;  // element (r, c) of the block at base[r * ldr + c * ldc]
+  if (d.stiles) {
+    const int2 bt = d.blk_tile[blk];
+    const int ro = bt.y & 0xff, co = (bt.y >> 8) & 0xff;
+    base = d.stiles + (long long)bt.x * kSTileElems + co * 48 + ro;
+    const bool tr = (bt.y >> 16) & 1;
+    ldr = tr ? 48 : 1;
+    ldc = tr ? 1 : 48;
+  } else {
+    base = d.schur + 6LL * cc.y * n + 6LL * cc.x;
+    ldr = 1;
+    ldc = n;
+  }
+  const bool diag = cc.x == cc.y && !d.cred;  // sharded: H~_cc is added after the rank sum
+  if (count == 1) {
+    if (slot == 0) {  // lanes 0..3: one 3x3 corner each
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          const int r = r0 + x, c = c0 + y;
+          double v = -acc[x * 3 + y];
+          if (diag) v += h[sym6(r, c)];
+          base[r * ldr + c * ldc] = v;
+        }
     }
-#pragma unroll
-    for (int x = 0; x < 3; ++x)
-#pragma unroll
-      for (int y = 0; y < 3; ++y) {
-        const int r = r0 + x, c = c0 + y;
-        double v = -acc[x * 3 + y];
-        if (cc.x == cc.y && !d.cred) v += h[sym6(r, c)];  // sharded: added after the rank sum
-        base[r * ldr + c * ldc] = v;
-      }
+    return;
+  }
+  {
+    const int r = lane / 6, c = lane % 6;
+    double v = -v36;
+    if (diag) v += h[sym6(r, c)];
+    base[r * ldr + c * ldc] = v;
+  }
+  if (lane < 4) {
+    const int e = 32 + lane, r = e / 6, c = e % 6;
+    double v = -v36b;
+    if (diag) v += h[sym6(r, c)];
+    base[r * ldr + c * ldc] = v;
   }
 }
 
@@ -1875,7 +1923,8 @@ int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) 
 int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
   int n = 0;
   if (d.nblk > 0) {
-    k_schur_dense<<<(d.nblk + 7) / 8, 256, 0, s>>>(d);
+    cudaMemsetAsync(d.blk_ticket, 0, sizeof(unsigned) * d.nblk, s);
+    k_schur_dense<<<(d.nchunk + 7) / 8, 256, 0, s>>>(d);
     ++n;
   }
   if (comm) {  // the direct solve's exchange: the reduced matrix, once per LM iteration

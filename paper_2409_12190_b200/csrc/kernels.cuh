@@ -41,6 +41,7 @@ cudaError_t launch_pcg_persistent(const Dev& d, const SmemSizes& sm, int grid, l
 int launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s);
 int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
 int launch_commit(const Dev& d, cudaStream_t s);
+constexpr int kSchurChunk = 128;  // pairs per k_schur_dense warp (at most)
 int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm);
 
 }  // namespace bae

@@ -389,6 +389,11 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.blk_ptr = nullptr;
   d.blk_cam = nullptr;
   d.blk_ord = nullptr;
+  d.chunks = nullptr;
+  d.nchunk = 0;
+  d.blk_nchunk = nullptr;
+  d.blk_ticket = nullptr;
+  d.schur_part = nullptr;
   d.nblk = 0;
   d.schur = nullptr;
   ht.mark("allocs");
@@ -722,6 +727,25 @@ void Problem::build_direct() {
     for (std::size_t b = 0; b < bcam.size(); ++b)
       if (bcam[b].x != bcam[b].y) ord.push_back(static_cast<int>(b));
     d_.blk_ord = upload(ord);
+    // work chunks in that block order: about 32 warps' worth per SM, at
+    // least kSchurChunk pairs each (short blocks stay whole, long ones split)
+    const long long np = bptr.back();
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, opt_.device);
+    const int U = static_cast<int>(std::clamp<long long>(np / (32LL * nsm) / 8 * 8, kSchurChunk, 8 * kSchurChunk));
+    std::vector<int4> chunks;
+    std::vector<int> nch(bcam.size(), 0);
+    for (int b : ord) {
+      const int q0 = bptr[b], q1 = bptr[b + 1];
+      const int first = static_cast<int>(chunks.size());
+      for (int q = q0; q < q1 || q == q0; q += U) chunks.push_back(int4{b, q, std::min(q + U, q1), first});
+      nch[b] = static_cast<int>(chunks.size()) - first;
+    }
+    d_.chunks = upload(chunks);
+    d_.nchunk = static_cast<int>(chunks.size());
+    d_.blk_nchunk = upload(nch);
+    d_.blk_ticket = dalloc<unsigned>(bcam.size());
+    d_.schur_part = dalloc<double>(36 * chunks.size());
   }
   d_.nblk = static_cast<int>(bcam.size());
   ht.mark("direct: pair list");
