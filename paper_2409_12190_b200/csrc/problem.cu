@@ -421,6 +421,7 @@ Problem::~Problem() {
   for (std::size_t i = 0; i < allocs_.size(); ++i) chunk_give(opt_.device, allocs_[i], alloc_bytes_[i]);
   pinned_give(pcg_host_);
   pinned_give(lm_host_);
+  pinned_give(lm_reset_host_);
   if (stream_) cudaStreamDestroy(stream_);
   comm_.reset();
 }
@@ -542,12 +543,17 @@ void Problem::get_parameters(double* poses7, double* points3) {
 
 // Clears the per-evaluation flags and the trial cost; keeps the cost and
 // ||J^T r||^2 of the current linearisation (needed by the next solve).
-void Problem::reset_lm_status() {
-  LmDev z{};
-  z.err_obs = INT_MAX;
+void Problem::reset_lm_status(bool keep_err) {
+  if (!lm_reset_host_) {
+    lm_reset_host_ = static_cast<LmDev*>(pinned_take());
+    *lm_reset_host_ = LmDev{};
+    lm_reset_host_->err_obs = INT_MAX;
+  }
   constexpr std::size_t off = offsetof(LmDev, new_cost);
-  ck(cudaMemcpyAsync(reinterpret_cast<char*>(d_.lm) + off, reinterpret_cast<const char*>(&z) + off,
-                     sizeof(LmDev) - off, cudaMemcpyHostToDevice, stream_),
+  // keep_err: a linearisation queued ahead of this trial still owns err_obs
+  const std::size_t end = keep_err ? offsetof(LmDev, err_obs) : sizeof(LmDev);
+  ck(cudaMemcpyAsync(reinterpret_cast<char*>(d_.lm) + off, reinterpret_cast<const char*>(lm_reset_host_) + off,
+                     end - off, cudaMemcpyHostToDevice, stream_),
      "H2D lm");
 }
 
@@ -590,11 +596,15 @@ double Problem::evaluate(double* resid2) {
   return lm_host_->cost;
 }
 
-void Problem::linearize() {
+void Problem::linearize_async() {
   reset_lm_status();
   phase_begin(kPhLinearize);
   launches_ += launch_linearize(d_, sm_, false, stream_, comm_.get());
   phase_end();
+}
+
+void Problem::linearize() {
+  linearize_async();
   read_lm();
   phase_collect();
   if (lm_host_->err_obs != INT_MAX)
@@ -966,11 +976,15 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
     }
     ck(cudaMemcpyAsync(host_info_, tchol_.fail, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H fail");
     ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
+    info.converged = true;
+    info.rel_residual = 0.0;
+    if (defer_factor_check_ && trace.empty()) {  // checked by the caller after its next synchronisation
+      info.pending = true;
+      return true;
+    }
     sync();
     phase_collect();
     if (*host_info_ != 0 || pcg_host_->not_spd) return false;  // NotSpdError (cholesky.hpp:229)
-    info.converged = true;
-    info.rel_residual = 0.0;
     return true;
   }
   ck(cudaMemcpyAsync(d_.x, d_.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream_), "rhs copy");
@@ -1115,26 +1129,51 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   rep = bae_lm_report{};
   rep.reason = BAE_TERM_MAX_ITERS;
   const auto t0 = std::chrono::steady_clock::now();
+  // Direct solves leave the factorisation's failure word and the next
+  // linearisation's cost / gradient in flight: the trial's read-back is the
+  // one host synchronisation of an LM iteration (a failed factorisation
+  // rejects the step as before; its trial result is ignored).
+  defer_factor_check_ = cfg.solver == BAE_SOLVER_CHOLESKY;
+  struct DeferReset {
+    bool& f;
+    ~DeferReset() { f = false; }
+  } defer_reset{defer_factor_check_};
+  bool lin_pending = false;
   while (iterations < cfg.max_iterations) {
     const double lambda_used = lambda;
     const bool saturated = lambda >= cfg.damping_max;
     if (need_lin) {
-      linearize();
-      grad = std::sqrt(lm_host_->grad_sq);
+      if (defer_factor_check_) {
+        linearize_async();
+        lin_pending = true;
+      } else {
+        linearize();
+        grad = std::sqrt(lm_host_->grad_sq);
+      }
       need_lin = false;
     }
     SolveInfo info;
-    const bool ok = solve(lambda_used, cfg, info);
+    bool ok = solve(lambda_used, cfg, info);
     total_pcg += info.iters;
     bool accepted = false;
     double trial_cost = std::numeric_limits<double>::quiet_NaN();
-    if (ok) {
-      reset_lm_status();
-      phase_begin(kPhTrial);
-      launches_ += launch_trial(d_, sm_, stream_, comm_.get());
-      phase_end();
+    if (ok || lin_pending) {
+      if (ok) {
+        reset_lm_status(lin_pending);
+        phase_begin(kPhTrial);
+        launches_ += launch_trial(d_, sm_, stream_, comm_.get());
+        phase_end();
+      }
       read_lm();
       phase_collect();
+      if (lin_pending) {
+        lin_pending = false;
+        if (lm_host_->err_obs != INT_MAX) throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
+        grad = std::sqrt(lm_host_->grad_sq);
+      }
+      if (info.pending && (*host_info_ != 0 || pcg_host_->not_spd)) ok = false;  // NotSpdError (cholesky.hpp:229)
+    }
+    if (ok) {
       trial_cost = (lm_host_->retract_bad || lm_host_->trial_bad) ? std::numeric_limits<double>::infinity()
                                                                    : lm_host_->new_cost;
       if (trial_cost < cost) {

@@ -19,6 +19,7 @@ struct SolveInfo {
   long long iters = 0;
   bool converged = false;
   double rel_residual = 0.0;
+  bool pending = false;  // direct solve: the failure word is read after the caller's next synchronisation
 };
 
 bool plateau_stagnation(const double* h, std::size_t n, int patience, double tol);
@@ -85,7 +86,8 @@ class Problem {
   T* upload(const std::vector<T>& v);
   void sync();
   void ensure_point_staging();
-  void reset_lm_status();
+  void linearize_async();
+  void reset_lm_status(bool keep_err = false);
   void read_lm();
   void linearize();
   bool solve(double lambda, const bae_lm_config& cfg, SolveInfo& info);
@@ -123,6 +125,8 @@ class Problem {
   std::vector<std::int32_t> local_pts_;      // sharded: global ids of this rank's points, ascending
   int* src_of_internal_ = nullptr;           // single rank: caller id of each internal point (device)
   double* pts_user_ = nullptr;               // single rank: caller-ordered points (device staging)
+  LmDev* lm_reset_host_ = nullptr;           // pinned template of the per-evaluation LM flags
+  bool defer_factor_check_ = false;          // optimize: the direct factorisation's failure word read later
   Plan plan_;
   Dev d_{};
   SmemSizes sm_;
