@@ -1236,6 +1236,7 @@ double Problem::time_kernel(int kind, int reps) {
   if (kind == 1 || kind == 2) {
     linearize();
     SolveInfo info;
+    cfg.solver = BAE_SOLVER_PCG;  // the PCG state machine, whatever the default solver
     cfg.pcg_max_iters = 1;
     solve(1e-4, cfg, info);
     // force the state machine to keep iterating on the current direction
