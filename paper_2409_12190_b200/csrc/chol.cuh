@@ -87,13 +87,16 @@ struct TileChol {
   const int* pos_cam;   // camera at each position (n / 6), -1 for a padding slot
   const unsigned long long* padmask;  // per tile: bit r set when row r is padding (unit pivot)
   unsigned* flags;      // nnz + nt epoch flags: one per stored tile (factor), one per column (backward)
-  unsigned* next;       // 2 work counters (factor, backward): CTAs claim columns in topological order
+  unsigned* next;       // 3 words: work counters (factor, backward; CTAs claim columns in topological
+                        // order) and the epoch, the flag value of the current solve
   int* fail;            // set when a pivot is not positive (NotSpdError, cholesky.hpp:229)
   unsigned long long* trace;  // BAE_CHOL_TRACE: 8 globaltimer stamps per column, or null
 };
 
-// Factor + solve on stream s (two launches). `epoch` must increase by one per call.
-int launch_tile_chol(const TileChol& t, unsigned epoch, int grid, cudaStream_t s);
+// Factor + solve on stream s (three launches: counters and epoch, factor,
+// backward); the epoch lives on the device (next[2]), so the sequence can be
+// captured in a graph and replayed.
+int launch_tile_chol(const TileChol& t, int grid, cudaStream_t s);
 int tile_chol_grid(int nt);
 
 }  // namespace bae

@@ -600,6 +600,7 @@ constexpr WsDims kPrepDirWs{16, 12, 6, 0};
 template <bool kShared, bool kDirect>
 __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char* smem, int slice, double lambda,
                                           double clo, double chi) {
+  if (kDirect) lambda = *d.lam;  // direct solves keep lambda on the device (graph-replayed LM iterations)
   constexpr int SW = kDirect ? 6 : 27;
   const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kDirect ? kPrepDirWs : kPrepWs, g.ncam, g.npts, g.nobs);
   const int lane = lane_id();
@@ -719,6 +720,7 @@ __global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, d
 // Camera side of the direct solver's prep (block per camera): damped H~_cc
 // and the Schur RHS b = -g_c + sum_k J_c^T J_p H~_pp^-1 g_p.
 __global__ void __launch_bounds__(128) k_cam_prep_direct(Dev d, double lambda, double clo, double chi) {
+  lambda = *d.lam;
   __shared__ double red[20 * 6];
   __shared__ double acc[6];
   const int c = blockIdx.x;

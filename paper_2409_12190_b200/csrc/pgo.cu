@@ -539,7 +539,8 @@ PgoProblem::PgoProblem(const double* poses7, int n, const std::int32_t* ei, cons
   t.flags = dalloc<unsigned>(static_cast<std::size_t>(t.nnz) + nt);
   ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (static_cast<std::size_t>(t.nnz) + nt), stream_), "memset");
   t.fail = dalloc<int>(1);
-  t.next = dalloc<unsigned>(2);
+  t.next = dalloc<unsigned>(3);
+  ck(cudaMemsetAsync(t.next, 0, 3 * sizeof(unsigned), stream_), "memset counters");
   t.trace = nullptr;
   chol_grid_ = tile_chol_grid(std::max(nt, 1));
   ck(cudaMallocHost(&scal_host_, 8 * sizeof(double)), "cudaMallocHost");
@@ -628,7 +629,7 @@ bool PgoProblem::solve(double lambda, const bae_lm_config& cfg) {
   k_pgo_assemble<<<blocks_of(warps, 8), 256, 0, stream_>>>(d_, lambda, cfg.clamp_min, cfg.clamp_max);
   k_pgo_grad<<<1, 1024, 0, stream_>>>(d_);
   ck(cudaMemsetAsync(tchol_.fail, 0, sizeof(int), stream_), "memset fail");
-  launches_ += 2 + launch_tile_chol(tchol_, ++chol_epoch_, chol_grid_, stream_);
+  launches_ += 2 + launch_tile_chol(tchol_, chol_grid_, stream_);
   ck(cudaMemcpyAsync(fail_host_, tchol_.fail, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
   read_scal();
   return *fail_host_ == 0;

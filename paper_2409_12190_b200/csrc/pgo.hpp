@@ -76,7 +76,6 @@ class PgoProblem {
   PgoDev d_{};
   TileChol tchol_{};
   int chol_grid_ = 0;
-  unsigned chol_epoch_ = 0;
   cudaStream_t stream_ = nullptr;
   std::vector<void*> allocs_;
   double* scal_host_ = nullptr;

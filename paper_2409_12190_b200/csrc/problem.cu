@@ -385,6 +385,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.resid = nullptr;
   d.trace = nullptr;
   d.wstore = nullptr;
+  d.lam = nullptr;
   d.pairs = nullptr;
   d.blk_ptr = nullptr;
   d.blk_cam = nullptr;
@@ -422,6 +423,7 @@ Problem::~Problem() {
   pinned_give(pcg_host_);
   pinned_give(lm_host_);
   pinned_give(lm_reset_host_);
+  pinned_give(lam_host_);
   if (stream_) cudaStreamDestroy(stream_);
   comm_.reset();
 }
@@ -758,6 +760,11 @@ void Problem::build_direct() {
     d_.schur_part = dalloc<double>(36 * chunks.size());
   }
   d_.nblk = static_cast<int>(bcam.size());
+  if (!d_.wstore) d_.wstore = dalloc<double>(18 * static_cast<std::size_t>(plan_.N));
+  if (!d_.lam) {
+    d_.lam = dalloc<double>(1);
+    lam_host_ = static_cast<double*>(pinned_take());
+  }
   ht.mark("direct: pair list");
   if (use_tiles_) {
     build_tile_chol(bcam);
@@ -900,8 +907,8 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (static_cast<std::size_t>(t.nnz) + nt), stream_),
      "memset flags");
   t.fail = dalloc<int>(1);
-  t.next = dalloc<unsigned>(2);
-  chol_epoch_ = 0;
+  t.next = dalloc<unsigned>(3);
+  ck(cudaMemsetAsync(t.next, 0, 3 * sizeof(unsigned), stream_), "memset counters");
   chol_grid_ = tile_chol_grid(nt);
   chol_updates_ = static_cast<long long>(pl.usrc.size());
   if (!host_info_) host_info_ = static_cast<int*>(pinned_take());
@@ -914,7 +921,9 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
 bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
   build_direct();
   const long long n = 6LL * d_.C;
-  if (!d_.wstore) d_.wstore = dalloc<double>(18 * static_cast<std::size_t>(plan_.N));
+  *lam_host_ = lambda;  // pinned: a graph replay reads it when the copy executes
+  ck(cudaMemcpyAsync(const_cast<double*>(d_.lam), lam_host_, sizeof(double), cudaMemcpyHostToDevice, stream_),
+     "H2D lambda");
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
   launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
@@ -937,7 +946,7 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
       ck(cudaMalloc(&tchol_.trace, 8 * sizeof(unsigned long long) * tchol_.nt), "cudaMalloc");
       ck(cudaMemsetAsync(tchol_.trace, 0, 8 * sizeof(unsigned long long) * tchol_.nt, stream_), "memset");
     }
-    launches_ += launch_tile_chol(tchol_, ++chol_epoch_, chol_grid_, stream_);
+    launches_ += launch_tile_chol(tchol_, chol_grid_, stream_);
     phase_end();
     if (tchol_.trace) {
       trace.resize(8 * static_cast<std::size_t>(tchol_.nt));
@@ -1275,7 +1284,7 @@ double Problem::time_kernel(int kind, int reps) {
         launches_ += launch_linearize(d_, sm_, true, stream_, comm_.get());
         break;
       case 4:  // tile Cholesky factor + both substitutions (re-factors the factor: same work)
-        launches_ += launch_tile_chol(tchol_, ++chol_epoch_, chol_grid_, stream_);
+        launches_ += launch_tile_chol(tchol_, chol_grid_, stream_);
         break;
       default:
         throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");

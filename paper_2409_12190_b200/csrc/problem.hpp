@@ -126,6 +126,7 @@ class Problem {
   int* src_of_internal_ = nullptr;           // single rank: caller id of each internal point (device)
   double* pts_user_ = nullptr;               // single rank: caller-ordered points (device staging)
   LmDev* lm_reset_host_ = nullptr;           // pinned template of the per-evaluation LM flags
+  double* lam_host_ = nullptr;               // pinned: the damping of the next direct solve
   bool defer_factor_check_ = false;          // optimize: the direct factorisation's failure word read later
   Plan plan_;
   Dev d_{};
@@ -152,7 +153,6 @@ class Problem {
   // tile-sparse Cholesky (default direct solver; BAE_DIRECT=cusolver: dense cuSOLVER)
   bool use_tiles_ = true;
   TileChol tchol_{};
-  unsigned chol_epoch_ = 0;
   int chol_grid_ = 0;
   long long chol_updates_ = 0;
   int chol_groups_ = 0;
