@@ -419,6 +419,8 @@ Problem::~Problem() {
   if (stream_) cudaStreamSynchronize(stream_);  // the chunks are reused by the next problem
   pinned_give(host_info_);
   if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
+  if (lm_graph_solve_) cudaGraphExecDestroy(lm_graph_solve_);
+  if (lm_graph_lin_) cudaGraphExecDestroy(lm_graph_lin_);
   for (std::size_t i = 0; i < allocs_.size(); ++i) chunk_give(opt_.device, allocs_[i], alloc_bytes_[i]);
   pinned_give(pcg_host_);
   pinned_give(lm_host_);
@@ -440,6 +442,7 @@ void Problem::require_single(const char* what) const {
 void Problem::activate() { ck(cudaSetDevice(opt_.device), "cudaSetDevice"); }
 
 void Problem::phase_begin(int ph) {
+  if (capturing_) return;  // a captured graph has no host-visible events
   if (ev_pool_.empty()) {
     ev_pool_.resize(512);
     for (auto& e : ev_pool_) ck(cudaEventCreate(&e), "event");
@@ -452,6 +455,7 @@ void Problem::phase_begin(int ph) {
 }
 
 void Problem::phase_end() {
+  if (capturing_) return;
   ck(cudaEventRecord(ev_pool_[ev_open_.back().second + 1], stream_), "event record");
   ph_cur_ = -1;
 }
@@ -683,6 +687,77 @@ void Problem::build_pcg_graph() {
   ck(cudaStreamEndCapture(stream_, &g), "end capture");
   ck(cudaGraphInstantiate(&pcg_graph_, g, 0), "graph instantiate");
   cudaGraphDestroy(g);
+}
+
+// The direct path's LM iteration as two graphs (one launch each instead of a
+// few dozen API calls): G_lin = commit of the accepted trial + the next
+// linearisation; G_solve = damping copy, prep, Schur assembly, tile
+// Cholesky, the failure words, the trial and the LM read-back. The damping
+// is read from pinned memory when the copy node runs; clamps are kernel
+// arguments, so a different LmConfig clamp re-captures. Returns false (and
+// the caller keeps the plain launches) when capture is not possible.
+bool Problem::build_lm_graphs(const bae_lm_config& cfg) {
+  if (lm_graph_solve_ && graph_clo_ == cfg.clamp_min && graph_chi_ == cfg.clamp_max) return true;
+  if (lm_graph_failed_) return false;
+  if (lm_graph_solve_) cudaGraphExecDestroy(lm_graph_solve_);
+  if (lm_graph_lin_) cudaGraphExecDestroy(lm_graph_lin_);
+  lm_graph_solve_ = lm_graph_lin_ = nullptr;
+  auto capture = [&](auto&& body, cudaGraphExec_t& out, long long& nlaunch) {
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+    capturing_ = true;
+    const long long l0 = launches_;
+    bool ok = true;
+    try {
+      body();
+    } catch (...) {
+      ok = false;
+    }
+    capturing_ = false;
+    nlaunch = launches_ - l0;
+    launches_ = l0;
+    const cudaError_t e = cudaStreamEndCapture(stream_, &g);
+    if (!ok || e != cudaSuccess || !g) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return false;
+    }
+    const cudaError_t ei = cudaGraphInstantiate(&out, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+      cudaGetLastError();
+      out = nullptr;
+      return false;
+    }
+    return true;
+  };
+  const bool a = capture(
+      [&] {
+        launches_ += launch_commit(d_, stream_);
+        reset_lm_status();
+        launches_ += launch_linearize(d_, sm_, false, stream_, nullptr);
+      },
+      lm_graph_lin_, graph_lin_launches_);
+  const bool b = a && capture(
+                          [&] {
+                            SolveInfo info;
+                            solve_direct(*lam_host_, cfg, info);  // deferred: no synchronisation inside
+                            reset_lm_status(true);
+                            launches_ += launch_trial(d_, sm_, stream_, nullptr);
+                            ck(cudaMemcpyAsync(lm_host_, d_.lm, sizeof(LmDev), cudaMemcpyDeviceToHost, stream_),
+                               "D2H lm");
+                          },
+                          lm_graph_solve_, graph_solve_launches_);
+  if (!b) {
+    if (lm_graph_lin_) cudaGraphExecDestroy(lm_graph_lin_);
+    if (lm_graph_solve_) cudaGraphExecDestroy(lm_graph_solve_);
+    lm_graph_lin_ = lm_graph_solve_ = nullptr;
+    lm_graph_failed_ = true;
+    return false;
+  }
+  graph_clo_ = cfg.clamp_min;
+  graph_chi_ = cfg.clamp_max;
+  return true;
 }
 
 // Damped solve for one lambda with the configured solver; returns false when
@@ -1141,32 +1216,53 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   // Direct solves leave the factorisation's failure word and the next
   // linearisation's cost / gradient in flight: the trial's read-back is the
   // one host synchronisation of an LM iteration (a failed factorisation
-  // rejects the step as before; its trial result is ignored).
+  // rejects the step as before; its trial result is ignored). On a single
+  // rank the iteration runs as captured graphs (build_lm_graphs), the commit
+  // of an accepted trial riding with the next linearisation.
   defer_factor_check_ = cfg.solver == BAE_SOLVER_CHOLESKY;
   struct DeferReset {
     bool& f;
     ~DeferReset() { f = false; }
   } defer_reset{defer_factor_check_};
-  bool lin_pending = false;
+  const char* lg = std::getenv("BAE_LM_GRAPH");
+  const bool graphs = defer_factor_check_ && use_tiles_ && !comm_ && !std::getenv("BAE_CHOL_TRACE") &&
+                      !(lg && lg[0] == '0') && build_lm_graphs(cfg);
+  bool lin_pending = false, commit_pending = false;
   while (iterations < cfg.max_iterations) {
     const double lambda_used = lambda;
     const bool saturated = lambda >= cfg.damping_max;
-    if (need_lin) {
-      if (defer_factor_check_) {
-        linearize_async();
-        lin_pending = true;
-      } else {
-        linearize();
-        grad = std::sqrt(lm_host_->grad_sq);
-      }
-      need_lin = false;
-    }
     SolveInfo info;
-    bool ok = solve(lambda_used, cfg, info);
+    bool ok = true;
+    if (graphs) {
+      if (need_lin) {  // commit of the accepted trial + the next linearisation
+        ck(cudaGraphLaunch(lm_graph_lin_, stream_), "graph launch");
+        launches_ += graph_lin_launches_;
+        commit_pending = false;
+        lin_pending = true;
+        need_lin = false;
+      }
+      *lam_host_ = lambda_used;
+      ck(cudaGraphLaunch(lm_graph_solve_, stream_), "graph launch");
+      launches_ += graph_solve_launches_;
+      sync();
+      info.pending = true;
+    } else {
+      if (need_lin) {
+        if (defer_factor_check_) {
+          linearize_async();
+          lin_pending = true;
+        } else {
+          linearize();
+          grad = std::sqrt(lm_host_->grad_sq);
+        }
+        need_lin = false;
+      }
+      ok = solve(lambda_used, cfg, info);
+    }
     total_pcg += info.iters;
     bool accepted = false;
     double trial_cost = std::numeric_limits<double>::quiet_NaN();
-    if (ok || lin_pending) {
+    if (!graphs && (ok || lin_pending)) {
       if (ok) {
         reset_lm_status(lin_pending);
         phase_begin(kPhTrial);
@@ -1175,20 +1271,24 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
       }
       read_lm();
       phase_collect();
-      if (lin_pending) {
-        lin_pending = false;
-        if (lm_host_->err_obs != INT_MAX) throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
-        grad = std::sqrt(lm_host_->grad_sq);
-      }
-      if (info.pending && (*host_info_ != 0 || pcg_host_->not_spd)) ok = false;  // NotSpdError (cholesky.hpp:229)
     }
+    if (lin_pending) {
+      lin_pending = false;
+      if (lm_host_->err_obs != INT_MAX) throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
+      grad = std::sqrt(lm_host_->grad_sq);
+    }
+    if (info.pending && (*host_info_ != 0 || pcg_host_->not_spd)) ok = false;  // NotSpdError (cholesky.hpp:229)
     if (ok) {
       trial_cost = (lm_host_->retract_bad || lm_host_->trial_bad) ? std::numeric_limits<double>::infinity()
                                                                    : lm_host_->new_cost;
       if (trial_cost < cost) {
-        phase_begin(kPhCommit);
-        launches_ += launch_commit(d_, stream_);
-        phase_end();
+        if (graphs) {
+          commit_pending = true;  // with the next linearisation (G_lin), or after the loop
+        } else {
+          phase_begin(kPhCommit);
+          launches_ += launch_commit(d_, stream_);
+          phase_end();
+        }
         cost = trial_cost;
         history.push_back(cost);
         ++accepted_steps;
@@ -1216,6 +1316,7 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
       break;
     }
   }
+  if (commit_pending) launches_ += launch_commit(d_, stream_);  // the last accepted trial
   ck(cudaEventRecord(ev1, stream_), "event record");
   sync();
   phase_collect();

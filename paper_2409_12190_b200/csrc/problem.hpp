@@ -87,6 +87,7 @@ class Problem {
   void sync();
   void ensure_point_staging();
   void linearize_async();
+  bool build_lm_graphs(const bae_lm_config& cfg);
   void reset_lm_status(bool keep_err = false);
   void read_lm();
   void linearize();
@@ -127,6 +128,11 @@ class Problem {
   double* pts_user_ = nullptr;               // single rank: caller-ordered points (device staging)
   LmDev* lm_reset_host_ = nullptr;           // pinned template of the per-evaluation LM flags
   double* lam_host_ = nullptr;               // pinned: the damping of the next direct solve
+  bool capturing_ = false;                   // stream capture in progress: no phase events
+  cudaGraphExec_t lm_graph_solve_ = nullptr, lm_graph_lin_ = nullptr;  // build_lm_graphs
+  long long graph_solve_launches_ = 0, graph_lin_launches_ = 0;
+  double graph_clo_ = 0.0, graph_chi_ = 0.0;
+  bool lm_graph_failed_ = false;
   bool defer_factor_check_ = false;          // optimize: the direct factorisation's failure word read later
   Plan plan_;
   Dev d_{};
