@@ -70,10 +70,13 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # the timed region is tens of ms: start it once the sampler is running
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
         return self
@@ -84,6 +87,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.03)  # the sample that covers the end of the region
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
