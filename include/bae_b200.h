@@ -315,8 +315,9 @@ int bae_partition_points(int32_t num_cameras, int32_t num_points, const int32_t*
  * reductions), 1 = one implicit Schur S*x product (one PCG iteration's
  * operator), 2 = one full PCG iteration, 3 = fused residual+Jacobian to HBM
  * (stored J), 4 = tile-sparse Cholesky factorisation + forward/backward
- * substitution of the reduced camera system (direct solver). ms receives the
- * mean milliseconds per launch. */
+ * substitution of the reduced camera system (direct solver), 5 = the direct
+ * solver's prep (damped point blocks, V = W L^-T, right-hand side), 6 = its
+ * Schur assembly. ms receives the mean milliseconds per launch. */
 int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms);
 /* Number of kernel launches issued by this handle since creation. */
 int64_t bae_launch_count(const bae_problem* p);
@@ -330,6 +331,9 @@ int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32
 /* Direct solver structure (after its first use): [tile columns, stored
  * 48x48 tiles, tile updates, nested-dissection groups, camera positions]. */
 int bae_direct_stats(const bae_problem* p, int64_t* out5);
+/* Schur assembly size (after the direct solver's first use): the (k, l)
+ * observation pairs and the 6x6 camera blocks they sum into. */
+int bae_direct_pairs(const bae_problem* p, int64_t* pairs, int64_t* blocks);
 /* Static sizes the roofline arithmetic needs: [N, P, C, tiles, tile-camera
  * entries, max obs per tile]. */
 int bae_problem_stats(const bae_problem* p, int64_t* out6);

@@ -117,6 +117,7 @@ SIGNATURES = {
     "bae_time_kernel": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, c_double_p]),
     "bae_launch_count": (ctypes.c_int64, [ctypes.c_void_p]),
     "bae_phase_times": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int32]),
+    "bae_direct_pairs": (ctypes.c_int, [ctypes.c_void_p, c_int64_p, c_int64_p]),
     "bae_problem_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
     "bae_problem_shard": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p]),
     "bae_direct_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),

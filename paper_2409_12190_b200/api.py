@@ -324,7 +324,11 @@ class TracedProblem:
         out = np.zeros(5, np.int64)
         _check(_lib.load().bae_direct_stats(self._h, ptr(out, ctypes.c_int64)))
         keys = ("tile_columns", "tiles", "tile_updates", "nd_groups", "positions")
-        return dict(zip(keys, (int(v) for v in out)))
+        st = dict(zip(keys, (int(v) for v in out)))
+        npairs, nblocks = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.load().bae_direct_pairs(self._h, ctypes.byref(npairs), ctypes.byref(nblocks)))
+        st.update(pairs=int(npairs.value), camera_blocks=int(nblocks.value))
+        return st
 
     def stats(self):
         out = np.empty(6, np.int64)

@@ -356,6 +356,13 @@ int bae_direct_stats(const bae_problem* p, int64_t* out5) {
   });
 }
 
+int bae_direct_pairs(const bae_problem* p, int64_t* pairs, int64_t* blocks) {
+  return guarded([&] {
+    if (pairs) *pairs = ba(p)->direct_pairs();
+    if (blocks) *blocks = ba(p)->direct_blocks();
+  });
+}
+
 int bae_problem_stats(const bae_problem* p, int64_t* out6) {
   return guarded([&] {
     const bae::Plan& pl = ba(p)->plan();

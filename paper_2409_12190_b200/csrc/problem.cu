@@ -794,6 +794,7 @@ void Problem::build_direct() {
       const long long np = count_pairs(d_, off, stream_);
       if (np >= (1LL << 31) - 1) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
       int2* pairs = dalloc<int2>(static_cast<std::size_t>(std::max(np, 1LL)));
+      npairs_ = np;
       build_pairs(d_, off, np, pairs, bcam, bptr, stream_);
       d_.pairs = pairs;
     } catch (...) {
@@ -1357,13 +1358,13 @@ double Problem::time_kernel(int kind, int reps) {
     s.tol = 0.0;
     ck(cudaMemcpy(d_.pcg, &s, sizeof(PcgDev), cudaMemcpyHostToDevice), "H2D pcg");
   }
-  if (kind == 4) {  // one damped direct solve first: S assembled, plan built
+  if (kind == 4 || kind == 5 || kind == 6) {  // one damped direct solve first: S assembled, plan built
     linearize();
     SolveInfo info;
     bae_lm_config c2 = cfg;
     c2.solver = BAE_SOLVER_CHOLESKY;
     solve(1e-4, c2, info);
-    if (!use_tiles_) throw Error(BAE_ERR_UNSUPPORTED, "time_kernel 4 needs the tile solver");
+    if (!use_tiles_) throw Error(BAE_ERR_UNSUPPORTED, "time_kernel 4..6 need the tile solver");
   }
   double* js = nullptr;
   if (kind == 3) {
@@ -1386,6 +1387,12 @@ double Problem::time_kernel(int kind, int reps) {
         break;
       case 4:  // tile Cholesky factor + both substitutions (re-factors the factor: same work)
         launches_ += launch_tile_chol(tchol_, chol_grid_, stream_);
+        break;
+      case 5:  // direct prep: damped point blocks, V = W L^-T, Schur right-hand side
+        launches_ += launch_prep(d_, sm_, 1e-4, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, nullptr, true);
+        break;
+      case 6:  // Schur assembly of the reduced camera matrix into its tiles
+        launches_ += launch_schur_dense(d_, stream_, nullptr);
         break;
       default:
         throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");

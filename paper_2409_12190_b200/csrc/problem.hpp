@@ -71,6 +71,8 @@ class Problem {
                 std::vector<bae_iter_record>& traj, bae_lm_report& rep);
   double time_kernel(int kind, int reps);
   // [tile columns, stored tiles, tile updates, ordering groups, positions] of the tile Cholesky (0 before use)
+  long long direct_pairs() const { return npairs_; }
+  long long direct_blocks() const { return d_.nblk; }
   void direct_stats(long long* out5) const {
     out5[0] = tchol_.nt;
     out5[1] = tchol_.nnz;
@@ -133,6 +135,7 @@ class Problem {
   long long graph_solve_launches_ = 0, graph_lin_launches_ = 0;
   double graph_clo_ = 0.0, graph_chi_ = 0.0;
   bool lm_graph_failed_ = false;
+  long long npairs_ = 0;                     // direct solver: (k, l) pairs of the Schur assembly
   bool defer_factor_check_ = false;          // optimize: the direct factorisation's failure word read later
   Plan plan_;
   Dev d_{};
