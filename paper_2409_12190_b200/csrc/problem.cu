@@ -805,15 +805,21 @@ void Problem::build_direct() {
   }
   d_.blk_ptr = upload(bptr);
   d_.blk_cam = upload(bcam);
-  {  // diagonal blocks first (the heaviest: every observation of the camera),
-     // then the rest row by row: a CTA's warps get blocks of similar length
-     // and neighbouring rows, which keeps the V_k they share in L2
+  {  // blocks row by row (c1 ascending, c2 ascending): the chunks below keep
+     // the long diagonal blocks from stalling a CTA, and the blocks in flight
+     // share the V of a few hundred neighbouring cameras, which stays in L2
+     // (BAE_SCHUR_ORDER=diagfirst: the diagonal blocks first)
     std::vector<int> ord;
     ord.reserve(bcam.size());
-    for (std::size_t b = 0; b < bcam.size(); ++b)
-      if (bcam[b].x == bcam[b].y) ord.push_back(static_cast<int>(b));
-    for (std::size_t b = 0; b < bcam.size(); ++b)
-      if (bcam[b].x != bcam[b].y) ord.push_back(static_cast<int>(b));
+    const char* so = std::getenv("BAE_SCHUR_ORDER");
+    if (so && std::string(so) == "diagfirst") {
+      for (std::size_t b = 0; b < bcam.size(); ++b)
+        if (bcam[b].x == bcam[b].y) ord.push_back(static_cast<int>(b));
+      for (std::size_t b = 0; b < bcam.size(); ++b)
+        if (bcam[b].x != bcam[b].y) ord.push_back(static_cast<int>(b));
+    } else {
+      for (std::size_t b = 0; b < bcam.size(); ++b) ord.push_back(static_cast<int>(b));
+    }
     d_.blk_ord = upload(ord);
     // work chunks in that block order: about 32 warps' worth per SM, at
     // least kSchurChunk pairs each (short blocks stay whole, long ones split)
