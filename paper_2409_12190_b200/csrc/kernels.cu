@@ -595,6 +595,7 @@ __global__ void k_finish_cost(Dev d, int trial) {
 // RHS), and W, W H~_pp^-1 of every slot kept for the assembly of S.
 // ---------------------------------------------------------------------------
 constexpr WsDims kPrepWs{16, 12, 27, 0};
+constexpr int kVStride = 20;  // doubles per V = W L^-T record (two 16-byte aligned halves of 9)
 constexpr WsDims kPrepDirWs{16, 12, 6, 0};
 
 template <bool kShared, bool kDirect>
@@ -685,16 +686,21 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
           st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
     } else {  // direct solver: keep V = W L^-T (V V^T = W H~^-1 W^T) of this slot
       const double* lf = sp + 3;
-      double* vo = d.wstore + (long long)(g.ob + s) * 18;
+      double vv[kVStride];  // rows 0..2 at [0, 9), rows 3..5 at [10, 19): 16-byte aligned halves
 #pragma unroll
       for (int a = 0; a < 6; ++a) {
         const double v0 = W[a * 3] * lf[0];
         const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
         const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
-        vo[a * 3] = v0;
-        vo[a * 3 + 1] = v1;
-        vo[a * 3 + 2] = v2;
+        const int o = a * 3 + (a >= 3 ? 1 : 0);
+        vv[o] = v0;
+        vv[o + 1] = v1;
+        vv[o + 2] = v2;
       }
+      vv[9] = vv[19] = 0.0;  // whole sectors written
+      double2* vo = reinterpret_cast<double2*>(d.wstore + (long long)(g.ob + s) * kVStride);
+#pragma unroll
+      for (int j = 0; j < kVStride / 2; ++j) vo[j] = make_double2(vv[2 * j], vv[2 * j + 1]);
     }
     const double* vp = sp + 9;
 #pragma unroll
@@ -860,14 +866,21 @@ __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
 #pragma unroll 2
   for (int q = ch.y + slot; q < qe; q += 8) {
     const int2 pr = d.pairs[q];
-    const double* wh = d.wstore + (long long)pr.x * 18 + 3 * r0;  // V_k rows r0..r0+2
-    const double* w = d.wstore + (long long)pr.y * 18 + 3 * c0;   // V_l rows c0..c0+2
+    // V_k rows r0..r0+2 and V_l rows c0..c0+2: 16-byte aligned 9-double halves
+    const double* wh = d.wstore + (long long)pr.x * kVStride + (r0 ? 10 : 0);
+    const double* w = d.wstore + (long long)pr.y * kVStride + (c0 ? 10 : 0);
     double a[9], b[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) {
-      a[j] = wh[j];
-      b[j] = w[j];
+    for (int j = 0; j < 4; ++j) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(wh) + j);
+      const double2 y = __ldg(reinterpret_cast<const double2*>(w) + j);
+      a[2 * j] = x.x;
+      a[2 * j + 1] = x.y;
+      b[2 * j] = y.x;
+      b[2 * j + 1] = y.y;
     }
+    a[8] = __ldg(wh + 8);
+    b[8] = __ldg(w + 8);
 #pragma unroll
     for (int x = 0; x < 3; ++x)
 #pragma unroll
