@@ -298,28 +298,33 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
   }
   if (bad != INT_MAX) atomicMin(&d.lm->err_obs, bad);
   __syncwarp();
-  // camera side: (entry, component) tasks over the H_cc upper triangle + g_c
-  for (int idx = lane; idx < g.ncam * 27; idx += 32) {
-    const int e = idx / 27, j = idx - e * 27;
-    int a, b;
-    if (j < 21) {  // row-major upper-triangle index -> (a, b)
+  // camera side: lane j < 27 owns component j (the H_cc upper triangle
+  // row-major, then g_c) of every entry; the warp walks the entries together
+  // (no per-lane trip counts, no index decoding). Per component:
+  // st[a] st[b0] + st[6 + a] st[b1] over the entry's observations in order.
+  {
+    const int j = min(lane, 26);
+    int a = j - 21, b0 = 18, b1 = 19;  // g_c: J_c^T r
+    if (j < 21) {
       a = 0;
       int rem = j;
-      while (rem >= 6 - a) {
-        rem -= 6 - a;
-        ++a;
+#pragma unroll
+      for (int r = 0; r < 5; ++r)
+        if (rem >= 6 - a) {
+          rem -= 6 - a;
+          ++a;
+        }
+      b0 = a + rem;
+      b1 = 6 + b0;
+    }
+    for (int e = 0; e < g.ncam; ++e) {
+      double acc = 0.0;
+      for (int q = ws.ent[e]; q < ws.ent[e + 1]; ++q) {
+        const double* st = ws.stage + q * 20;
+        acc += st[a] * st[b0] + st[6 + a] * st[b1];
       }
-      b = a + rem;
-    } else {
-      a = j - 21;
-      b = -1;
+      if (lane < 27) d.partial[(long long)(g.eb + e) * 27 + lane] = acc;
     }
-    double acc = 0.0;
-    for (int q = ws.ent[e]; q < ws.ent[e + 1]; ++q) {
-      const double* st = ws.stage + q * 20;
-      acc += b >= 0 ? st[a] * st[b] + st[6 + a] * st[6 + b] : st[a] * st[18] + st[6 + a] * st[19];
-    }
-    d.partial[(long long)(g.eb + e) * 27 + j] = acc;
   }
   // point side: H_pp (6) and g_p (3) per point, observations in id order
   double gsq = 0.0;
