@@ -826,7 +826,9 @@ void Problem::build_direct() {
     const long long np = bptr.back();
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, opt_.device);
-    const int U = static_cast<int>(std::clamp<long long>(np / (32LL * nsm) / 8 * 8, kSchurChunk, 8 * kSchurChunk));
+    int ucap = 8 * kSchurChunk;
+    if (const char* e = std::getenv("BAE_SCHUR_CHUNK_CAP")) ucap = std::max(kSchurChunk, std::atoi(e));
+    const int U = static_cast<int>(std::clamp<long long>(np / (32LL * nsm) / 8 * 8, kSchurChunk, ucap));
     std::vector<int4> chunks;
     std::vector<int> nch(bcam.size(), 0);
     for (int b : ord) {
