@@ -317,13 +317,19 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
       b0 = a + rem;
       b1 = 6 + b0;
     }
+    int qb = ws.ent[0];
     for (int e = 0; e < g.ncam; ++e) {
-      double acc = 0.0;
-      for (int q = ws.ent[e]; q < ws.ent[e + 1]; ++q) {
-        const double* st = ws.stage + q * 20;
-        acc += st[a] * st[b0] + st[6 + a] * st[b1];
+      const int qe = ws.ent[e + 1];
+      const double* st = ws.stage + qb * 20;
+      double acc0 = 0.0, acc1 = 0.0;  // two interleaved partial sums, slot order
+      int q = qb;
+      for (; q + 1 < qe; q += 2, st += 40) {
+        acc0 += st[a] * st[b0] + st[6 + a] * st[b1];
+        acc1 += st[20 + a] * st[20 + b0] + st[26 + a] * st[20 + b1];
       }
-      if (lane < 27) d.partial[(long long)(g.eb + e) * 27 + lane] = acc;
+      if (q < qe) acc0 += st[a] * st[b0] + st[6 + a] * st[b1];
+      if (lane < 27) d.partial[(long long)(g.eb + e) * 27 + lane] = acc0 + acc1;
+      qb = qe;
     }
   }
   // point side: H_pp (6) and g_p (3) per point, observations in id order
