@@ -122,8 +122,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Batched warp copy global -> workspace: each lane issues kBatch independent,
-// unconditional loads (indices clamped into range) before its first store.
+// Batched warp copy global -> workspace: each lane issues up to kBatch
+// independent loads before its first store; loads past the end are
+// predicated off (no duplicate requests for short arrays).
 // `addr(i)` returns the source address of element i.
 constexpr int kBatch = 8;
 template <class T, class Addr, class Store>
@@ -131,7 +132,8 @@ __device__ __forceinline__ void warp_copy(int n, Addr addr, Store store) {
   for (int base = lane_id(); base < n; base += kBatch * 32) {
     T v[kBatch];
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) v[b] = *addr(min(base + b * 32, n - 1));
+    for (int b = 0; b < kBatch; ++b)
+      if (base + b * 32 < n) v[b] = *addr(base + b * 32);
 #pragma unroll
     for (int b = 0; b < kBatch; ++b)
       if (base + b * 32 < n) store(base + b * 32, v[b]);
