@@ -270,3 +270,23 @@ def test_duplicates_lm_trajectory(oracle):
             break
         assert a.accepted == b["accepted"]
     assert abs(rep.final_cost - oref["final_cost"]) <= 1e-6 * oref["final_cost"]
+
+
+def test_graph_replayed_iterations_match_plain_launches(monkeypatch):
+    """The direct path's LM iterations replayed from captured CUDA graphs
+    (damping from pinned memory, tile-Cholesky epoch on the device) give the
+    same trajectory, bit for bit, as plain launches (BAE_LM_GRAPH=0)."""
+    s = _scene(C=40, P=800, N=4000, seed=31)
+    cfg = bae.LmConfig(max_iterations=12)
+    runs = []
+    for graph in ("1", "0"):
+        monkeypatch.setenv("BAE_LM_GRAPH", graph)
+        gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+        rep = bae.optimize(gpu, s.poses, s.points, cfg)
+        rep2 = bae.optimize(gpu, s.poses, s.points, cfg)  # replays the same graphs again
+        runs.append((rep, rep2, gpu.get_parameters()))
+    (a, a2, pa), (b, b2, pb) = runs
+    for x, y in ((a, b), (a2, b2), (a, a2)):
+        assert [(r.cost, r.lmbda, r.accepted) for r in x.trajectory] == \
+               [(r.cost, r.lmbda, r.accepted) for r in y.trajectory]
+    assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
