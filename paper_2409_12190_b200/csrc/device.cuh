@@ -79,6 +79,7 @@ struct Dev {
   double* p;
   double* y;
   double* partial;    // E * 27
+  double* partial6;   // E * 6: Schur RHS pieces of the fused linearisation + prep
   double* tile_red;   // T * 2
   // Sharded runs: per-rank camera-sized partial sums that the
   // communicator sums in place between a tile pass and its camera pass;

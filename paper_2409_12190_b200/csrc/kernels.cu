@@ -240,6 +240,71 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
   o[15] = intr[c * 4 + 3];
 }
 
+constexpr int kVStride = 20;  // doubles per V = W L^-T record (two 16-byte aligned halves of 9)
+// Direct solver, per point: damped H~_pp, its inverse (d.hinv, for the
+// back-substitution), its Cholesky factor L (1/l00, l10, l20, 1/l11, l21,
+// 1/l22) into sp[3..8] and v = H~_pp^-1 g_p into sp[9..11]. h: the packed
+// H_pp (6), g: g_p (3). Returns false when the damped block is not SPD.
+__device__ __forceinline__ bool prep_point_direct(const Dev& d, long long ip, double (&h)[6], const double* g,
+                                                  double lambda, double clo, double chi, double* sp) {
+  double inv[9];
+  h[0] = damp_diag(h[0], lambda, clo, chi);
+  h[3] = damp_diag(h[3], lambda, clo, chi);
+  h[5] = damp_diag(h[5], lambda, clo, chi);
+  const bool pfail = !spd_inverse<3>(h, inv);
+  if (pfail) {
+#pragma unroll
+    for (int j = 0; j < 9; ++j) inv[j] = 0.0;
+  }
+  const double hi[6] = {inv[0], inv[1], inv[2], inv[4], inv[5], inv[8]};
+#pragma unroll
+  for (int j = 0; j < 6; ++j) d.hinv[ip * 6 + j] = hi[j];
+  double lf[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (!pfail) {
+    const double l00 = sqrt(h[0]), l10 = h[1] / l00, l20 = h[2] / l00;
+    const double l11 = sqrt(h[3] - l10 * l10), l21 = (h[4] - l20 * l10) / l11;
+    const double l22 = sqrt(h[5] - l20 * l20 - l21 * l21);
+    lf[0] = 1.0 / l00;
+    lf[1] = l10;
+    lf[2] = l20;
+    lf[3] = 1.0 / l11;
+    lf[4] = l21;
+    lf[5] = 1.0 / l22;
+  }
+#pragma unroll
+  for (int j = 0; j < 6; ++j) sp[3 + j] = lf[j];
+  sp[9] = inv[0] * g[0] + inv[1] * g[1] + inv[2] * g[2];
+  sp[10] = inv[3] * g[0] + inv[4] * g[1] + inv[5] * g[2];
+  sp[11] = inv[6] * g[0] + inv[7] * g[1] + inv[8] * g[2];
+  return !pfail;
+}
+
+// Direct solver, per observation slot: V = W L^-T (V V^T = W H~^-1 W^T)
+// stored as two 16-byte aligned halves, and the Schur right-hand side piece
+// W v into rhs[0..5].
+__device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, const double (&W)[18],
+                                                const double* sp, double* rhs) {
+  const double* lf = sp + 3;
+  double vv[kVStride];  // rows 0..2 at [0, 9), rows 3..5 at [10, 19)
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    const double v0 = W[a * 3] * lf[0];
+    const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
+    const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
+    const int o = a * 3 + (a >= 3 ? 1 : 0);
+    vv[o] = v0;
+    vv[o + 1] = v1;
+    vv[o + 2] = v2;
+  }
+  vv[9] = vv[19] = 0.0;  // whole sectors written
+  double2* vo = reinterpret_cast<double2*>(d.wstore + slot * kVStride);
+#pragma unroll
+  for (int j = 0; j < kVStride / 2; ++j) vo[j] = make_double2(vv[2 * j], vv[2 * j + 1]);
+  const double* vp = sp + 9;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) rhs[a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
+}
+
 // ---------------------------------------------------------------------------
 // K1: fused residual + Jacobian + block reductions (the linearisation).
 // Replaces evaluate + sparse_jacobian + the CC/LL SpGEMM quadrants and the
@@ -252,25 +317,34 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
 // cam: [t3 q4 k4 R9] (20) ; pt: p3 ; stage: Jc12 Jp6 r2 (20)
 // ---------------------------------------------------------------------------
 constexpr WsDims kLinWs{20, 3, 20, 0};
+// fused with the direct prep: camera + t3 of the record, point p3 L6 v3
+constexpr WsDims kLinPrepWs{23, 12, 20, 0};
 
-template <bool kShared>
+// kPrep: the direct solver's prep fused in (accepted LM steps: linearise and
+// damp in one pass over the tile's data): the point side goes on to the
+// damped point block and its factor, each observation to V and its
+// right-hand side piece (entries into d.partial6). W comes from the camera
+// record's R, t exactly as k_prep forms it, so the fused and the separate
+// prep agree bit for bit.
+template <bool kShared, bool kPrep = false>
 __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t,
-                                         int write_jac) {
-  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kLinWs, g.ncam, g.npts, g.nobs);
+                                         int write_jac, double clo = 0.0, double chi = 0.0) {
+  constexpr int kPtw = kPrep ? 12 : 3, kCw = kPrep ? 23 : 20;
+  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kPrep ? kLinPrepWs : kLinWs, g.ncam, g.npts, g.nobs);
   const int lane = lane_id();
-  load_point_fields<3>(ws, 3, 0, d.pts, g.pb, g.npts);
+  load_point_fields<3>(ws, kPtw, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
   __syncwarp();
-  load_cam_fields<7>(ws, g.ncam, 20, 0, d.pose, 7);
-  load_cam_fields<4>(ws, g.ncam, 20, 7, d.intr, 4);
-  load_cam_fields<9>(ws, g.ncam, 20, 11, d.camrec, kCamRec);
+  load_cam_fields<7>(ws, g.ncam, kCw, 0, d.pose, 7);
+  load_cam_fields<4>(ws, g.ncam, kCw, 7, d.intr, 4);
+  load_cam_fields<kPrep ? 12 : 9>(ws, g.ncam, kCw, 11, d.camrec, kCamRec);
   __syncwarp();
   double cost = 0.0;
   int bad = INT_MAX;
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
-    const double* cam = ws.cam + (lcpt & 0xffff) * 20;
-    const double* pt = ws.pt + (lcpt >> 16) * 3;
+    const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
+    const double* pt = ws.pt + (lcpt >> 16) * kPtw;
     const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
     double* st = ws.stage + s * 20;
     double r0 = 0.0, r1 = 0.0;
@@ -336,6 +410,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
   }
   // point side: H_pp (6) and g_p (3) per point, observations in id order
   double gsq = 0.0;
+  int pfail = 0;
   for (int lp = lane; lp < g.npts; lp += 32) {
     double h[9];
 #pragma unroll
@@ -357,6 +432,10 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
 #pragma unroll
     for (int j = 0; j < 3; ++j) d.gp[ip * 3 + j] = h[6 + j];
     gsq += h[6] * h[6] + h[7] * h[7] + h[8] * h[8];
+    if (kPrep) {
+      double h6[6] = {h[0], h[1], h[2], h[3], h[4], h[5]};
+      if (!prep_point_direct(d, ip, h6, h + 6, *d.lam, clo, chi, ws.pt + lp * kPtw)) pfail = 1;
+    }
   }
   cost = warp_sum(cost);
   gsq = warp_sum(gsq);
@@ -364,7 +443,48 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     d.tile_red[t * 2] = cost;
     d.tile_red[t * 2 + 1] = gsq;
   }
+  if (kPrep) {
+    if (pfail) atomicExch(&d.pcg->not_spd, 1);
+    __syncwarp();
+    for (int s = lane; s < g.nobs; s += 32) {  // V and the right-hand side pieces
+      const std::uint32_t lcpt = ws.lcpt[s];
+      const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
+      const double* R = cam + 11;  // record R9 t3; intrinsics at cam + 7
+      const double* sp = ws.pt + (lcpt >> 16) * kPtw;
+      P3 y;
+      y.x = R[0] * sp[0] + R[1] * sp[1] + R[2] * sp[2] + R[9];
+      y.y = R[3] * sp[0] + R[4] * sp[1] + R[5] * sp[2] + R[10];
+      y.z = R[6] * sp[0] + R[7] * sp[1] + R[8] * sp[2] + R[11];
+      double D[6], Jc[12], Jp[6];
+      cam_dproj(d.pinhole, y, cam + 7, D);
+      jac_cam(D, y, Jc);
+      jac_pt(D, R, Jp);
+      double W[18];
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) W[a * 3 + j] = Jc[a] * Jp[j] + Jc[6 + a] * Jp[3 + j];
+      double rhs[6];
+      prep_obs_direct(d, g.ob + s, W, sp, rhs);
+      double* st = ws.stage + s * 20;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) st[a] = rhs[a];
+    }
+    __syncwarp();
+    entries_from_stage<6, 20>(ws, g.ncam, g.eb, d.partial6);
+  }
   __syncwarp();
+}
+
+__global__ void __launch_bounds__(256) k_lin_prep(Dev d, int slice, double clo, double chi) {
+  extern __shared__ __align__(16) char smem[];
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= d.T) return;
+  const TileGeom g = tile_geom(d, t);
+  if (g.big >= 0)
+    lin_tile<false, true>(d, g, smem, slice, t, 0, clo, chi);
+  else
+    lin_tile<true, true>(d, g, smem, slice, t, 0, clo, chi);
 }
 
 __global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_jac) {
@@ -443,26 +563,29 @@ __device__ __forceinline__ void warp_entry_sum(const Dev& d, int c, double (&acc
 // block) takes the camera's entries s, s + S, s + 2S, ... with four loads in
 // flight per lane and coalesced W-double rows; the S slot sums are then added
 // in slot order. out[0..W) (shared) is valid after the call.
+// NT is the summation layout's thread count: a larger block runs it with its
+// first NT threads (same order, same bits) and joins the barriers.
 template <int W, int NT>
-__device__ __forceinline__ void block_entry_sum(const Dev& d, int c, double* red, double* out) {
+__device__ __forceinline__ void block_entry_sum(const Dev& d, int c, double* red, double* out,
+                                                const double* __restrict__ src) {
   constexpr int G = 32 / W, S = G * (NT / 32);
   const int lane = lane_id(), warp = threadIdx.x >> 5;
   const int slot = warp * G + lane / W, j = lane % W;
-  const bool active = lane < G * W;
+  const bool active = lane < G * W && threadIdx.x < NT;
   const int e = d.cam_ent_ptr[c + 1];
   double acc = 0.0;
   if (active) {
     int q = d.cam_ent_ptr[c] + slot;
     for (; q + 3 * S < e; q += 4 * S) {
       const int e0 = d.cam_ent[q], e1 = d.cam_ent[q + S], e2 = d.cam_ent[q + 2 * S], e3 = d.cam_ent[q + 3 * S];
-      const double v0 = d.partial[(long long)e0 * W + j], v1 = d.partial[(long long)e1 * W + j];
-      const double v2 = d.partial[(long long)e2 * W + j], v3 = d.partial[(long long)e3 * W + j];
+      const double v0 = src[(long long)e0 * W + j], v1 = src[(long long)e1 * W + j];
+      const double v2 = src[(long long)e2 * W + j], v3 = src[(long long)e3 * W + j];
       acc += v0;
       acc += v1;
       acc += v2;
       acc += v3;
     }
-    for (; q < e; q += S) acc += d.partial[(long long)d.cam_ent[q] * W + j];
+    for (; q < e; q += S) acc += src[(long long)d.cam_ent[q] * W + j];
     red[slot * W + j] = acc;
   }
   __syncthreads();
@@ -482,7 +605,7 @@ __device__ __forceinline__ void cam_block_acc(const Dev& d, int c, double* red, 
     if (threadIdx.x < W) out[threadIdx.x] = d.cred[(long long)c * W + threadIdx.x];
     __syncthreads();
   } else {
-    block_entry_sum<W, NT>(d, c, red, out);
+    block_entry_sum<W, NT>(d, c, red, out, d.partial);
   }
 }
 
@@ -517,7 +640,7 @@ __global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg
     return;
   }
   const int c = blockIdx.x;
-  block_entry_sum<W, NT>(d, c, red, acc);
+  block_entry_sum<W, NT>(d, c, red, acc, d.partial);
   if (threadIdx.x < W) d.cred[(long long)c * W + threadIdx.x] = acc[threadIdx.x];
 }
 
@@ -532,6 +655,38 @@ __global__ void __launch_bounds__(256) k_cam_linearize(Dev d) {
   if (t < 21) d.hcc[(long long)c * 21 + t] = acc[t];
   else if (t < 27) d.gc[(long long)c * 6 + (t - 21)] = acc[t];
   if (t == 0) {
+    double gsq = 0.0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) gsq += acc[21 + j] * acc[21 + j];
+    d.cam_dot[c] = gsq;
+  }
+}
+
+// Camera side of the fused linearisation + direct prep (block per camera,
+// single rank): k_cam_linearize's H_cc, g_c, |g_c|^2 and
+// k_cam_prep_direct's damped H~_cc and Schur RHS, with the same summation
+// orders as those two kernels.
+__global__ void __launch_bounds__(256) k_cam_lin_prep(Dev d, double clo, double chi) {
+  __shared__ double red[8 * 27];
+  __shared__ double acc[27];
+  __shared__ double acc6[6];
+  const int c = blockIdx.x;
+  block_entry_sum<27, 256>(d, c, red, acc, d.partial);
+  block_entry_sum<6, 128>(d, c, red, acc6, d.partial6);
+  const int t = threadIdx.x;
+  if (t < 21) {
+    double h = acc[t];
+    d.hcc[(long long)c * 21 + t] = h;
+    if (t == sym6(0, 0) || t == sym6(1, 1) || t == sym6(2, 2) || t == sym6(3, 3) || t == sym6(4, 4) ||
+        t == sym6(5, 5))
+      h = damp_diag(h, *d.lam, clo, chi);
+    d.hccd[(long long)c * 21 + t] = h;
+  } else if (t < 27) {
+    d.gc[(long long)c * 6 + (t - 21)] = acc[t];
+  } else if (t >= 32 && t < 38) {
+    const int a = t - 32;
+    d.rhs[(long long)c * 6 + a] = -acc[21 + a] + acc6[a];
+  } else if (t == 64) {
     double gsq = 0.0;
 #pragma unroll
     for (int j = 0; j < 6; ++j) gsq += acc[21 + j] * acc[21 + j];
@@ -608,7 +763,6 @@ __global__ void k_finish_cost(Dev d, int trial) {
 // RHS), and W, W H~_pp^-1 of every slot kept for the assembly of S.
 // ---------------------------------------------------------------------------
 constexpr WsDims kPrepWs{16, 12, 27, 0};
-constexpr int kVStride = 20;  // doubles per V = W L^-T record (two 16-byte aligned halves of 9)
 constexpr WsDims kPrepDirWs{16, 12, 6, 0};
 
 template <bool kShared, bool kDirect>
@@ -1790,6 +1944,8 @@ long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) {
       return ws_bytes(kPrepWs, ncam, npts, nobs);
     case kWsPrepDir:
       return ws_bytes(kPrepDirWs, ncam, npts, nobs);
+    case kWsLinPrep:
+      return ws_bytes(kLinPrepWs, ncam, npts, nobs);
     case kWsSchur:
       return ws_bytes(kSxWs, ncam, npts, nobs);
     case kWsTrial:
@@ -1800,6 +1956,7 @@ long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) {
 
 void set_smem_limits(int max_bytes) {
   cudaFuncSetAttribute(k_linearize, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
+  cudaFuncSetAttribute(k_lin_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_cost, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
@@ -1866,6 +2023,13 @@ int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStre
   k_cam_linearize<<<d.C, 256, 0, s>>>(d);
   k_lin_totals<<<1, 1024, 0, s>>>(d);
   return n;
+}
+int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
+  k_lin_prep<<<tile_blocks(d.T, sm.linprep), 32 * sm.linprep.wpb, sm.linprep.wpb * sm.linprep.slice, s>>>(
+      d, sm.linprep.slice, clo, chi);
+  k_cam_lin_prep<<<d.C, 256, 0, s>>>(d, clo, chi);
+  k_lin_totals<<<1, 1024, 0, s>>>(d);
+  return 3;
 }
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   k_cost<<<tile_blocks(d.T, sm.cost), 32 * sm.cost.wpb, sm.cost.wpb * sm.cost.slice, s>>>(d, sm.cost.slice);

@@ -8,7 +8,7 @@
 
 namespace bae {
 
-enum WsKind { kWsLin = 0, kWsCost = 1, kWsPrep = 2, kWsSchur = 3, kWsTrial = 4, kWsPrepDir = 5, kWsKinds = 6 };
+enum WsKind { kWsLin = 0, kWsCost = 1, kWsPrep = 2, kWsSchur = 3, kWsTrial = 4, kWsPrepDir = 5, kWsLinPrep = 6, kWsKinds = 7 };
 
 // Launch shape of one warp-tile kernel: `slice` bytes of shared memory per
 // warp (largest small tile of that kind) and `wpb` warps (tiles) per CTA.
@@ -16,7 +16,7 @@ struct TileLaunch {
   int slice = 0, wpb = 1;
 };
 struct SmemSizes {
-  TileLaunch lin, cost, prep, schur, trial, prepd;
+  TileLaunch lin, cost, prep, schur, trial, prepd, linprep;
 };
 
 long long tile_ws_bytes(int kind, int ncam, int npts, int nobs);
@@ -29,6 +29,10 @@ int launch_camrec(const Dev& d, bool trial, cudaStream_t s);
 int launch_gather_pixels(const double* raw, const int* orig, double* px, long long N, cudaStream_t s);
 int launch_points_permute(const double* in, const int* src, double* out, int P, bool to_internal, cudaStream_t s);
 int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm);
+// Single rank, direct solver, after an accepted step: the linearisation
+// and the prep for the damping in d.lam in one pass (k_lin_prep,
+// k_cam_lin_prep, k_lin_totals). Needs d.pcg zeroed first.
+int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s);
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
 // direct = true: the direct solver's prep (RHS, damped H_cc, per-slot W and
 // W H~_pp^-1; no block-Jacobi preconditioner and no PCG start state).

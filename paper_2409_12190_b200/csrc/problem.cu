@@ -240,7 +240,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   Plan& pl = plan_;
   long long big_stride = 0;
   int nbig = 0;
-  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial, &sm_.prepd};
+  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial, &sm_.prepd, &sm_.linprep};
   std::vector<int4> desc(static_cast<std::size_t>(pl.T), int4{0, 0, 0, 0});
   std::vector<char> blob;
   std::vector<int> small_tiles, big_tiles;
@@ -372,6 +372,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.p = dalloc<double>(6 * static_cast<std::size_t>(C));
   d.y = dalloc<double>(6 * static_cast<std::size_t>(C));
   d.partial = dalloc<double>(27 * static_cast<std::size_t>(std::max(pl.E, 1)));
+  d.partial6 = dalloc<double>(6 * static_cast<std::size_t>(std::max(pl.E, 1)));
   d.tile_red = dalloc<double>(2 * static_cast<std::size_t>(pl.T));
   d.cred = dist ? dalloc<double>(27 * static_cast<std::size_t>(C) + 8) : nullptr;
   d.cam_dot = dalloc<double>(2 * static_cast<std::size_t>(C));
@@ -420,7 +421,7 @@ Problem::~Problem() {
   pinned_give(host_info_);
   if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
   if (lm_graph_solve_) cudaGraphExecDestroy(lm_graph_solve_);
-  if (lm_graph_lin_) cudaGraphExecDestroy(lm_graph_lin_);
+  if (lm_graph_acc_) cudaGraphExecDestroy(lm_graph_acc_);
   for (std::size_t i = 0; i < allocs_.size(); ++i) chunk_give(opt_.device, allocs_[i], alloc_bytes_[i]);
   pinned_give(pcg_host_);
   pinned_give(lm_host_);
@@ -609,6 +610,24 @@ void Problem::linearize_async() {
   phase_end();
 }
 
+bool Problem::fuse_lin_prep(const bae_lm_config& cfg) const {
+  const char* e = std::getenv("BAE_LIN_PREP");
+  return cfg.solver == BAE_SOLVER_CHOLESKY && !comm_ && !(e && e[0] == '0');
+}
+
+void Problem::linearize_prep_async(double lambda, const bae_lm_config& cfg) {
+  build_direct();
+  reset_lm_status();
+  *lam_host_ = lambda;  // pinned: a graph replay reads it when the copy executes
+  ck(cudaMemcpyAsync(const_cast<double*>(d_.lam), lam_host_, sizeof(double), cudaMemcpyHostToDevice, stream_),
+     "H2D lambda");
+  ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+  phase_begin(kPhLinearize);
+  launches_ += launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_);
+  phase_end();
+  prep_fused_ = true;
+}
+
 void Problem::linearize() {
   linearize_async();
   read_lm();
@@ -689,10 +708,11 @@ void Problem::build_pcg_graph() {
   cudaGraphDestroy(g);
 }
 
-// The direct path's LM iteration as two graphs (one launch each instead of a
-// few dozen API calls): G_lin = commit of the accepted trial + the next
-// linearisation; G_solve = damping copy, prep, Schur assembly, tile
-// Cholesky, the failure words, the trial and the LM read-back. The damping
+// The direct path's LM iteration as one graph launch instead of a few dozen
+// API calls: G_solve = damping copy, prep, Schur assembly, tile Cholesky,
+// the failure words, the trial and the LM read-back (the retry after a
+// rejected step); G_acc = commit of the accepted trial, the linearisation
+// fused with the prep (linearize_prep_async), then G_solve's tail. The damping
 // is read from pinned memory when the copy node runs; clamps are kernel
 // arguments, so a different LmConfig clamp re-captures. Returns false (and
 // the caller keeps the plain launches) when capture is not possible.
@@ -700,8 +720,8 @@ bool Problem::build_lm_graphs(const bae_lm_config& cfg) {
   if (lm_graph_solve_ && graph_clo_ == cfg.clamp_min && graph_chi_ == cfg.clamp_max) return true;
   if (lm_graph_failed_) return false;
   if (lm_graph_solve_) cudaGraphExecDestroy(lm_graph_solve_);
-  if (lm_graph_lin_) cudaGraphExecDestroy(lm_graph_lin_);
-  lm_graph_solve_ = lm_graph_lin_ = nullptr;
+  if (lm_graph_acc_) cudaGraphExecDestroy(lm_graph_acc_);
+  lm_graph_solve_ = lm_graph_acc_ = nullptr;
   auto capture = [&](auto&& body, cudaGraphExec_t& out, long long& nlaunch) {
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
@@ -731,27 +751,26 @@ bool Problem::build_lm_graphs(const bae_lm_config& cfg) {
     }
     return true;
   };
-  const bool a = capture(
-      [&] {
-        launches_ += launch_commit(d_, stream_);
-        reset_lm_status();
-        launches_ += launch_linearize(d_, sm_, false, stream_, nullptr);
-      },
-      lm_graph_lin_, graph_lin_launches_);
+  auto solve_trial = [&] {
+    SolveInfo info;
+    solve_direct(*lam_host_, cfg, info);  // deferred: no synchronisation inside
+    reset_lm_status(true);
+    launches_ += launch_trial(d_, sm_, stream_, nullptr);
+    ck(cudaMemcpyAsync(lm_host_, d_.lm, sizeof(LmDev), cudaMemcpyDeviceToHost, stream_), "D2H lm");
+  };
+  const bool a = capture(solve_trial, lm_graph_solve_, graph_solve_launches_);
   const bool b = a && capture(
                           [&] {
-                            SolveInfo info;
-                            solve_direct(*lam_host_, cfg, info);  // deferred: no synchronisation inside
-                            reset_lm_status(true);
-                            launches_ += launch_trial(d_, sm_, stream_, nullptr);
-                            ck(cudaMemcpyAsync(lm_host_, d_.lm, sizeof(LmDev), cudaMemcpyDeviceToHost, stream_),
-                               "D2H lm");
+                            launches_ += launch_commit(d_, stream_);
+                            linearize_prep_async(*lam_host_, cfg);
+                            solve_trial();
                           },
-                          lm_graph_solve_, graph_solve_launches_);
+                          lm_graph_acc_, graph_acc_launches_);
+  prep_fused_ = false;
   if (!b) {
-    if (lm_graph_lin_) cudaGraphExecDestroy(lm_graph_lin_);
+    if (lm_graph_acc_) cudaGraphExecDestroy(lm_graph_acc_);
     if (lm_graph_solve_) cudaGraphExecDestroy(lm_graph_solve_);
-    lm_graph_lin_ = lm_graph_solve_ = nullptr;
+    lm_graph_acc_ = lm_graph_solve_ = nullptr;
     lm_graph_failed_ = true;
     return false;
   }
@@ -1005,14 +1024,17 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
 bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
   build_direct();
   const long long n = 6LL * d_.C;
-  *lam_host_ = lambda;  // pinned: a graph replay reads it when the copy executes
-  ck(cudaMemcpyAsync(const_cast<double*>(d_.lam), lam_host_, sizeof(double), cudaMemcpyHostToDevice, stream_),
-     "H2D lambda");
-  ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
-  phase_begin(kPhPrep);
-  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
-                           true);
-  phase_end();
+  if (!prep_fused_) {
+    *lam_host_ = lambda;  // pinned: a graph replay reads it when the copy executes
+    ck(cudaMemcpyAsync(const_cast<double*>(d_.lam), lam_host_, sizeof(double), cudaMemcpyHostToDevice, stream_),
+       "H2D lambda");
+    ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+    phase_begin(kPhPrep);
+    launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
+                             true);
+    phase_end();
+  }
+  prep_fused_ = false;
   phase_begin(kPhAssemble);
   if (use_tiles_)
     ck(cudaMemsetAsync(d_.stiles, 0, sizeof(double) * kTT * d_.stile_count, stream_), "memset S tiles");
@@ -1234,7 +1256,8 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
     ~DeferReset() { f = false; }
   } defer_reset{defer_factor_check_};
   const char* lg = std::getenv("BAE_LM_GRAPH");
-  const bool graphs = defer_factor_check_ && use_tiles_ && !comm_ && !std::getenv("BAE_CHOL_TRACE") &&
+  prep_fused_ = false;
+  const bool graphs = defer_factor_check_ && use_tiles_ && fuse_lin_prep(cfg) && !std::getenv("BAE_CHOL_TRACE") &&
                       !(lg && lg[0] == '0') && build_lm_graphs(cfg);
   bool lin_pending = false, commit_pending = false;
   while (iterations < cfg.max_iterations) {
@@ -1243,22 +1266,26 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
     SolveInfo info;
     bool ok = true;
     if (graphs) {
-      if (need_lin) {  // commit of the accepted trial + the next linearisation
-        ck(cudaGraphLaunch(lm_graph_lin_, stream_), "graph launch");
-        launches_ += graph_lin_launches_;
+      *lam_host_ = lambda_used;
+      if (need_lin) {  // commit of the accepted trial + the next linearisation and solve
+        ck(cudaGraphLaunch(lm_graph_acc_, stream_), "graph launch");
+        launches_ += graph_acc_launches_;
         commit_pending = false;
         lin_pending = true;
         need_lin = false;
+      } else {
+        ck(cudaGraphLaunch(lm_graph_solve_, stream_), "graph launch");
+        launches_ += graph_solve_launches_;
       }
-      *lam_host_ = lambda_used;
-      ck(cudaGraphLaunch(lm_graph_solve_, stream_), "graph launch");
-      launches_ += graph_solve_launches_;
       sync();
       info.pending = true;
     } else {
       if (need_lin) {
         if (defer_factor_check_) {
-          linearize_async();
+          if (fuse_lin_prep(cfg))
+            linearize_prep_async(lambda_used, cfg);
+          else
+            linearize_async();
           lin_pending = true;
         } else {
           linearize();

@@ -89,6 +89,10 @@ class Problem {
   void sync();
   void ensure_point_staging();
   void linearize_async();
+  // linearisation fused with the direct prep for `lambda` (single rank); the
+  // next solve_direct then starts at the Schur assembly
+  void linearize_prep_async(double lambda, const bae_lm_config& cfg);
+  bool fuse_lin_prep(const bae_lm_config& cfg) const;
   bool build_lm_graphs(const bae_lm_config& cfg);
   void reset_lm_status(bool keep_err = false);
   void read_lm();
@@ -131,8 +135,10 @@ class Problem {
   LmDev* lm_reset_host_ = nullptr;           // pinned template of the per-evaluation LM flags
   double* lam_host_ = nullptr;               // pinned: the damping of the next direct solve
   bool capturing_ = false;                   // stream capture in progress: no phase events
-  cudaGraphExec_t lm_graph_solve_ = nullptr, lm_graph_lin_ = nullptr;  // build_lm_graphs
-  long long graph_solve_launches_ = 0, graph_lin_launches_ = 0;
+  // build_lm_graphs: G_solve (a rejected step's retry), G_acc (after an accepted step)
+  cudaGraphExec_t lm_graph_solve_ = nullptr, lm_graph_acc_ = nullptr;
+  long long graph_solve_launches_ = 0, graph_acc_launches_ = 0;
+  bool prep_fused_ = false;  // the pending solve_direct's prep ran with the linearisation
   double graph_clo_ = 0.0, graph_chi_ = 0.0;
   bool lm_graph_failed_ = false;
   long long npairs_ = 0;                     // direct solver: (k, l) pairs of the Schur assembly
