@@ -201,6 +201,8 @@ def _alg_bytes(kernel, st):
         return 6 * N + 72 * P + 224 * E + 32 * T
     if kernel == "prep_direct":  # obs index 6, V 144 written; points + H_pp/g_p 96, H~pp^-1 48 w; entry RHS 48 w
         return 150 * N + 144 * P + 48 * E + 128 * C
+    if kernel == "lin_prep":  # linearize + V 144 w, H~pp^-1 48 w, entry RHS 48 w + 48 r, H~cc 168 + rhs 48 w
+        return 166 * N + 144 * P + 528 * E + 584 * C + 16 * T
     raise ValueError(kernel)
 
 
@@ -387,10 +389,15 @@ def run_b200(args):
             st2 = pr.stats()
             ds2 = pr.direct_stats()
             ms_p, ms_s = pr.time_kernel(5, 5), pr.time_kernel(6, 5)
+            ms_lp = pr.time_kernel(7, 5) if world == 1 else None
             kern2 = []
             for kname, ms_k, nbytes in (("k_linearize + camera pass", ms_l, _alg_bytes("linearize", st2)),
                                         ("k_prep<direct> + camera pass", ms_p, _alg_bytes("prep_direct", st2)),
+                                        ("k_lin_prep + k_cam_lin_prep (fused; after an accepted step)", ms_lp,
+                                         _alg_bytes("lin_prep", st2)),
                                         ("k_schur_dense (Schur assembly)", ms_s, _schur_bytes(st2, ds2))):
+                if ms_k is None:
+                    continue
                 gbs = nbytes / (ms_k * 1e-3) / 1e9
                 kern2.append({"kernel": kname, "us": 1e3 * ms_k, "bound": "hbm", "algorithmic_bytes": nbytes,
                               "achieved": gbs, "unit": "GB/s", "peak": peak_hbm, "frac": gbs / peak_hbm})

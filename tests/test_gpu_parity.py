@@ -290,3 +290,31 @@ def test_graph_replayed_iterations_match_plain_launches(monkeypatch):
         assert [(r.cost, r.lmbda, r.accepted) for r in x.trajectory] == \
                [(r.cost, r.lmbda, r.accepted) for r in y.trajectory]
     assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_fused_linearize_prep_matches_separate_passes(monkeypatch, graph):
+    """After an accepted step the linearisation and the direct prep run as one
+    pass (k_lin_prep + k_cam_lin_prep); the trajectory and the parameters are
+    bit for bit those of the separate k_linearize / k_prep passes
+    (BAE_LIN_PREP=0), with and without the captured LM graphs."""
+    s = _scene(C=40, P=800, N=4000, seed=32)
+    cfg = bae.LmConfig(max_iterations=10)
+    monkeypatch.setenv("BAE_LM_GRAPH", graph)
+    runs = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("BAE_LIN_PREP", fuse)
+        gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+        rep = bae.optimize(gpu, s.poses, s.points, cfg)
+        runs.append((rep, gpu.get_parameters()))
+    (a, pa), (b, pb) = runs
+    assert sum(r.accepted for r in a.trajectory) >= 2
+    assert [(r.cost, r.lmbda, r.accepted) for r in a.trajectory] == \
+           [(r.cost, r.lmbda, r.accepted) for r in b.trajectory]
+    assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
+
+
+def test_time_kernel_fused_lin_prep():
+    s = _scene(C=20, P=300, N=1500, seed=33)
+    gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+    assert gpu.time_kernel(7, 2) > 0.0

@@ -6,7 +6,9 @@ import sys
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = [a for a in sys.argv[3:] if a.startswith("-k=")]
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] +
+                     (["-k", kf[0][3:]] if kf else []),
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 agg = collections.Counter()
