@@ -61,6 +61,24 @@ struct TileCholPlan {
 // stay one group (BFS order).
 std::vector<std::vector<int>> nd_camera_groups(int C, const std::vector<std::pair<int, int>>& edges, int leaf);
 
+// Update helpers: a tile below the diagonal whose column holds at least
+// `min_ops` updates into it from columns other than the column's last
+// contributing one (k_last) gets a helper task -- another CTA applies those
+// updates (same order, same arithmetic: bitwise the same tile) while the
+// column's owner works on its diagonal, so a separator column's dozens of
+// tile updates no longer run on one SM. Tasks are {column, target position
+// (0: the owner), first op, end op}, in queue order (a column's helpers just
+// before its owner; every task only waits on tasks queued before it). `bptr`
+// / `bop` are rewritten: the owner's ops per column, then the helpers' ops.
+struct TileCholTasks {
+  std::vector<int> tasks;            // 4 per task
+  std::vector<unsigned> hmask;       // per column: bit s set when tile position s has a helper
+  std::vector<int> bptr, bop;        // the owner's ops per column, then the helper ranges
+  int helpers = 0;
+};
+// Only the queue's last `tail_tasks` tasks (the grid size) get helpers.
+TileCholTasks plan_chol_tasks(const TileCholPlan& pl, int min_ops, int tail_tasks);
+
 // Tile-level symbolic Cholesky from the lower-triangular tile pattern of S:
 // `lower_pairs` lists tile pairs (i, j), i >= j (duplicates allowed); every
 // diagonal tile is included automatically.
@@ -87,6 +105,10 @@ struct TileChol {
   const int* pos_cam;   // camera at each position (n / 6), -1 for a padding slot
   const unsigned long long* padmask;  // per tile: bit r set when row r is padding (unit pivot)
   unsigned* flags;      // nnz + nt epoch flags: one per stored tile (factor), one per column (backward)
+  unsigned* pflags;     // nnz: a helper's tile is pre-updated (or null without helpers)
+  const int* tasks;     // 4 per task (plan_chol_tasks), or null: task i = column i, no helpers
+  const unsigned* hmask;  // per column helper positions (with tasks)
+  int ntask;
   unsigned* next;       // 3 words: work counters (factor, backward; CTAs claim columns in topological
                         // order) and the epoch, the flag value of the current solve
   int* fail;            // set when a pivot is not positive (NotSpdError, cholesky.hpp:229)
@@ -97,6 +119,6 @@ struct TileChol {
 // backward); the epoch lives on the device (next[2]), so the sequence can be
 // captured in a graph and replayed.
 int launch_tile_chol(const TileChol& t, int grid, cudaStream_t s);
-int tile_chol_grid(int nt);
+int tile_chol_grid(int ntask);
 
 }  // namespace bae

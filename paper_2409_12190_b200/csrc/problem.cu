@@ -997,8 +997,17 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.uptr = upload(pl.uptr);
   t.usrc = upload(pl.usrc);
   t.udst = upload(pl.udst);
-  t.bptr = upload(pl.bptr);
-  t.bop = upload(pl.bop);
+  // update helpers for tiles with many updates (BAE_CHOL_HELP = minimum
+  // count, 0 = off): a separator column's tile updates spread over CTAs
+  int help_min = 2;
+  if (const char* h = std::getenv("BAE_CHOL_HELP")) help_min = std::max(0, std::atoi(h));
+  const TileCholTasks tk = plan_chol_tasks(pl, help_min, tile_chol_grid(1 << 30));
+  t.bptr = upload(tk.bptr);
+  t.bop = upload(tk.bop);
+  t.tasks = upload(tk.tasks);
+  t.hmask = upload(tk.hmask);
+  t.ntask = static_cast<int>(tk.tasks.size() / 4);
+  chol_helpers_ = tk.helpers;
   t.tiles = d_.stiles;
   t.rhs = d_.rhs;
   t.y = dalloc<double>(static_cast<std::size_t>(nt) * kTB);
@@ -1006,13 +1015,14 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.pos_cam = upload(pos_cam);
   t.padmask = upload(padmask);
   t.nnz = static_cast<int>(pl.nnz_tiles());
-  t.flags = dalloc<unsigned>(static_cast<std::size_t>(t.nnz) + nt);
-  ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (static_cast<std::size_t>(t.nnz) + nt), stream_),
+  t.flags = dalloc<unsigned>(2 * static_cast<std::size_t>(t.nnz) + nt);
+  t.pflags = t.flags + t.nnz + nt;
+  ck(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * (2 * static_cast<std::size_t>(t.nnz) + nt), stream_),
      "memset flags");
   t.fail = dalloc<int>(1);
   t.next = dalloc<unsigned>(3);
   ck(cudaMemsetAsync(t.next, 0, 3 * sizeof(unsigned), stream_), "memset counters");
-  chol_grid_ = tile_chol_grid(nt);
+  chol_grid_ = tile_chol_grid(t.ntask);
   chol_updates_ = static_cast<long long>(pl.usrc.size());
   if (!host_info_) host_info_ = static_cast<int*>(pinned_take());
 }
@@ -1075,9 +1085,10 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
       }
       const double nt = tchol_.nt;
       std::fprintf(stderr,
-                   "[bae chol] groups %d nt %d tiles %lld updates %lld: factor span %.1f us, backward span %.1f us; per column "
+                   "[bae chol] groups %d nt %d tiles %lld updates %lld helpers %d: factor span %.1f us, backward span %.1f us; per column "
                    "mean: wait+update %.2f potrf %.2f below-diagonal %.2f backward %.2f us\n",
-                   chol_groups_, tchol_.nt, static_cast<long long>(d_.stile_count), chol_updates_, (t1 - t0) * 1e-3,
+                   chol_groups_, tchol_.nt, static_cast<long long>(d_.stile_count), chol_updates_, chol_helpers_,
+                   (t1 - t0) * 1e-3,
                    (tb1 - tb0) * 1e-3, upd / nt * 1e-3, pot / nt * 1e-3, trs / nt * 1e-3, bwd / nt * 1e-3);
       if (std::getenv("BAE_CHOL_TRACE")[0] == '2')  // fast-path columns: absolute times from the first start
         for (int j = 0; j < tchol_.nt; ++j) {

@@ -169,6 +169,7 @@ class Problem {
   bool use_tiles_ = true;
   TileChol tchol_{};
   int chol_grid_ = 0;
+  int chol_helpers_ = 0;  // helper tasks of the tile Cholesky (plan_chol_tasks)
   long long chol_updates_ = 0;
   int chol_groups_ = 0;
   long long pcg_chunk_launches_ = 0;  // kernels in one captured PCG chunk

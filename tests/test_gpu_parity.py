@@ -318,3 +318,22 @@ def test_time_kernel_fused_lin_prep():
     s = _scene(C=20, P=300, N=1500, seed=33)
     gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
     assert gpu.time_kernel(7, 2) > 0.0
+
+
+def test_chol_update_helpers_are_bitwise_neutral(monkeypatch):
+    """Tile-Cholesky update helpers (other CTAs pre-apply a tile's updates
+    from all but the last contributing column, same order) leave the
+    trajectory and the parameters bit for bit unchanged (BAE_CHOL_HELP=0:
+    every update on the column's own CTA)."""
+    s = bae.synthetic.config_scene("trafalgar-257")
+    cfg = bae.LmConfig(max_iterations=6)
+    runs = []
+    for h in ("1", "0"):  # 1: a helper for every tile with an early update
+        monkeypatch.setenv("BAE_CHOL_HELP", h)
+        gpu = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
+        rep = bae.optimize(gpu, s.poses, s.points, cfg)
+        runs.append((rep, gpu.get_parameters()))
+    (a, pa), (b, pb) = runs
+    assert [(r.cost, r.lmbda, r.accepted) for r in a.trajectory] == \
+           [(r.cost, r.lmbda, r.accepted) for r in b.trajectory]
+    assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
