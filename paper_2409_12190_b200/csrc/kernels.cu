@@ -646,11 +646,16 @@ __global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg
 
 // Camera side of the linearisation (block per camera): H_cc (21) and g_c (6)
 // from the camera's entries; |g_c|^2 per camera for the totals.
-__global__ void __launch_bounds__(256) k_cam_linearize(Dev d) {
-  __shared__ double red[8 * 27];
+// kCamNT threads per camera block for the LM-loop camera passes (16 slots
+// of 27-wide entries, 80 of 6-wide ones): few cameras, so the per-camera
+// sums are latency-bound and want many loads in flight.
+constexpr int kCamNT = 512;
+
+__global__ void __launch_bounds__(kCamNT) k_cam_linearize(Dev d) {
+  __shared__ double red[16 * 27];
   __shared__ double acc[27];
   const int c = blockIdx.x;
-  cam_block_acc<27, 256>(d, c, red, acc);
+  cam_block_acc<27, kCamNT>(d, c, red, acc);
   const int t = threadIdx.x;
   if (t < 21) d.hcc[(long long)c * 21 + t] = acc[t];
   else if (t < 27) d.gc[(long long)c * 6 + (t - 21)] = acc[t];
@@ -666,13 +671,13 @@ __global__ void __launch_bounds__(256) k_cam_linearize(Dev d) {
 // single rank): k_cam_linearize's H_cc, g_c, |g_c|^2 and
 // k_cam_prep_direct's damped H~_cc and Schur RHS, with the same summation
 // orders as those two kernels.
-__global__ void __launch_bounds__(256) k_cam_lin_prep(Dev d, double clo, double chi) {
-  __shared__ double red[8 * 27];
+__global__ void __launch_bounds__(kCamNT) k_cam_lin_prep(Dev d, double clo, double chi) {
+  __shared__ double red[80 * 6];  // >= 16 * 27
   __shared__ double acc[27];
   __shared__ double acc6[6];
   const int c = blockIdx.x;
-  block_entry_sum<27, 256>(d, c, red, acc, d.partial);
-  block_entry_sum<6, 128>(d, c, red, acc6, d.partial6);
+  block_entry_sum<27, kCamNT>(d, c, red, acc, d.partial);
+  block_entry_sum<6, kCamNT>(d, c, red, acc6, d.partial6);
   const int t = threadIdx.x;
   if (t < 21) {
     double h = acc[t];
@@ -892,12 +897,12 @@ __global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, d
 
 // Camera side of the direct solver's prep (block per camera): damped H~_cc
 // and the Schur RHS b = -g_c + sum_k J_c^T J_p H~_pp^-1 g_p.
-__global__ void __launch_bounds__(128) k_cam_prep_direct(Dev d, double lambda, double clo, double chi) {
+__global__ void __launch_bounds__(kCamNT) k_cam_prep_direct(Dev d, double lambda, double clo, double chi) {
   lambda = *d.lam;
-  __shared__ double red[20 * 6];
+  __shared__ double red[80 * 6];
   __shared__ double acc[6];
   const int c = blockIdx.x;
-  cam_block_acc<6, 128>(d, c, red, acc);
+  cam_block_acc<6, kCamNT>(d, c, red, acc);
   if (threadIdx.x == 0 && c == 0 && d.cred && d.cred[6LL * d.C] > 0.0)
     atomicExch(&d.pcg->not_spd, 1);  // a point block failed on some rank
   if (threadIdx.x < 21) {
@@ -2007,8 +2012,13 @@ int launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
   return 1;
 }
 // Sharded runs: this rank's camera partials -> cross-rank sum in d.cred.
+// (the same block layout as the single-rank camera pass it stands in for:
+// the linearisation's kCamNT, the PCG prep's 256)
 static int reduce_cams27(const Dev& d, int extra, int nextra, Comm* comm, cudaStream_t s) {
-  k_cam_entry_sums<27, 256><<<d.C + 1, 256, 0, s>>>(d, extra, 0);
+  if (extra == 1)
+    k_cam_entry_sums<27, kCamNT><<<d.C + 1, kCamNT, 0, s>>>(d, extra, 0);
+  else
+    k_cam_entry_sums<27, 256><<<d.C + 1, 256, 0, s>>>(d, extra, 0);
   comm->allreduce_sum(d.cred, 27 * static_cast<std::size_t>(d.C) + nextra, s);
   return 1;
 }
@@ -2020,14 +2030,14 @@ int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStre
     n += reduce_cams27(d, 1, 2, comm, s);
     comm->allreduce_min(&d.lm->err_obs, 1, s);
   }
-  k_cam_linearize<<<d.C, 256, 0, s>>>(d);
+  k_cam_linearize<<<d.C, kCamNT, 0, s>>>(d);
   k_lin_totals<<<1, 1024, 0, s>>>(d);
   return n;
 }
 int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
   k_lin_prep<<<tile_blocks(d.T, sm.linprep), 32 * sm.linprep.wpb, sm.linprep.wpb * sm.linprep.slice, s>>>(
       d, sm.linprep.slice, clo, chi);
-  k_cam_lin_prep<<<d.C, 256, 0, s>>>(d, clo, chi);
+  k_cam_lin_prep<<<d.C, kCamNT, 0, s>>>(d, clo, chi);
   k_lin_totals<<<1, 1024, 0, s>>>(d);
   return 3;
 }
@@ -2047,11 +2057,11 @@ int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, do
         d, sm.prepd.slice, lambda, clo, chi);
     int n = 2;
     if (comm) {
-      k_cam_entry_sums<6, 128><<<d.C + 1, 128, 0, s>>>(d, 2, 0);
+      k_cam_entry_sums<6, kCamNT><<<d.C + 1, kCamNT, 0, s>>>(d, 2, 0);
       comm->allreduce_sum(d.cred, 6 * static_cast<std::size_t>(d.C) + 1, s);
       ++n;
     }
-    k_cam_prep_direct<<<d.C, 128, 0, s>>>(d, lambda, clo, chi);
+    k_cam_prep_direct<<<d.C, kCamNT, 0, s>>>(d, lambda, clo, chi);
     return n;
   }
   int n = 3;
