@@ -302,6 +302,16 @@ int bae_nd_order(int32_t num_cameras, int64_t num_edges, const int32_t* edges2, 
  * rows ascending) of L's tiles. */
 int bae_tile_symbolic(int32_t nt, int64_t num_pairs, const int32_t* pairs2, int32_t* colptr, int32_t* rowidx,
                       int64_t capacity, int64_t* nnz);
+/* Work queue of the tile factorisation with update helpers (host logic of
+ * plan_chol_tasks, for tests): the original per-column update lists
+ * (orig_bptr nt + 1, orig_ops 4 per update: target position, L(i,k) slot,
+ * L(j,k) slot, row-structure entry), the rewritten lists (bptr: the owner's
+ * updates per column; ops: owners first, then the helper ranges), the tasks
+ * (4 each: column, helper position or 0 for the owner, first op, end op) and
+ * the per-column helper masks. capacity bounds ops, orig_ops and tasks. */
+int bae_chol_tasks(int32_t nt, int64_t num_pairs, const int32_t* pairs2, int32_t min_ops, int32_t tail_tasks,
+                   int64_t capacity, int32_t* orig_bptr, int32_t* orig_ops, int32_t* bptr, int32_t* ops,
+                   int32_t* tasks, int32_t* num_tasks, uint32_t* hmask);
 
 /* ---- multi-GPU landmark partition, host only ----------------- */
 /* Contiguous ranges of the internal point order balanced by observation

@@ -129,6 +129,9 @@ SIGNATURES = {
                                      c_int32_p]),
     "bae_tile_symbolic": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, c_int32_p, c_int32_p, c_int32_p,
                                           ctypes.c_int64, c_int64_p]),
+    "bae_chol_tasks": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, c_int32_p, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.c_int64, c_int32_p, c_int32_p, c_int32_p, c_int32_p, c_int32_p,
+                                       c_int32_p, ctypes.POINTER(ctypes.c_uint32)]),
     "bae_bal_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     "bae_bal_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
     "bae_bal_synthetic": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_double,

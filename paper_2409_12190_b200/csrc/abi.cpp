@@ -419,6 +419,27 @@ int bae_tile_symbolic(int32_t nt, int64_t npairs, const int32_t* pairs2, int32_t
   });
 }
 
+int bae_chol_tasks(int32_t nt, int64_t npairs, const int32_t* pairs2, int32_t min_ops, int32_t tail_tasks,
+                   int64_t cap, int32_t* orig_bptr, int32_t* orig_ops, int32_t* bptr, int32_t* ops, int32_t* tasks,
+                   int32_t* ntask, uint32_t* hmask) {
+  return guarded([&] {
+    std::vector<std::pair<int, int>> tp(static_cast<std::size_t>(npairs));
+    for (int64_t i = 0; i < npairs; ++i) tp[i] = {pairs2[2 * i], pairs2[2 * i + 1]};
+    const bae::TileCholPlan pl = bae::plan_tile_chol(nt * bae::kTB, tp);
+    const bae::TileCholTasks tk = bae::plan_chol_tasks(pl, min_ops, tail_tasks);
+    if (static_cast<int64_t>(pl.bop.size() / 4) > cap || static_cast<int64_t>(tk.bop.size() / 4) > cap ||
+        static_cast<int64_t>(tk.tasks.size() / 4) > cap)
+      throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "capacity too small");
+    std::memcpy(orig_bptr, pl.bptr.data(), pl.bptr.size() * sizeof(int32_t));
+    std::memcpy(orig_ops, pl.bop.data(), pl.bop.size() * sizeof(int32_t));
+    std::memcpy(bptr, tk.bptr.data(), tk.bptr.size() * sizeof(int32_t));
+    std::memcpy(ops, tk.bop.data(), tk.bop.size() * sizeof(int32_t));
+    std::memcpy(tasks, tk.tasks.data(), tk.tasks.size() * sizeof(int32_t));
+    std::memcpy(hmask, tk.hmask.data(), tk.hmask.size() * sizeof(uint32_t));
+    *ntask = static_cast<int32_t>(tk.tasks.size() / 4);
+  });
+}
+
 // ---- BAL files, the reference's synthetic scene, the CSV trajectory ---------
 int bae_bal_read(const char* path, bae_bal** out) {
   return guarded([&] {

@@ -118,3 +118,62 @@ def test_nd_order_disconnected_components():
     edges = ring_edges(30, 2) + [(a + 30, b + 30) for a, b in ring_edges(30, 2)]
     order, gptr = nd_order(60, edges)
     assert np.array_equal(np.sort(order), np.arange(60))
+
+
+def chol_tasks(nt, pairs, min_ops, tail):
+    pr = np.ascontiguousarray(np.asarray(pairs, np.int32).reshape(-1, 2))
+    cap = 4 * nt * nt * nt + 64
+    ob, oo = np.empty(nt + 1, np.int32), np.empty(4 * cap, np.int32)
+    bp, op = np.empty(nt + 1, np.int32), np.empty(4 * cap, np.int32)
+    tk, nt_, hm = np.empty(4 * cap, np.int32), ctypes.c_int32(), np.empty(nt, np.uint32)
+    assert _lib.load().bae_chol_tasks(nt, pr.shape[0], ptr(pr, ctypes.c_int32), min_ops, tail, cap,
+                                      ptr(ob, ctypes.c_int32), ptr(oo, ctypes.c_int32), ptr(bp, ctypes.c_int32),
+                                      ptr(op, ctypes.c_int32), ptr(tk, ctypes.c_int32), ctypes.byref(nt_),
+                                      hm.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))) == 0
+    return ob, oo.reshape(-1, 4), bp, op.reshape(-1, 4), tk[:4 * nt_.value].reshape(-1, 4), hm
+
+
+@pytest.mark.parametrize("min_ops,tail", [(1, 1 << 20), (2, 1 << 20), (1, 8), (0, 1 << 20)])
+def test_chol_helper_tasks_partition_the_updates(min_ops, tail):
+    """Update helpers: every update of the factorisation runs
+    exactly once, a helper's updates are its tile's non-k_last updates in the
+    owner's order, the queue is ordered so that every task only waits on
+    tasks before it (column order, a column's helpers before its owner), and
+    only the queue's last `tail` tasks belong to columns with helpers."""
+    C = 96
+    order, gptr = nd_order(C, ring_edges(C, 6), 24)
+    pos = np.empty(C, int)
+    at = 0
+    for g in range(len(gptr) - 1):  # groups padded to whole tiles of 8 cameras
+        for c in order[gptr[g]:gptr[g + 1]]:
+            pos[c] = at
+            at += 1
+        at = (at + 7) // 8 * 8
+    nt = at // 8
+    pairs = sorted({(max(pos[a] // 8, pos[b] // 8), min(pos[a] // 8, pos[b] // 8)) for a, b in ring_edges(C, 6)})
+    ob, oo, bp, op, tasks, hm = chol_tasks(nt, pairs, min_ops, tail)
+    seen = []
+    last_col, owner_seen = -1, set()
+    for qi, (j, s, b, e) in enumerate(tasks):
+        assert j >= last_col  # column order
+        last_col = j
+        orig = [tuple(x) for x in oo[ob[j]:ob[j + 1]]]
+        qlast = max((x[3] for x in orig), default=-1)
+        mine = [tuple(x) for x in op[b:e]]
+        if s == 0:
+            assert (b, e) == (bp[j], bp[j + 1])
+            assert mine == [x for x in orig if not ((hm[j] >> x[0]) & 1 and x[3] != qlast)]
+            owner_seen.add(j)
+        else:
+            assert j not in owner_seen and (hm[j] >> s) & 1  # a helper runs before its owner
+            assert mine == [x for x in orig if x[0] == s and x[3] != qlast]
+            assert len(mine) >= max(min_ops, 1)
+        seen += mine
+    assert owner_seen == set(range(nt))
+    assert sorted(seen) == sorted(tuple(x) for x in oo[:ob[nt]])
+    helped = [j for j in range(nt) if hm[j]]
+    if helped:
+        first = min(qi for qi, t in enumerate(tasks) if t[0] == helped[0])
+        assert len(tasks) - first <= tail
+    if min_ops == 0:
+        assert not helped and len(tasks) == nt
