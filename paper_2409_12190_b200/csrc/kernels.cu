@@ -241,7 +241,9 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
 }
 
 constexpr int kVStride = 20;  // doubles per V = W L^-T record (two 16-byte aligned halves of 9)
-// Direct solver, per point: damped H~_pp, its inverse (d.hinv, for the
+// Direct solver prep, shared by k_prep<true> and the fused k_lin_prep (one
+// copy of the arithmetic, so the two agree bit for bit).
+// Per point: damped H~_pp, its inverse (d.hinv, for the
 // back-substitution), its Cholesky factor L (1/l00, l10, l20, 1/l11, l21,
 // 1/l22) into sp[3..8] and v = H~_pp^-1 g_p into sp[9..11]. h: the packed
 // H_pp (6), g: g_p (3). Returns false when the damped block is not SPD.
@@ -787,6 +789,12 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     double h[6], inv[9];
 #pragma unroll
     for (int j = 0; j < 6; ++j) h[j] = d.hpp[ip * 6 + j];
+    double* sp = ws.pt + lp * 12;
+    if (kDirect) {  // the Cholesky factor L of H~_pp instead of its inverse (shared with k_lin_prep)
+      const double g3[3] = {d.gp[ip * 3], d.gp[ip * 3 + 1], d.gp[ip * 3 + 2]};
+      if (!prep_point_direct(d, ip, h, g3, lambda, clo, chi, sp)) fail = 1;
+      continue;
+    }
     h[0] = damp_diag(h[0], lambda, clo, chi);
     h[3] = damp_diag(h[3], lambda, clo, chi);
     h[5] = damp_diag(h[5], lambda, clo, chi);
@@ -796,29 +804,11 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
 #pragma unroll
       for (int j = 0; j < 9; ++j) inv[j] = 0.0;
     }
-    double* sp = ws.pt + lp * 12;
     const double hi[6] = {inv[0], inv[1], inv[2], inv[4], inv[5], inv[8]};
 #pragma unroll
     for (int j = 0; j < 6; ++j) d.hinv[ip * 6 + j] = hi[j];
-    if (kDirect) {  // the Cholesky factor L of H~_pp instead (1/l00, l10, l20, 1/l11, l21, 1/l22)
-      double lf[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      if (!pfail) {
-        const double l00 = sqrt(h[0]), l10 = h[1] / l00, l20 = h[2] / l00;
-        const double l11 = sqrt(h[3] - l10 * l10), l21 = (h[4] - l20 * l10) / l11;
-        const double l22 = sqrt(h[5] - l20 * l20 - l21 * l21);
-        lf[0] = 1.0 / l00;
-        lf[1] = l10;
-        lf[2] = l20;
-        lf[3] = 1.0 / l11;
-        lf[4] = l21;
-        lf[5] = 1.0 / l22;
-      }
 #pragma unroll
-      for (int j = 0; j < 6; ++j) sp[3 + j] = lf[j];
-    } else {
-#pragma unroll
-      for (int j = 0; j < 6; ++j) sp[3 + j] = hi[j];
-    }
+    for (int j = 0; j < 6; ++j) sp[3 + j] = hi[j];
     const double g0 = d.gp[ip * 3], g1 = d.gp[ip * 3 + 1], g2 = d.gp[ip * 3 + 2];
     sp[9] = inv[0] * g0 + inv[1] * g1 + inv[2] * g2;
     sp[10] = inv[3] * g0 + inv[4] * g1 + inv[5] * g2;
@@ -856,23 +846,9 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
 #pragma unroll
         for (int b = a; b < 6; ++b)
           st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
-    } else {  // direct solver: keep V = W L^-T (V V^T = W H~^-1 W^T) of this slot
-      const double* lf = sp + 3;
-      double vv[kVStride];  // rows 0..2 at [0, 9), rows 3..5 at [10, 19): 16-byte aligned halves
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const double v0 = W[a * 3] * lf[0];
-        const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
-        const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
-        const int o = a * 3 + (a >= 3 ? 1 : 0);
-        vv[o] = v0;
-        vv[o + 1] = v1;
-        vv[o + 2] = v2;
-      }
-      vv[9] = vv[19] = 0.0;  // whole sectors written
-      double2* vo = reinterpret_cast<double2*>(d.wstore + (long long)(g.ob + s) * kVStride);
-#pragma unroll
-      for (int j = 0; j < kVStride / 2; ++j) vo[j] = make_double2(vv[2 * j], vv[2 * j + 1]);
+    } else {  // direct solver: V = W L^-T of this slot and its RHS piece (shared with k_lin_prep)
+      prep_obs_direct(d, g.ob + s, W, sp, st);
+      continue;
     }
     const double* vp = sp + 9;
 #pragma unroll
