@@ -30,7 +30,7 @@ void ck(cudaError_t e, const char* what) {
 }
 constexpr int kSmemLimit = 200 * 1024;
 constexpr int kSliceLimit = 48 * 1024;    // per-warp tile workspace
-constexpr int kCtaSmemBudget = 100 * 1024; // two CTAs per SM
+constexpr int kCtaSmemBudget = 112 * 1024; // two CTAs per SM (2 x (112 + 1 reserved) KB <= 228 KB)
 constexpr int kPcgChunk = 8;
 
 // BAE_HOST_TIMING=1: host-side phase times on stderr (setup profiling).
@@ -296,11 +296,13 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
       for (int i = 0; i < nobs; ++i) ptl[i] = pl.ptobs[ob + i];
     }
   });
+  int cta_budget = kCtaSmemBudget;
+  if (const char* e = std::getenv("BAE_CTA_SMEM_KB")) cta_budget = std::clamp(std::atoi(e), 16, 200) * 1024;
   for (int k = 0; k < kWsKinds; ++k) {
     TileLaunch& tl = *kinds[k];
     tl.slice = std::max(16, (tl.slice + 15) / 16 * 16);
     // up to 8 warp-tiles per CTA, two CTAs per SM within the shared-memory budget
-    tl.wpb = std::max(1, std::min(8, kCtaSmemBudget / tl.slice));
+    tl.wpb = std::max(1, std::min(8, cta_budget / tl.slice));
   }
   ht.mark("tile blobs");
   sm_.schur.slice = kPipeWarpBytes;  // pipelined double buffer per warp
