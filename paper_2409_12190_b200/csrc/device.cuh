@@ -130,7 +130,7 @@ struct Dev {
 // kPipePts points; its index blob is
 //   [hdr int x8: ob nobs pb npts eb ncam 0 0 | camid[ncam] | ent[ncam+1] |
 //    pptr[npts+1] | lcpt u32[nobs] | ptl u16[nobs] ] padded to 16 bytes.
-constexpr int kPipeObs = 64, kPipeCams = 16, kPipePts = 32;
+constexpr int kPipeObs = 96, kPipeCams = 16, kPipePts = 32;
 constexpr int kBlobCap = 32 + 4 * kPipeCams + 4 * (kPipeCams + 1) + 4 * (kPipePts + 1) + 6 * kPipeObs + 16;
 constexpr int kBufBlob = 0;
 constexpr int kBufPts = (kBlobCap + 15) / 16 * 16;                  // point window (+8 B alignment slack)

@@ -1412,11 +1412,12 @@ __device__ __forceinline__ void sx_pipe_tile(const Dev& d, const PcgDev& st, cha
     __syncwarp();
   }
   // phase 1: s_k = J_p^T J_c v
-  double cD[2][6];
-  P3 cy[2];
-  std::uint32_t lc[2];
+  constexpr int kRounds = (kPipeObs + 31) / 32;  // observations per lane
+  double cD[kRounds][6];
+  P3 cy[kRounds];
+  std::uint32_t lc[kRounds];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < kRounds; ++r) {
     const int s = r * 32 + lane;
     lc[r] = lcpt[min(s, nobs - 1)];
     if (s < nobs) {
@@ -1449,7 +1450,7 @@ __device__ __forceinline__ void sx_pipe_tile(const Dev& d, const PcgDev& st, cha
   __syncwarp();
   // phase 3: z_k = J_c^T J_p t_p -> stage rows 0..5
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
+  for (int r = 0; r < kRounds; ++r) {
     const int s = r * 32 + lane;
     if (s < nobs) {
       double z[6];

@@ -203,7 +203,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   ck(cudaSetDevice(opt.device), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   ht.mark("validate+partition");
-  int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : 64;
+  int tile_obs = opt.tile_obs > 0 ? opt.tile_obs : kPipeObs;
   if (const char* t = std::getenv("BAE_TILE_OBS")) tile_obs = std::max(8, std::atoi(t));
   int tile_cams = 32;
   if (const char* t = std::getenv("BAE_TILE_CAMS")) tile_cams = std::max(1, std::atoi(t));
