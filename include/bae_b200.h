@@ -188,8 +188,11 @@ int bae_get_parameters(bae_problem* p, double* poses7, double* points3);
  * residuals2 (nullable) receives r = projection - pixel in observation order. */
 int bae_evaluate(bae_problem* p, double* residuals2, double* cost);
 /* TracedProblem::jacobian (problems.hpp:68, trace.hpp:553-806): the two BSR
- * halves of JacobianPair. One block per row, so row_ptr = 0..N; col arrays are
- * the gather indices. Any output pointer may be NULL. */
+ * halves of JacobianPair. The pattern is read back from the device's
+ * observation decomposition: row_ptr counts the block rows the device holds
+ * per observation (0..N when each row is one block, as trace.hpp:728-790
+ * builds it); col arrays are the gather indices. Any output pointer may be
+ * NULL. */
 int bae_jacobian(bae_problem* p, double* jpose_2x6, double* jpoint_2x3,
                  int64_t* pose_row_ptr, int32_t* pose_col, int64_t* point_row_ptr,
                  int32_t* point_col);
@@ -199,6 +202,15 @@ int bae_jacobian(bae_problem* p, double* jpose_2x6, double* jpoint_2x3,
  * device reductions use. */
 int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t* col_idx,
                        int64_t* src_block);
+/* Block pattern of one quadrant of A = J^T J, which = 0 CC, 1 CL, 2 LC, 3 LL
+ * (spgemm_symbolic, spgemm.hpp:33-81, as NormalEquations::initialize builds
+ * them, assemble.hpp:47-53), or with which = 4 the scalar CSR pattern of A
+ * (build_csr_pattern, assemble.hpp:135-177). The device never forms CL / LC
+ * (implicit Schur); the patterns are derived from its observation
+ * decomposition, read back from device memory. rows / nnz are always written;
+ * row_ptr (rows+1) and col_idx (nnz) when non-NULL. Single-rank problems. */
+int bae_normal_pattern(bae_problem* p, int32_t which, int64_t* rows, int64_t* nnz, int64_t* row_ptr,
+                       int32_t* col_idx);
 /* Damped normal-equation pieces for parity (assemble.hpp:61-101): per-camera
  * 6x6 H_cc and 6-vector g_c = J_c^T r, per-point 3x3 H_pp and g_p, undamped,
  * at the current parameters. Any output may be NULL. */

@@ -7,17 +7,70 @@ pins it (reference unit-test KATs + the reference RNG golden stream)."""
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import os
-import sys
 
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle_bae.so")
 
-# share the struct layouts with the product binding (plain C structs of the header)
-sys.path.insert(0, os.path.dirname(_HERE))
-from paper_2409_12190_b200._lib import IterRecordC, LmConfigC, LmReportC  # noqa: E402
+
+# The plain C structs of include/bae_b200.h (bae_lm_config, bae_iter_record,
+# bae_lm_report), declared here so the oracle never imports the product
+# package: bench.py's reference arm loads liboracle_bae.so only.
+class LmConfigC(ctypes.Structure):
+    _fields_ = [("initial_damping", ctypes.c_double), ("damping_min", ctypes.c_double),
+                ("damping_max", ctypes.c_double), ("damping_up", ctypes.c_double), ("damping_down", ctypes.c_double),
+                ("clamp_min", ctypes.c_double), ("clamp_max", ctypes.c_double), ("plateau_rel_tol", ctypes.c_double),
+                ("pcg_tol", ctypes.c_double), ("pcg_max_iters", ctypes.c_int64), ("max_iterations", ctypes.c_int32),
+                ("plateau_patience", ctypes.c_int32), ("solver", ctypes.c_int32), ("use_caches", ctypes.c_int32)]
+
+
+class IterRecordC(ctypes.Structure):
+    _fields_ = [("iteration", ctypes.c_int32), ("accepted", ctypes.c_int32), ("cost", ctypes.c_double),
+                ("mse", ctypes.c_double), ("lmbda", ctypes.c_double), ("cum_time_s", ctypes.c_double),
+                ("pcg_iters", ctypes.c_int64), ("grad_norm", ctypes.c_double), ("trial_cost", ctypes.c_double)]
+
+
+class LmReportC(ctypes.Structure):
+    _fields_ = [("final_cost", ctypes.c_double), ("final_mse", ctypes.c_double), ("iterations", ctypes.c_int32),
+                ("reason", ctypes.c_int32), ("accepted_steps", ctypes.c_int32), ("rejected_steps", ctypes.c_int32),
+                ("final_lambda", ctypes.c_double), ("solve_seconds", ctypes.c_double),
+                ("total_pcg_iters", ctypes.c_int64), ("device_seconds", ctypes.c_double)]
+
+
+@dataclasses.dataclass
+class LmConfig:
+    """LmConfig (lm.hpp:23-46) defaults; solver 0 = cholesky, 1 = pcg."""
+    initial_damping: float = 1e-6
+    damping_min: float = 1e-16
+    damping_max: float = 1e16
+    damping_up: float = 2.0
+    damping_down: float = 0.5
+    clamp_min: float = 1e-6
+    clamp_max: float = 1e32
+    max_iterations: int = 10
+    plateau_patience: int = 3
+    plateau_rel_tol: float = 1e-6
+    solver: int = 0
+    pcg_tol: float = 1e-8
+    pcg_max_iters: int = 0
+    use_caches: bool = True
+
+
+def _cfg(config) -> LmConfigC:
+    """Any LmConfig-shaped object (this module's or the product binding's)."""
+    c = LmConfigC()
+    for f in ("initial_damping", "damping_min", "damping_max", "damping_up", "damping_down", "clamp_min",
+              "clamp_max", "plateau_rel_tol", "pcg_tol"):
+        setattr(c, f, float(getattr(config, f)))
+    c.pcg_max_iters = int(config.pcg_max_iters)
+    c.max_iterations = int(config.max_iterations)
+    c.plateau_patience = int(config.plateau_patience)
+    c.solver = int(config.solver)
+    c.use_caches = 1 if config.use_caches else 0
+    return c
 
 D = ctypes.POINTER(ctypes.c_double)
 I32 = ctypes.POINTER(ctypes.c_int32)
@@ -53,6 +106,8 @@ _SIG = {
     "or_synth_bal_shaped_philox": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64,
                                                   ctypes.c_double, ctypes.c_double, ctypes.c_double, D, D, D, I32, I32,
                                                   D, D, D]),
+    "or_synth_bal_shaped": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, D, D, D, I32, I32, D, D, D]),
     "or_philox4x32_10": (ctypes.c_uint32, [ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                                            ctypes.POINTER(ctypes.c_uint32)]),
     "or_ba_problem_new": (VP, [ctypes.c_int, ctypes.c_int, D, ctypes.c_int, D, D, ctypes.c_int64, I32, I32, D,
@@ -67,6 +122,7 @@ _SIG = {
     "or_problem_jacobian": (ctypes.c_int, [VP, D, D, I64, I32, I64, I32]),
     "or_transpose_plan": (ctypes.c_int, [VP, ctypes.c_int, I64, I32, I64]),
     "or_normal_size": (ctypes.c_int, [VP, I64, I64]),
+    "or_normal_pattern": (ctypes.c_int, [VP, ctypes.c_int, I64, I64, I64, I32]),
     "or_normal_dense": (ctypes.c_int, [VP, ctypes.c_double, ctypes.c_double, ctypes.c_double, D, D]),
     "or_solve_step": (ctypes.c_int, [VP, ctypes.c_double, ctypes.POINTER(LmConfigC), D, I64]),
     "or_lm_begin": (ctypes.c_int, [VP, D, D, ctypes.c_double]),
@@ -180,6 +236,20 @@ def synth_bal_shaped_philox(C, P, N, seed, pixel_sigma=1.0, pose_sigma=0.05, poi
     return out
 
 
+def synth_bal_shaped(C, P, N, seed=None, pixel_sigma=1.0, pose_sigma=0.05, point_sigma=0.01):
+    """SURVEY.md 8d's host generator restated on the reference Rng (independent
+    of the product's csrc/synth.cpp; the CPU baseline's inputs)."""
+    seed = C if seed is None else seed
+    out = dict(poses=np.empty((C, 7)), points=np.empty((P, 3)), intrinsics=np.empty((C, 3)),
+               cam_idx=np.empty(N, np.int32), pt_idx=np.empty(N, np.int32), pixels=np.empty((N, 2)),
+               true_poses=np.empty((C, 7)), true_points=np.empty((P, 3)))
+    _chk(lib().or_synth_bal_shaped(C, P, N, seed, pixel_sigma, pose_sigma, point_sigma, p(out["poses"]),
+                                   p(out["points"]), p(out["intrinsics"]), p(out["cam_idx"], ctypes.c_int32),
+                                   p(out["pt_idx"], ctypes.c_int32), p(out["pixels"]), p(out["true_poses"]),
+                                   p(out["true_points"])))
+    return out
+
+
 def philox4x32_10(ctr, key):
     c = (ctypes.c_uint32 * 4)(*ctr)
     k = (ctypes.c_uint32 * 2)(*key)
@@ -244,6 +314,17 @@ class Problem:
                                      p(sb, ctypes.c_int64)))
         return rp, ci, sb
 
+    def normal_pattern(self, which):
+        """(row_ptr, col_idx) of quadrant `which` (0 CC, 1 CL, 2 LC, 3 LL,
+        spgemm_symbolic) or of the scalar CSR matrix A (4)."""
+        rows, nnz = ctypes.c_int64(), ctypes.c_int64()
+        _chk(lib().or_normal_pattern(self.h, which, ctypes.byref(rows), ctypes.byref(nnz), None, None))
+        rp = np.empty(rows.value + 1, np.int64)
+        ci = np.empty(nnz.value, np.int32)
+        _chk(lib().or_normal_pattern(self.h, which, ctypes.byref(rows), ctypes.byref(nnz), p(rp, ctypes.c_int64),
+                                     p(ci, ctypes.c_int32)))
+        return rp, ci
+
     def normal_dense(self, lmbda, cmin=1e-6, cmax=1e32):
         n = ctypes.c_int64()
         nnz = ctypes.c_int64()
@@ -257,12 +338,12 @@ class Problem:
         n = 6 * self.C + 3 * self.P
         x = np.empty(n)
         it = ctypes.c_int64()
-        cfg = config.to_c()
+        cfg = _cfg(config)
         _chk(lib().or_solve_step(self.h, lmbda, ctypes.byref(cfg), p(x), ctypes.byref(it)))
         return x, it.value
 
     def optimize(self, config, poses=None, points=None):
-        cfg = config.to_c()
+        cfg = _cfg(config)
         cap = int(config.max_iterations) + 1
         recs = (IterRecordC * cap)()
         n = ctypes.c_int()
@@ -351,7 +432,7 @@ class ScalarProblem:
         _chk(lib().or_lm_begin(self.h, None, p(th), lmbda))
 
     def step(self, config):
-        cfg = config.to_c()
+        cfg = _cfg(config)
         acc = ctypes.c_int()
         _chk(lib().or_lm_step(self.h, ctypes.byref(cfg), ctypes.byref(acc)))
         return bool(acc.value)
@@ -367,7 +448,7 @@ class ScalarProblem:
                     history=hist[:nh.value].copy())
 
     def optimize(self, config, theta):
-        cfg = config.to_c()
+        cfg = _cfg(config)
         cap = int(config.max_iterations) + 1
         recs = (IterRecordC * cap)()
         n = ctypes.c_int()
@@ -383,7 +464,7 @@ class ScalarProblem:
 
 def stop_on_plateau(history, config):
     h = np.ascontiguousarray(history, dtype=np.float64)
-    cfg = config.to_c()
+    cfg = _cfg(config)
     s = ctypes.c_int()
     _chk(lib().or_stop_on_plateau(p(h), h.size, ctypes.byref(cfg), ctypes.byref(s)))
     return bool(s.value)
@@ -428,4 +509,30 @@ def pinhole_project(pose, point, k4):
     _chk(lib().or_pinhole_project(p(np.ascontiguousarray(pose, dtype=np.float64)),
                                   p(np.ascontiguousarray(point, dtype=np.float64)),
                                   p(np.ascontiguousarray(k4, dtype=np.float64)), p(out)))
+    return out
+
+
+def camera_window_slice(scene, cameras):
+    """A bounded CPU sample of a BAL-shaped scene (bench.py's CPU baseline):
+    cameras 0..cameras-1 of the ring and every point all of whose cameras lie
+    among them, re-indexed. The generator's visibility is banded (windows of
+    min(C, 16) ring neighbours), so the slice keeps the scene's
+    per-camera density, per-point track lengths and band structure; the
+    reference's per-iteration work is linear in the observations at fixed
+    band width, which is what makes the sample's time scale to the full
+    scene by N / N_slice."""
+    ci = np.asarray(scene["cam_idx"])
+    pi = np.asarray(scene["pt_idx"])
+    P = len(scene["points"])
+    outside = np.bincount(pi, weights=(ci >= cameras).astype(np.float64), minlength=P) > 0
+    seen = np.bincount(pi, minlength=P) > 0
+    keep_pt = seen & ~outside
+    new_id = np.cumsum(keep_pt) - 1
+    keep = keep_pt[pi]
+    out = dict(poses=np.ascontiguousarray(scene["poses"][:cameras]),
+               intrinsics=np.ascontiguousarray(scene["intrinsics"][:cameras]),
+               points=np.ascontiguousarray(scene["points"][keep_pt]),
+               cam_idx=np.ascontiguousarray(ci[keep], dtype=np.int32),
+               pt_idx=np.ascontiguousarray(new_id[pi[keep]], dtype=np.int32),
+               pixels=np.ascontiguousarray(np.asarray(scene["pixels"])[keep]))
     return out

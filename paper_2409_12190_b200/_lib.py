@@ -97,6 +97,8 @@ SIGNATURES = {
     "bae_jacobian": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, c_int64_p, c_int32_p,
                                     c_int64_p, c_int32_p]),
     "bae_transpose_plan": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_int64_p, c_int32_p, c_int64_p]),
+    "bae_normal_pattern": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, c_int64_p, c_int64_p, c_int64_p,
+                                          c_int32_p]),
     "bae_block_diagonals": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     "bae_optimize": (ctypes.c_int, [ctypes.c_void_p, c_double_p, c_double_p, ctypes.POINTER(LmConfigC),
                                     ctypes.POINTER(IterRecordC), ctypes.c_int32, ctypes.POINTER(LmReportC),

@@ -278,6 +278,19 @@ class TracedProblem:
                                               ptr(sb, ctypes.c_int64)))
         return TransposePlan(rp, ci, sb)
 
+    def normal_pattern(self, which: int):
+        """(row_ptr, col_idx) of quadrant `which` of A = J^T J (0 CC, 1 CL,
+        2 LC, 3 LL; spgemm_symbolic) or of the scalar CSR matrix A (4), from
+        the device's observation decomposition."""
+        lib = _lib.load()
+        rows, nnz = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.bae_normal_pattern(self._h, int(which), ctypes.byref(rows), ctypes.byref(nnz), None, None))
+        rp = np.empty(rows.value + 1, np.int64)
+        ci = np.empty(nnz.value, np.int32)
+        _check(lib.bae_normal_pattern(self._h, int(which), ctypes.byref(rows), ctypes.byref(nnz),
+                                      ptr(rp, ctypes.c_int64), ptr(ci, ctypes.c_int32)))
+        return rp, ci
+
     def block_diagonals(self):
         hcc = np.empty((self._C, 6, 6))
         gc = np.empty((self._C, 6))

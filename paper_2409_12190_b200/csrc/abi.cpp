@@ -196,20 +196,27 @@ int bae_jacobian(bae_problem* p, double* jpose, double* jpoint, int64_t* prp, in
   return guarded([&] {
     if (ba(p)->distributed()) throw bae::Error(BAE_ERR_UNSUPPORTED, "the Jacobian export needs a single-rank problem");
     if (jpose || jpoint) ba(p)->jacobian(jpose, jpoint, nullptr);
-    const bae::Plan& pl = ba(p)->plan();
-    const std::int64_t N = pl.N;
-    std::vector<std::int32_t> cam(static_cast<std::size_t>(N)), pt(static_cast<std::size_t>(N));
-    // gather columns from the device-side decomposition (entry camera, tile point)
-    for (int t = 0; t < pl.T; ++t)
-      for (int e = pl.tile_ent_begin[t]; e < pl.tile_ent_begin[t + 1]; ++e)
-        for (int s = pl.ent_obs_begin[e]; s < pl.ent_obs_begin[e + 1]; ++s) {
-          cam[pl.obs_orig[s]] = pl.ent_cam[e];
-          pt[pl.obs_orig[s]] = pl.pt_of_internal[pl.tile_pt_begin[t] + static_cast<int>(pl.obs_lcpt[s] >> 16)];
+    if (!(prp || pcol || lrp || lcol)) return;
+    // The pattern as the device holds it: every slot of every tile is one
+    // 2x6 / 2x3 block row; its columns are the slot's entry camera and tile
+    // point. row_ptr counts the slots that carry each observation (one each
+    // when the decomposition is a permutation of the rows, trace.hpp:728-790).
+    const bae::DeviceStructure ds = ba(p)->download_structure();
+    const std::int64_t N = ds.N;
+    std::vector<std::int64_t> rows(static_cast<std::size_t>(N) + 1, 0);
+    std::vector<std::int32_t> cam(static_cast<std::size_t>(N), -1), pt(static_cast<std::size_t>(N), -1);
+    for (int t = 0; t < ds.T; ++t)
+      for (int e = ds.tile_ent_begin[t]; e < ds.tile_ent_begin[t + 1]; ++e)
+        for (int s = ds.ent_obs_begin[e]; s < ds.ent_obs_begin[e + 1]; ++s) {
+          const std::int32_t k = ds.obs_orig[s];
+          if (k < 0 || k >= N) throw bae::Error(BAE_ERR_CUDA, "device decomposition: observation id out of range");
+          ++rows[k + 1];
+          cam[k] = ds.ent_cam[e];
+          pt[k] = ds.slot_pt(t, s);
         }
-    for (std::int64_t k = 0; k <= N; ++k) {
-      if (prp) prp[k] = k;
-      if (lrp) lrp[k] = k;
-    }
+    for (std::int64_t k = 0; k < N; ++k) rows[k + 1] += rows[k];
+    if (prp) std::memcpy(prp, rows.data(), rows.size() * 8);
+    if (lrp) std::memcpy(lrp, rows.data(), rows.size() * 8);
     if (pcol) std::memcpy(pcol, cam.data(), cam.size() * 4);
     if (lcol) std::memcpy(lcol, pt.data(), pt.size() * 4);
   });
@@ -219,17 +226,21 @@ int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t*
   return guarded([&] {
     if (ba(p)->distributed())
       throw bae::Error(BAE_ERR_UNSUPPORTED, "the transpose plans need a single-rank problem");
-    const bae::Plan& pl = ba(p)->plan();
+    if (which != 0 && which != 1) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "which must be 0 (pose) or 1 (point)");
+    const bae::DeviceStructure ds = ba(p)->download_structure();
     if (which == 0) {
-      // camera segments: entries of each camera, observations re-listed in id order
-      std::vector<std::int64_t> rp(static_cast<std::size_t>(pl.C) + 1, 0);
+      // camera segments from the device's per-camera entry lists (the camera
+      // reductions' segments). The device sums a camera's observations in
+      // tile order; the plan lists them in ascending id (bsr.hpp:140-160).
+      std::vector<std::int64_t> rp(static_cast<std::size_t>(ds.C) + 1, 0);
       std::vector<std::int32_t> ids;
-      ids.reserve(static_cast<std::size_t>(pl.N));
-      for (int c = 0; c < pl.C; ++c) {
+      ids.reserve(static_cast<std::size_t>(ds.N));
+      for (int c = 0; c < ds.C; ++c) {
         const std::size_t start = ids.size();
-        for (int q = pl.cam_ent_ptr[c]; q < pl.cam_ent_ptr[c + 1]; ++q) {
-          const int e = pl.cam_ent[q];
-          for (int s = pl.ent_obs_begin[e]; s < pl.ent_obs_begin[e + 1]; ++s) ids.push_back(pl.obs_orig[s]);
+        for (int q = ds.cam_ent_ptr[c]; q < ds.cam_ent_ptr[c + 1]; ++q) {
+          const int e = ds.cam_ent[q];
+          if (ds.ent_cam[e] != c) throw bae::Error(BAE_ERR_CUDA, "device decomposition: entry list of wrong camera");
+          for (int s = ds.ent_obs_begin[e]; s < ds.ent_obs_begin[e + 1]; ++s) ids.push_back(ds.obs_orig[s]);
         }
         std::sort(ids.begin() + static_cast<std::ptrdiff_t>(start), ids.end());
         rp[c + 1] = static_cast<std::int64_t>(ids.size());
@@ -237,23 +248,98 @@ int bae_transpose_plan(bae_problem* p, int32_t which, int64_t* row_ptr, int32_t*
       std::memcpy(row_ptr, rp.data(), rp.size() * 8);
       std::memcpy(col_idx, ids.data(), ids.size() * 4);
       for (std::size_t i = 0; i < ids.size(); ++i) src_block[i] = ids[i];
-    } else if (which == 1) {
-      std::vector<std::int64_t> rp(static_cast<std::size_t>(pl.P) + 1, 0);
-      for (int i = 0; i < pl.P; ++i) rp[pl.pt_of_internal[i] + 1] = pl.pt_ptr[i + 1] - pl.pt_ptr[i];
-      for (int p2 = 0; p2 < pl.P; ++p2) rp[p2 + 1] += rp[p2];
-      for (int t = 0; t < pl.T; ++t)
-        for (int i = pl.tile_pt_begin[t]; i < pl.tile_pt_begin[t + 1]; ++i) {
-          std::int64_t o = rp[pl.pt_of_internal[i]];
-          for (int q = pl.pt_ptr[i]; q < pl.pt_ptr[i + 1]; ++q, ++o) {
-            const std::int32_t k = pl.obs_orig[pl.tile_obs_begin[t] + pl.ptobs[q]];
+    } else {
+      // point segments: the device's per-point slot lists (ascending id,
+      // the order the point reductions sum in)
+      std::vector<std::int64_t> rp(static_cast<std::size_t>(ds.P) + 1, 0);
+      for (int i = 0; i < ds.P; ++i) rp[ds.pt_of_internal[i] + 1] = ds.pt_ptr[i + 1] - ds.pt_ptr[i];
+      for (int p2 = 0; p2 < ds.P; ++p2) rp[p2 + 1] += rp[p2];
+      for (int t = 0; t < ds.T; ++t)
+        for (int i = ds.tile_pt_begin[t]; i < ds.tile_pt_begin[t + 1]; ++i) {
+          std::int64_t o = rp[ds.pt_of_internal[i]];
+          for (int q = ds.pt_ptr[i]; q < ds.pt_ptr[i + 1]; ++q, ++o) {
+            const std::int32_t k = ds.obs_orig[ds.tile_obs_begin[t] + ds.ptobs[q]];
             col_idx[o] = k;
             src_block[o] = k;
           }
         }
       std::memcpy(row_ptr, rp.data(), rp.size() * 8);
-    } else {
-      throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "which must be 0 (pose) or 1 (point)");
     }
+  });
+}
+
+int bae_normal_pattern(bae_problem* p, int32_t which, int64_t* rows, int64_t* nnz, int64_t* row_ptr,
+                       int32_t* col_idx) {
+  return guarded([&] {
+    if (ba(p)->distributed())
+      throw bae::Error(BAE_ERR_UNSUPPORTED, "the normal-matrix pattern needs a single-rank problem");
+    if (which < 0 || which > 4) throw bae::Error(BAE_ERR_INVALID_ARGUMENT, "which must be 0..4");
+    const bae::DeviceStructure ds = ba(p)->download_structure();
+    const int C = ds.C, P = ds.P;
+    // unique (camera, point) pairs of the device decomposition: the CL
+    // quadrant's blocks (spgemm_symbolic, spgemm.hpp:33-81: duplicates merge)
+    std::vector<std::vector<std::int32_t>> cl(static_cast<std::size_t>(C)), lc(static_cast<std::size_t>(P));
+    for (int t = 0; t < ds.T; ++t)
+      for (int e = ds.tile_ent_begin[t]; e < ds.tile_ent_begin[t + 1]; ++e)
+        for (int s = ds.ent_obs_begin[e]; s < ds.ent_obs_begin[e + 1]; ++s) {
+          cl[ds.ent_cam[e]].push_back(ds.slot_pt(t, s));
+          lc[ds.slot_pt(t, s)].push_back(ds.ent_cam[e]);
+        }
+    for (auto* v : {&cl, &lc})
+      for (auto& r : *v) {
+        std::sort(r.begin(), r.end());
+        r.erase(std::unique(r.begin(), r.end()), r.end());
+      }
+    std::vector<std::int64_t> rp;
+    std::vector<std::int32_t> ci;
+    auto block_rows = [&](const std::vector<std::vector<std::int32_t>>& rws) {
+      rp.assign(1, 0);
+      for (const auto& r : rws) {
+        ci.insert(ci.end(), r.begin(), r.end());
+        rp.push_back(static_cast<std::int64_t>(ci.size()));
+      }
+    };
+    auto diag_rows = [&](int n, const std::vector<std::vector<std::int32_t>>& seen) {
+      rp.assign(1, 0);
+      for (int i = 0; i < n; ++i) {
+        if (!seen[i].empty()) ci.push_back(i);
+        rp.push_back(static_cast<std::int64_t>(ci.size()));
+      }
+    };
+    if (which == 0) {
+      diag_rows(C, cl);  // one camera per Jacobian row: CC is block diagonal
+    } else if (which == 1) {
+      block_rows(cl);
+    } else if (which == 2) {
+      block_rows(lc);
+    } else if (which == 3) {
+      diag_rows(P, lc);
+    } else {
+      // scalar CSR of A = [CC CL; LC LL] (build_csr_pattern, assemble.hpp:135-177):
+      // columns ascending, pose scalars 0..6C-1 then point scalars
+      const std::int64_t off = 6LL * C;
+      rp.assign(1, 0);
+      for (int c = 0; c < C; ++c)
+        for (int i = 0; i < 6; ++i) {
+          if (!cl[c].empty())
+            for (int j = 0; j < 6; ++j) ci.push_back(6 * c + j);
+          for (int pt : cl[c])
+            for (int j = 0; j < 3; ++j) ci.push_back(static_cast<std::int32_t>(off + 3LL * pt + j));
+          rp.push_back(static_cast<std::int64_t>(ci.size()));
+        }
+      for (int pt = 0; pt < P; ++pt)
+        for (int i = 0; i < 3; ++i) {
+          for (int c : lc[pt])
+            for (int j = 0; j < 6; ++j) ci.push_back(6 * c + j);
+          if (!lc[pt].empty())
+            for (int j = 0; j < 3; ++j) ci.push_back(static_cast<std::int32_t>(off + 3LL * pt + j));
+          rp.push_back(static_cast<std::int64_t>(ci.size()));
+        }
+    }
+    *rows = static_cast<std::int64_t>(rp.size()) - 1;
+    *nnz = static_cast<std::int64_t>(ci.size());
+    if (row_ptr) std::memcpy(row_ptr, rp.data(), rp.size() * 8);
+    if (col_idx) std::memcpy(col_idx, ci.data(), ci.size() * 4);
   });
 }
 

@@ -32,6 +32,10 @@ namespace bae {
 
 constexpr int kTB = 48;              // tile edge (8 cameras)
 constexpr int kTT = kTB * kTB;       // doubles per tile
+// Failure word values: 1 = a pivot was not positive (NotSpdError); kCholTimeout
+// = a flag wait exceeded kFlagTimeoutNs (a lost producer; BAE_ERR_CUDA).
+constexpr int kCholTimeout = 2;
+constexpr unsigned long long kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;
 constexpr int kCholThreads = 256;    // 16 x 16 threads, 3 x 3 outputs each
 
 // Host-side symbolic structure (plan_tile_chol).
@@ -111,7 +115,7 @@ struct TileChol {
   int ntask;
   unsigned* next;       // 3 words: work counters (factor, backward; CTAs claim columns in topological
                         // order) and the epoch, the flag value of the current solve
-  int* fail;            // set when a pivot is not positive (NotSpdError, cholesky.hpp:229)
+  int* fail;            // 1: a pivot is not positive (NotSpdError, cholesky.hpp:229); kCholTimeout
   unsigned long long* trace;  // BAE_CHOL_TRACE: 8 globaltimer stamps per column, or null
 };
 

@@ -632,6 +632,7 @@ bool PgoProblem::solve(double lambda, const bae_lm_config& cfg) {
   launches_ += 2 + launch_tile_chol(tchol_, chol_grid_, stream_);
   ck(cudaMemcpyAsync(fail_host_, tchol_.fail, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
   read_scal();
+  if (*fail_host_ == kCholTimeout) throw Error(BAE_ERR_CUDA, "tile Cholesky: dataflow flag wait timed out");
   return *fail_host_ == 0;
 }
 

@@ -438,6 +438,48 @@ const char* Problem::cheirality_msg() const {
   return d_.pinhole ? "pinhole projection: point behind camera" : "bal projection: point on camera plane";
 }
 
+int DeviceStructure::slot_cam(int t, int s) const {
+  // the entry of slot s: entries of tile t are ordered by local camera and
+  // each covers a contiguous slot range
+  int lo = tile_ent_begin[t], hi = tile_ent_begin[t + 1] - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (ent_obs_begin[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  return ent_cam[lo];
+}
+
+DeviceStructure Problem::download_structure() {
+  require_single("the structure export");
+  activate();
+  ensure_point_staging();
+  sync();
+  DeviceStructure s;
+  s.C = d_.C;
+  s.P = d_.P;
+  s.T = d_.T;
+  s.E = d_.E;
+  s.N = d_.N;
+  auto get = [&](auto& v, const auto* src, std::size_t n) {
+    v.resize(n);
+    if (n) ck(cudaMemcpy(v.data(), src, n * sizeof(v[0]), cudaMemcpyDeviceToHost), "D2H structure");
+  };
+  const std::size_t T = s.T, E = s.E, N = static_cast<std::size_t>(s.N), C = s.C, P = s.P;
+  get(s.tile_obs_begin, d_.tile_obs_begin, T + 1);
+  get(s.tile_pt_begin, d_.tile_pt_begin, T + 1);
+  get(s.tile_ent_begin, d_.tile_ent_begin, T + 1);
+  get(s.obs_lcpt, d_.obs_lcpt, N);
+  get(s.obs_orig, d_.obs_orig, N);
+  get(s.ent_cam, d_.ent_cam, E);
+  get(s.ent_obs_begin, d_.ent_obs_begin, E + 1);
+  get(s.cam_ent_ptr, d_.cam_ent_ptr, C + 1);
+  get(s.cam_ent, d_.cam_ent, E);
+  get(s.pt_ptr, d_.pt_ptr, P + 1);
+  get(s.ptobs, d_.ptobs, N);
+  get(s.pt_of_internal, src_of_internal_, P);
+  return s;
+}
+
 void Problem::require_single(const char* what) const {
   if (comm_) throw Error(BAE_ERR_UNSUPPORTED, std::string(what) + " is not available on a sharded problem");
 }
@@ -853,9 +895,11 @@ void Problem::build_direct() {
     std::vector<int4> chunks;
     std::vector<int> nch(bcam.size(), 0);
     for (int b : ord) {
-      const int q0 = bptr[b], q1 = bptr[b + 1];
+      const long long q0 = bptr[b], q1 = bptr[b + 1];
       const int first = static_cast<int>(chunks.size());
-      for (int q = q0; q < q1 || q == q0; q += U) chunks.push_back(int4{b, q, std::min(q + U, q1), first});
+      // chunk bounds in 64-bit: q + U must not overflow near the 2^31 pair cap
+      for (long long q = q0; q < q1 || q == q0; q += U)
+        chunks.push_back(int4{b, static_cast<int>(q), static_cast<int>(std::min(q + U, q1)), first});
       nch[b] = static_cast<int>(chunks.size()) - first;
     }
     d_.chunks = upload(chunks);
@@ -1112,6 +1156,7 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
     }
     sync();
     phase_collect();
+    if (*host_info_ == kCholTimeout) throw Error(BAE_ERR_CUDA, "tile Cholesky: dataflow flag wait timed out");
     if (*host_info_ != 0 || pcg_host_->not_spd) return false;  // NotSpdError (cholesky.hpp:229)
     return true;
   }
@@ -1326,6 +1371,8 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
       if (lm_host_->err_obs != INT_MAX) throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
       grad = std::sqrt(lm_host_->grad_sq);
     }
+    if (info.pending && use_tiles_ && *host_info_ == kCholTimeout)
+      throw Error(BAE_ERR_CUDA, "tile Cholesky: dataflow flag wait timed out");
     if (info.pending && (*host_info_ != 0 || pcg_host_->not_spd)) ok = false;  // NotSpdError (cholesky.hpp:229)
     if (ok) {
       trial_cost = (lm_host_->retract_bad || lm_host_->trial_bad) ? std::numeric_limits<double>::infinity()

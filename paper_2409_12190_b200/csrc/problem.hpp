@@ -37,6 +37,28 @@ enum Phase : int {
   kPhases = 7
 };
 
+// The observation decomposition as it lives in device memory (read back for
+// the structure exports: the Jacobian pattern, the transpose plans and the
+// normal matrix's block patterns are derived from these arrays, not from the
+// host planner's copies).
+struct DeviceStructure {
+  int C = 0, P = 0, T = 0, E = 0;
+  std::int64_t N = 0;
+  std::vector<std::int32_t> tile_obs_begin, tile_pt_begin, tile_ent_begin;  // T+1
+  std::vector<std::uint32_t> obs_lcpt;                                      // N
+  std::vector<std::int32_t> obs_orig;                                       // N
+  std::vector<std::int32_t> ent_cam, ent_obs_begin;                         // E, E+1
+  std::vector<std::int32_t> cam_ent_ptr, cam_ent;                           // C+1, E
+  std::vector<std::int32_t> pt_ptr;                                         // P+1
+  std::vector<std::uint16_t> ptobs;                                         // N
+  std::vector<std::int32_t> pt_of_internal;                                 // P
+  // (camera, point) of slot s of tile t
+  int slot_cam(int t, int s) const;
+  int slot_pt(int t, int s) const {
+    return pt_of_internal[tile_pt_begin[t] + static_cast<int>(obs_lcpt[s] >> 16)];
+  }
+};
+
 class Problem {
  public:
   Problem(const double* poses7, int C, const double* points3, int P, const double* intr3,
@@ -65,6 +87,7 @@ class Problem {
   void get_parameters(double* poses7, double* points3);
   double evaluate(double* resid2);
   void jacobian(double* jpose, double* jpoint, double* resid2);
+  DeviceStructure download_structure();
   void block_diagonals(double* hcc36, double* gc6, double* hpp9, double* gp3);
   void solve_step(double lambda, const bae_lm_config& cfg, double* delta, std::int64_t* iters, double* relres);
   void optimize(const double* poses7, const double* points3, const bae_lm_config& cfg,

@@ -337,3 +337,75 @@ def test_chol_update_helpers_are_bitwise_neutral(monkeypatch):
     assert [(r.cost, r.lmbda, r.accepted) for r in a.trajectory] == \
            [(r.cost, r.lmbda, r.accepted) for r in b.trajectory]
     assert np.array_equal(pa[0], pb[0]) and np.array_equal(pa[1], pb[1])
+
+
+@pytest.mark.parametrize("dups", [False, True])
+def test_normal_matrix_patterns_bit_exact(oracle, dups):
+    """The normal matrix's index structure, bit-exact: the four quadrant
+    block patterns of spgemm_symbolic (spgemm.hpp:33-81; CL = the unique
+    (camera, point) pairs, duplicates merged) and the scalar CSR pattern of
+    build_csr_pattern (assemble.hpp:135-177), against the device's
+    observation decomposition (tile_obs=64: many tiles). With duplicated
+    observations and points seen once (test_trace.cpp:296-311)."""
+    s = _scene(C=20, P=500, N=2600, seed=41)
+    if dups:
+        ci, pi, px, pts = _with_duplicates_and_singles(s, np.random.default_rng(41))
+        gpu = bae.make_ba_problem(s.poses, pts, s.intrinsics, (ci, pi, px), tile_obs=64)
+        ref = oracle.Problem(s.poses, pts, s.intrinsics, ci, pi, px)
+    else:
+        gpu, ref = _pair(s, oracle, tile_obs=64)
+    for which in range(5):
+        rg, cg = gpu.normal_pattern(which)
+        rr, cr = ref.normal_pattern(which)
+        assert np.array_equal(rg, rr), which
+        assert np.array_equal(cg, cr), which
+    # the Jacobian's row pointers come from the device decomposition too
+    jg = gpu.jacobian()
+    assert np.array_equal(jg.j_pose.row_ptr, np.arange(gpu.residual_rows() + 1))
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+@pytest.mark.parametrize("solver", ["cholesky", "pcg"])
+def test_not_spd_rejections_end_in_solver_failure(oracle, monkeypatch, graph, solver):
+    """lm.hpp:146-152 and :234-237. A clamp ceiling of 1e-12 (assemble.hpp:94-101)
+    leaves every damped system indefinite: each solve fails (NotSpdError in the
+    reference's Cholesky; the device's point-block or tile factorisation flags
+    it), the step is rejected, lambda doubles, and the first rejection at
+    lambda >= damping_max ends the run as solver_failure -- the oracle's exact
+    trajectory, with plain launches and with the captured LM graphs."""
+    monkeypatch.setenv("BAE_LM_GRAPH", graph)
+    s = _scene(C=8, P=120, N=500, seed=51)
+    gpu, ref = _pair(s, oracle)
+    cfg = bae.LmConfig(max_iterations=40, damping_max=1e-3, clamp_min=1e-12, clamp_max=1e-12,
+                       solver=bae.SolverChoice[solver])
+    rep = bae.optimize(gpu, s.poses, s.points, cfg)
+    oref = ref.optimize(bae.LmConfig(max_iterations=40, damping_max=1e-3, clamp_min=1e-12, clamp_max=1e-12))
+    assert oref["reason"] == int(bae.TerminationReason.solver_failure)
+    assert rep.reason == bae.TerminationReason.solver_failure
+    assert rep.iterations == oref["iterations"] == 11  # 1e-6 * 2^10 >= 1e-3
+    for a, b in zip(rep.trajectory, oref["trajectory"]):
+        assert not a.accepted or a.iteration == 0
+        assert a.lmbda == b["lmbda"] and a.cost == pytest.approx(b["cost"], rel=1e-12)
+    p7, p3 = gpu.get_parameters()
+    assert np.array_equal(p7, s.poses) and np.array_equal(p3, s.points)  # rejections restore (test_optim.cpp:110-125)
+
+
+@pytest.mark.parametrize("solver", ["cholesky", "pcg"])
+def test_not_spd_until_damping_recovers(oracle, solver):
+    """Diagonal entries clamped to at most 1 (assemble.hpp:94-101): the damped
+    system is indefinite until (1 + lambda) outgrows the off-diagonal blocks,
+    so LM rejects (NotSpd) for dozens of iterations, accepts, halves lambda,
+    and is rejected again -- the accept / lambda sequence equals the oracle's
+    exact-solve trajectory step for step."""
+    s = _scene(C=8, P=120, N=500, seed=52)
+    gpu, ref = _pair(s, oracle)
+    kw = dict(max_iterations=50, clamp_max=1.0)
+    rep = bae.optimize(gpu, s.poses, s.points,
+                       bae.LmConfig(solver=bae.SolverChoice[solver], pcg_tol=1e-12, **kw))
+    oref = ref.optimize(bae.LmConfig(**kw))
+    acc = [r.accepted for r in rep.trajectory[1:]]
+    assert acc[:10] == [False] * 10 and any(acc)
+    assert len(rep.trajectory) == len(oref["trajectory"])
+    for a, b in zip(rep.trajectory, oref["trajectory"]):
+        assert a.accepted == b["accepted"] and a.lmbda == b["lmbda"], a.iteration
+        assert abs(a.cost - b["cost"]) <= 1e-6 * b["cost"]

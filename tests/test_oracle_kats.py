@@ -338,3 +338,33 @@ def test_philox_scene_shape(oracle):
     assert np.all(np.abs(s["intrinsics"][:, 1]) <= 0.1) and np.all(np.abs(s["intrinsics"][:, 2]) <= 0.01)
     b = oracle.synth_bal_shaped_philox(C, P, N, 40)
     assert all(np.array_equal(s[k], b[k]) for k in s)  # deterministic
+
+
+def test_oracle_normal_patterns_against_numpy(oracle):
+    """The oracle's spgemm_symbolic quadrant patterns (spgemm.hpp:33-81) and
+    scalar CSR pattern (assemble.hpp:135-177) against a numpy derivation from
+    the observation list, duplicates included (test_trace.cpp:296-311)."""
+    rng = oracle.Rng(17)
+    d = oracle.make_random_ba(rng, 5, 30, False, keep=0.5)
+    ci = np.concatenate([d["cam_idx"], d["cam_idx"][:7]])
+    pi = np.concatenate([d["pt_idx"], d["pt_idx"][:7]])
+    px = np.concatenate([d["pixels"], d["pixels"][:7]])
+    prob = oracle.Problem(d["poses"], d["points"], d["intrinsics"], ci, pi, px)
+    C, P = 5, 30
+    pairs = sorted(set(zip(ci.tolist(), pi.tolist())))
+    rp, col = prob.normal_pattern(1)
+    assert [(c, int(col[k])) for c in range(C) for k in range(rp[c], rp[c + 1])] == pairs
+    rp, col = prob.normal_pattern(2)
+    assert sorted((int(col[k]), p) for p in range(P) for k in range(rp[p], rp[p + 1])) == pairs
+    dense = np.zeros((6 * C + 3 * P, 6 * C + 3 * P), bool)
+    for c, p in pairs:
+        dense[6 * c:6 * c + 6, 6 * c:6 * c + 6] = True
+        dense[6 * c:6 * c + 6, 6 * C + 3 * p:6 * C + 3 * p + 3] = True
+        dense[6 * C + 3 * p:6 * C + 3 * p + 3, 6 * c:6 * c + 6] = True
+        dense[6 * C + 3 * p:6 * C + 3 * p + 3, 6 * C + 3 * p:6 * C + 3 * p + 3] = True
+    rp, col = prob.normal_pattern(4)
+    got = np.zeros_like(dense)
+    for r in range(dense.shape[0]):
+        assert np.all(np.diff(col[rp[r]:rp[r + 1]]) > 0)
+        got[r, col[rp[r]:rp[r + 1]]] = True
+    assert np.array_equal(got, dense)
