@@ -22,6 +22,16 @@
 #include "pairs.cuh"
 #include "problem.hpp"
 
+// Launch wrappers return their kernel count; BAE_CHECK_LAUNCH=1 also checks
+// the runtime's error state after every one (a debugging aid: a failed launch
+// is named at its call site instead of surfacing at a later API call).
+#define BAE_LAUNCHED(x)                                                 \
+  do {                                                                  \
+    if (check_launch_) ck(cudaPeekAtLastError(), "before launch: " #x); \
+    launches_ += (x);                                                   \
+    if (check_launch_) ck(cudaPeekAtLastError(), "launch: " #x);        \
+  } while (0)
+
 namespace bae {
 
 namespace {
@@ -333,7 +343,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     double* raw = nullptr;
     ck(cudaMallocAsync(reinterpret_cast<void**>(&raw), 2 * sizeof(double) * use_N, stream_), "cudaMallocAsync");
     ck(cudaMemcpyAsync(raw, px2, 2 * sizeof(double) * use_N, cudaMemcpyHostToDevice, stream_), "H2D pixels");
-    launches_ += launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_);
+    BAE_LAUNCHED(launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_));
     ck(cudaFreeAsync(raw, stream_), "cudaFreeAsync");
     d.obs_px = px;
   }
@@ -398,6 +408,18 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.blk_nchunk = nullptr;
   d.blk_ticket = nullptr;
   d.schur_part = nullptr;
+  d.sup_a = d.sup_b = nullptr;
+  d.sup_chunk = d.unit_pr = nullptr;
+  d.chunk_blob = nullptr;
+  d.chunk_meta = nullptr;
+  d.cta_chunk = d.cta_nreg = nullptr;
+  d.sup_grid = 0;
+  d.sblob = nullptr;
+  d.spairs = nullptr;
+  d.upart = nullptr;
+  d.blk_uptr = d.blk_units = nullptr;
+  d.nsup = 0;
+  d.nsup_single = 0;
   d.nblk = 0;
   d.schur = nullptr;
   ht.mark("allocs");
@@ -528,7 +550,7 @@ void Problem::set_parameters(const double* poses7, const double* points3) {
   if (points3 && !comm_) {  // caller order up, permuted into the internal order on the device
     ensure_point_staging();
     ck(cudaMemcpyAsync(pts_user_, points3, 3 * sizeof(double) * P, cudaMemcpyHostToDevice, stream_), "H2D points");
-    launches_ += launch_points_permute(pts_user_, src_of_internal_, d_.pts, P, true, stream_);
+    BAE_LAUNCHED(launch_points_permute(pts_user_, src_of_internal_, d_.pts, P, true, stream_));
   } else if (points3) {
     std::vector<double> pts(3 * static_cast<std::size_t>(P));
     for (int i = 0; i < P; ++i) {
@@ -541,7 +563,7 @@ void Problem::set_parameters(const double* poses7, const double* points3) {
        "H2D points");
     sync();
   }
-  launches_ += launch_camrec(d_, false, stream_);
+  BAE_LAUNCHED(launch_camrec(d_, false, stream_));
   sync();
 }
 
@@ -586,7 +608,7 @@ void Problem::get_parameters(double* poses7, double* points3) {
     }
   } else if (points3) {  // permuted back to the caller's order on the device
     ensure_point_staging();
-    launches_ += launch_points_permute(d_.pts, src_of_internal_, pts_user_, P, false, stream_);
+    BAE_LAUNCHED(launch_points_permute(d_.pts, src_of_internal_, pts_user_, P, false, stream_));
     ck(cudaMemcpyAsync(points3, pts_user_, 3 * sizeof(double) * P, cudaMemcpyDeviceToHost, stream_), "D2H points");
     sync();
   }
@@ -631,7 +653,7 @@ double Problem::evaluate(double* resid2) {
     ck(cudaMalloc(&rbuf, 2 * sizeof(double) * plan_.N), "cudaMalloc");
     d_.resid = rbuf;
   }
-  launches_ += launch_cost(d_, sm_, stream_, comm_.get());
+  BAE_LAUNCHED(launch_cost(d_, sm_, stream_, comm_.get()));
   d_.resid = nullptr;
   read_lm();
   if (lm_host_->err_obs != INT_MAX) {
@@ -650,7 +672,7 @@ double Problem::evaluate(double* resid2) {
 void Problem::linearize_async() {
   reset_lm_status();
   phase_begin(kPhLinearize);
-  launches_ += launch_linearize(d_, sm_, false, stream_, comm_.get());
+  BAE_LAUNCHED(launch_linearize(d_, sm_, false, stream_, comm_.get()));
   phase_end();
 }
 
@@ -667,7 +689,7 @@ void Problem::linearize_prep_async(double lambda, const bae_lm_config& cfg) {
      "H2D lambda");
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhLinearize);
-  launches_ += launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_);
+  BAE_LAUNCHED(launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_));
   phase_end();
   prep_fused_ = true;
 }
@@ -691,7 +713,7 @@ void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
   d_.jstore = js;
   d_.resid = rs;
   reset_lm_status();
-  launches_ += launch_linearize(d_, sm_, true, stream_, nullptr);
+  BAE_LAUNCHED(launch_linearize(d_, sm_, true, stream_, nullptr));
   d_.jstore = nullptr;
   d_.resid = nullptr;
   read_lm();
@@ -799,13 +821,13 @@ bool Problem::build_lm_graphs(const bae_lm_config& cfg) {
     SolveInfo info;
     solve_direct(*lam_host_, cfg, info);  // deferred: no synchronisation inside
     reset_lm_status(true);
-    launches_ += launch_trial(d_, sm_, stream_, nullptr);
+    BAE_LAUNCHED(launch_trial(d_, sm_, stream_, nullptr));
     ck(cudaMemcpyAsync(lm_host_, d_.lm, sizeof(LmDev), cudaMemcpyDeviceToHost, stream_), "D2H lm");
   };
   const bool a = capture(solve_trial, lm_graph_solve_, graph_solve_launches_);
   const bool b = a && capture(
                           [&] {
-                            launches_ += launch_commit(d_, stream_);
+                            BAE_LAUNCHED(launch_commit(d_, stream_));
                             linearize_prep_async(*lam_host_, cfg);
                             solve_trial();
                           },
@@ -909,7 +931,38 @@ void Problem::build_direct() {
     d_.schur_part = dalloc<double>(36 * chunks.size());
   }
   d_.nblk = static_cast<int>(bcam.size());
-  if (!d_.wstore) d_.wstore = dalloc<double>(20 * static_cast<std::size_t>(plan_.N));  // kVStride
+  {  // supertiles of the Schur assembly (BAE_SCHUR=pairs: the pair-chunk kernel instead)
+    const char* sm = std::getenv("BAE_SCHUR");
+    if (!(sm && std::string(sm) == "pairs") && npairs_ > 0) {
+      SuperHost sh;
+      unsigned* sp = dalloc<unsigned>(static_cast<std::size_t>(npairs_));
+      int nsm = 148;
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, opt_.device);
+      build_super(d_, plan_, d_.pairs, d_.blk_ptr, bptr, npairs_, sp, sh, nsm,
+                  [this](std::size_t n) { return static_cast<void*>(dalloc<char>(n)); }, stream_);
+      d_.spairs = sp;
+      d_.sblob = sh.blob;
+      d_.chunk_blob = sh.chunk_blob;
+      d_.chunk_meta = upload(sh.chunk_meta);
+      d_.cta_chunk = upload(sh.cta_chunk);
+      d_.cta_nreg = upload(sh.cta_nreg);
+      d_.sup_grid = static_cast<int>(sh.cta_nreg.size());
+      d_.sup_a = upload(sh.sup_a);
+      d_.sup_b = upload(sh.sup_b);
+      d_.sup_chunk = upload(sh.sup_chunk);
+      d_.unit_pr = upload(sh.unit_pr);
+      d_.blk_uptr = upload(sh.blk_uptr);
+      d_.blk_units = upload(sh.blk_units);
+      d_.upart = dalloc<double>(36 * static_cast<std::size_t>(sh.units));
+      d_.nsup = static_cast<int>(sh.sup_a.size());
+      d_.nsup_single = sh.single;
+      sup_regular_ = sh.regular;
+      sup_single_ = sh.single;
+      sup_units_ = sh.units;
+      sup_chunks_ = static_cast<long long>(sh.sup_chunk.size());
+    }
+  }
+  if (!d_.wstore) d_.wstore = dalloc<double>(18 * static_cast<std::size_t>(plan_.N));  // kVStride
   if (!d_.lam) {
     d_.lam = dalloc<double>(1);
     lam_host_ = static_cast<double*>(pinned_take());
@@ -1086,8 +1139,8 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
        "H2D lambda");
     ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
     phase_begin(kPhPrep);
-    launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
-                             true);
+    BAE_LAUNCHED(launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, comm_.get(),
+                             true));
     phase_end();
   }
   prep_fused_ = false;
@@ -1096,7 +1149,7 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
     ck(cudaMemsetAsync(d_.stiles, 0, sizeof(double) * kTT * d_.stile_count, stream_), "memset S tiles");
   else
     ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
-  launches_ += launch_schur_dense(d_, stream_, comm_.get());
+  BAE_LAUNCHED(launch_schur_dense(d_, stream_, comm_.get()));
   phase_end();
   if (use_tiles_) {
     // tile-sparse Cholesky + both substitutions: x = S^-1 rhs straight into d_.x
@@ -1108,7 +1161,7 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
       ck(cudaMalloc(&tchol_.trace, 8 * sizeof(unsigned long long) * tchol_.nt), "cudaMalloc");
       ck(cudaMemsetAsync(tchol_.trace, 0, 8 * sizeof(unsigned long long) * tchol_.nt, stream_), "memset");
     }
-    launches_ += launch_tile_chol(tchol_, chol_grid_, stream_);
+    BAE_LAUNCHED(launch_tile_chol(tchol_, chol_grid_, stream_));
     phase_end();
     if (tchol_.trace) {
       trace.resize(8 * static_cast<std::size_t>(tchol_.nt));
@@ -1190,8 +1243,8 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
       cfg.pcg_max_iters > 0 ? cfg.pcg_max_iters : std::max<long long>(250, 2LL * (d_.C + P_global_));
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhPrep);
-  launches_ += launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_, comm_.get(),
-                           false);
+  BAE_LAUNCHED(launch_prep(d_, sm_, lambda, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, budget, stream_, comm_.get(),
+                           false));
   phase_end();
   phase_begin(kPhPcg);
   if (comm_ && !comm_->capturable()) {
@@ -1206,7 +1259,7 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
     build_pcg_graph();
     for (;;) {
       ck(cudaGraphLaunch(pcg_graph_, stream_), "graph launch");
-      launches_ += pcg_chunk_launches_;
+      BAE_LAUNCHED(pcg_chunk_launches_);
       ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
       sync();
       if (pcg_host_->state >= kPcgDone) break;
@@ -1215,7 +1268,7 @@ bool Problem::solve_pcg(double lambda, const bae_lm_config& cfg, SolveInfo& info
     if (pcg_grid_ == 0) pcg_grid_ = pcg_persistent_grid(d_, sm_);
     for (;;) {
       ck(launch_pcg_persistent(d_, sm_, pcg_grid_, 4096, stream_), "cooperative launch");
-      launches_ += 1;
+      BAE_LAUNCHED(1);
       ck(cudaMemcpyAsync(pcg_host_, d_.pcg, sizeof(PcgDev), cudaMemcpyDeviceToHost, stream_), "D2H pcg");
       sync();
       if (pcg_host_->state >= kPcgDone) break;
@@ -1239,7 +1292,7 @@ void Problem::solve_step(double lambda, const bae_lm_config& cfg, double* delta,
   SolveInfo info;
   if (!solve(lambda, cfg, info)) throw Error(BAE_ERR_NUMERICAL_BREAKDOWN, "damped system not SPD or PCG breakdown");
   reset_lm_status();
-  launches_ += launch_trial(d_, sm_, stream_, comm_.get());
+  BAE_LAUNCHED(launch_trial(d_, sm_, stream_, comm_.get()));
   sync();
   const int C = d_.C, P = d_.P;
   ck(cudaMemcpy(delta, d_.x, 6 * sizeof(double) * C, cudaMemcpyDeviceToHost), "D2H dc");
@@ -1327,13 +1380,13 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
       *lam_host_ = lambda_used;
       if (need_lin) {  // commit of the accepted trial + the next linearisation and solve
         ck(cudaGraphLaunch(lm_graph_acc_, stream_), "graph launch");
-        launches_ += graph_acc_launches_;
+        BAE_LAUNCHED(graph_acc_launches_);
         commit_pending = false;
         lin_pending = true;
         need_lin = false;
       } else {
         ck(cudaGraphLaunch(lm_graph_solve_, stream_), "graph launch");
-        launches_ += graph_solve_launches_;
+        BAE_LAUNCHED(graph_solve_launches_);
       }
       sync();
       info.pending = true;
@@ -1360,7 +1413,7 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
       if (ok) {
         reset_lm_status(lin_pending);
         phase_begin(kPhTrial);
-        launches_ += launch_trial(d_, sm_, stream_, comm_.get());
+        BAE_LAUNCHED(launch_trial(d_, sm_, stream_, comm_.get()));
         phase_end();
       }
       read_lm();
@@ -1382,7 +1435,7 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
           commit_pending = true;  // with the next linearisation (G_lin), or after the loop
         } else {
           phase_begin(kPhCommit);
-          launches_ += launch_commit(d_, stream_);
+          BAE_LAUNCHED(launch_commit(d_, stream_));
           phase_end();
         }
         cost = trial_cost;
@@ -1470,28 +1523,28 @@ double Problem::time_kernel(int kind, int reps) {
   auto launch = [&]() {
     switch (kind) {
       case 0:
-        launches_ += launch_linearize(d_, sm_, false, stream_, comm_.get());
+        BAE_LAUNCHED(launch_linearize(d_, sm_, false, stream_, comm_.get()));
         break;
       case 1:
-        launches_ += launch_schur_only(d_, sm_, stream_);
+        BAE_LAUNCHED(launch_schur_only(d_, sm_, stream_));
         break;
       case 2:
-        launches_ += launch_pcg_iteration(d_, sm_, stream_, comm_.get());
+        BAE_LAUNCHED(launch_pcg_iteration(d_, sm_, stream_, comm_.get()));
         break;
       case 3:
-        launches_ += launch_linearize(d_, sm_, true, stream_, comm_.get());
+        BAE_LAUNCHED(launch_linearize(d_, sm_, true, stream_, comm_.get()));
         break;
       case 4:  // tile Cholesky factor + both substitutions (re-factors the factor: same work)
-        launches_ += launch_tile_chol(tchol_, chol_grid_, stream_);
+        BAE_LAUNCHED(launch_tile_chol(tchol_, chol_grid_, stream_));
         break;
       case 5:  // direct prep: damped point blocks, V = W L^-T, Schur right-hand side
-        launches_ += launch_prep(d_, sm_, 1e-4, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, nullptr, true);
+        BAE_LAUNCHED(launch_prep(d_, sm_, 1e-4, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_, nullptr, true));
         break;
       case 6:  // Schur assembly of the reduced camera matrix into its tiles
-        launches_ += launch_schur_dense(d_, stream_, nullptr);
+        BAE_LAUNCHED(launch_schur_dense(d_, stream_, nullptr));
         break;
       case 7:  // linearisation fused with the direct prep (the step after an accepted trial)
-        launches_ += launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_);
+        BAE_LAUNCHED(launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_));
         break;
       default:
         throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");
