@@ -358,11 +358,6 @@ int bae_direct_stats(const bae_problem* p, int64_t* out5);
 /* Schur assembly size (after the direct solver's first use): the (k, l)
  * observation pairs and the 6x6 camera blocks they sum into. */
 int bae_direct_pairs(const bae_problem* p, int64_t* pairs, int64_t* blocks);
-/* Supertile Schur assembly (after the direct solver's first use; zeros on the
- * pair-chunk path, BAE_SCHUR=pairs): [regular supertiles, single supertiles
- * (one long warp-tile each), units (one thread's range of a camera block's
- * pairs), staged chunks]. */
-int bae_schur_stats(const bae_problem* p, int64_t* out4);
 /* Static sizes the roofline arithmetic needs: [N, P, C, tiles, tile-camera
  * entries, max obs per tile]. */
 int bae_problem_stats(const bae_problem* p, int64_t* out6);

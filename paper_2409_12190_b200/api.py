@@ -332,13 +332,6 @@ class TracedProblem:
                                              ctypes.byref(lo)))
         return r.value, w.value, lp.value, lo.value
 
-    def schur_stats(self):
-        """Supertile Schur assembly structure (zeros before the direct solver's
-        first use, or on the pair-chunk path)."""
-        out = np.zeros(4, np.int64)
-        _check(_lib.load().bae_schur_stats(self._h, ptr(out, ctypes.c_int64)))
-        return dict(zip(("supertiles", "single_supertiles", "units", "chunks"), (int(v) for v in out)))
-
     def direct_stats(self):
         """Tile Cholesky structure of the direct solver (zeros before its first use)."""
         out = np.zeros(5, np.int64)

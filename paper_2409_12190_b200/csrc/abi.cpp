@@ -442,14 +442,6 @@ int bae_direct_stats(const bae_problem* p, int64_t* out5) {
   });
 }
 
-int bae_schur_stats(const bae_problem* p, int64_t* out4) {
-  return guarded([&] {
-    long long v[4];
-    ba(p)->schur_stats(v);
-    for (int i = 0; i < 4; ++i) out4[i] = v[i];
-  });
-}
-
 int bae_direct_pairs(const bae_problem* p, int64_t* pairs, int64_t* blocks) {
   return guarded([&] {
     if (pairs) *pairs = ba(p)->direct_pairs();

@@ -113,26 +113,6 @@ struct Dev {
   unsigned* blk_ticket;     // per block: chunks done (reset before every assembly)
   double* schur_part;       // 36 per chunk: partial 6x6 sums of multi-chunk blocks
   const int2* blk_tile;
-  // supertile Schur assembly (k_schur_super, DESIGN.md 5.3 step 3): a
-  // supertile is a run of consecutive warp-tiles touching at most kSupCams
-  // cameras; its V records are staged through shared memory chunk by chunk
-  // and every (camera block, pair range) "unit" is accumulated by one thread
-  // in registers across the chunks.
-  const int4* sup_a;        // per supertile {first slot, slots, first chunk, chunks}
-  const int4* sup_b;        // per supertile {first unit, units, single (V read from global, units looped), 0}
-  const int2* sup_chunk;    // per chunk [first slot, end slot) (global slots)
-  const int2* chunk_blob;   // per chunk {byte offset / 16, bytes} of its pair blob in sblob (regular supertiles)
-  const int2* chunk_meta;   // per chunk {supertile (-1: single), first unit slot of the supertile}
-  const int* cta_chunk;     // persistent k_schur_super: CTA i streams chunks [cta_chunk[i], cta_chunk[i + 1])
-  const int* cta_nreg;      // ... of which cta_nreg[i] are regular
-  int sup_grid;
-  const char* sblob;
-  const int2* unit_pr;      // per unit [first pair, end pair) into spairs
-  const unsigned* spairs;   // pairs k | l << 16, supertile-local slots, (supertile, block, point) order
-  double* upart;            // 36 per unit: the unit's sum of V_k V_l^T (row-major)
-  const int* blk_uptr;      // nblk + 1
-  const int* blk_units;     // per camera block its units in (supertile, part) order
-  int nsup, nsup_single;
   double* stiles;
   long long stile_count;
   unsigned long long* trace;  // per-tile phase timestamps (BAE_TRACE) or null
@@ -164,46 +144,11 @@ constexpr int kScrTp = kScrStage + 6 * kPipeObs * 8;                // t_p [kPip
 constexpr int kScrBar = kScrTp + kPipePts * 24;                     // 4 mbarriers
 constexpr int kPipeWarpBytes = (kScrBar + 32 + 127) / 128 * 128;
 
-// ---- supertile Schur assembly (k_schur_super) ----
-// A regular supertile touches at most kSupCams cameras (<= 136 camera blocks)
-// and is streamed through kSupBufs shared-memory stages, each holding one
-// chunk (whole warp-tiles, at most kSupChunkObs V records and kSupChunkPairs
-// pairs): the chunk's V records and its pair blob (the pair offsets of every
-// unit slot, then the pairs, chunk-local k | l << 16). One producer warp
-// issues the TMA copies; each of the kSupConsumerWarps consumer warps owns up
-// to kSupJ of the supertile's camera blocks (unit slots warp * kSupJ + j) and
-// accumulates them on the FP64 tensor cores. A warp-tile over any cap is a
-// "single" supertile of its own: V read from global memory, a thread per unit
-// in turn (k_schur_single).
-constexpr int kSupCams = 16, kSupMaxObs = 8192;
-constexpr int kSupWarps = 12, kSupConsumerWarps = 11, kSupJ = 16, kSupUnits = kSupConsumerWarps * kSupJ;
-constexpr int kSupBufs = 4, kSupChunkObs = 320, kSupChunkPairs = 2048;
-static_assert(kSupChunkObs * 18 * 8 < 65536, "pair words hold 16-bit byte offsets of V records");
-constexpr int kVRec = 18;  // doubles per V record (6 x 3 row-major)
-constexpr int kSupOffBytes = (2 * (kSupUnits + 1) + 15) / 16 * 16;
-constexpr int kSupVBytes = kSupChunkObs * kVRec * 8;
-constexpr int kSupStage = kSupVBytes + kSupOffBytes + 4 * kSupChunkPairs;
-constexpr int kSupSmem = kSupBufs * kSupStage + 2 * kSupBufs * 8 + kSupBufs * 8;
-constexpr int kSupKeyStride = 512;  // pair sort key: chunk * kSupKeyStride + unit slot
-
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Non-blocking: has the phase of the given parity completed?
-__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
-  unsigned ok = 0;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
 }
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {

@@ -240,7 +240,7 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
   o[15] = intr[c * 4 + 3];
 }
 
-constexpr int kVStride = kVRec;  // doubles per V = W L^-T record (6 x 3 row-major, 144 B: 16-byte aligned)
+constexpr int kVStride = 20;  // doubles per V = W L^-T record (two 16-byte aligned halves of 9)
 // Direct solver prep, shared by k_prep<true> and the fused k_lin_prep (one
 // copy of the arithmetic, so the two agree bit for bit).
 // Per point: damped H~_pp, its inverse (d.hinv, for the
@@ -282,21 +282,23 @@ __device__ __forceinline__ bool prep_point_direct(const Dev& d, long long ip, do
 }
 
 // Direct solver, per observation slot: V = W L^-T (V V^T = W H~^-1 W^T)
-// stored as one 144-byte record (6 x 3 row-major), and the Schur right-hand
-// side piece W v into rhs[0..5].
+// stored as two 16-byte aligned halves, and the Schur right-hand side piece
+// W v into rhs[0..5].
 __device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, const double (&W)[18],
                                                 const double* sp, double* rhs) {
   const double* lf = sp + 3;
-  double vv[kVStride];
+  double vv[kVStride];  // rows 0..2 at [0, 9), rows 3..5 at [10, 19)
 #pragma unroll
   for (int a = 0; a < 6; ++a) {
     const double v0 = W[a * 3] * lf[0];
     const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
     const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
-    vv[a * 3] = v0;
-    vv[a * 3 + 1] = v1;
-    vv[a * 3 + 2] = v2;
+    const int o = a * 3 + (a >= 3 ? 1 : 0);
+    vv[o] = v0;
+    vv[o + 1] = v1;
+    vv[o + 2] = v2;
   }
+  vv[9] = vv[19] = 0.0;  // whole sectors written
   double2* vo = reinterpret_cast<double2*>(d.wstore + slot * kVStride);
 #pragma unroll
   for (int j = 0; j < kVStride / 2; ++j) vo[j] = make_double2(vv[2 * j], vv[2 * j + 1]);
@@ -1012,15 +1014,21 @@ __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
 #pragma unroll 2
   for (int q = ch.y + slot; q < qe; q += 8) {
     const int2 pr = d.pairs[q];
-    // V_k rows r0..r0+2 and V_l rows c0..c0+2: 9 contiguous doubles each
-    const double* wh = d.wstore + (long long)pr.x * kVStride + 3 * r0;
-    const double* w = d.wstore + (long long)pr.y * kVStride + 3 * c0;
+    // V_k rows r0..r0+2 and V_l rows c0..c0+2: 16-byte aligned 9-double halves
+    const double* wh = d.wstore + (long long)pr.x * kVStride + (r0 ? 10 : 0);
+    const double* w = d.wstore + (long long)pr.y * kVStride + (c0 ? 10 : 0);
     double a[9], b[9];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) {
-      a[j] = __ldg(wh + j);
-      b[j] = __ldg(w + j);
+    for (int j = 0; j < 4; ++j) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(wh) + j);
+      const double2 y = __ldg(reinterpret_cast<const double2*>(w) + j);
+      a[2 * j] = x.x;
+      a[2 * j + 1] = x.y;
+      b[2 * j] = y.x;
+      b[2 * j + 1] = y.y;
     }
+    a[8] = __ldg(wh + 8);
+    b[8] = __ldg(w + 8);
 #pragma unroll
     for (int x = 0; x < 3; ++x)
 #pragma unroll
@@ -1102,232 +1110,6 @@ __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
     double v = -v36b;
     if (diag) v += h[sym6(r, c)];
     base[r * ldr + c * ldc] = v;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// F2': supertile Schur assembly (default; DESIGN.md 5.3 step 3). One CTA per
-// supertile (a run of warp-tiles touching at most kSupCams cameras). Its V
-// records arrive chunk by chunk (TMA bulk copies into two shared-memory
-// buffers, the next chunk in flight while the current one is consumed); each
-// thread owns one unit -- a range of one camera block's pairs in (point, k, l)
-// order -- and accumulates sum V_k V_l^T (36 FMA chains) in registers across
-// the chunks, so every V record crosses HBM once and the pair products read
-// shared memory. k_schur_reduce then adds each block's units in (supertile,
-// range) order. Every order is fixed by the plan: deterministic, no atomics.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void pair_acc(const double* __restrict__ vk, const double* __restrict__ vl,
-                                         double (&acc)[36]) {
-  double a[18];
-#pragma unroll
-  for (int j = 0; j < 9; ++j) {
-    const double2 x = reinterpret_cast<const double2*>(vk)[j];
-    a[2 * j] = x.x;
-    a[2 * j + 1] = x.y;
-  }
-#pragma unroll
-  for (int m = 0; m < 6; m += 2) {  // rows m, m + 1 of V_l (one 48-byte band): columns m, m + 1 of the block
-    const double2 x0 = reinterpret_cast<const double2*>(vl)[3 * (m >> 1)];
-    const double2 x1 = reinterpret_cast<const double2*>(vl)[3 * (m >> 1) + 1];
-    const double2 x2 = reinterpret_cast<const double2*>(vl)[3 * (m >> 1) + 2];
-    const double b[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};
-#pragma unroll
-    for (int mm = 0; mm < 2; ++mm)
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        double t = acc[i * 6 + m + mm];
-        t = fma(a[3 * i], b[3 * mm], t);
-        t = fma(a[3 * i + 1], b[3 * mm + 1], t);
-        t = fma(a[3 * i + 2], b[3 * mm + 2], t);
-        acc[i * 6 + m + mm] = t;
-      }
-  }
-}
-
-__device__ __forceinline__ void store_unit(const Dev& d, int u, const double (&acc)[36]) {
-  double2* o = reinterpret_cast<double2*>(d.upart + 36LL * u);
-#pragma unroll
-  for (int j = 0; j < 18; ++j) o[j] = make_double2(acc[2 * j], acc[2 * j + 1]);
-}
-
-__global__ void __launch_bounds__(32 * kSupWarps, 1) k_schur_super(Dev d) {
-  // Persistent: CTA i streams the regular chunks of its supertile range
-  // (d.cta_chunk, balanced by pairs) through kSupBufs stages; the producer
-  // warp passes each chunk's supertile {index, first unit slot} with it.
-  extern __shared__ __align__(128) char smem[];
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + kSupBufs * kSupStage);
-  unsigned long long* empty = full + kSupBufs;
-  int2* meta = reinterpret_cast<int2*>(empty + kSupBufs);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g0 = d.cta_chunk[blockIdx.x], g1 = d.cta_chunk[blockIdx.x + 1];
-  const int ntot = d.cta_nreg[blockIdx.x];  // regular chunks in [g0, g1)
-  if (tid == 0) {
-    for (int b = 0; b < kSupBufs; ++b) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], kSupConsumerWarps);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (warp == kSupConsumerWarps) {  // producer
-    int n = 0;                      // chunks issued
-    for (int base = g0; base < g1; base += 32) {
-      const int g = base + lane;
-      int2 sr = make_int2(0, 0), bl = make_int2(0, 0), mt = make_int2(-1, 0);
-      if (g < g1) {
-        sr = d.sup_chunk[g];
-        bl = d.chunk_blob[g];
-        mt = d.chunk_meta[g];
-      }
-      const int cnt = min(32, g1 - base);
-      for (int j = 0; j < cnt; ++j) {
-        const int sx = __shfl_sync(0xffffffffu, sr.x, j), sy = __shfl_sync(0xffffffffu, sr.y, j);
-        const int bx = __shfl_sync(0xffffffffu, bl.x, j), by = __shfl_sync(0xffffffffu, bl.y, j);
-        const int mx = __shfl_sync(0xffffffffu, mt.x, j), my = __shfl_sync(0xffffffffu, mt.y, j);
-        if (mx < 0) continue;  // a single supertile's chunk (k_schur_single)
-        if (lane == 0) {
-          const int b = n % kSupBufs;
-          if (n >= kSupBufs) mbar_wait(&empty[b], ((n / kSupBufs) - 1) & 1);
-          meta[b] = make_int2(mx, my);
-          const unsigned vbytes = (unsigned)(sy - sx) * (unsigned)(kVRec * 8);
-          char* st = smem + b * kSupStage;
-          mbar_expect_tx(&full[b], vbytes + (unsigned)by);
-          bulk_g2s(st, d.wstore + (long long)sx * kVRec, vbytes, &full[b]);
-          bulk_g2s(st + kSupVBytes, d.sblob + 16LL * bx, (unsigned)by, &full[b]);
-        }
-        ++n;
-      }
-    }
-    return;
-  }
-  // Consumers: warp w owns unit slots w * kSupJ + j of the current supertile
-  // (one camera block each) and sums V_k V_l^T over each block's pairs with
-  // FP64 MMA (m8n8k4): K runs over (pair, component), four per MMA; lane
-  // (g, t) = (lane / 4, lane % 4) feeds A[g][t] = V_k[g][comp] and
-  // B[t][g] = V_l[g][comp] (rows g >= 6 zero) and holds C[g][2t, 2t + 1] of
-  // the 8 x 8 accumulator (the 6 x 6 block in its top-left corner). A warp
-  // releases chunk n (one arrival on its stage's empty barrier) when done;
-  // at a supertile change it stores its used blocks. Every sum's order is
-  // fixed by the plan (pairs in point order, K in component order).
-  const int g = lane >> 2, t = lane & 3;
-  double acc[kSupJ][2];
-#pragma unroll
-  for (int j = 0; j < kSupJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-  unsigned usedmask = 0;
-  int sup = -1, slot0 = 0;
-  auto store = [&]() {
-    if (g < 6 && t < 3) {
-#pragma unroll
-      for (int j = 0; j < kSupJ; ++j)
-        if (usedmask >> j & 1u)
-          *reinterpret_cast<double2*>(d.upart + 36LL * (slot0 + warp * kSupJ + j) + g * 6 + 2 * t) =
-              make_double2(acc[j][0], acc[j][1]);
-    }
-  };
-  for (int n = 0; n < ntot; ++n) {
-    const int b = n % kSupBufs;
-    mbar_wait(&full[b], (n / kSupBufs) & 1);
-    const int2 mt = meta[b];
-    if (mt.x != sup) {
-      store();
-#pragma unroll
-      for (int j = 0; j < kSupJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-      usedmask = 0;
-      sup = mt.x;
-      slot0 = mt.y;
-    }
-    const char* st = smem + b * kSupStage;
-    const double* V = reinterpret_cast<const double*>(st);
-    const unsigned short* off = reinterpret_cast<const unsigned short*>(st + kSupVBytes) + warp * kSupJ;
-    const unsigned* pr = reinterpret_cast<const unsigned*>(st + kSupVBytes + kSupOffBytes);
-#pragma unroll
-    for (int j = 0; j < kSupJ; ++j) {
-      const int q0 = off[j], np3 = 3 * (off[j + 1] - q0);
-      if (np3 == 0) continue;
-      usedmask |= 1u << j;
-      double c0 = acc[j][0], c1 = acc[j][1];
-      // 4 pairs = 12 K values = 3 MMAs; MMA m takes K = 4m + t, i.e. pair
-      // (4m + t) / 3 of the group, component (4m + t) % 3 (constants per
-      // lane); the pair words hold byte offsets of the V records. Lanes past
-      // the pairs or on padding rows (g >= 6) load a valid address and feed 0.
-      const int np = np3 / 3;
-      const char* Vb = reinterpret_cast<const char*>(V);
-      for (int base = 0; base < np; base += 4) {
-        const int left3 = 3 * (np - base);
-        double av[3], bv[3];
-#pragma unroll
-        for (int m = 0; m < 3; ++m) {
-          const int pi = base + (4 * m + t) / 3;
-          const bool ok = g < 6 && pi < np;
-          const unsigned w = pr[q0 + (ok ? pi : 0)];
-          const int o = 8 * (3 * (g < 6 ? g : 0) + (4 * m + t) % 3);
-          const double x = *reinterpret_cast<const double*>(Vb + (w & 0xffffu) + o);
-          const double y = *reinterpret_cast<const double*>(Vb + (w >> 16) + o);
-          av[m] = ok ? x : 0.0;
-          bv[m] = ok ? y : 0.0;
-        }
-#pragma unroll
-        for (int m = 0; m < 3; ++m)
-          if (4 * m < left3)  // warp-uniform: the rest of the group is padding
-            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                : "+d"(c0), "+d"(c1)
-                : "d"(av[m]), "d"(bv[m]));
-      }
-      acc[j][0] = c0;
-      acc[j][1] = c1;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);
-  }
-  store();
-}
-
-// Supertiles of one long warp-tile (over kSupChunkObs observations or
-// kSupCams cameras): V straight from global memory, a thread per unit in turn.
-__global__ void __launch_bounds__(256) k_schur_single(Dev d) {
-  const int sp = blockIdx.x;
-  const int4 A = d.sup_a[sp];
-  const int4 B = d.sup_b[sp];
-  if (!B.z) return;
-  const double* V = d.wstore + (long long)A.x * kVRec;
-  double acc[36];
-  for (int u = threadIdx.x; u < B.y; u += blockDim.x) {
-#pragma unroll
-    for (int j = 0; j < 36; ++j) acc[j] = 0.0;
-    const int2 pr = d.unit_pr[B.x + u];
-    for (int q = pr.x; q < pr.y; ++q) {
-      const unsigned p = d.spairs[q];
-      pair_acc(V + (long long)(p & 0xffffu) * kVRec, V + (long long)(p >> 16) * kVRec, acc);
-    }
-    store_unit(d, B.x + u, acc);
-  }
-}
-
-// S blocks from their units (thread per block entry): sum in (supertile,
-// range) order, negate, add H~_cc on the diagonal (single rank), place into
-// the block's tile (or the dense S). Diagonal blocks take the upper triangle
-// of the sum for both halves (exactly symmetric).
-__global__ void __launch_bounds__(256) k_schur_reduce(Dev d) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= 36LL * d.nblk) return;
-  const int blk = (int)(idx / 36), e = (int)(idx % 36), r = e / 6, c = e % 6;
-  const int2 cc = d.blk_cam[blk];
-  const bool dg = cc.x == cc.y;
-  const int src = dg ? min(r, c) * 6 + max(r, c) : e;
-  double v = 0.0;
-  const int u1 = d.blk_uptr[blk + 1];
-  for (int i = d.blk_uptr[blk]; i < u1; ++i) v += d.upart[36LL * d.blk_units[i] + src];
-  v = -v;
-  if (dg && !d.cred) v += d.hccd[(long long)cc.x * 21 + sym6(r, c)];
-  if (d.stiles) {
-    const int2 bt = d.blk_tile[blk];
-    const int ro = bt.y & 0xff, co = (bt.y >> 8) & 0xff;
-    const bool tr = (bt.y >> 16) & 1;
-    double* base = d.stiles + (long long)bt.x * kSTileElems + co * 48 + ro;
-    base[tr ? r * 48 + c : r + c * 48] = v;
-  } else {
-    const long long n = 6LL * d.C;
-    d.schur[(6LL * cc.y + c) * n + 6LL * cc.x + r] = v;
   }
 }
 
@@ -2163,7 +1945,6 @@ void set_smem_limits(int max_bytes) {
   cudaFuncSetAttribute(k_schur_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_backsub_trial, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
   cudaFuncSetAttribute(k_pcg_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
-  cudaFuncSetAttribute(k_schur_super, cudaFuncAttributeMaxDynamicSharedMemorySize, kSupSmem);
 }
 
 static inline int cam_blocks(int C) { return (C + kWarpsPerCamBlock - 1) / kWarpsPerCamBlock; }
@@ -2320,15 +2101,7 @@ int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) 
 }
 int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
   int n = 0;
-  if (d.nblk > 0 && d.nsup > 0) {
-    k_schur_super<<<d.sup_grid, 32 * kSupWarps, kSupSmem, s>>>(d);
-    if (d.nsup_single) {
-      k_schur_single<<<d.nsup, 256, 0, s>>>(d);
-      ++n;
-    }
-    k_schur_reduce<<<elt_blocks(36LL * d.nblk, 256), 256, 0, s>>>(d);
-    n += 2;
-  } else if (d.nblk > 0) {
+  if (d.nblk > 0) {
     cudaMemsetAsync(d.blk_ticket, 0, sizeof(unsigned) * d.nblk, s);
     k_schur_dense<<<(d.nchunk + 7) / 8, 256, 0, s>>>(d);
     ++n;

@@ -23,8 +23,9 @@
 #include "problem.hpp"
 
 // Launch wrappers return their kernel count; BAE_CHECK_LAUNCH=1 also checks
-// the runtime's error state after every one (a debugging aid: a failed launch
-// is named at its call site instead of surfacing at a later API call).
+// the runtime's error state before and after every one (a debugging aid: a
+// failed launch or API call is named near its call site instead of
+// surfacing at a later, unrelated API call).
 #define BAE_LAUNCHED(x)                                                 \
   do {                                                                  \
     if (check_launch_) ck(cudaPeekAtLastError(), "before launch: " #x); \
@@ -408,18 +409,6 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.blk_nchunk = nullptr;
   d.blk_ticket = nullptr;
   d.schur_part = nullptr;
-  d.sup_a = d.sup_b = nullptr;
-  d.sup_chunk = d.unit_pr = nullptr;
-  d.chunk_blob = nullptr;
-  d.chunk_meta = nullptr;
-  d.cta_chunk = d.cta_nreg = nullptr;
-  d.sup_grid = 0;
-  d.sblob = nullptr;
-  d.spairs = nullptr;
-  d.upart = nullptr;
-  d.blk_uptr = d.blk_units = nullptr;
-  d.nsup = 0;
-  d.nsup_single = 0;
   d.nblk = 0;
   d.schur = nullptr;
   ht.mark("allocs");
@@ -931,38 +920,7 @@ void Problem::build_direct() {
     d_.schur_part = dalloc<double>(36 * chunks.size());
   }
   d_.nblk = static_cast<int>(bcam.size());
-  {  // supertiles of the Schur assembly (BAE_SCHUR=pairs: the pair-chunk kernel instead)
-    const char* sm = std::getenv("BAE_SCHUR");
-    if (!(sm && std::string(sm) == "pairs") && npairs_ > 0) {
-      SuperHost sh;
-      unsigned* sp = dalloc<unsigned>(static_cast<std::size_t>(npairs_));
-      int nsm = 148;
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, opt_.device);
-      build_super(d_, plan_, d_.pairs, d_.blk_ptr, bptr, npairs_, sp, sh, nsm,
-                  [this](std::size_t n) { return static_cast<void*>(dalloc<char>(n)); }, stream_);
-      d_.spairs = sp;
-      d_.sblob = sh.blob;
-      d_.chunk_blob = sh.chunk_blob;
-      d_.chunk_meta = upload(sh.chunk_meta);
-      d_.cta_chunk = upload(sh.cta_chunk);
-      d_.cta_nreg = upload(sh.cta_nreg);
-      d_.sup_grid = static_cast<int>(sh.cta_nreg.size());
-      d_.sup_a = upload(sh.sup_a);
-      d_.sup_b = upload(sh.sup_b);
-      d_.sup_chunk = upload(sh.sup_chunk);
-      d_.unit_pr = upload(sh.unit_pr);
-      d_.blk_uptr = upload(sh.blk_uptr);
-      d_.blk_units = upload(sh.blk_units);
-      d_.upart = dalloc<double>(36 * static_cast<std::size_t>(sh.units));
-      d_.nsup = static_cast<int>(sh.sup_a.size());
-      d_.nsup_single = sh.single;
-      sup_regular_ = sh.regular;
-      sup_single_ = sh.single;
-      sup_units_ = sh.units;
-      sup_chunks_ = static_cast<long long>(sh.sup_chunk.size());
-    }
-  }
-  if (!d_.wstore) d_.wstore = dalloc<double>(18 * static_cast<std::size_t>(plan_.N));  // kVStride
+  if (!d_.wstore) d_.wstore = dalloc<double>(20 * static_cast<std::size_t>(plan_.N));  // kVStride
   if (!d_.lam) {
     d_.lam = dalloc<double>(1);
     lam_host_ = static_cast<double*>(pinned_take());

@@ -98,12 +98,6 @@ class Problem {
   // [tile columns, stored tiles, tile updates, ordering groups, positions] of the tile Cholesky (0 before use)
   long long direct_pairs() const { return npairs_; }
   long long direct_blocks() const { return d_.nblk; }
-  void schur_stats(long long* out4) const {
-    out4[0] = sup_regular_;
-    out4[1] = sup_single_;
-    out4[2] = sup_units_;
-    out4[3] = sup_chunks_;
-  }
   void direct_stats(long long* out5) const {
     out5[0] = tchol_.nt;
     out5[1] = tchol_.nnz;
@@ -173,9 +167,7 @@ class Problem {
   double graph_clo_ = 0.0, graph_chi_ = 0.0;
   bool lm_graph_failed_ = false;
   long long npairs_ = 0;
-  bool check_launch_ = std::getenv("BAE_CHECK_LAUNCH") != nullptr;
-  int sup_regular_ = 0, sup_single_ = 0;       // Schur assembly supertiles (regular / one long warp-tile)
-  long long sup_units_ = 0, sup_chunks_ = 0;                     // direct solver: (k, l) pairs of the Schur assembly
+  bool check_launch_ = std::getenv("BAE_CHECK_LAUNCH") != nullptr;  // BAE_LAUNCHED (problem.cu)                     // direct solver: (k, l) pairs of the Schur assembly
   bool defer_factor_check_ = false;          // optimize: the direct factorisation's failure word read later
   Plan plan_;
   Dev d_{};

@@ -17,4 +17,4 @@ for _ in range(reps):
     t = time.perf_counter()
     g.solve_step(1e-4, bae.LmConfig())
     print(f"solve_step {1e3 * (time.perf_counter() - t):.2f} ms")
-print(g.schur_stats(), g.direct_stats())
+print(g.direct_stats())
