@@ -224,9 +224,11 @@ int bae_optimize(bae_problem* p, const double* init_poses7, const double* init_p
                  const bae_lm_config* cfg, bae_iter_record* traj, int32_t traj_cap,
                  bae_lm_report* report, double* poses_out, double* points_out);
 
-/* ---- reduced-camera-system solve, one damping value (assemble + pcg) -------- */
-/* Linearises at the current parameters, damps with lambda and solves with the
- * implicit-Schur PCG; delta receives [6C pose tangents | 3P point deltas] in
+/* ---- one damped solve (lm.hpp:126-145) --------------------------------------- */
+/* Linearises at the current parameters, damps with lambda and solves with
+ * cfg->solver: the tile-sparse Cholesky of the reduced camera system
+ * (BAE_SOLVER_CHOLESKY, the reference default) or the implicit-Schur PCG
+ * (BAE_SOLVER_PCG); delta receives [6C pose tangents | 3P point deltas] in
  * the reference's column order (lm.hpp:159-173). */
 int bae_solve_step(bae_problem* p, double lambda, const bae_lm_config* cfg, double* delta,
                    int64_t* pcg_iters, double* rel_residual);
