@@ -143,6 +143,13 @@ constexpr int kScrStage = 2 * kBufBytes;                            // stage [6]
 constexpr int kScrTp = kScrStage + 6 * kPipeObs * 8;                // t_p [kPipePts][3]
 constexpr int kScrBar = kScrTp + kPipePts * 24;                     // 4 mbarriers
 constexpr int kPipeWarpBytes = (kScrBar + 32 + 127) / 128 * 128;
+// Warp-tiles per CTA of the pipelined Schur product (k_schur_tiles,
+// k_pcg_persistent): two such CTAs fill an SM's shared memory.
+constexpr int kSchurWarps = 4;
+// Their register cap: no spills (the 128 of two 256-thread CTAs spilled),
+// 168 measured fastest (200 and 255 schedule worse: Venice tile pass
+// 234 vs 296 us).
+constexpr int kSchurMaxReg = 168;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));

@@ -1627,7 +1627,7 @@ __device__ __forceinline__ void sx_all_tiles(const Dev& d, const PcgDev& st, cha
   for (int i = gwarp; i < d.n_big_tiles; i += nwarps) sx_tile(d, st, d.big_tiles[i], smem, 0);
 }
 
-__global__ void __launch_bounds__(256, 2) k_schur_tiles(Dev d, int slice) {
+__global__ void __maxnreg__(kSchurMaxReg) k_schur_tiles(Dev d, int slice) {
   extern __shared__ __align__(128) char smem[];
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
@@ -1716,7 +1716,7 @@ __device__ __forceinline__ void sum_block_partials(const double* part, int nbloc
 // vector update separated by grid barriers; the scalar recurrence is
 // evaluated redundantly (bit-identically) by every block, so no block waits
 // on another for alpha / beta. Runs up to max_iters iterations per launch.
-__global__ void __launch_bounds__(256, 2) k_pcg_persistent(Dev d, int slice, long long max_iters) {
+__global__ void __launch_bounds__(32 * kSchurWarps, 2) k_pcg_persistent(Dev d, int slice, long long max_iters) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) char smem[];

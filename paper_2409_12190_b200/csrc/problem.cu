@@ -317,7 +317,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   }
   ht.mark("tile blobs");
   sm_.schur.slice = kPipeWarpBytes;  // pipelined double buffer per warp
-  sm_.schur.wpb = 4;
+  sm_.schur.wpb = kSchurWarps;
   big_stride = (big_stride + 255) / 256 * 256;
   set_smem_limits(kSmemLimit);
 
