@@ -1664,36 +1664,43 @@ __global__ void __launch_bounds__(128) k_schur_cams(Dev d) {
   d.cam_dot[c] = pap;
 }
 
-// PCG step on the camera vectors (one block, fixed-order sums): alpha from
-// p.Sp (pcg.hpp:73-77), x/r/z update and the recurrence / true-residual
-// decision (pcg.hpp:78-129).
-__global__ void __launch_bounds__(1024) k_pcg_update(Dev d) {
+// PCG step on the camera vectors (pcg.hpp:73-129), a thread per camera:
+// every block forms p.Sp from the per-camera dots in the same fixed order
+// (so all blocks hold the identical alpha), updates x, r, z of its cameras,
+// and the last block to finish sums the blocks' r.r, r.z in block order and
+// runs the recurrence / true-residual decision.
+constexpr int kUpdNT = 256;
+__global__ void __launch_bounds__(kUpdNT) k_pcg_update(Dev d) {
   __shared__ double red[32];
   __shared__ double s_pap;
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
-  double pap = 0.0;
-  for (int c = threadIdx.x; c < d.C; c += blockDim.x) pap += d.cam_dot[c];
-  pap = block_sum(pap, red);
-  if (threadIdx.x == 0) s_pap = pap;
-  __syncthreads();
   double alpha = 0.0;
   if (st.dir != kDirX) {
+    double pap = 0.0;
+    for (int c = threadIdx.x; c < d.C; c += blockDim.x) pap += d.cam_dot[c];
+    pap = block_sum(pap, red);
+    if (threadIdx.x == 0) s_pap = pap;
+    __syncthreads();
     alpha = st.rz / s_pap;
-    if (!isfinite(alpha)) {  // pcg.hpp:77
-      if (threadIdx.x == 0) d.pcg->state = kPcgBreakdown;
+    if (!isfinite(alpha)) {  // pcg.hpp:77 (every block sees it and stops)
+      if (blockIdx.x == 0 && threadIdx.x == 0) d.pcg->state = kPcgBreakdown;
       return;
     }
   }
   double rr = 0.0, rz = 0.0;
-  for (int c = threadIdx.x; c < d.C; c += blockDim.x) pcg_camera_update(d, st, alpha, c, rr, rz);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < d.C) pcg_camera_update(d, st, alpha, c, rr, rz);
+  __syncthreads();
   rr = block_sum(rr, red);
   __syncthreads();
   rz = block_sum(rz, red);
-  if (threadIdx.x == 0) {
+  const double part[2] = {rr, rz};
+  double tot[2];
+  if (grid_reduce<2>(part, d.block_red, d.tickets, tot) && threadIdx.x == 0) {
     PcgDev o = st;
     o.alpha = alpha;
-    pcg_decide(o, rr, rz);
+    pcg_decide(o, tot[0], tot[1]);
     *d.pcg = o;
   }
 }
@@ -2058,7 +2065,7 @@ int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm
     ++n;
   }
   k_schur_cams<<<d.C, 128, 0, s>>>(d);
-  k_pcg_update<<<1, 1024, 0, s>>>(d);
+  k_pcg_update<<<elt_blocks(d.C, kUpdNT), kUpdNT, 0, s>>>(d);
   return n;
 }
 static int resident_grid(const void* fn, int threads, int smem) {
