@@ -144,8 +144,9 @@ int64_t bae_last_error_index(void);
 /* 128-byte NCCL unique id for bae_create_options.nccl_id (rank 0 creates it;
  * NCCL is loaded at run time, BAE_ERR_NCCL if libnccl.so.2 is absent). */
 int bae_nccl_unique_id(void* out128);
-/* In-process rank group of `world` ranks (1..16) for bae_create_options.group;
- * destroy it after every problem that uses it. */
+/* In-process rank group of `world` ranks (1..16) for bae_create_options.group.
+ * Reference counted: the caller's handle and every problem created with it
+ * own it, so bae_group_destroy may come before the problems are destroyed. */
 int bae_group_create(int32_t world, bae_group** out);
 void bae_group_destroy(bae_group* g);
 

@@ -406,7 +406,8 @@ def make_pgo_problem(poses, edge_i=None, edge_j=None, measurements=None, informa
 
 class RankGroup:
     """In-process rank group: ``world`` ranks in one process, one host thread
-    per rank (bae_group_create). Keep it alive while its problems exist."""
+    per rank (bae_group_create). Its problems keep the native group alive
+    after this handle is dropped."""
 
     def __init__(self, world: int):
         self._h = ctypes.c_void_p()
@@ -474,7 +475,9 @@ def make_ba_problem(poses, points, intrinsics, observations, *, device: int = 0,
     h = ctypes.c_void_p()
     _check(lib.bae_create_ba(ptr(p7), C, ptr(p3), P, ptr(k3), ptr(ci, ctypes.c_int32), ptr(pi, ctypes.c_int32),
                              ptr(px), N, ctypes.byref(opt), ctypes.byref(h)))
-    return TracedProblem(h, C, P, N)
+    tp = TracedProblem(h, C, P, N)
+    tp._group = group  # the group also outlives its handle on the C side (reference counted)
+    return tp
 
 
 def optimize(model: TracedProblem, init_poses, init_points, config: LmConfig,

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -22,6 +23,10 @@ constexpr int kMaxGroup = 16;
 // done reading). Owned by the caller (bae_group_create / bae_group_destroy).
 struct bae_group {
   int world = 0;
+  // owners: the caller's handle (bae_group_destroy) and every rank's
+  // communicator; the last one to let go frees the group, so a problem may
+  // outlive the caller's handle
+  std::atomic<int> refs{1};
   std::mutex m;
   std::condition_variable cv;
   int arrived = 0;
@@ -154,9 +159,14 @@ __global__ void k_group_min(PtrPack<int> src, int world, long long n, int* __res
   }
 }
 
+void group_release(bae_group* g) {
+  if (g && g->refs.fetch_sub(1) == 1) delete g;
+}
+
 class GroupComm final : public Comm {
  public:
   GroupComm(bae_group* g, int rank, int device) : Comm(rank, g->world), g_(g), device_(device) {
+    g->refs.fetch_add(1);
     ck(cudaSetDevice(device), "cudaSetDevice");
     ck(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming), "event");
@@ -177,6 +187,7 @@ class GroupComm final : public Comm {
     cudaEventDestroy(g_->done[rank()]);
     g_->ready[rank()] = nullptr;
     g_->done[rank()] = nullptr;
+    group_release(g_);
   }
 
   void allreduce_sum(double* buf, std::size_t n, cudaStream_t s) override {
@@ -268,7 +279,7 @@ bae_group* group_create(int world) {
   return g;
 }
 
-void group_destroy(bae_group* g) { delete g; }
+void group_destroy(bae_group* g) { group_release(g); }
 
 }  // namespace bae
 
