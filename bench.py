@@ -149,6 +149,10 @@ class ClockSampler:
 def _dist_init():
     rank, world = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1)
     if world > 1:
+        # NCCL's INIT lines (communicator size, ranks, NVLink/NVLS paths) on
+        # stderr, so a multi-GPU run's log shows the ranks that took part
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("gloo")
         return rank, world, dist

@@ -72,6 +72,9 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -91,9 +94,11 @@ const NcclApi& nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+    api.Reduce = reinterpret_cast<decltype(api.Reduce)>(dlsym(h, "ncclReduce"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(dlsym(h, "ncclBroadcast"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
     if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllReduce || !api.AllGather ||
-        !api.GetErrorString) {
+        !api.Reduce || !api.Broadcast || !api.GetErrorString) {
       err = "libnccl.so.2 lacks an expected symbol";
       api = NcclApi{};
     }
@@ -124,6 +129,12 @@ class NcclComm final : public Comm {
   }
   void allreduce_min(int* buf, std::size_t n, cudaStream_t s) override {
     nck(nccl().AllReduce(buf, buf, n, ncclInt32, ncclMin, comm_, s), "ncclAllReduce(min)");
+  }
+  void reduce_sum(double* buf, std::size_t n, int root, cudaStream_t s) override {
+    nck(nccl().Reduce(buf, buf, n, ncclFloat64, ncclSum, root, comm_, s), "ncclReduce(sum)");
+  }
+  void broadcast(void* buf, std::size_t bytes, int root, cudaStream_t s) override {
+    nck(nccl().Broadcast(buf, buf, bytes, ncclUint8, root, comm_, s), "ncclBroadcast");
   }
   void allgather(const void* send, void* recv, std::size_t bytes, cudaStream_t s) override {
     nck(nccl().AllGather(send, recv, bytes, ncclUint8, comm_, s), "ncclAllGather");
@@ -200,6 +211,20 @@ class GroupComm final : public Comm {
       k_group_min<<<blocks, 256, 0, s>>>(pk, world(), static_cast<long long>(n), static_cast<int*>(out));
     });
   }
+  void reduce_sum(double* buf, std::size_t n, int root, cudaStream_t s) override {
+    reduce<double>(
+        buf, n, s,
+        [&](const PtrPack<double>& pk, int blocks, void* out) {
+          k_group_sum<<<blocks, 256, 0, s>>>(pk, world(), static_cast<long long>(n), static_cast<double*>(out));
+        },
+        root);
+  }
+  void broadcast(void* buf, std::size_t bytes, int root, cudaStream_t s) override {
+    if (bytes == 0) return;
+    publish(buf, s);
+    if (rank() != root) ck(cudaMemcpyAsync(buf, g_->src[root], bytes, cudaMemcpyDefault, s), "group broadcast");
+    retire(s);
+  }
   void allgather(const void* send, void* recv, std::size_t bytes, cudaStream_t s) override {
     publish(send, s);
     for (int q = 0; q < world(); ++q)
@@ -225,10 +250,13 @@ class GroupComm final : public Comm {
     for (int q = 0; q < world(); ++q)
       if (q != rank()) ck(cudaStreamWaitEvent(s, g_->done[q], 0), "stream wait");
   }
+  // Element-wise reduction of every rank's buf (fixed rank order) into buf
+  // of every rank, or of `root` only (root >= 0).
   template <class T, class Launch>
-  void reduce(T* buf, std::size_t n, cudaStream_t s, Launch launch) {
+  void reduce(T* buf, std::size_t n, cudaStream_t s, Launch launch, int root = -1) {
     if (n == 0) return;
-    if (scratch_bytes_ < n * sizeof(T)) {
+    const bool mine = root < 0 || root == rank();
+    if (mine && scratch_bytes_ < n * sizeof(T)) {
       if (scratch_) ck(cudaFree(scratch_), "cudaFree");
       scratch_ = nullptr;
       ck(cudaMalloc(&scratch_, n * sizeof(T)), "cudaMalloc");
@@ -238,10 +266,12 @@ class GroupComm final : public Comm {
     PtrPack<T> pk{};
     for (int q = 0; q < world(); ++q) pk.p[q] = static_cast<const T*>(g_->src[q]);
     const int blocks = static_cast<int>(std::min<std::size_t>((n + 255) / 256, 1184));
-    launch(pk, blocks, scratch_);
-    ck(cudaGetLastError(), "group reduce launch");
+    if (mine) {
+      launch(pk, blocks, scratch_);
+      ck(cudaGetLastError(), "group reduce launch");
+    }
     retire(s);
-    ck(cudaMemcpyAsync(buf, scratch_, n * sizeof(T), cudaMemcpyDeviceToDevice, s), "group result");
+    if (mine) ck(cudaMemcpyAsync(buf, scratch_, n * sizeof(T), cudaMemcpyDeviceToDevice, s), "group result");
   }
 
   bae_group* g_;

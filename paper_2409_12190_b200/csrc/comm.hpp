@@ -44,6 +44,10 @@ class Comm {
   virtual void allreduce_sum(double* buf, std::size_t n, cudaStream_t s) = 0;
   // In-place element-wise minimum of n int32 over all ranks.
   virtual void allreduce_min(int* buf, std::size_t n, cudaStream_t s) = 0;
+  // In-place element-wise sum of n doubles over all ranks, valid on `root` only.
+  virtual void reduce_sum(double* buf, std::size_t n, int root, cudaStream_t s) = 0;
+  // buf (bytes) of `root` into buf of every rank.
+  virtual void broadcast(void* buf, std::size_t bytes, int root, cudaStream_t s) = 0;
   // recv[r * bytes .. (r+1) * bytes) = send of rank r.
   virtual void allgather(const void* send, void* recv, std::size_t bytes, cudaStream_t s) = 0;
   // Whether the collectives may be captured into a CUDA graph.

@@ -2115,10 +2115,12 @@ int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
   }
   if (comm) {  // the direct solve's exchange: the reduced matrix, once per LM iteration
     const std::size_t nn = 6 * static_cast<std::size_t>(d.C);
-    if (d.stiles)
-      comm->allreduce_sum(d.stiles, static_cast<std::size_t>(d.stile_count) * kSTileElems, s);
-    else
+    if (d.stiles) {  // summed onto rank 0, which factors it (solve_direct broadcasts the step)
+      comm->reduce_sum(d.stiles, static_cast<std::size_t>(d.stile_count) * kSTileElems, 0, s);
+      if (comm->rank() != 0) return n;
+    } else {
       comm->allreduce_sum(d.schur, nn * nn, s);
+    }
     k_add_hccd<<<elt_blocks(36LL * d.C, 256), 256, 0, s>>>(d);
     ++n;
   }

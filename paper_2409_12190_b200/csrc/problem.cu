@@ -1119,7 +1119,13 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
       ck(cudaMalloc(&tchol_.trace, 8 * sizeof(unsigned long long) * tchol_.nt), "cudaMalloc");
       ck(cudaMemsetAsync(tchol_.trace, 0, 8 * sizeof(unsigned long long) * tchol_.nt, stream_), "memset");
     }
-    BAE_LAUNCHED(launch_tile_chol(tchol_, chol_grid_, stream_));
+    // sharded runs: rank 0 holds the summed S, factors it and broadcasts the
+    // camera step and its failure word (no redundant factorisations)
+    if (!comm_ || comm_->rank() == 0) BAE_LAUNCHED(launch_tile_chol(tchol_, chol_grid_, stream_));
+    if (comm_) {
+      comm_->broadcast(d_.x, sizeof(double) * static_cast<std::size_t>(n), 0, stream_);
+      comm_->broadcast(tchol_.fail, sizeof(int), 0, stream_);
+    }
     phase_end();
     if (tchol_.trace) {
       trace.resize(8 * static_cast<std::size_t>(tchol_.nt));
