@@ -355,6 +355,16 @@ int bae_phase_times(bae_problem* p, double* ms7, int32_t reset);
 /* This handle's shard: rank, world, points and observations it owns. */
 int bae_problem_shard(const bae_problem* p, int32_t* rank, int32_t* world, int32_t* local_points,
                       int64_t* local_observations);
+/* The plan's device arrays (single rank), for parity of the device and the
+ * host planner: which = 0 tile_obs_begin, 1 tile_pt_begin, 2 tile_ent_begin,
+ * 3 tile_ws, 4 obs_lcpt, 5 obs_orig, 6 ent_cam, 7 ent_obs_begin,
+ * 8 cam_ent_ptr, 9 cam_ent, 10 pt_ptr, 11 ptobs (2-byte), 12 pt_of_internal,
+ * 13 tile_desc (4 ints per tile), 14 small_tiles, 15 big_tiles, 16 pixels in
+ * slot order (doubles), 17 launch shapes (slice, warps per CTA per kernel
+ * kind, big tiles, big stride, empty camera, empty point, max tile
+ * observations), 18 index blobs (bytes). *count = elements, *elem_bytes =
+ * their size; out (capacity cap elements) may be NULL. */
+int bae_plan_array(bae_problem* p, int32_t which, void* out, int64_t cap, int64_t* count, int32_t* elem_bytes);
 /* Direct solver structure (after its first use): [tile columns, stored
  * 48x48 tiles, tile updates, nested-dissection groups, camera positions]. */
 int bae_direct_stats(const bae_problem* p, int64_t* out5);

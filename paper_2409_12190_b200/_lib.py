@@ -123,6 +123,8 @@ SIGNATURES = {
     "bae_problem_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
     "bae_problem_shard": (ctypes.c_int, [ctypes.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p]),
     "bae_direct_stats": (ctypes.c_int, [ctypes.c_void_p, c_int64_p]),
+    "bae_plan_array": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64,
+                                      c_int64_p, ctypes.POINTER(ctypes.c_int32)]),
     "bae_create_pgo": (ctypes.c_int, [c_double_p, ctypes.c_int32, c_int32_p, c_int32_p, c_double_p, c_double_p,
                                       c_int32_p, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(CreateOptionsC),
                                       ctypes.POINTER(ctypes.c_void_p)]),

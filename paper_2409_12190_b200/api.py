@@ -332,6 +332,17 @@ class TracedProblem:
                                              ctypes.byref(lo)))
         return r.value, w.value, lp.value, lo.value
 
+    def plan_array(self, which: int) -> np.ndarray:
+        """One of the plan's device arrays (bae_plan_array), for planner parity tests."""
+        lib = _lib.load()
+        n, eb = ctypes.c_int64(), ctypes.c_int32()
+        _check(lib.bae_plan_array(self._h, int(which), None, 0, ctypes.byref(n), ctypes.byref(eb)))
+        dt = {1: np.uint8, 2: np.uint16, 4: np.int32, 8: np.float64}[eb.value]
+        out = np.zeros(max(n.value, 1), dt)
+        _check(lib.bae_plan_array(self._h, int(which), out.ctypes.data_as(ctypes.c_void_p), n.value, ctypes.byref(n),
+                                  ctypes.byref(eb)))
+        return out[:n.value]
+
     def direct_stats(self):
         """Tile Cholesky structure of the direct solver (zeros before its first use)."""
         out = np.zeros(5, np.int64)

@@ -434,6 +434,15 @@ int bae_phase_times(bae_problem* p, double* ms7, int32_t reset) {
   });
 }
 
+int bae_plan_array(bae_problem* p, int32_t which, void* out, int64_t cap, int64_t* count, int32_t* elem_bytes) {
+  return guarded([&] {
+    int eb = 0;
+    const int64_t n = ba(p)->plan_array(which, out, cap, &eb);
+    if (count) *count = n;
+    if (elem_bytes) *elem_bytes = eb;
+  });
+}
+
 int bae_direct_stats(const bae_problem* p, int64_t* out5) {
   return guarded([&] {
     long long v[5];

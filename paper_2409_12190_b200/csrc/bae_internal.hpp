@@ -69,6 +69,11 @@ struct Plan {
   bool has_empty_camera = false, has_empty_point = false;
 };
 
+// Tile packing segments of the planners (plan.cpp, plan_device.cu): internal
+// points [P s / n, P (s + 1) / n) for s < n, n = max(1, P / kPlanSegPts).
+constexpr int kPlanSegPts = 8192;
+inline int plan_segments(int P) { return P / kPlanSegPts > 1 ? P / kPlanSegPts : 1; }
+
 // Host worker count for the setup passes: BAE_HOST_THREADS, else the
 // hardware concurrency, capped at 16.
 inline int host_threads() {
@@ -147,7 +152,12 @@ void parallel_chunks(std::int64_t n, int chunks, F&& f) {
 
 // Validation follows make_ba_problem (problems.hpp:90-110): per observation,
 // camera index before point index, IndexError carries the position.
-void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N);
+// make_ba_problem's checks (problems.hpp:87-136): observation count, then
+// (indices = true) the lowest out-of-range camera / point index as
+// IndexError(position) -- the device planner checks the indices itself --
+// then empty camera / point groups.
+void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N,
+                     bool indices = true);
 
 Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, const double* px2,
                 std::int64_t N, int tile_obs_target, int tile_cam_cap, int tile_pts_cap, int smem_tile_obs_cap);

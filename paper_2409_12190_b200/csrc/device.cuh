@@ -228,6 +228,34 @@ __host__ __device__ __forceinline__ long long ws_bytes(WsDims w, int ncam, int n
   return dbl * 8 + (long long)(ncam + 1) * 4 + (long long)(npts + 1) * 4 + (long long)nobs * 4 +
          ((long long)nobs * 2 + 15) / 16 * 16 + (long long)ncam * 4;
 }
+// Workspace shapes of the warp-tile kernels (doubles per camera, per point,
+// per observation, per piece), kernels.cu:
+//   lin (K1): cam [t3 q4 k4 R9] pt p3 stage Jc12 Jp6 r2
+//   lin+prep (K1+F1): cam + t3 of the record, pt p3 L6 v3
+//   cost (K1c), prep (K3/K4; direct: RHS stage only), Schur product (K5),
+//   trial (K7/K8)
+constexpr WsDims kLinWs{20, 3, 20, 0};
+constexpr WsDims kLinPrepWs{23, 12, 20, 0};
+constexpr WsDims kCostWs{11, 3, 0, 0};
+constexpr WsDims kPrepWs{16, 12, 27, 0};
+constexpr WsDims kPrepDirWs{16, 12, 6, 0};
+constexpr WsDims kSxWs{24, 3, 6, 0};
+constexpr WsDims kTrialWs{29, 6, 3, 0};
+// Workspace bytes of one tile for a kernel kind (WsKind order, kernels.cuh:
+// lin, cost, prep, schur, trial, prep-direct, lin+prep).
+__host__ __device__ __forceinline__ long long kind_ws_bytes(int kind, int ncam, int npts, int nobs) {
+  switch (kind) {
+    case 0: return ws_bytes(kLinWs, ncam, npts, nobs);
+    case 1: return ws_bytes(kCostWs, ncam, npts, nobs);
+    case 2: return ws_bytes(kPrepWs, ncam, npts, nobs);
+    case 3: return ws_bytes(kSxWs, ncam, npts, nobs);
+    case 4: return ws_bytes(kTrialWs, ncam, npts, nobs);
+    case 5: return ws_bytes(kPrepDirWs, ncam, npts, nobs);
+    default: return ws_bytes(kLinPrepWs, ncam, npts, nobs);
+  }
+}
+constexpr int kWsKindCount = 7;
+
 __device__ __forceinline__ Ws ws_carve(char* base, WsDims w, int ncam, int npts, int nobs) {
   Ws ws;
   double* d = reinterpret_cast<double*>(base);

@@ -318,9 +318,7 @@ __device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, co
 // Jacobian uses that forward value y (trace.hpp:612-629).
 // cam: [t3 q4 k4 R9] (20) ; pt: p3 ; stage: Jc12 Jp6 r2 (20)
 // ---------------------------------------------------------------------------
-constexpr WsDims kLinWs{20, 3, 20, 0};
 // fused with the direct prep: camera + t3 of the record, point p3 L6 v3
-constexpr WsDims kLinPrepWs{23, 12, 20, 0};
 
 // kPrep: the direct solver's prep fused in (accepted LM steps: linearise and
 // damp in one pass over the tile's data): the point side goes on to the
@@ -499,7 +497,6 @@ __global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_j
 
 // Residual only (evaluate + squared_norm, problems.hpp:66, lm.hpp:81-85) at
 // the current parameters; writes resid when requested.
-constexpr WsDims kCostWs{11, 3, 0, 0};
 
 template <bool kShared>
 __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t) {
@@ -769,8 +766,6 @@ __global__ void k_finish_cost(Dev d, int trial) {
 // Direct solver (kDirect): no block-Jacobi blocks (PCG only), stage 6 (the
 // RHS), and W, W H~_pp^-1 of every slot kept for the assembly of S.
 // ---------------------------------------------------------------------------
-constexpr WsDims kPrepWs{16, 12, 27, 0};
-constexpr WsDims kPrepDirWs{16, 12, 6, 0};
 
 template <bool kShared, bool kDirect>
 __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char* smem, int slice, double lambda,
@@ -1141,7 +1136,6 @@ __global__ void k_add_hccd(Dev d) {
 // lane that owns them. D and y of a lane's first kCacheRounds observations
 // stay in registers between the two observation phases.
 // ---------------------------------------------------------------------------
-constexpr WsDims kSxWs{24, 3, 6, 0};
 constexpr int kCacheRounds = 2;
 
 // The PCG direction is formed lazily (p = z + beta p) by both the tile and
@@ -1831,7 +1825,6 @@ __global__ void k_cam_retract(Dev d) {
 }
 
 // cam: R9 t3 k4 dc6 | trial t3 q4 (29), intrinsics at 12..15 ; pt: p3 ptrial3 ; stage 3
-constexpr WsDims kTrialWs{29, 6, 3, 0};
 
 template <bool kShared>
 __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t) {
@@ -1923,25 +1916,7 @@ __global__ void k_commit(Dev d) {
 // ---------------------------------------------------------------------------
 // launch wrappers
 // ---------------------------------------------------------------------------
-long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) {
-  switch (kind) {
-    case kWsLin:
-      return ws_bytes(kLinWs, ncam, npts, nobs);
-    case kWsCost:
-      return ws_bytes(kCostWs, ncam, npts, nobs);
-    case kWsPrep:
-      return ws_bytes(kPrepWs, ncam, npts, nobs);
-    case kWsPrepDir:
-      return ws_bytes(kPrepDirWs, ncam, npts, nobs);
-    case kWsLinPrep:
-      return ws_bytes(kLinPrepWs, ncam, npts, nobs);
-    case kWsSchur:
-      return ws_bytes(kSxWs, ncam, npts, nobs);
-    case kWsTrial:
-      return ws_bytes(kTrialWs, ncam, npts, nobs);
-  }
-  return 0;
-}
+long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) { return kind_ws_bytes(kind, ncam, npts, nobs); }
 
 void set_smem_limits(int max_bytes) {
   cudaFuncSetAttribute(k_linearize, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);

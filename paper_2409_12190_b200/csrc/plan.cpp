@@ -34,9 +34,11 @@ struct StageTimer {
 };
 }  // namespace
 
-void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N) {
+void validate_inputs(int C, int P, const std::int32_t* cam_idx, const std::int32_t* pt_idx, std::int64_t N,
+                     bool indices) {
   if (N <= 0) throw Error(BAE_ERR_INVALID_ARGUMENT, "make_ba_problem: no observations");
   if (N >= (std::int64_t{1} << 31) - 1) throw Error(BAE_ERR_UNSUPPORTED, "more than 2^31-2 observations");
+  if (!indices) return;  // with N > 0, empty groups mean an out-of-range index: the device plan reports it
   for (std::int64_t k = 0; k < N; ++k) {
     if (cam_idx[k] < 0 || cam_idx[k] >= C) throw Error(BAE_ERR_INDEX, "make_ba_problem: camera index out of range", k);
     if (pt_idx[k] < 0 || pt_idx[k] >= P) throw Error(BAE_ERR_INDEX, "make_ba_problem: point index out of range", k);
@@ -153,9 +155,10 @@ Plan build_plan(int C, int P, const std::int32_t* cam_idx, const std::int32_t* p
 
   st.mark("internal order");
   // Greedy tile packing over internal points, in a fixed number of segments
-  // (a function of P only, so the tiling does not depend on the thread
-  // count); each segment starts a fresh tile and is packed independently.
-  const int nseg = std::clamp(P / 8192, 1, 64);
+  // (a function of P only, so the tiling depends neither on the thread count
+  // nor on which planner runs: plan_device.cu packs the same segments); each
+  // segment starts a fresh tile and is packed independently.
+  const int nseg = plan_segments(P);
   struct Seg {
     std::vector<std::int32_t> pt_begin, obs_count;  // per tile
     std::vector<std::vector<std::int32_t>> cams;

@@ -20,6 +20,7 @@
 #include <limits>
 
 #include "pairs.cuh"
+#include "plan_device.cuh"
 #include "problem.hpp"
 
 // Launch wrappers return their kernel count; BAE_CHECK_LAUNCH=1 also checks
@@ -155,7 +156,14 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
                  const bae_create_options& opt)
     : opt_(opt) {
   HostTimer ht;
-  validate_inputs(C, P, cam_idx, pt_idx, N);
+  // The plan: on the device for a single-rank problem large enough to gain
+  // (plan_device.cu, which also checks the indices; BAE_PLAN=host / device
+  // forces one), else on the host (plan.cpp; sharded ranks plan their own
+  // partition there). Both give the same plan element for element.
+  const bool sharded = opt.world > 1 || opt.nccl_id != nullptr || opt.group != nullptr;
+  bool dev_plan = !sharded && N >= (1 << 17);
+  if (const char* e = std::getenv("BAE_PLAN")) dev_plan = !sharded && std::string(e) == "device";
+  validate_inputs(C, P, cam_idx, pt_idx, N, !dev_plan);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(BAE_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
@@ -220,21 +228,129 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (const char* t = std::getenv("BAE_TILE_CAMS")) tile_cams = std::max(1, std::atoi(t));
   if (const char* m = std::getenv("BAE_PCG_MODE")) use_graph_pcg_ = std::string(m) != "persistent";
   if (comm_) use_graph_pcg_ = true;  // the persistent kernel has no place for the cross-rank sum
-  // single rank: the pixels go up in the caller's order and are gathered into
-  // slot order on the device (a random gather over N on the host otherwise)
-  plan_ = build_plan(C, use_P, use_cam, use_pt, dist ? use_px : nullptr, use_N, std::min(tile_obs, kPipeObs),
-                     std::min(tile_cams, kPipeCams), kPipePts, 1 << 30);
-  ht.mark("build_plan");
-  if (dist) {
-    // observation ids and the missing-diagonal checks refer to the whole problem
-    for (auto& k : plan_.obs_orig) k = gobs[k];
-    std::vector<char> cam_seen(static_cast<std::size_t>(C), 0), pt_seen(static_cast<std::size_t>(P), 0);
-    for (std::int64_t k = 0; k < N; ++k) {
-      cam_seen[cam_idx[k]] = 1;
-      pt_seen[pt_idx[k]] = 1;
+  Plan& pl = plan_;
+  long long big_stride = 0;
+  int nbig = 0;
+  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial, &sm_.prepd, &sm_.linprep};
+  std::vector<int4> desc;
+  std::vector<char> blob;
+  std::vector<int> small_tiles, big_tiles;
+  DevicePlan dp;
+  int* dcam = nullptr;  // raw observation indices on the device (device plan)
+  if (dev_plan) {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&dcam), 2 * sizeof(int) * static_cast<std::size_t>(use_N), stream_),
+       "cudaMallocAsync observation indices");
+    ck(cudaMemcpyAsync(dcam, use_cam, sizeof(int) * use_N, cudaMemcpyHostToDevice, stream_), "H2D cameras");
+    ck(cudaMemcpyAsync(dcam + use_N, use_pt, sizeof(int) * use_N, cudaMemcpyHostToDevice, stream_), "H2D points");
+    try {
+      build_plan_device(C, use_P, dcam, dcam + use_N, use_N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
+                        kPipePts, kSliceLimit, [this](std::size_t n) { return static_cast<void*>(dalloc<char>(n)); },
+                        stream_, dp);
+    } catch (...) {
+      cudaFreeAsync(dcam, stream_);
+      throw;
     }
-    plan_.has_empty_camera = std::find(cam_seen.begin(), cam_seen.end(), 0) != cam_seen.end();
-    plan_.has_empty_point = std::find(pt_seen.begin(), pt_seen.end(), 0) != pt_seen.end();
+    ck(cudaFreeAsync(dcam, stream_), "cudaFreeAsync");
+    if (use_P < 1) throw Error(BAE_ERR_INVALID_ARGUMENT, "track_points: empty group");
+    pl.C = C;
+    pl.P = use_P;
+    pl.N = use_N;
+    pl.tile_obs_target = std::min(tile_obs, kPipeObs);
+    pl.tile_cam_cap = std::min(tile_cams, kPipeCams);
+    pl.T = dp.T;
+    pl.E = dp.E;
+    pl.max_tile_obs = dp.max_tile_obs;
+    pl.max_tile_cams = dp.max_tile_cams;
+    pl.max_tile_pts = dp.max_tile_pts;
+    pl.n_big = dp.n_big;
+    pl.has_empty_camera = dp.has_empty_camera;
+    pl.has_empty_point = dp.has_empty_point;
+    // the point order for the host-side permutations (obs_orig stays on the
+    // device until an export asks for it: host_obs_orig)
+    pl.pt_of_internal.resize(static_cast<std::size_t>(use_P));
+    ck(cudaMemcpyAsync(pl.pt_of_internal.data(), dp.pt_of_internal, sizeof(int) * use_P, cudaMemcpyDeviceToHost,
+                       stream_),
+       "D2H point order");
+    sync();
+    src_of_internal_ = dp.pt_of_internal;
+    for (int k = 0; k < kWsKinds; ++k) kinds[k]->slice = dp.kind_slice[k];
+    nbig = dp.n_big;
+    big_stride = dp.big_need;
+    ht.mark("device plan");
+  } else {
+    // single rank: the pixels go up in the caller's order and are gathered into
+    // slot order on the device (a random gather over N on the host otherwise)
+    plan_ = build_plan(C, use_P, use_cam, use_pt, dist ? use_px : nullptr, use_N, std::min(tile_obs, kPipeObs),
+                       std::min(tile_cams, kPipeCams), kPipePts, 1 << 30);
+    ht.mark("build_plan");
+    if (dist) {
+      // observation ids and the missing-diagonal checks refer to the whole problem
+      for (auto& k : plan_.obs_orig) k = gobs[k];
+      std::vector<char> cam_seen(static_cast<std::size_t>(C), 0), pt_seen(static_cast<std::size_t>(P), 0);
+      for (std::int64_t k = 0; k < N; ++k) {
+        cam_seen[cam_idx[k]] = 1;
+        pt_seen[pt_idx[k]] = 1;
+      }
+      plan_.has_empty_camera = std::find(cam_seen.begin(), cam_seen.end(), 0) != cam_seen.end();
+      plan_.has_empty_point = std::find(pt_seen.begin(), pt_seen.end(), 0) != pt_seen.end();
+    }
+    // Tile classes. "Small" tiles (within the kPipe* caps) take the pipelined
+    // TMA path of the Schur product and a per-warp shared-memory slice in the
+    // other tile kernels; any other tile (one very long track) runs every kind
+    // from a global workspace slot.
+    desc.assign(static_cast<std::size_t>(pl.T), int4{0, 0, 0, 0});
+    // sizes and offsets first (serial, per-tile arithmetic), then the index
+    // blobs filled in parallel chunks of tiles
+    std::size_t blob_bytes = 0;
+    for (int t = 0; t < pl.T; ++t) {
+      const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
+      const int nobs = pl.tile_obs_begin[t + 1] - ob;
+      const int npts = pl.tile_pt_begin[t + 1] - pb;
+      const int ncam = pl.tile_ent_begin[t + 1] - eb;
+      long long need = 0;
+      for (int k = 0; k < kWsKinds; ++k) need = std::max(need, tile_ws_bytes(k, ncam, npts, nobs));
+      const bool small = nobs > 0 && nobs <= kPipeObs && ncam <= kPipeCams && npts <= kPipePts && need <= kSliceLimit;
+      if (!small) {
+        pl.tile_ws[t] = nbig++;
+        big_stride = std::max(big_stride, need);
+        big_tiles.push_back(t);
+        continue;
+      }
+      pl.tile_ws[t] = -1;
+      for (int k = 0; k < kWsKinds; ++k)
+        kinds[k]->slice = std::max<int>(kinds[k]->slice, static_cast<int>(tile_ws_bytes(k, ncam, npts, nobs)));
+      // index blob: hdr | camid | ent | pptr | lcpt | ptl, padded to 16 bytes
+      const int bytes = (32 + 4 * ncam + 4 * (ncam + 1) + 4 * (npts + 1) + 6 * nobs + 15) / 16 * 16;
+      desc[t] = int4{static_cast<int>(blob_bytes / 16), bytes, pb, npts};
+      blob_bytes += static_cast<std::size_t>(bytes);
+      small_tiles.push_back(t);
+    }
+    blob.assign(blob_bytes, 0);
+    parallel_chunks(static_cast<std::int64_t>(small_tiles.size()), small_tiles.size() >= 1024 ? host_threads() : 1,
+                    [&](int, std::int64_t i0, std::int64_t i1) {
+      for (std::int64_t ii = i0; ii < i1; ++ii) {
+        const int t = small_tiles[ii];
+        const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
+        const int nobs = pl.tile_obs_begin[t + 1] - ob;
+        const int npts = pl.tile_pt_begin[t + 1] - pb;
+        const int ncam = pl.tile_ent_begin[t + 1] - eb;
+        int* w = reinterpret_cast<int*>(blob.data() + 16 * static_cast<std::size_t>(desc[t].x));
+        w[0] = ob;
+        w[1] = nobs;
+        w[2] = pb;
+        w[3] = npts;
+        w[4] = eb;
+        w[5] = ncam;
+        int* q = w + 8;
+        for (int l = 0; l < ncam; ++l) *q++ = pl.ent_cam[eb + l];
+        for (int l = 0; l <= ncam; ++l) *q++ = pl.ent_obs_begin[eb + l] - ob;
+        for (int i = 0; i <= npts; ++i) *q++ = pl.pt_ptr[pb + i] - ob;
+        std::uint32_t* lc = reinterpret_cast<std::uint32_t*>(q);
+        for (int i = 0; i < nobs; ++i) lc[i] = pl.obs_lcpt[ob + i];
+        std::uint16_t* ptl = reinterpret_cast<std::uint16_t*>(lc + nobs);
+        for (int i = 0; i < nobs; ++i) ptl[i] = pl.ptobs[ob + i];
+      }
+    });
   }
   // intrinsics as 4 doubles per camera: BAL [f k1 k2 0], pinhole [fx fy cx cy]
   const bool pinhole = opt.camera_model == BAE_CAMERA_PINHOLE;
@@ -244,69 +360,6 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   for (int c = 0; c < C; ++c)
     for (int j = 0; j < kw; ++j) intr_host_[4 * static_cast<std::size_t>(c) + j] = intr3[kw * static_cast<std::size_t>(c) + j];
 
-  // Tile classes. "Small" tiles (within the kPipe* caps) take the pipelined
-  // TMA path of the Schur product and a per-warp shared-memory slice in the
-  // other tile kernels; any other tile (one very long track) runs every kind
-  // from a global workspace slot.
-  Plan& pl = plan_;
-  long long big_stride = 0;
-  int nbig = 0;
-  TileLaunch* kinds[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial, &sm_.prepd, &sm_.linprep};
-  std::vector<int4> desc(static_cast<std::size_t>(pl.T), int4{0, 0, 0, 0});
-  std::vector<char> blob;
-  std::vector<int> small_tiles, big_tiles;
-  // sizes and offsets first (serial, per-tile arithmetic), then the index
-  // blobs filled in parallel chunks of tiles
-  std::size_t blob_bytes = 0;
-  for (int t = 0; t < pl.T; ++t) {
-    const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
-    const int nobs = pl.tile_obs_begin[t + 1] - ob;
-    const int npts = pl.tile_pt_begin[t + 1] - pb;
-    const int ncam = pl.tile_ent_begin[t + 1] - eb;
-    long long need = 0;
-    for (int k = 0; k < kWsKinds; ++k) need = std::max(need, tile_ws_bytes(k, ncam, npts, nobs));
-    const bool small = nobs > 0 && nobs <= kPipeObs && ncam <= kPipeCams && npts <= kPipePts && need <= kSliceLimit;
-    if (!small) {
-      pl.tile_ws[t] = nbig++;
-      big_stride = std::max(big_stride, need);
-      big_tiles.push_back(t);
-      continue;
-    }
-    pl.tile_ws[t] = -1;
-    for (int k = 0; k < kWsKinds; ++k)
-      kinds[k]->slice = std::max<int>(kinds[k]->slice, static_cast<int>(tile_ws_bytes(k, ncam, npts, nobs)));
-    // index blob: hdr | camid | ent | pptr | lcpt | ptl, padded to 16 bytes
-    const int bytes = (32 + 4 * ncam + 4 * (ncam + 1) + 4 * (npts + 1) + 6 * nobs + 15) / 16 * 16;
-    desc[t] = int4{static_cast<int>(blob_bytes / 16), bytes, pb, npts};
-    blob_bytes += static_cast<std::size_t>(bytes);
-    small_tiles.push_back(t);
-  }
-  blob.assign(blob_bytes, 0);
-  parallel_chunks(static_cast<std::int64_t>(small_tiles.size()), small_tiles.size() >= 1024 ? host_threads() : 1,
-                  [&](int, std::int64_t i0, std::int64_t i1) {
-    for (std::int64_t ii = i0; ii < i1; ++ii) {
-      const int t = small_tiles[ii];
-      const int ob = pl.tile_obs_begin[t], pb = pl.tile_pt_begin[t], eb = pl.tile_ent_begin[t];
-      const int nobs = pl.tile_obs_begin[t + 1] - ob;
-      const int npts = pl.tile_pt_begin[t + 1] - pb;
-      const int ncam = pl.tile_ent_begin[t + 1] - eb;
-      int* w = reinterpret_cast<int*>(blob.data() + 16 * static_cast<std::size_t>(desc[t].x));
-      w[0] = ob;
-      w[1] = nobs;
-      w[2] = pb;
-      w[3] = npts;
-      w[4] = eb;
-      w[5] = ncam;
-      int* q = w + 8;
-      for (int l = 0; l < ncam; ++l) *q++ = pl.ent_cam[eb + l];
-      for (int l = 0; l <= ncam; ++l) *q++ = pl.ent_obs_begin[eb + l] - ob;
-      for (int i = 0; i <= npts; ++i) *q++ = pl.pt_ptr[pb + i] - ob;
-      std::uint32_t* lc = reinterpret_cast<std::uint32_t*>(q);
-      for (int i = 0; i < nobs; ++i) lc[i] = pl.obs_lcpt[ob + i];
-      std::uint16_t* ptl = reinterpret_cast<std::uint16_t*>(lc + nobs);
-      for (int i = 0; i < nobs; ++i) ptl[i] = pl.ptobs[ob + i];
-    }
-  });
   int cta_budget = kCtaSmemBudget;
   if (const char* e = std::getenv("BAE_CTA_SMEM_KB")) cta_budget = std::clamp(std::atoi(e), 16, 200) * 1024;
   for (int k = 0; k < kWsKinds; ++k) {
@@ -330,16 +383,23 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.N = static_cast<int>(use_N);
   d.nbig = nbig;
   d.big_stride = big_stride;
-  d.tile_obs_begin = upload(pl.tile_obs_begin);
-  ht.mark("first chunk + upload");
-  d.tile_pt_begin = upload(pl.tile_pt_begin);
-  d.tile_ent_begin = upload(pl.tile_ent_begin);
-  d.tile_ws = upload(pl.tile_ws);
-  d.obs_lcpt = upload(pl.obs_lcpt);
-  d.obs_orig = upload(pl.obs_orig);
-  if (dist) {
-    d.obs_px = upload(pl.obs_px);
-  } else {
+  if (dev_plan) {
+    d.tile_obs_begin = dp.tile_obs_begin;
+    d.tile_pt_begin = dp.tile_pt_begin;
+    d.tile_ent_begin = dp.tile_ent_begin;
+    d.tile_ws = dp.tile_ws;
+    d.obs_lcpt = dp.obs_lcpt;
+    d.obs_orig = dp.obs_orig;
+    d.ent_cam = dp.ent_cam;
+    d.ent_obs_begin = dp.ent_obs_begin;
+    d.cam_ent_ptr = dp.cam_ent_ptr;
+    d.cam_ent = dp.cam_ent;
+    d.pt_ptr = dp.pt_ptr;
+    d.ptobs = dp.ptobs;
+    d.tile_desc = dp.tile_desc;
+    d.tile_blob = dp.tile_blob;
+    d.small_tiles = dp.small_tiles;
+    d.big_tiles = dp.big_tiles;
     double* px = dalloc<double>(2 * static_cast<std::size_t>(use_N));
     double* raw = nullptr;
     ck(cudaMallocAsync(reinterpret_cast<void**>(&raw), 2 * sizeof(double) * use_N, stream_), "cudaMallocAsync");
@@ -347,18 +407,39 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     BAE_LAUNCHED(launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_));
     ck(cudaFreeAsync(raw, stream_), "cudaFreeAsync");
     d.obs_px = px;
+    small_tiles.resize(static_cast<std::size_t>(dp.n_small));  // counts only below
+    big_tiles.resize(static_cast<std::size_t>(dp.n_big));
+  } else {
+    d.tile_obs_begin = upload(pl.tile_obs_begin);
+    ht.mark("first chunk + upload");
+    d.tile_pt_begin = upload(pl.tile_pt_begin);
+    d.tile_ent_begin = upload(pl.tile_ent_begin);
+    d.tile_ws = upload(pl.tile_ws);
+    d.obs_lcpt = upload(pl.obs_lcpt);
+    d.obs_orig = upload(pl.obs_orig);
+    if (dist) {
+      d.obs_px = upload(pl.obs_px);
+    } else {
+      double* px = dalloc<double>(2 * static_cast<std::size_t>(use_N));
+      double* raw = nullptr;
+      ck(cudaMallocAsync(reinterpret_cast<void**>(&raw), 2 * sizeof(double) * use_N, stream_), "cudaMallocAsync");
+      ck(cudaMemcpyAsync(raw, px2, 2 * sizeof(double) * use_N, cudaMemcpyHostToDevice, stream_), "H2D pixels");
+      BAE_LAUNCHED(launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_));
+      ck(cudaFreeAsync(raw, stream_), "cudaFreeAsync");
+      d.obs_px = px;
+    }
+    d.ent_cam = upload(pl.ent_cam);
+    d.ent_obs_begin = upload(pl.ent_obs_begin);
+    d.cam_ent_ptr = upload(pl.cam_ent_ptr);
+    d.cam_ent = upload(pl.cam_ent);
+    d.pt_ptr = upload(pl.pt_ptr);
+    d.ptobs = upload(pl.ptobs);
+    if (blob.empty()) blob.resize(16);
+    d.tile_desc = upload(desc);
+    d.tile_blob = upload(blob);
+    d.small_tiles = upload(small_tiles);
+    d.big_tiles = upload(big_tiles);
   }
-  d.ent_cam = upload(pl.ent_cam);
-  d.ent_obs_begin = upload(pl.ent_obs_begin);
-  d.cam_ent_ptr = upload(pl.cam_ent_ptr);
-  d.cam_ent = upload(pl.cam_ent);
-  d.pt_ptr = upload(pl.pt_ptr);
-  d.ptobs = upload(pl.ptobs);
-  if (blob.empty()) blob.resize(16);
-  d.tile_desc = upload(desc);
-  d.tile_blob = upload(blob);
-  d.small_tiles = upload(small_tiles);
-  d.big_tiles = upload(big_tiles);
   ht.mark("uploads");
   d.n_small = static_cast<int>(small_tiles.size());
   d.n_big_tiles = static_cast<int>(big_tiles.size());
@@ -458,6 +539,68 @@ int DeviceStructure::slot_cam(int t, int s) const {
     if (ent_obs_begin[mid] <= s) lo = mid; else hi = mid - 1;
   }
   return ent_cam[lo];
+}
+
+std::int64_t Problem::plan_array(int which, void* out, std::int64_t cap, int* elem_bytes) {
+  require_single("the plan export");
+  activate();
+  ensure_point_staging();
+  sync();
+  const std::int64_t T = d_.T, E = d_.E, N = d_.N, C = d_.C, P = d_.P;
+  const void* src = nullptr;
+  std::int64_t n = 0;
+  int eb = 4;
+  std::vector<int> meta;
+  switch (which) {
+    case 0: src = d_.tile_obs_begin; n = T + 1; break;
+    case 1: src = d_.tile_pt_begin; n = T + 1; break;
+    case 2: src = d_.tile_ent_begin; n = T + 1; break;
+    case 3: src = d_.tile_ws; n = T; break;
+    case 4: src = d_.obs_lcpt; n = N; break;
+    case 5: src = d_.obs_orig; n = N; break;
+    case 6: src = d_.ent_cam; n = E; break;
+    case 7: src = d_.ent_obs_begin; n = E + 1; break;
+    case 8: src = d_.cam_ent_ptr; n = C + 1; break;
+    case 9: src = d_.cam_ent; n = E; break;
+    case 10: src = d_.pt_ptr; n = P + 1; break;
+    case 11: src = d_.ptobs; n = N; eb = 2; break;
+    case 12: src = src_of_internal_; n = P; break;
+    case 13: src = d_.tile_desc; n = 4 * T; break;
+    case 14: src = d_.small_tiles; n = d_.n_small; break;
+    case 15: src = d_.big_tiles; n = d_.n_big_tiles; break;
+    case 16: src = d_.obs_px; n = 2 * N; eb = 8; break;
+    case 17: {  // launch shapes: per kind slice and warps per CTA, big tiles, big stride
+      const TileLaunch* k[kWsKinds] = {&sm_.lin, &sm_.cost, &sm_.prep, &sm_.schur, &sm_.trial, &sm_.prepd, &sm_.linprep};
+      for (int i = 0; i < kWsKinds; ++i) {
+        meta.push_back(k[i]->slice);
+        meta.push_back(k[i]->wpb);
+      }
+      meta.push_back(d_.nbig);
+      meta.push_back(static_cast<int>(d_.big_stride));
+      meta.push_back(plan_.has_empty_camera ? 1 : 0);
+      meta.push_back(plan_.has_empty_point ? 1 : 0);
+      meta.push_back(plan_.max_tile_obs);
+      n = static_cast<std::int64_t>(meta.size());
+      break;
+    }
+    case 18: {  // the small tiles' index blobs (bytes)
+      std::vector<int4> desc(static_cast<std::size_t>(T));
+      if (T) ck(cudaMemcpy(desc.data(), d_.tile_desc, T * sizeof(int4), cudaMemcpyDeviceToHost), "D2H");
+      for (const int4& q : desc) n = std::max<std::int64_t>(n, 16LL * q.x + q.y);
+      src = d_.tile_blob;
+      eb = 1;
+      break;
+    }
+    default:
+      throw Error(BAE_ERR_INVALID_ARGUMENT, "plan export: unknown array");
+  }
+  if (elem_bytes) *elem_bytes = eb;
+  if (out && n > 0) {
+    if (cap < n) throw Error(BAE_ERR_INVALID_ARGUMENT, "plan export: capacity too small");
+    if (!meta.empty()) std::memcpy(out, meta.data(), meta.size() * sizeof(int));
+    else ck(cudaMemcpy(out, src, static_cast<std::size_t>(n) * eb, cudaMemcpyDeviceToHost), "D2H plan");
+  }
+  return n;
 }
 
 DeviceStructure Problem::download_structure() {
@@ -560,8 +703,10 @@ void Problem::set_parameters(const double* poses7, const double* points3) {
 // permutation runs as a kernel instead of a host loop over P.
 void Problem::ensure_point_staging() {
   if (pts_user_) return;
-  std::vector<int> src(plan_.pt_of_internal.begin(), plan_.pt_of_internal.end());
-  src_of_internal_ = upload(src);
+  if (!src_of_internal_) {  // the device plan left its own copy
+    std::vector<int> src(plan_.pt_of_internal.begin(), plan_.pt_of_internal.end());
+    src_of_internal_ = upload(src);
+  }
   pts_user_ = dalloc<double>(3 * static_cast<std::size_t>(d_.P));
 }
 
@@ -624,6 +769,14 @@ void Problem::read_lm() {
   sync();
 }
 
+// The original observation id of every slot on the host: the device plan
+// keeps it on the device until an export needs it.
+void Problem::ensure_host_obs_orig() {
+  if (static_cast<std::int64_t>(plan_.obs_orig.size()) == plan_.N) return;
+  plan_.obs_orig.resize(static_cast<std::size_t>(plan_.N));
+  ck(cudaMemcpy(plan_.obs_orig.data(), d_.obs_orig, sizeof(int) * plan_.N, cudaMemcpyDeviceToHost), "D2H slot ids");
+}
+
 void Problem::unpermute_slots(const std::vector<double>& src, int comps, double* dst) const {
   // src: component-major [comp][N] in slot order -> dst: [N][comps] original order
   const std::int64_t N = plan_.N;
@@ -653,6 +806,7 @@ double Problem::evaluate(double* resid2) {
     std::vector<double> h(2 * static_cast<std::size_t>(plan_.N));
     ck(cudaMemcpy(h.data(), rbuf, h.size() * sizeof(double), cudaMemcpyDeviceToHost), "D2H resid");
     cudaFree(rbuf);
+    ensure_host_obs_orig();
     unpermute_slots(h, 2, resid2);
   }
   return lm_host_->cost;
@@ -713,6 +867,7 @@ void Problem::jacobian(double* jpose, double* jpoint, double* resid2) {
   cudaFree(rs);
   if (lm_host_->err_obs != INT_MAX)
     throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
+  ensure_host_obs_orig();
   for (std::int64_t s = 0; s < N; ++s) {
     const std::int64_t k = plan_.obs_orig[s];
     if (jpose)

@@ -90,6 +90,9 @@ class Problem {
   double evaluate(double* resid2);
   void jacobian(double* jpose, double* jpoint, double* resid2);
   DeviceStructure download_structure();
+  // The plan's device arrays for parity tests of the two planners
+  // (bae_plan_array); returns the element count, copies when out != null.
+  std::int64_t plan_array(int which, void* out, std::int64_t cap, int* elem_bytes);
   void block_diagonals(double* hcc36, double* gc6, double* hpp9, double* gp3);
   void solve_step(double lambda, const bae_lm_config& cfg, double* delta, std::int64_t* iters, double* relres);
   void optimize(const double* poses7, const double* points3, const bae_lm_config& cfg,
@@ -130,6 +133,7 @@ class Problem {
   void build_tile_chol(const std::vector<int2>& bcam);
   void require_single(const char* what) const;
   const char* cheirality_msg() const;
+  void ensure_host_obs_orig();
   void unpermute_slots(const std::vector<double>& src, int comps, double* dst) const;
   void phase_begin(int ph);
   void phase_end();
