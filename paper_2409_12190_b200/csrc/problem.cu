@@ -122,6 +122,88 @@ void pinned_give(void* p) {
   std::lock_guard<std::mutex> l(c.m);
   c.pinned.push_back(p);
 }
+
+// Large host -> device copies of pageable memory. The driver stages pageable
+// copies through its own buffer one at a time (≈ 10 GB/s on the GPU box);
+// here two pinned staging buffers per device (process-wide, kept) are filled
+// by the host worker pool, chunk by chunk, while the other one is in flight.
+constexpr std::size_t kStageBytes = 32u << 20;
+constexpr std::size_t kStageMin = 64u << 20;  // below: a plain pageable copy
+struct PinnedStage {
+  std::mutex m;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+PinnedStage& pinned_stage(int device) {
+  static std::mutex gm;
+  static std::map<int, PinnedStage*>* stages = new std::map<int, PinnedStage*>;  // leaked, as mem_cache
+  std::lock_guard<std::mutex> l(gm);
+  PinnedStage*& p = (*stages)[device];
+  if (!p) p = new PinnedStage;
+  return *p;
+}
+void upload_pageable(void* dst, const void* src, std::size_t bytes, cudaStream_t s, int device) {
+  if (bytes < kStageMin) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+    return;
+  }
+  PinnedStage& st = pinned_stage(device);
+  std::lock_guard<std::mutex> l(st.m);
+  for (int b = 0; b < 2; ++b) {
+    if (!st.buf[b]) ck(cudaMallocHost(&st.buf[b], kStageBytes), "cudaMallocHost staging");
+    if (!st.ev[b]) ck(cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming), "event");
+  }
+  const int nth = host_threads();
+  std::size_t i = 0;
+  for (std::size_t off = 0; off < bytes; off += kStageBytes, ++i) {
+    const int b = static_cast<int>(i & 1);
+    const std::size_t n = std::min(kStageBytes, bytes - off);
+    if (i >= 2) ck(cudaEventSynchronize(st.ev[b]), "staging reuse");
+    char* to = static_cast<char*>(st.buf[b]);
+    const char* from = static_cast<const char*>(src) + off;
+    parallel_chunks(static_cast<std::int64_t>(n), nth, [&](int, std::int64_t a, std::int64_t e) {
+      std::memcpy(to + a, from + a, static_cast<std::size_t>(e - a));
+    });
+    ck(cudaMemcpyAsync(static_cast<char*>(dst) + off, to, n, cudaMemcpyHostToDevice, s), "H2D staged");
+    ck(cudaEventRecord(st.ev[b], s), "event record");
+  }
+  for (int b = 0; b < 2; ++b) ck(cudaEventSynchronize(st.ev[b]), "staging");  // buffers free for the next caller
+}
+// The reverse: DMA into the staging buffers, the host pool copies out
+// (synchronises s).
+void download_pageable(void* dst, const void* src, std::size_t bytes, cudaStream_t s, int device) {
+  if (bytes < kStageMin) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "D2H");
+    return;
+  }
+  PinnedStage& st = pinned_stage(device);
+  std::lock_guard<std::mutex> l(st.m);
+  for (int b = 0; b < 2; ++b) {
+    if (!st.buf[b]) ck(cudaMallocHost(&st.buf[b], kStageBytes), "cudaMallocHost staging");
+    if (!st.ev[b]) ck(cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming), "event");
+  }
+  const int nth = host_threads();
+  const std::size_t nchunk = (bytes + kStageBytes - 1) / kStageBytes;
+  auto issue = [&](std::size_t i) {
+    const int b = static_cast<int>(i & 1);
+    const std::size_t off = i * kStageBytes, n = std::min(kStageBytes, bytes - off);
+    ck(cudaMemcpyAsync(st.buf[b], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, s), "D2H staged");
+    ck(cudaEventRecord(st.ev[b], s), "event record");
+  };
+  issue(0);
+  for (std::size_t i = 0; i < nchunk; ++i) {
+    const int b = static_cast<int>(i & 1);
+    ck(cudaEventSynchronize(st.ev[b]), "staging");
+    if (i + 1 < nchunk) issue(i + 1);  // the other buffer: its copy-out finished last round
+    const std::size_t off = i * kStageBytes, n = std::min(kStageBytes, bytes - off);
+    const char* from = static_cast<const char*>(st.buf[b]);
+    char* to = static_cast<char*>(dst) + off;
+    parallel_chunks(static_cast<std::int64_t>(n), nth, [&](int, std::int64_t a, std::int64_t e) {
+      std::memcpy(to + a, from + a, static_cast<std::size_t>(e - a));
+    });
+  }
+}
 }  // namespace
 
 template <class T>
@@ -240,8 +322,8 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (dev_plan) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&dcam), 2 * sizeof(int) * static_cast<std::size_t>(use_N), stream_),
        "cudaMallocAsync observation indices");
-    ck(cudaMemcpyAsync(dcam, use_cam, sizeof(int) * use_N, cudaMemcpyHostToDevice, stream_), "H2D cameras");
-    ck(cudaMemcpyAsync(dcam + use_N, use_pt, sizeof(int) * use_N, cudaMemcpyHostToDevice, stream_), "H2D points");
+    upload_pageable(dcam, use_cam, sizeof(int) * use_N, stream_, opt.device);
+    upload_pageable(dcam + use_N, use_pt, sizeof(int) * use_N, stream_, opt.device);
     try {
       build_plan_device(C, use_P, dcam, dcam + use_N, use_N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
                         kPipePts, kSliceLimit, [this](std::size_t n) { return static_cast<void*>(dalloc<char>(n)); },
@@ -403,7 +485,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     double* px = dalloc<double>(2 * static_cast<std::size_t>(use_N));
     double* raw = nullptr;
     ck(cudaMallocAsync(reinterpret_cast<void**>(&raw), 2 * sizeof(double) * use_N, stream_), "cudaMallocAsync");
-    ck(cudaMemcpyAsync(raw, px2, 2 * sizeof(double) * use_N, cudaMemcpyHostToDevice, stream_), "H2D pixels");
+    upload_pageable(raw, px2, 2 * sizeof(double) * use_N, stream_, opt.device);
     BAE_LAUNCHED(launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_));
     ck(cudaFreeAsync(raw, stream_), "cudaFreeAsync");
     d.obs_px = px;
@@ -681,7 +763,7 @@ void Problem::set_parameters(const double* poses7, const double* points3) {
     ck(cudaMemcpyAsync(d_.pose, poses7, 7 * sizeof(double) * C, cudaMemcpyHostToDevice, stream_), "H2D poses");
   if (points3 && !comm_) {  // caller order up, permuted into the internal order on the device
     ensure_point_staging();
-    ck(cudaMemcpyAsync(pts_user_, points3, 3 * sizeof(double) * P, cudaMemcpyHostToDevice, stream_), "H2D points");
+    upload_pageable(pts_user_, points3, 3 * sizeof(double) * P, stream_, opt_.device);
     BAE_LAUNCHED(launch_points_permute(pts_user_, src_of_internal_, d_.pts, P, true, stream_));
   } else if (points3) {
     std::vector<double> pts(3 * static_cast<std::size_t>(P));
@@ -743,7 +825,7 @@ void Problem::get_parameters(double* poses7, double* points3) {
   } else if (points3) {  // permuted back to the caller's order on the device
     ensure_point_staging();
     BAE_LAUNCHED(launch_points_permute(d_.pts, src_of_internal_, pts_user_, P, false, stream_));
-    ck(cudaMemcpyAsync(points3, pts_user_, 3 * sizeof(double) * P, cudaMemcpyDeviceToHost, stream_), "D2H points");
+    download_pageable(points3, pts_user_, 3 * sizeof(double) * P, stream_, opt_.device);
     sync();
   }
 }
