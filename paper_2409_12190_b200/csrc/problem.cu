@@ -1187,6 +1187,7 @@ void Problem::build_direct() {
 // Tile pattern of S (camera blocks -> 48 x 48 tiles, the union over ranks on
 // sharded runs), its symbolic factorisation and the device structures.
 void Problem::build_tile_chol(const std::vector<int2>& bcam) {
+  HostTimer ht;
   const int C = d_.C;
   // camera graph: pairs of distinct cameras that share a point (the union
   // over ranks on sharded runs, so that every rank derives the same order)
@@ -1223,6 +1224,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
     std::sort(keys.begin(), keys.end());
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
   }
+  ht.mark("chol: camera graph");
   std::vector<std::pair<int, int>> edges;
   edges.reserve(keys.size());
   for (long long k : keys) edges.emplace_back(static_cast<int>(k / C), static_cast<int>(k % C));
@@ -1237,6 +1239,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
     if (const char* l = std::getenv("BAE_ND_LEAF")) leaf = std::max(1, std::atoi(l));
     groups = nd_camera_groups(C, edges, leaf);
   }
+  ht.mark("chol: nested dissection");
   // positions: groups in order, each padded to whole tiles (8 cameras)
   std::vector<int> pos(static_cast<std::size_t>(C), -1), pos_cam;
   for (const auto& g : groups) {
@@ -1257,6 +1260,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
     tp.emplace_back(std::max(a, b), std::min(a, b));
   }
   const TileCholPlan pl = plan_tile_chol(n, tp);
+  ht.mark("chol: symbolic");
   auto slot_of = [&](int ti, int tj) {
     const auto first = pl.rowidx.begin() + pl.colptr[tj], last = pl.rowidx.begin() + pl.colptr[tj + 1];
     const auto it = std::lower_bound(first, last, ti);
@@ -1295,7 +1299,9 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   // count, 0 = off): a separator column's tile updates spread over CTAs
   int help_min = 2;
   if (const char* h = std::getenv("BAE_CHOL_HELP")) help_min = std::max(0, std::atoi(h));
+  ht.mark("chol: tile slots + uploads");
   const TileCholTasks tk = plan_chol_tasks(pl, help_min, tile_chol_grid(1 << 30));
+  ht.mark("chol: task queue");
   t.bptr = upload(tk.bptr);
   t.bop = upload(tk.bop);
   t.tasks = upload(tk.tasks);
