@@ -487,6 +487,7 @@ def run_b200(args):
     # --- end to end through the public API with host buffers: make_ba_problem
     # (planning, uploads) + optimize + read-back of the final parameters ---
     e2e_iters, e2e_s = 0, 0.0
+    e2e_steps_s = []
     e2e_steps = max(1, min(args.steps, 3))
     for i in range(e2e_steps + 1):
         kws = comm_kw()
@@ -502,6 +503,7 @@ def run_b200(args):
         r2 = on_ranks(e2e)[0]
         torch.cuda.synchronize()
         el = time.perf_counter() - ts
+        e2e_steps_s.append(el)
         if i > 0:  # the first one warms host allocations
             e2e_iters += r2.iterations
             e2e_s += el
@@ -588,6 +590,7 @@ def run_b200(args):
             "configs": extra,
             "e2e": {"value": e2e_value, "unit": "LM iter/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "includes": "make_ba_problem (planning, uploads) + optimize + parameter read-back, every step",
+                    "step_s": e2e_steps_s,
                     "warm": {"value": e2e_warm, "unit": "LM iter/s", "h2d_bytes_per_step": 56 * C + 24 * P,
                              "d2h_bytes_per_step": d2h,
                              "includes": "optimize(initial parameters from host) + read-back, existing problem"}},

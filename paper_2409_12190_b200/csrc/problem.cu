@@ -66,7 +66,18 @@ struct HostTimer {
 // destroy loop does not pay cudaMalloc / cudaMallocHost each time (bounded;
 // the rest is freed).
 constexpr std::size_t kArenaChunk = 32u << 20;
-constexpr std::size_t kChunkCacheLimit = 8ull << 30;
+// the cache keeps at most a quarter of the device memory (and 48 GB)
+std::size_t chunk_cache_limit(int device) {
+  static std::mutex m;
+  static std::map<int, std::size_t> lim;
+  std::lock_guard<std::mutex> l(m);
+  auto it = lim.find(device);
+  if (it != lim.end()) return it->second;
+  std::size_t total = 32ull << 30;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) total = prop.totalGlobalMem;
+  return lim[device] = std::min<std::size_t>(total / 4, 48ull << 30);
+}
 constexpr std::size_t kPinnedWord = 4096;
 
 namespace {
@@ -95,7 +106,7 @@ void* chunk_take(int device, std::size_t want, std::size_t& got) {
 void chunk_give(int device, void* p, std::size_t bytes) {  // the device is current
   MemCache& c = mem_cache();
   std::lock_guard<std::mutex> l(c.m);
-  if (c.cached + bytes > kChunkCacheLimit) {
+  if (c.cached + bytes > chunk_cache_limit(device)) {
     cudaFree(p);
     return;
   }
