@@ -154,74 +154,125 @@ __device__ __forceinline__ void push_set(int (&v)[kPipeCams + 1], int c) {
   v[0] = c;
 }
 
+// One warp per segment. The open tile's camera set lives in lanes 16..31
+// (slot q in lane 16 + q; ncur slots, or ncur = cam_cap + 1 once over the
+// cap) and a point's cameras in lanes 0..15, so one __match_any_sync tells
+// each point lane whether its camera is in the set and whether a lower lane
+// of the point has it too; the fresh cameras are appended in lane order. A
+// point with more than 16 observations runs the register path of one lane on
+// a gathered copy of the set. Decisions equal plan.cpp's exact set.
 __global__ void k_pack(const int* __restrict__ istart, const int* __restrict__ lcam, int P, int nseg, int obs_cap,
                        int cam_cap, int pts_cap, int* __restrict__ seg_tiles, int* __restrict__ tmp_pt,
                        int* __restrict__ tmp_nobs) {
-  // one segment per CTA, one thread: the segments' serial loops never share
-  // a warp (no divergence) and spread over all SMs
+  static_assert(kPipeCams <= 16, "the set fits lanes 16..31");
   const int sg = blockIdx.x;
-  if (sg >= nseg || threadIdx.x != 0) return;
+  if (sg >= nseg) return;
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
   const int i0 = static_cast<int>(static_cast<long long>(P) * sg / nseg);
   const int i1 = static_cast<int>(static_cast<long long>(P) * (sg + 1) / nseg);
   if (i1 <= i0) {
-    seg_tiles[sg] = 0;
+    if (lane == 0) seg_tiles[sg] = 0;
     return;
   }
-  int cams[kPipeCams + 1];
-#pragma unroll
-  for (int q = 0; q < kPipeCams + 1; ++q) cams[q] = -1;
-  int ncur = 0;  // > cam_cap: over the cap
-  int t_obs = 0, t_pts = 0;
-  int out = i0;
-  tmp_pt[out] = i0;
+  const bool set_lane = lane >= 16;
+  const int empty = -100 - lane;  // a value no camera and no other lane has
+  int val = set_lane ? empty : -2 - lane;  // set lanes: slot value; point lanes: this point's camera
+  int ncur = 0, t_obs = 0, t_pts = 0, out = i0;
+  if (lane == 0) tmp_pt[out] = i0;
   int b = istart[i0];
   for (int i = i0; i < i1; ++i) {
     const int e = istart[i + 1], m = e - b;
-    bool close = false;
-    if (t_pts > 0) {
-      if (t_obs + m > obs_cap || t_pts + 1 > pts_cap || ncur > cam_cap) {
-        close = true;
-      } else {  // distinct cameras of the point outside the set, up to the first over the cap
-        int fresh[kPipeCams + 1];
-        int nnew = 0;
-        for (int a = b; a < e && !close; ++a) {
-          const int c = lcam[a];
-          if (!in_set(cams, ncur, c) && !in_set(fresh, nnew, c)) {
-            if (ncur + nnew + 1 > cam_cap) close = true;
-            else {
-              push_set(fresh, c);
-              ++nnew;
+    bool close = t_pts > 0 && (t_obs + m > obs_cap || t_pts + 1 > pts_cap || ncur > cam_cap);
+    if (m <= 16) {
+      if (!set_lane) val = lane < m ? lcam[b + lane] : -2 - lane;
+      auto fresh_of = [&]() {  // point lanes whose camera is new to the set and first in the point
+        const unsigned same = __match_any_sync(full, val);
+        const bool f = !set_lane && lane < m && (same >> 16) == 0u && (__ffs(same) - 1) == lane;
+        return __ballot_sync(full, f);
+      };
+      unsigned fresh = 0u;
+      if (t_pts > 0 && !close) {
+        fresh = fresh_of();
+        close = ncur + __popc(fresh) > cam_cap;
+      }
+      if (close || t_pts == 0) {  // the point opens a tile: all its distinct cameras are fresh
+        if (set_lane) val = empty;
+        fresh = fresh_of();
+      }
+      if (close) {
+        if (lane == 0) tmp_nobs[out] = t_obs;
+        ++out;
+        if (lane == 0) tmp_pt[out] = i;
+        t_obs = 0;
+        t_pts = 0;
+        ncur = 0;
+      }
+      const int nnew = __popc(fresh);
+      if (ncur + nnew > cam_cap) {
+        ncur = cam_cap + 1;
+      } else {  // set slot ncur + r takes the camera of the r-th fresh lane
+        const int r = lane - 16 - ncur;
+        const bool take = set_lane && r >= 0 && r < nnew;
+        const int v = __shfl_sync(full, val, take ? static_cast<int>(__fns(fresh, 0, r + 1)) : 0);
+        if (take) val = v;
+        ncur += nnew;
+      }
+    } else {  // a long track: lane 0 on a gathered copy of the set
+      int cams[kPipeCams + 1];
+#pragma unroll
+      for (int q = 0; q < kPipeCams; ++q) cams[q] = __shfl_sync(full, val, 16 + q);
+      cams[kPipeCams] = -1;
+      int dec = 0;  // lane 0: close | set size << 1
+      if (lane == 0) {
+        int n = ncur;
+        bool cl = close;
+        if (t_pts > 0 && !cl) {
+          int fr[kPipeCams + 1];
+          int nf = 0;
+          for (int a = b; a < e && !cl; ++a) {
+            const int cc = lcam[a];
+            if (!in_set(cams, n, cc) && !in_set(fr, nf, cc)) {
+              if (n + nf + 1 > cam_cap) cl = true;
+              else push_set(fr, cc), ++nf;
             }
           }
         }
-      }
-    }
-    if (close) {
-      tmp_nobs[out] = t_obs;
-      ++out;
-      tmp_pt[out] = i;
-      t_obs = 0;
-      t_pts = 0;
-      ncur = 0;
-    }
-    // the point joins: add its distinct cameras (or mark the set over the cap)
-    for (int a = b; a < e && ncur <= cam_cap; ++a) {
-      const int c = lcam[a];
-      if (!in_set(cams, ncur, c)) {
-        if (ncur == cam_cap) {
-          ncur = cam_cap + 1;
-        } else {
-          push_set(cams, c);
-          ++ncur;
+        if (cl || t_pts == 0) n = 0;
+        for (int a = b; a < e && n <= cam_cap; ++a) {  // the point joins: its distinct cameras
+          const int cc = lcam[a];
+          if (!in_set(cams, n, cc)) {
+            if (n == cam_cap) n = cam_cap + 1;
+            else push_set(cams, cc), ++n;
+          }
         }
+        dec = (cl ? 1 : 0) | (n << 1);
       }
+      dec = __shfl_sync(full, dec, 0);
+      close = dec & 1;
+      const int n = dec >> 1;
+#pragma unroll
+      for (int q = 0; q < kPipeCams; ++q) {
+        const int v = __shfl_sync(full, cams[q], 0);
+        if (lane == 16 + q) val = q < n ? v : empty;
+      }
+      if (close) {
+        if (lane == 0) tmp_nobs[out] = t_obs;
+        ++out;
+        if (lane == 0) tmp_pt[out] = i;
+        t_obs = 0;
+        t_pts = 0;
+      }
+      ncur = n;
     }
     t_obs += m;
     ++t_pts;
     b = e;
   }
-  tmp_nobs[out] = t_obs;
-  seg_tiles[sg] = out - i0 + 1;
+  if (lane == 0) {
+    tmp_nobs[out] = t_obs;
+    seg_tiles[sg] = out - i0 + 1;
+  }
 }
 
 // Segment scratch ranges -> the tile list (tile_pt_begin, tile observations).
