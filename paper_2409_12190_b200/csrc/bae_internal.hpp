@@ -71,7 +71,7 @@ struct Plan {
 
 // Tile packing segments of the planners (plan.cpp, plan_device.cu): internal
 // points [P s / n, P (s + 1) / n) for s < n, n = max(1, P / kPlanSegPts).
-constexpr int kPlanSegPts = 8192;
+constexpr int kPlanSegPts = 2048;
 inline int plan_segments(int P) { return P / kPlanSegPts > 1 ? P / kPlanSegPts : 1; }
 
 // Host worker count for the setup passes: BAE_HOST_THREADS, else the
