@@ -127,40 +127,53 @@ __device__ __forceinline__ double warp_sum(double v) {
 // predicated off (no duplicate requests for short arrays).
 // `addr(i)` returns the source address of element i.
 constexpr int kBatch = 8;
-template <class T, class Addr, class Store>
-__device__ __forceinline__ void warp_copy(int n, Addr addr, Store store) {
-  for (int base = lane_id(); base < n; base += kBatch * 32) {
+// The tile's thread index in a group of NT threads (a warp, or the warp pair
+// of the linearisation: kLinThreads).
+template <int NT>
+__device__ __forceinline__ int tile_tid() {
+  return static_cast<int>(threadIdx.x) & (NT - 1);
+}
+template <int NT, class T, class Addr, class Store>
+__device__ __forceinline__ void group_copy(int n, Addr addr, Store store) {
+  for (int base = tile_tid<NT>(); base < n; base += kBatch * NT) {
     T v[kBatch];
 #pragma unroll
     for (int b = 0; b < kBatch; ++b)
-      if (base + b * 32 < n) v[b] = *addr(base + b * 32);
+      if (base + b * NT < n) v[b] = *addr(base + b * NT);
 #pragma unroll
     for (int b = 0; b < kBatch; ++b)
-      if (base + b * 32 < n) store(base + b * 32, v[b]);
+      if (base + b * NT < n) store(base + b * NT, v[b]);
   }
+}
+template <class T, class Addr, class Store>
+__device__ __forceinline__ void warp_copy(int n, Addr addr, Store store) {
+  group_copy<32, T>(n, addr, store);
 }
 
 // Tile index data: entry boundaries, camera ids, point-list offsets, slot
 // camera/point codes and the point lists (all independent loads).
+template <int NT = 32>
 __device__ __forceinline__ void load_tile_index(const Dev& d, const TileGeom& g, const Ws& ws) {
   const int* eo = d.ent_obs_begin + g.eb;
   const int* ec = d.ent_cam + g.eb;
   const int* pp = d.pt_ptr + g.pb;
   const std::uint32_t* lc = d.obs_lcpt + g.ob;
   const std::uint16_t* pl = d.ptobs + g.ob;
-  warp_copy<int>(g.ncam + 1, [&](int i) { return eo + i; }, [&](int i, int v) { ws.ent[i] = v - g.ob; });
-  warp_copy<int>(g.ncam, [&](int i) { return ec + i; }, [&](int i, int v) { ws.camid[i] = v; });
-  warp_copy<int>(g.npts + 1, [&](int i) { return pp + i; }, [&](int i, int v) { ws.pptr[i] = v - g.ob; });
-  warp_copy<std::uint32_t>(g.nobs, [&](int i) { return lc + i; }, [&](int i, std::uint32_t v) { ws.lcpt[i] = v; });
-  warp_copy<std::uint16_t>(g.nobs, [&](int i) { return pl + i; }, [&](int i, std::uint16_t v) { ws.ptl[i] = v; });
+  group_copy<NT, int>(g.ncam + 1, [&](int i) { return eo + i; }, [&](int i, int v) { ws.ent[i] = v - g.ob; });
+  group_copy<NT, int>(g.ncam, [&](int i) { return ec + i; }, [&](int i, int v) { ws.camid[i] = v; });
+  group_copy<NT, int>(g.npts + 1, [&](int i) { return pp + i; }, [&](int i, int v) { ws.pptr[i] = v - g.ob; });
+  group_copy<NT, std::uint32_t>(g.nobs, [&](int i) { return lc + i; },
+                                [&](int i, std::uint32_t v) { ws.lcpt[i] = v; });
+  group_copy<NT, std::uint16_t>(g.nobs, [&](int i) { return pl + i; },
+                                [&](int i, std::uint16_t v) { ws.ptl[i] = v; });
 }
 
 // W consecutive doubles per point from src[(pb + lp) * W] into ws.pt[lp * ptw + off].
-template <int W>
+template <int W, int NT = 32>
 __device__ __forceinline__ void load_point_fields(const Ws& ws, int ptw, int off, const double* src, int pb,
                                                   int npts) {
   const double* base = src + (long long)pb * W;
-  warp_copy<double>(
+  group_copy<NT, double>(
       npts * W, [&](int i) { return base + i; },
       [&](int i, double v) {
         const int lp = i / W;
@@ -169,11 +182,11 @@ __device__ __forceinline__ void load_point_fields(const Ws& ws, int ptw, int off
 }
 
 // W consecutive doubles per camera from src[camid * stride] into
-// ws.cam[l * camw + off]. Needs ws.camid (load_tile_index + __syncwarp).
-template <int W>
+// ws.cam[l * camw + off]. Needs ws.camid (load_tile_index + a tile barrier).
+template <int W, int NT = 32>
 __device__ __forceinline__ void load_cam_fields(const Ws& ws, int ncam, int camw, int off, const double* src,
                                                 int stride) {
-  warp_copy<double>(
+  group_copy<NT, double>(
       ncam * W,
       [&](int i) {
         const int l = i / W;
@@ -187,9 +200,9 @@ __device__ __forceinline__ void load_cam_fields(const Ws& ws, int ncam, int camw
 
 // Per (tile camera, component): sum of the staged W-vectors over the
 // camera's slot range, in slot order (two interleaved partial sums).
-template <int W, int SW>
+template <int W, int SW, int NT = 32>
 __device__ __forceinline__ void entries_from_stage(const Ws& ws, int ncam, int eb, double* out) {
-  for (int idx = lane_id(); idx < ncam * W; idx += 32) {
+  for (int idx = tile_tid<NT>(); idx < ncam * W; idx += NT) {
     const int e = idx / W, j = idx - e * W;
     const int b = ws.ent[e], en = ws.ent[e + 1];
     double a0 = 0.0, a1 = 0.0;
@@ -326,22 +339,59 @@ __device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, co
 // right-hand side piece (entries into d.partial6). W comes from the camera
 // record's R, t exactly as k_prep forms it, so the fused and the separate
 // prep agree bit for bit.
-template <bool kShared, bool kPrep = false>
+//
+// A tile is worked by a warp pair (kLinThreads threads on one workspace
+// slice, synchronised by the pair's named barrier): twice the resident warps
+// of a warp per tile for the same shared memory. Every per-observation,
+// per-point and per-entry result keeps its order (an entry's or a point's
+// sum runs on one thread), and the tile totals are SplitSums, so the group
+// size does not change a bit.
+// k_lin_prep runs warp pairs (kLinThreads); k_linearize, with its smaller
+// workspace, is faster with a warp per tile (NT = 32).
+// Tile cost / |g|^2 totals in one order for every group size: item i goes to
+// partial (i & 32) of its lane, each partial takes the warp's fixed tree,
+// total = tree(even runs) + tree(odd runs). A warp pair's thread sees items
+// of one parity only, so its warp totals are the two trees.
+struct SplitSum {
+  double a = 0.0, b = 0.0;
+  __device__ __forceinline__ void add(int i, double v) {
+    if (i & 32)
+      b += v;
+    else
+      a += v;
+  }
+  __device__ __forceinline__ double warp_total() const { return warp_sum(a) + warp_sum(b); }
+};
+constexpr int kLinThreads = 64;
+template <int NT>
+__device__ __forceinline__ void tile_sync() {
+  if constexpr (NT == 32)
+    __syncwarp();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + static_cast<int>(threadIdx.x) / NT), "n"(NT) : "memory");
+}
+template <int NT>
+__device__ __forceinline__ int group_tile_index() {
+  return blockIdx.x * (blockDim.x / NT) + threadIdx.x / NT;
+}
+
+template <bool kShared, bool kPrep, int NT>
 __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* smem, int slice, int t,
                                          int write_jac, double clo = 0.0, double chi = 0.0) {
   constexpr int kPtw = kPrep ? 12 : 3, kCw = kPrep ? 23 : 20;
-  const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kPrep ? kLinPrepWs : kLinWs, g.ncam, g.npts, g.nobs);
-  const int lane = lane_id();
-  load_point_fields<3>(ws, kPtw, 0, d.pts, g.pb, g.npts);
-  load_tile_index(d, g, ws);
-  __syncwarp();
-  load_cam_fields<7>(ws, g.ncam, kCw, 0, d.pose, 7);
-  load_cam_fields<4>(ws, g.ncam, kCw, 7, d.intr, 4);
-  load_cam_fields<kPrep ? 12 : 9>(ws, g.ncam, kCw, 11, d.camrec, kCamRec);
-  __syncwarp();
-  double cost = 0.0;
+  char* base = kShared ? smem + (threadIdx.x / NT) * slice : d.bigws + (long long)g.big * d.big_stride;
+  const Ws ws = ws_carve(base, kPrep ? kLinPrepWs : kLinWs, g.ncam, g.npts, g.nobs);
+  const int tt = tile_tid<NT>(), lane = tt & 31, wp = tt >> 5;
+  load_point_fields<3, NT>(ws, kPtw, 0, d.pts, g.pb, g.npts);
+  load_tile_index<NT>(d, g, ws);
+  tile_sync<NT>();
+  load_cam_fields<7, NT>(ws, g.ncam, kCw, 0, d.pose, 7);
+  load_cam_fields<4, NT>(ws, g.ncam, kCw, 7, d.intr, 4);
+  load_cam_fields<kPrep ? 12 : 9, NT>(ws, g.ncam, kCw, 11, d.camrec, kCamRec);
+  tile_sync<NT>();
+  SplitSum cost;
   int bad = INT_MAX;
-  for (int s = lane; s < g.nobs; s += 32) {
+  for (int s = tt; s < g.nobs; s += NT) {
     const std::uint32_t lcpt = ws.lcpt[s];
     const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
     const double* pt = ws.pt + (lcpt >> 16) * kPtw;
@@ -356,7 +406,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
       jac_pt(D, cam + 11, st + 12);
       st[18] = r0;
       st[19] = r1;
-      cost += r0 * r0 + r1 * r1;
+      cost.add(s, r0 * r0 + r1 * r1);
       if (write_jac && d.jstore) {
         const long long gs = g.ob + s;
 #pragma unroll
@@ -373,10 +423,10 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     }
   }
   if (bad != INT_MAX) atomicMin(&d.lm->err_obs, bad);
-  __syncwarp();
-  // camera side: lane j < 27 owns component j (the H_cc upper triangle
-  // row-major, then g_c) of every entry; the warp walks the entries together
-  // (no per-lane trip counts, no index decoding). Per component:
+  tile_sync<NT>();
+  // camera side: lane j < 27 of each warp owns component j (the H_cc upper
+  // triangle row-major, then g_c) of the entries e = wp, wp + 2, ... (no
+  // per-lane trip counts, no index decoding). Per component:
   // st[a] st[b0] + st[6 + a] st[b1] over the entry's observations in order.
   {
     const int j = min(lane, 26);
@@ -393,9 +443,8 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
       b0 = a + rem;
       b1 = 6 + b0;
     }
-    int qb = ws.ent[0];
-    for (int e = 0; e < g.ncam; ++e) {
-      const int qe = ws.ent[e + 1];
+    for (int e = wp; e < g.ncam; e += NT / 32) {
+      const int qb = ws.ent[e], qe = ws.ent[e + 1];
       const double* st = ws.stage + qb * 20;
       double acc0 = 0.0, acc1 = 0.0;  // two interleaved partial sums, slot order
       int q = qb;
@@ -405,13 +454,12 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
       }
       if (q < qe) acc0 += st[a] * st[b0] + st[6 + a] * st[b1];
       if (lane < 27) d.partial[(long long)(g.eb + e) * 27 + lane] = acc0 + acc1;
-      qb = qe;
     }
   }
   // point side: H_pp (6) and g_p (3) per point, observations in id order
-  double gsq = 0.0;
+  SplitSum gsq;
   int pfail = 0;
-  for (int lp = lane; lp < g.npts; lp += 32) {
+  for (int lp = tt; lp < g.npts; lp += NT) {
     double h[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) h[j] = 0.0;
@@ -431,22 +479,36 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     for (int j = 0; j < 6; ++j) d.hpp[ip * 6 + j] = h[j];
 #pragma unroll
     for (int j = 0; j < 3; ++j) d.gp[ip * 3 + j] = h[6 + j];
-    gsq += h[6] * h[6] + h[7] * h[7] + h[8] * h[8];
+    gsq.add(lp, h[6] * h[6] + h[7] * h[7] + h[8] * h[8]);
     if (kPrep) {
       double h6[6] = {h[0], h[1], h[2], h[3], h[4], h[5]};
       if (!prep_point_direct(d, ip, h6, h + 6, *d.lam, clo, chi, ws.pt + lp * kPtw)) pfail = 1;
     }
   }
-  cost = warp_sum(cost);
-  gsq = warp_sum(gsq);
-  if (lane == 0) {
-    d.tile_red[t * 2] = cost;
-    d.tile_red[t * 2 + 1] = gsq;
+  // tile totals: a warp pair adds warp 1's trees to warp 0's through
+  // tile_red (global; ordered by the pair barrier)
+  const double ct = cost.warp_total(), gt = gsq.warp_total();
+  if constexpr (NT == 32) {
+    if (lane == 0) {
+      d.tile_red[t * 2] = ct;
+      d.tile_red[t * 2 + 1] = gt;
+    }
+  } else {
+    static_assert(NT == 64, "warp or warp pair");
+    if (wp == 1 && lane == 0) {
+      d.tile_red[t * 2] = ct;
+      d.tile_red[t * 2 + 1] = gt;
+    }
+    tile_sync<NT>();
+    if (wp == 0 && lane == 0) {
+      d.tile_red[t * 2] = ct + d.tile_red[t * 2];
+      d.tile_red[t * 2 + 1] = gt + d.tile_red[t * 2 + 1];
+    }
   }
   if (kPrep) {
     if (pfail) atomicExch(&d.pcg->not_spd, 1);
-    __syncwarp();
-    for (int s = lane; s < g.nobs; s += 32) {  // V and the right-hand side pieces
+    tile_sync<NT>();
+    for (int s = tt; s < g.nobs; s += NT) {  // V and the right-hand side pieces
       const std::uint32_t lcpt = ws.lcpt[s];
       const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
       const double* R = cam + 11;  // record R9 t3; intrinsics at cam + 7
@@ -470,29 +532,32 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
 #pragma unroll
       for (int a = 0; a < 6; ++a) st[a] = rhs[a];
     }
-    __syncwarp();
-    entries_from_stage<6, 20>(ws, g.ncam, g.eb, d.partial6);
+    tile_sync<NT>();
+    entries_from_stage<6, 20, NT>(ws, g.ncam, g.eb, d.partial6);
   }
-  __syncwarp();
+  tile_sync<NT>();
 }
 
-__global__ void __launch_bounds__(256) k_lin_prep(Dev d, int slice, double clo, double chi) {
+__global__ void __launch_bounds__(512) k_lin_prep(Dev d, int slice, double clo, double chi) {
   extern __shared__ __align__(16) char smem[];
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int t = group_tile_index<kLinThreads>();
   if (t >= d.T) return;
   const TileGeom g = tile_geom(d, t);
   if (g.big >= 0)
-    lin_tile<false, true>(d, g, smem, slice, t, 0, clo, chi);
+    lin_tile<false, true, kLinThreads>(d, g, smem, slice, t, 0, clo, chi);
   else
-    lin_tile<true, true>(d, g, smem, slice, t, 0, clo, chi);
+    lin_tile<true, true, kLinThreads>(d, g, smem, slice, t, 0, clo, chi);
 }
 
 __global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_jac) {
   extern __shared__ __align__(16) char smem[];
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int t = group_tile_index<32>();
   if (t >= d.T) return;
   const TileGeom g = tile_geom(d, t);
-  BAE_TILE_DISPATCH(lin_tile, d, g, smem, slice, t, write_jac);
+  if (g.big >= 0)
+    lin_tile<false, false, 32>(d, g, smem, slice, t, write_jac);
+  else
+    lin_tile<true, false, 32>(d, g, smem, slice, t, write_jac);
 }
 
 // Residual only (evaluate + squared_norm, problems.hpp:66, lm.hpp:81-85) at
@@ -508,7 +573,7 @@ __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char*
   load_cam_fields<7>(ws, g.ncam, 11, 0, d.pose, 7);
   load_cam_fields<4>(ws, g.ncam, 11, 7, d.intr, 4);
   __syncwarp();
-  double cost = 0.0;
+  SplitSum cost;
   int bad = INT_MAX;
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
@@ -520,14 +585,14 @@ __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char*
         d.resid[g.ob + s] = r0;
         d.resid[(long long)d.N + g.ob + s] = r1;
       }
-      cost += r0 * r0 + r1 * r1;
+      cost.add(s, r0 * r0 + r1 * r1);
     } else {
       bad = min(bad, d.obs_orig[g.ob + s]);
     }
   }
   if (bad != INT_MAX) atomicMin(&d.lm->err_obs, bad);
-  cost = warp_sum(cost);
-  if (lane == 0) d.tile_red[t * 2] = cost;
+  const double ct = cost.warp_total();
+  if (lane == 0) d.tile_red[t * 2] = ct;
   __syncwarp();
 }
 
@@ -1874,7 +1939,7 @@ __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char
     d.pts_t[ip * 3 + 2] = n2;
   }
   __syncwarp();
-  double cost = 0.0;
+  SplitSum cost;
   int bad = 0;
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
@@ -1887,13 +1952,13 @@ __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char
     double r0, r1;
     P3 y;
     if (residual(d.pinhole, tc, pt, px, r0, r1, y))
-      cost += r0 * r0 + r1 * r1;
+      cost.add(s, r0 * r0 + r1 * r1);
     else
       bad = 1;  // CheiralityError in the trial evaluate -> cost = inf (lm.hpp:176-181)
   }
   if (bad) atomicExch(&d.lm->trial_bad, 1);
-  cost = warp_sum(cost);
-  if (lane == 0) d.tile_red[t * 2] = cost;
+  const double ct = cost.warp_total();
+  if (lane == 0) d.tile_red[t * 2] = ct;
   __syncwarp();
 }
 
@@ -1994,7 +2059,7 @@ int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStre
   return n;
 }
 int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
-  k_lin_prep<<<tile_blocks(d.T, sm.linprep), 32 * sm.linprep.wpb, sm.linprep.wpb * sm.linprep.slice, s>>>(
+  k_lin_prep<<<tile_blocks(d.T, sm.linprep), kLinThreads * sm.linprep.wpb, sm.linprep.wpb * sm.linprep.slice, s>>>(
       d, sm.linprep.slice, clo, chi);
   k_cam_lin_prep<<<d.C, kCamNT, 0, s>>>(d, clo, chi);
   k_lin_totals<<<1, 1024, 0, s>>>(d);
