@@ -253,7 +253,7 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
   o[15] = intr[c * 4 + 3];
 }
 
-constexpr int kVStride = 20;  // doubles per V = W L^-T record (two 16-byte aligned halves of 9)
+constexpr int kVStride = 20;  // doubles per V = W L^-T record (6 x 3 row-major + 2 pad: 160 bytes, 32-byte aligned)
 // Direct solver prep, shared by k_prep<true> and the fused k_lin_prep (one
 // copy of the arithmetic, so the two agree bit for bit).
 // Per point: damped H~_pp, its inverse (d.hinv, for the
@@ -295,26 +295,28 @@ __device__ __forceinline__ bool prep_point_direct(const Dev& d, long long ip, do
 }
 
 // Direct solver, per observation slot: V = W L^-T (V V^T = W H~^-1 W^T)
-// stored as two 16-byte aligned halves, and the Schur right-hand side piece
+// stored row-major (kVStride doubles), and the Schur right-hand side piece
 // W v into rhs[0..5].
 __device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, const double (&W)[18],
                                                 const double* sp, double* rhs) {
   const double* lf = sp + 3;
-  double vv[kVStride];  // rows 0..2 at [0, 9), rows 3..5 at [10, 19)
+  double vv[kVStride];
 #pragma unroll
   for (int a = 0; a < 6; ++a) {
     const double v0 = W[a * 3] * lf[0];
     const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
     const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
-    const int o = a * 3 + (a >= 3 ? 1 : 0);
-    vv[o] = v0;
-    vv[o + 1] = v1;
-    vv[o + 2] = v2;
+    vv[a * 3] = v0;
+    vv[a * 3 + 1] = v1;
+    vv[a * 3 + 2] = v2;
   }
-  vv[9] = vv[19] = 0.0;  // whole sectors written
-  double2* vo = reinterpret_cast<double2*>(d.wstore + slot * kVStride);
+  vv[18] = vv[19] = 0.0;  // whole sectors written
+  double* vo = d.wstore + slot * kVStride;
 #pragma unroll
-  for (int j = 0; j < kVStride / 2; ++j) vo[j] = make_double2(vv[2 * j], vv[2 * j + 1]);
+  for (int j = 0; j < kVStride / 4; ++j)  // whole 32-byte sectors per store
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(vo + 4 * j), "d"(vv[4 * j]), "d"(vv[4 * j + 1]),
+                 "d"(vv[4 * j + 2]), "d"(vv[4 * j + 3])
+                 : "memory");
   const double* vp = sp + 9;
 #pragma unroll
   for (int a = 0; a < 6; ++a) rhs[a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
@@ -538,7 +540,9 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
   tile_sync<NT>();
 }
 
-__global__ void __launch_bounds__(512) k_lin_prep(Dev d, int slice, double clo, double chi) {
+// 96 registers: two CTAs of up to 10 warps (5 pairs, the Final-13682 slice)
+// per SM; 98 (rounded to 104) left one.
+__global__ void __maxnreg__(96) k_lin_prep(Dev d, int slice, double clo, double chi) {
   extern __shared__ __align__(16) char smem[];
   const int t = group_tile_index<kLinThreads>();
   if (t >= d.T) return;
@@ -1050,74 +1054,102 @@ __global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long lo
 // strided over the block's pairs, fixed xor tree; column-major lower
 // triangle for potrf.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
+// 256-bit read-only global load (sm_100: one instruction per 32-byte sector)
+__device__ __forceinline__ void ldg_v4(const double* p, double* o) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+               : "l"(p));
+}
+constexpr int kSchurDenseThreads = 128;
+__global__ void __launch_bounds__(kSchurDenseThreads, 3) k_schur_dense(Dev d) {
   // Warp per chunk of at most kSchurChunk pairs of one camera block (a long
   // block -- a diagonal one holds every observation of its camera -- is cut
   // into several, so no warp walks a whole camera's observations alone).
-  // Lane = 4 * slot + part: 8 pairs in flight, each pair's 6x6 product split
-  // in four 3x3 corners (rows 3 (part & 1), columns 3 (part >> 1)), so a lane
-  // loads two contiguous 9-double row bands (V_k and V_l) and keeps 9
-  // accumulators; the 8 slot sums are combined by a fixed shuffle tree. A
-  // block of one chunk is written at once; otherwise each chunk stores its
-  // 6x6 partial and the block's last chunk to finish (ticket) adds the
-  // partials in chunk order. Every order depends only on the block.
+  // Lane = pair slot: each lane forms the whole 6x6 V_k V_l^T of its pairs
+  // (both 144-byte records reach its registers once: the LSU writeback of
+  // loaded bytes, not L1 or DRAM, bounds this kernel; ~168 registers, so
+  // 4-warp CTAs, 3 per SM), then a fixed
+  // reduce-scatter tree over the 32 slots leaves elements
+  // 9 g .. 9 g + 8 of the chunk sum in lane group g = lane >> 3. A block of
+  // one chunk is written at once; otherwise each chunk stores its 6x6
+  // partial and the block's last chunk to finish (ticket) adds the partials
+  // in chunk order. Every order depends only on the block.
   const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (wid >= d.nchunk) return;
   const int4 ch = d.chunks[wid];  // block, first pair, end pair, index of the block's first chunk
   const int blk = ch.x;
-  const int lane = lane_id(), slot = lane >> 2, part = lane & 3;
-  const int r0 = 3 * (part & 1), c0 = 3 * (part >> 1);
-  double acc[9];
+  const int lane = lane_id();
+  double acc[36];
 #pragma unroll
-  for (int j = 0; j < 9; ++j) acc[j] = 0.0;
-  const int qe = ch.z;
-#pragma unroll 2
-  for (int q = ch.y + slot; q < qe; q += 8) {
+  for (int j = 0; j < 36; ++j) acc[j] = 0.0;
+#pragma unroll 1
+  for (int q = ch.y + lane; q < ch.z; q += 32) {
     const int2 pr = d.pairs[q];
-    // V_k rows r0..r0+2 and V_l rows c0..c0+2: 16-byte aligned 9-double halves
-    const double* wh = d.wstore + (long long)pr.x * kVStride + (r0 ? 10 : 0);
-    const double* w = d.wstore + (long long)pr.y * kVStride + (c0 ? 10 : 0);
-    double a[9], b[9];
+    // five 32-byte loads a record: each touches one whole sector (16-byte
+    // loads touch every sector twice, and the L1 pays per sector touched)
+    const double* wa = d.wstore + (long long)pr.x * kVStride;
+    const double* wb = d.wstore + (long long)pr.y * kVStride;
+    double a[kVStride], b[kVStride];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double2 x = __ldg(reinterpret_cast<const double2*>(wh) + j);
-      const double2 y = __ldg(reinterpret_cast<const double2*>(w) + j);
-      a[2 * j] = x.x;
-      a[2 * j + 1] = x.y;
-      b[2 * j] = y.x;
-      b[2 * j + 1] = y.y;
+    for (int j = 0; j < kVStride / 4; ++j) {
+      ldg_v4(wa + 4 * j, a + 4 * j);
+      ldg_v4(wb + 4 * j, b + 4 * j);
     }
-    a[8] = __ldg(wh + 8);
-    b[8] = __ldg(w + 8);
 #pragma unroll
-    for (int x = 0; x < 3; ++x)
+    for (int m = 0; m < 6; ++m)
 #pragma unroll
-      for (int y = 0; y < 3; ++y)
-        acc[x * 3 + y] += a[x * 3] * b[y * 3] + a[x * 3 + 1] * b[y * 3 + 1] + a[x * 3 + 2] * b[y * 3 + 2];
+      for (int n = 0; n < 6; ++n) {
+        double& c = acc[m * 6 + n];
+        c = fma(a[3 * m], b[3 * n], c);
+        c = fma(a[3 * m + 1], b[3 * n + 1], c);
+        c = fma(a[3 * m + 2], b[3 * n + 2], c);
+      }
+  }
+  // reduce-scatter: xor 16 halves the 36 sums (bit 4 keeps [18 b4, +18)),
+  // xor 8 halves again (bit 3 keeps the upper 9), xor 4/2/1 finish the 9
+  // (a + b == b + a, so the partners agree bit for bit)
+  double h18[18];
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 18; ++i) {
+      const double keep = up ? acc[18 + i] : acc[i], give = up ? acc[i] : acc[18 + i];
+      h18[i] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
+    }
+  }
+  double v9[9];
+  {
+    const bool up = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const double keep = up ? h18[9 + i] : h18[i], give = up ? h18[i] : h18[9 + i];
+      v9[i] = keep + __shfl_xor_sync(0xffffffffu, give, 8);
+    }
   }
 #pragma unroll
-  for (int j = 0; j < 9; ++j)
+  for (int i = 0; i < 9; ++i)
 #pragma unroll
-    for (int off = 4; off < 32; off <<= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], off);
+    for (int off = 4; off > 0; off >>= 1) v9[i] += __shfl_xor_sync(0xffffffffu, v9[i], off);
+  // lane (g, j = lane & 7) owns element 9 g + j, and j == 0 also 9 g + 8
+  const int g9 = 9 * (lane >> 3), j8 = lane & 7;
+  double own = v9[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i)
+    if (j8 == i) own = v9[i];
+  const double own8 = v9[8];
   const int first = ch.w, count = d.blk_nchunk[blk];
-  bool writer = true;
   double v36 = 0.0;  // multi-chunk: entry (lane / 6, lane % 6) of the block sum, lanes 0..35 -> 0..31 + 4 below
   double v36b = 0.0;
   if (count > 1) {
     double* mine = d.schur_part + 36LL * wid;
-    if (slot == 0) {
-#pragma unroll
-      for (int x = 0; x < 3; ++x)
-#pragma unroll
-        for (int y = 0; y < 3; ++y) mine[(r0 + x) * 6 + c0 + y] = acc[x * 3 + y];
-    }
+    mine[g9 + j8] = own;
+    if (j8 == 0) mine[g9 + 8] = own8;
     __threadfence();
     __syncwarp();
     int t = 0;
     if (lane == 0) t = static_cast<int>(atomicAdd(d.blk_ticket + blk, 1u));
     t = __shfl_sync(0xffffffffu, t, 0);
-    writer = t == count - 1;
-    if (!writer) return;
+    if (t != count - 1) return;
     __threadfence();  // the other chunks' partials, published before their tickets
     for (int i = 0; i < count; ++i) {  // chunk order
       const double* pp = d.schur_part + 36LL * (first + i);
@@ -1146,16 +1178,15 @@ __global__ void __launch_bounds__(256, 3) k_schur_dense(Dev d) {
   }
   const bool diag = cc.x == cc.y && !d.cred;  // sharded: H~_cc is added after the rank sum
   if (count == 1) {
-    if (slot == 0) {  // lanes 0..3: one 3x3 corner each
-#pragma unroll
-      for (int x = 0; x < 3; ++x)
-#pragma unroll
-        for (int y = 0; y < 3; ++y) {
-          const int r = r0 + x, c = c0 + y;
-          double v = -acc[x * 3 + y];
-          if (diag) v += h[sym6(r, c)];
-          base[r * ldr + c * ldc] = v;
-        }
+    const int e = g9 + j8;
+    double v = -own;
+    if (diag) v += h[sym6(e / 6, e % 6)];
+    base[(e / 6) * ldr + (e % 6) * ldc] = v;
+    if (j8 == 0) {
+      const int e8 = g9 + 8;
+      double v8 = -own8;
+      if (diag) v8 += h[sym6(e8 / 6, e8 % 6)];
+      base[(e8 / 6) * ldr + (e8 % 6) * ldc] = v8;
     }
     return;
   }
@@ -2150,7 +2181,8 @@ int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
   int n = 0;
   if (d.nblk > 0) {
     cudaMemsetAsync(d.blk_ticket, 0, sizeof(unsigned) * d.nblk, s);
-    k_schur_dense<<<(d.nchunk + 7) / 8, 256, 0, s>>>(d);
+    k_schur_dense<<<(d.nchunk + kSchurDenseThreads / 32 - 1) / (kSchurDenseThreads / 32), kSchurDenseThreads, 0, s>>>(
+        d);
     ++n;
   }
   if (comm) {  // the direct solve's exchange: the reduced matrix, once per LM iteration
