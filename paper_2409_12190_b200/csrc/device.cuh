@@ -234,11 +234,15 @@ __host__ __device__ __forceinline__ long long ws_bytes(WsDims w, int ncam, int n
 //   lin+prep (K1+F1): cam + t3 of the record, pt p3 L6 v3
 //   cost (K1c), prep (K3/K4; direct: RHS stage only), Schur product (K5),
 //   trial (K7/K8)
-constexpr WsDims kLinWs{20, 3, 20, 0};
-constexpr WsDims kLinPrepWs{23, 12, 20, 0};
+// Stage rows of an odd number of doubles: lanes writing consecutive rows hit
+// distinct bank pairs (20-double rows put every 4th lane on the same banks).
+constexpr int kLinStW = 21;  // Jc12 Jp6 r2 + 1 pad
+constexpr int kPrepDirStW = 7;  // RHS piece 6 + 1 pad
+constexpr WsDims kLinWs{20, 3, kLinStW, 0};
+constexpr WsDims kLinPrepWs{23, 12, kLinStW, 0};
 constexpr WsDims kCostWs{11, 3, 0, 0};
 constexpr WsDims kPrepWs{16, 12, 27, 0};
-constexpr WsDims kPrepDirWs{16, 12, 6, 0};
+constexpr WsDims kPrepDirWs{16, 12, kPrepDirStW, 0};
 constexpr WsDims kSxWs{24, 3, 6, 0};
 constexpr WsDims kTrialWs{29, 6, 3, 0};
 // Workspace bytes of one tile for a kernel kind (WsKind order, kernels.cuh:

@@ -398,7 +398,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
     const double* pt = ws.pt + (lcpt >> 16) * kPtw;
     const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
-    double* st = ws.stage + s * 20;
+    double* st = ws.stage + s * kLinStW;
     double r0 = 0.0, r1 = 0.0;
     P3 y;
     if (residual(d.pinhole, cam, pt, px, r0, r1, y)) {
@@ -447,12 +447,12 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     }
     for (int e = wp; e < g.ncam; e += NT / 32) {
       const int qb = ws.ent[e], qe = ws.ent[e + 1];
-      const double* st = ws.stage + qb * 20;
+      const double* st = ws.stage + qb * kLinStW;
       double acc0 = 0.0, acc1 = 0.0;  // two interleaved partial sums, slot order
       int q = qb;
-      for (; q + 1 < qe; q += 2, st += 40) {
+      for (; q + 1 < qe; q += 2, st += 2 * kLinStW) {
         acc0 += st[a] * st[b0] + st[6 + a] * st[b1];
-        acc1 += st[20 + a] * st[20 + b0] + st[26 + a] * st[20 + b1];
+        acc1 += st[kLinStW + a] * st[kLinStW + b0] + st[kLinStW + 6 + a] * st[kLinStW + b1];
       }
       if (q < qe) acc0 += st[a] * st[b0] + st[6 + a] * st[b1];
       if (lane < 27) d.partial[(long long)(g.eb + e) * 27 + lane] = acc0 + acc1;
@@ -466,7 +466,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
 #pragma unroll
     for (int j = 0; j < 9; ++j) h[j] = 0.0;
     for (int q = ws.pptr[lp]; q < ws.pptr[lp + 1]; ++q) {
-      const double* st = ws.stage + ws.ptl[q] * 20;
+      const double* st = ws.stage + ws.ptl[q] * kLinStW;
       const double* jp = st + 12;
       int k = 0;
 #pragma unroll
@@ -530,12 +530,12 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
         for (int j = 0; j < 3; ++j) W[a * 3 + j] = Jc[a] * Jp[j] + Jc[6 + a] * Jp[3 + j];
       double rhs[6];
       prep_obs_direct(d, g.ob + s, W, sp, rhs);
-      double* st = ws.stage + s * 20;
+      double* st = ws.stage + s * kLinStW;
 #pragma unroll
       for (int a = 0; a < 6; ++a) st[a] = rhs[a];
     }
     tile_sync<NT>();
-    entries_from_stage<6, 20, NT>(ws, g.ncam, g.eb, d.partial6);
+    entries_from_stage<6, kLinStW, NT>(ws, g.ncam, g.eb, d.partial6);
   }
   tile_sync<NT>();
 }
@@ -840,7 +840,7 @@ template <bool kShared, bool kDirect>
 __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char* smem, int slice, double lambda,
                                           double clo, double chi) {
   if (kDirect) lambda = *d.lam;  // direct solves keep lambda on the device (graph-replayed LM iterations)
-  constexpr int SW = kDirect ? 6 : 27;
+  constexpr int SW = kDirect ? kPrepDirStW : 27;  // row stride; the direct RHS piece is 6 wide
   const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kDirect ? kPrepDirWs : kPrepWs, g.ncam, g.npts, g.nobs);
   const int lane = lane_id();
   load_point_fields<3>(ws, 12, 0, d.pts, g.pb, g.npts);
@@ -919,7 +919,7 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     for (int a = 0; a < 6; ++a) st[SW - 6 + a] = W[a * 3] * vp[0] + W[a * 3 + 1] * vp[1] + W[a * 3 + 2] * vp[2];
   }
   __syncwarp();
-  entries_from_stage<SW, SW>(ws, g.ncam, g.eb, d.partial);
+  entries_from_stage<kDirect ? 6 : SW, SW>(ws, g.ncam, g.eb, d.partial);
   __syncwarp();
 }
 
