@@ -168,8 +168,9 @@ __device__ __forceinline__ void load_tile_index(const Dev& d, const TileGeom& g,
                                 [&](int i, std::uint16_t v) { ws.ptl[i] = v; });
 }
 
-// W consecutive doubles per point from src[(pb + lp) * W] into ws.pt[lp * ptw + off].
-template <int W, int NT = 32>
+// W consecutive doubles per point from src[(pb + lp) * W] into ws.pt[lp * ptw + off]
+// (kSoA: into ws.pt[(off + k) * npts + lp], see pt_get).
+template <int W, int NT = 32, bool kSoA = false>
 __device__ __forceinline__ void load_point_fields(const Ws& ws, int ptw, int off, const double* src, int pb,
                                                   int npts) {
   const double* base = src + (long long)pb * W;
@@ -177,8 +178,25 @@ __device__ __forceinline__ void load_point_fields(const Ws& ws, int ptw, int off
       npts * W, [&](int i) { return base + i; },
       [&](int i, double v) {
         const int lp = i / W;
-        ws.pt[lp * ptw + off + (i - lp * W)] = v;
+        if (kSoA)
+          ws.pt[(off + i - lp * W) * npts + lp] = v;
+        else
+          ws.pt[lp * ptw + off + (i - lp * W)] = v;
       });
+}
+
+// Structure-of-arrays point area (the 12-double prep rows): field c of local
+// point lp at ws.pt[c * npts + lp], so lanes on consecutive points touch
+// consecutive bank pairs (12-double rows put every 4th point on one bank).
+template <int K>
+__device__ __forceinline__ void pt_get(const Ws& ws, int npts, int lp, int c0, double* out) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = ws.pt[(c0 + k) * npts + lp];
+}
+template <int K>
+__device__ __forceinline__ void pt_put(const Ws& ws, int npts, int lp, int c0, const double* in) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) ws.pt[(c0 + k) * npts + lp] = in[k];
 }
 
 // W consecutive doubles per camera from src[camid * stride] into
@@ -384,7 +402,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
   char* base = kShared ? smem + (threadIdx.x / NT) * slice : d.bigws + (long long)g.big * d.big_stride;
   const Ws ws = ws_carve(base, kPrep ? kLinPrepWs : kLinWs, g.ncam, g.npts, g.nobs);
   const int tt = tile_tid<NT>(), lane = tt & 31, wp = tt >> 5;
-  load_point_fields<3, NT>(ws, kPtw, 0, d.pts, g.pb, g.npts);
+  load_point_fields<3, NT, kPrep>(ws, kPtw, 0, d.pts, g.pb, g.npts);
   load_tile_index<NT>(d, g, ws);
   tile_sync<NT>();
   load_cam_fields<7, NT>(ws, g.ncam, kCw, 0, d.pose, 7);
@@ -396,7 +414,12 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
   for (int s = tt; s < g.nobs; s += NT) {
     const std::uint32_t lcpt = ws.lcpt[s];
     const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
-    const double* pt = ws.pt + (lcpt >> 16) * kPtw;
+    double pv[3];
+    const double* pt = pv;
+    if constexpr (kPrep)
+      pt_get<3>(ws, g.npts, lcpt >> 16, 0, pv);
+    else
+      pt = ws.pt + (lcpt >> 16) * kPtw;
     const double2 px = reinterpret_cast<const double2*>(d.obs_px)[g.ob + s];
     double* st = ws.stage + s * kLinStW;
     double r0 = 0.0, r1 = 0.0;
@@ -484,7 +507,9 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     gsq.add(lp, h[6] * h[6] + h[7] * h[7] + h[8] * h[8]);
     if (kPrep) {
       double h6[6] = {h[0], h[1], h[2], h[3], h[4], h[5]};
-      if (!prep_point_direct(d, ip, h6, h + 6, *d.lam, clo, chi, ws.pt + lp * kPtw)) pfail = 1;
+      double spl[12];
+      if (!prep_point_direct(d, ip, h6, h + 6, *d.lam, clo, chi, spl)) pfail = 1;
+      pt_put<9>(ws, g.npts, lp, 3, spl + 3);
     }
   }
   // tile totals: a warp pair adds warp 1's trees to warp 0's through
@@ -514,7 +539,8 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
       const std::uint32_t lcpt = ws.lcpt[s];
       const double* cam = ws.cam + (lcpt & 0xffff) * kCw;
       const double* R = cam + 11;  // record R9 t3; intrinsics at cam + 7
-      const double* sp = ws.pt + (lcpt >> 16) * kPtw;
+      double sp[12];
+      pt_get<12>(ws, g.npts, lcpt >> 16, 0, sp);
       P3 y;
       y.x = R[0] * sp[0] + R[1] * sp[1] + R[2] * sp[2] + R[9];
       y.y = R[3] * sp[0] + R[4] * sp[1] + R[5] * sp[2] + R[10];
@@ -843,7 +869,7 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
   constexpr int SW = kDirect ? kPrepDirStW : 27;  // row stride; the direct RHS piece is 6 wide
   const Ws ws = ws_carve(ws_base<kShared>(d, g, smem, slice), kDirect ? kPrepDirWs : kPrepWs, g.ncam, g.npts, g.nobs);
   const int lane = lane_id();
-  load_point_fields<3>(ws, 12, 0, d.pts, g.pb, g.npts);
+  load_point_fields<3, 32, true>(ws, 12, 0, d.pts, g.pb, g.npts);
   load_tile_index(d, g, ws);
   __syncwarp();
   load_cam_fields<16>(ws, g.ncam, 16, 0, d.camrec, kCamRec);
@@ -853,10 +879,11 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     double h[6], inv[9];
 #pragma unroll
     for (int j = 0; j < 6; ++j) h[j] = d.hpp[ip * 6 + j];
-    double* sp = ws.pt + lp * 12;
+    double sp[12];
     if (kDirect) {  // the Cholesky factor L of H~_pp instead of its inverse (shared with k_lin_prep)
       const double g3[3] = {d.gp[ip * 3], d.gp[ip * 3 + 1], d.gp[ip * 3 + 2]};
       if (!prep_point_direct(d, ip, h, g3, lambda, clo, chi, sp)) fail = 1;
+      pt_put<9>(ws, g.npts, lp, 3, sp + 3);
       continue;
     }
     h[0] = damp_diag(h[0], lambda, clo, chi);
@@ -877,13 +904,15 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
     sp[9] = inv[0] * g0 + inv[1] * g1 + inv[2] * g2;
     sp[10] = inv[3] * g0 + inv[4] * g1 + inv[5] * g2;
     sp[11] = inv[6] * g0 + inv[7] * g1 + inv[8] * g2;
+    pt_put<9>(ws, g.npts, lp, 3, sp + 3);
   }
   if (fail) atomicExch(&d.pcg->not_spd, 1);
   __syncwarp();
   for (int s = lane; s < g.nobs; s += 32) {
     const std::uint32_t lcpt = ws.lcpt[s];
     const double* cam = ws.cam + (lcpt & 0xffff) * 16;
-    const double* sp = ws.pt + (lcpt >> 16) * 12;
+    double sp[12];
+    pt_get<12>(ws, g.npts, lcpt >> 16, 0, sp);
     P3 y;
     double D[6], Jc[12], Jp[6];
     obs_geometry(d.pinhole, cam, sp, y, D);
