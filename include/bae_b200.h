@@ -343,7 +343,8 @@ int bae_partition_points(int32_t num_cameras, int32_t num_points, const int32_t*
  * substitution of the reduced camera system (direct solver), 5 = the direct
  * solver's prep (damped point blocks, V = W L^-T, right-hand side), 6 = its
  * Schur assembly, 7 = kinds 0 and 5 fused into one pass (what an LM
- * iteration after an accepted step runs; single rank). ms receives the mean
+ * iteration after an accepted step runs; single rank), 8 = the trial (camera
+ * retraction, point back-substitution, trial cost). ms receives the mean
  * milliseconds per launch. */
 int bae_time_kernel(bae_problem* p, int32_t kind, int32_t reps, double* ms);
 /* Number of kernel launches issued by this handle since creation. */

@@ -296,6 +296,48 @@ __device__ __forceinline__ TileGeom tile_geom(const Dev& d, int t) {
   return g;
 }
 
+// L2 prefetch of a byte range (TMA bulk prefetch, 16-byte granules): the
+// inputs of a tile that runs about one resident wave later, so that its
+// warp's dependent index / field loads hit L2 instead of HBM.
+__device__ __forceinline__ void l2_prefetch(const void* p, long long bytes) {
+  if (bytes <= 0) return;
+  const unsigned long long a = reinterpret_cast<unsigned long long>(p) & ~15ull;
+  const unsigned long long e = (reinterpret_cast<unsigned long long>(p) + bytes + 15) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<unsigned>(e - a)) : "memory");
+}
+struct TileSpan {
+  int ob, oe, pb, pe, eb, ee;
+};
+// Geometry of tile tn (empty past the last tile); loaded early, used late.
+__device__ __forceinline__ TileSpan tile_span(const Dev& d, int tn) {
+  TileSpan q{0, 0, 0, 0, 0, 0};
+  if (tn < d.T) {
+    q.ob = d.tile_obs_begin[tn];
+    q.oe = d.tile_obs_begin[tn + 1];
+    q.pb = d.tile_pt_begin[tn];
+    q.pe = d.tile_pt_begin[tn + 1];
+    q.eb = d.tile_ent_begin[tn];
+    q.ee = d.tile_ent_begin[tn + 1];
+  }
+  return q;
+}
+// The index arrays, pixels and point coordinates of a tile, plus up to two
+// per-point arrays of w doubles (e.g. g_p and H~_pp^-1 for the trial pass).
+__device__ __forceinline__ void prefetch_tile(const Dev& d, const TileSpan& q, const double* pa = nullptr, int wa = 0,
+                                              const double* pb = nullptr, int wb = 0) {
+  if (q.oe <= q.ob) return;
+  const long long no = q.oe - q.ob, np = q.pe - q.pb, ne = q.ee - q.eb;
+  l2_prefetch(d.obs_lcpt + q.ob, no * 4);
+  l2_prefetch(d.ptobs + q.ob, no * 2);
+  l2_prefetch(d.obs_px + 2LL * q.ob, no * 16);
+  l2_prefetch(d.pt_ptr + q.pb, (np + 1) * 4);
+  l2_prefetch(d.pts + 3LL * q.pb, np * 24);
+  l2_prefetch(d.ent_obs_begin + q.eb, (ne + 1) * 4);
+  l2_prefetch(d.ent_cam + q.eb, ne * 4);
+  if (pa) l2_prefetch(pa + (long long)wa * q.pb, np * wa * 8);
+  if (pb) l2_prefetch(pb + (long long)wb * q.pb, np * wb * 8);
+}
+
 // Warp-level segmented reduction over 32 consecutive tile slots. Segments
 // are contiguous runs of equal `seg` (the local camera); the head lane of each
 // run ends up with the run's sum and stores it as a "piece": lane 0 into its

@@ -18,6 +18,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
+#include <string>
 
 #include <cooperative_groups.h>
 
@@ -568,22 +569,27 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
 
 // 96 registers: two CTAs of up to 10 warps (5 pairs, the Final-13682 slice)
 // per SM; 98 (rounded to 104) left one.
-__global__ void __maxnreg__(96) k_lin_prep(Dev d, int slice, double clo, double chi) {
+__global__ void __maxnreg__(96) k_lin_prep(Dev d, int slice, double clo, double chi, int pf) {
   extern __shared__ __align__(16) char smem[];
   const int t = group_tile_index<kLinThreads>();
   if (t >= d.T) return;
+  const bool lead = threadIdx.x % kLinThreads == 0;
+  const TileSpan nx = pf > 0 && lead ? tile_span(d, t + pf) : TileSpan{0, 0, 0, 0, 0, 0};
   const TileGeom g = tile_geom(d, t);
+  if (lead) prefetch_tile(d, nx);  // one wave ahead
   if (g.big >= 0)
     lin_tile<false, true, kLinThreads>(d, g, smem, slice, t, 0, clo, chi);
   else
     lin_tile<true, true, kLinThreads>(d, g, smem, slice, t, 0, clo, chi);
 }
 
-__global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_jac) {
+__global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_jac, int pf) {
   extern __shared__ __align__(16) char smem[];
   const int t = group_tile_index<32>();
   if (t >= d.T) return;
+  const TileSpan nx = pf > 0 && lane_id() == 0 ? tile_span(d, t + pf) : TileSpan{0, 0, 0, 0, 0, 0};
   const TileGeom g = tile_geom(d, t);
+  if (lane_id() == 0) prefetch_tile(d, nx);  // one wave ahead
   if (g.big >= 0)
     lin_tile<false, false, 32>(d, g, smem, slice, t, write_jac);
   else
@@ -953,11 +959,13 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
 }
 
 template <bool kDirect>
-__global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, double clo, double chi) {
+__global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, double clo, double chi, int pf) {
   extern __shared__ __align__(16) char smem[];
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
+  const TileSpan nx = pf > 0 && lane_id() == 0 ? tile_span(d, t + pf) : TileSpan{0, 0, 0, 0, 0, 0};
   const TileGeom g = tile_geom(d, t);
+  if (lane_id() == 0) prefetch_tile(d, nx, d.hpp, 6, d.gp, 3);  // one wave ahead
   if (g.big >= 0)
     prep_tile<false, kDirect>(d, g, smem, slice, lambda, clo, chi);
   else
@@ -2022,11 +2030,13 @@ __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(256) k_backsub_trial(Dev d, int slice) {
+__global__ void __launch_bounds__(256) k_backsub_trial(Dev d, int slice, int pf) {
   extern __shared__ __align__(16) char smem[];
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
+  const TileSpan nx = pf > 0 && lane_id() == 0 ? tile_span(d, t + pf) : TileSpan{0, 0, 0, 0, 0, 0};
   const TileGeom g = tile_geom(d, t);
+  if (lane_id() == 0) prefetch_tile(d, nx, d.gp, 3, d.hinv, 6);  // one wave ahead
   BAE_TILE_DISPATCH(trial_tile, d, g, smem, slice, t);
 }
 
@@ -2042,6 +2052,19 @@ __global__ void k_commit(Dev d) {
 // launch wrappers
 // ---------------------------------------------------------------------------
 long long tile_ws_bytes(int kind, int ncam, int npts, int nobs) { return kind_ws_bytes(kind, ncam, npts, nobs); }
+
+static int resident_grid(const void* fn, int threads, int smem);
+// Tiles of one resident wave of a warp-tile kernel (its L2 prefetch
+// distance); BAE_PREFETCH=<waves> (0 disables).
+static int prefetch_distance(const void* fn, const TileLaunch& tl, int nt = 32) {
+  static const int waves = [] {
+    const char* e = std::getenv("BAE_PREFETCH");
+    return e ? std::max(0, std::atoi(e)) : 1;
+  }();
+  if (!waves) return 0;
+  return waves * resident_grid(fn, nt * tl.wpb, tl.wpb * tl.slice) * tl.wpb;
+}
+
 
 void set_smem_limits(int max_bytes) {
   cudaFuncSetAttribute(k_linearize, cudaFuncAttributeMaxDynamicSharedMemorySize, max_bytes);
@@ -2108,8 +2131,8 @@ static int reduce_cams27(const Dev& d, int extra, int nextra, Comm* comm, cudaSt
 }
 int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm) {
   int n = 3;
-  k_linearize<<<tile_blocks(d.T, sm.lin), 32 * sm.lin.wpb, sm.lin.wpb * sm.lin.slice, s>>>(d, sm.lin.slice,
-                                                                                         write_jac ? 1 : 0);
+  k_linearize<<<tile_blocks(d.T, sm.lin), 32 * sm.lin.wpb, sm.lin.wpb * sm.lin.slice, s>>>(
+      d, sm.lin.slice, write_jac ? 1 : 0, prefetch_distance((const void*)k_linearize, sm.lin));
   if (comm) {
     n += reduce_cams27(d, 1, 2, comm, s);
     comm->allreduce_min(&d.lm->err_obs, 1, s);
@@ -2120,7 +2143,7 @@ int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStre
 }
 int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
   k_lin_prep<<<tile_blocks(d.T, sm.linprep), kLinThreads * sm.linprep.wpb, sm.linprep.wpb * sm.linprep.slice, s>>>(
-      d, sm.linprep.slice, clo, chi);
+      d, sm.linprep.slice, clo, chi, prefetch_distance((const void*)k_lin_prep, sm.linprep, kLinThreads));
   k_cam_lin_prep<<<d.C, kCamNT, 0, s>>>(d, clo, chi);
   k_lin_totals<<<1, 1024, 0, s>>>(d);
   return 3;
@@ -2138,7 +2161,7 @@ int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, do
                 long long budget, cudaStream_t s, Comm* comm, bool direct) {
   if (direct) {  // RHS, damped H_cc and the per-slot W / W H~^-1 only
     k_prep<true><<<tile_blocks(d.T, sm.prepd), 32 * sm.prepd.wpb, sm.prepd.wpb * sm.prepd.slice, s>>>(
-        d, sm.prepd.slice, lambda, clo, chi);
+        d, sm.prepd.slice, lambda, clo, chi, prefetch_distance((const void*)k_prep<true>, sm.prepd));
     int n = 2;
     if (comm) {
       k_cam_entry_sums<6, kCamNT><<<d.C + 1, kCamNT, 0, s>>>(d, 2, 0);
@@ -2150,7 +2173,7 @@ int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, do
   }
   int n = 3;
   k_prep<false><<<tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s>>>(
-      d, sm.prep.slice, lambda, clo, chi);
+      d, sm.prep.slice, lambda, clo, chi, prefetch_distance((const void*)k_prep<false>, sm.prep));
   if (comm) n += reduce_cams27(d, 2, 1, comm, s);
   k_cam_prep<<<d.C, 256, 0, s>>>(d, lambda, clo, chi);
   k_prep_totals<<<1, 1024, 0, s>>>(d, tol, budget);
@@ -2199,7 +2222,7 @@ int launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
 int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   k_cam_retract<<<elt_blocks(d.C, 128), 128, 0, s>>>(d);
   k_backsub_trial<<<tile_blocks(d.T, sm.trial), 32 * sm.trial.wpb, sm.trial.wpb * sm.trial.slice, s>>>(
-      d, sm.trial.slice);
+      d, sm.trial.slice, prefetch_distance((const void*)k_backsub_trial, sm.trial));
   k_sum_tiles<<<1, 1024, 0, s>>>(d, 1);
   if (!comm) return 3;
   comm->allreduce_sum(d.cred, 2, s);

@@ -1724,13 +1724,13 @@ double Problem::time_kernel(int kind, int reps) {
     s.tol = 0.0;
     ck(cudaMemcpy(d_.pcg, &s, sizeof(PcgDev), cudaMemcpyHostToDevice), "H2D pcg");
   }
-  if (kind >= 4 && kind <= 7) {  // one damped direct solve first: S assembled, plan built
+  if (kind >= 4 && kind <= 8) {  // one damped direct solve first: S assembled, plan built
     linearize();
     SolveInfo info;
     bae_lm_config c2 = cfg;
     c2.solver = BAE_SOLVER_CHOLESKY;
     solve(1e-4, c2, info);
-    if (!use_tiles_) throw Error(BAE_ERR_UNSUPPORTED, "time_kernel 4..7 need the tile solver");
+    if (!use_tiles_) throw Error(BAE_ERR_UNSUPPORTED, "time_kernel 4..8 need the tile solver");
     if (kind == 7 && comm_) throw Error(BAE_ERR_UNSUPPORTED, "time_kernel 7: single rank only");
   }
   double* js = nullptr;
@@ -1763,6 +1763,9 @@ double Problem::time_kernel(int kind, int reps) {
         break;
       case 7:  // linearisation fused with the direct prep (the step after an accepted trial)
         BAE_LAUNCHED(launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_));
+        break;
+      case 8:  // retraction, point back-substitution and trial cost of the solved step
+        BAE_LAUNCHED(launch_trial(d_, sm_, stream_, comm_.get()));
         break;
       default:
         throw Error(BAE_ERR_INVALID_ARGUMENT, "time_kernel: unknown kind");

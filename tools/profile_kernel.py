@@ -1,7 +1,7 @@
 """Dev tool for ncu: run one kernel kind repeatedly in a live state (bae_time_kernel).
 usage: profile_kernel.py <config> <kind> <reps> [device-gen 0/1]
 kinds: 0 linearise, 1 Schur tile pass, 2 PCG iteration, 3 linearise + Jacobian store,
-       4 tile Cholesky, 5 direct prep, 6 Schur assembly, 7 fused linearise + prep"""
+       4 tile Cholesky, 5 direct prep, 6 Schur assembly, 7 fused linearise + prep, 8 trial"""
 import os
 import sys
 
