@@ -281,12 +281,12 @@ def _alg_bytes(kernel, st, ds=None):
         return 22 * N + 96 * P + 432 * E + 368 * C + 16 * T
     if kernel == "schur_tiles":  # blob 6/obs, points 24 + H~pp^-1 48, camera record+direction 176 + partial 48
         return 6 * N + 72 * P + 224 * E + 32 * T
-    if kernel == "prep_direct":  # obs index 6, V 144 written; points + H_pp/g_p 96, H~pp^-1 48 w; entry RHS 48 w
-        return 150 * N + 144 * P + 48 * E + 128 * C
-    if kernel == "lin_prep":  # linearize + V 144 w, H~pp^-1 48 w, entry RHS 48 w + 48 r, H~cc 168 + rhs 48 w
-        return 166 * N + 144 * P + 528 * E + 584 * C + 16 * T
-    if kernel == "schur_dense":  # every V read once (144 B / obs), the pair list (8 B / pair), tiles written
-        return 144 * N + 8 * ds["pairs"] + 48 * 48 * 8 * ds["tiles"]
+    if kernel == "prep_direct":  # obs index 6, V record [Q | y] 96 written; points + H_pp/g_p 96, H~pp^-1 48 w; entry RHS 48 w
+        return 102 * N + 144 * P + 48 * E + 128 * C
+    if kernel == "lin_prep":  # linearize + V record 96 w, H~pp^-1 48 w, entry RHS 48 w + 48 r, H~cc 168 + rhs 48 w
+        return 118 * N + 144 * P + 528 * E + 584 * C + 16 * T
+    if kernel == "schur_dense":  # every V record read once (96 B / obs), the pair list (8 B / pair), tiles written
+        return 96 * N + 8 * ds["pairs"] + 48 * 48 * 8 * ds["tiles"]
     raise ValueError(kernel)
 
 

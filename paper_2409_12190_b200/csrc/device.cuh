@@ -95,7 +95,7 @@ struct Dev {
   double* resid;   // 2 * N or null
   // direct solver (dense reduced camera system): per-slot W = J_c^T J_p and
   // W H~_pp^-1 (36 doubles, slot order), pair list grouped by camera block
-  double* wstore;           // direct solver: V = W L^-T per slot (18 doubles)
+  double* wstore;           // direct solver: compact V = W L^-T record per slot ([Q | y], 12 doubles)
   const double* lam;        // direct solver: the damping of the current solve (device copy)
   const int2* pairs;       // (slot k, slot l), c(k) >= c(l), grouped by block
   const int* blk_ptr;      // nblk + 1

@@ -272,7 +272,11 @@ __global__ void k_camrec(const double* __restrict__ pose, const double* __restri
   o[15] = intr[c * 4 + 3];
 }
 
-constexpr int kVStride = 20;  // doubles per V = W L^-T record (6 x 3 row-major + 2 pad: 160 bytes, 32-byte aligned)
+// Direct solver, per observation slot: V = W L^-T is 6 x 3, but W = J_c^T J_p
+// = [M; [y]x M] (J_c = D [I | -[y]x], M = D^T J_p), so V = [Q; [y]x Q] with
+// Q = M L^-T: the record keeps Q (row-major 9) and the camera-frame point y
+// (3): 96 bytes, three whole 32-byte sectors, instead of 144 (160 aligned).
+constexpr int kVStride = 12;
 // Direct solver prep, shared by k_prep<true> and the fused k_lin_prep (one
 // copy of the arithmetic, so the two agree bit for bit).
 // Per point: damped H~_pp, its inverse (d.hinv, for the
@@ -313,15 +317,14 @@ __device__ __forceinline__ bool prep_point_direct(const Dev& d, long long ip, do
   return !pfail;
 }
 
-// Direct solver, per observation slot: V = W L^-T (V V^T = W H~^-1 W^T)
-// stored row-major (kVStride doubles), and the Schur right-hand side piece
-// W v into rhs[0..5].
-__device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, const double (&W)[18],
+// Direct solver, per observation slot: the compact V record [Q | y] (see
+// kVStride) and the Schur right-hand side piece W v into rhs[0..5].
+__device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, const double (&W)[18], const P3& y,
                                                 const double* sp, double* rhs) {
   const double* lf = sp + 3;
   double vv[kVStride];
 #pragma unroll
-  for (int a = 0; a < 6; ++a) {
+  for (int a = 0; a < 3; ++a) {  // rows of Q = M L^-T (M = the top half of W)
     const double v0 = W[a * 3] * lf[0];
     const double v1 = (W[a * 3 + 1] - lf[1] * v0) * lf[3];
     const double v2 = (W[a * 3 + 2] - lf[2] * v0 - lf[4] * v1) * lf[5];
@@ -329,7 +332,9 @@ __device__ __forceinline__ void prep_obs_direct(const Dev& d, long long slot, co
     vv[a * 3 + 1] = v1;
     vv[a * 3 + 2] = v2;
   }
-  vv[18] = vv[19] = 0.0;  // whole sectors written
+  vv[9] = y.x;
+  vv[10] = y.y;
+  vv[11] = y.z;
   double* vo = d.wstore + slot * kVStride;
 #pragma unroll
   for (int j = 0; j < kVStride / 4; ++j)  // whole 32-byte sectors per store
@@ -556,7 +561,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
 #pragma unroll
         for (int j = 0; j < 3; ++j) W[a * 3 + j] = Jc[a] * Jp[j] + Jc[6 + a] * Jp[3 + j];
       double rhs[6];
-      prep_obs_direct(d, g.ob + s, W, sp, rhs);
+      prep_obs_direct(d, g.ob + s, W, y, sp, rhs);
       double* st = ws.stage + s * kLinStW;
 #pragma unroll
       for (int a = 0; a < 6; ++a) st[a] = rhs[a];
@@ -946,7 +951,7 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
         for (int b = a; b < 6; ++b)
           st[q++] = WH[a * 3] * W[b * 3] + WH[a * 3 + 1] * W[b * 3 + 1] + WH[a * 3 + 2] * W[b * 3 + 2];
     } else {  // direct solver: V = W L^-T of this slot and its RHS piece (shared with k_lin_prep)
-      prep_obs_direct(d, g.ob + s, W, sp, st);
+      prep_obs_direct(d, g.ob + s, W, y, sp, st);
       continue;
     }
     const double* vp = sp + 9;
@@ -1098,14 +1103,16 @@ __device__ __forceinline__ void ldg_v4(const double* p, double* o) {
                : "l"(p));
 }
 constexpr int kSchurDenseThreads = 128;
-__global__ void __launch_bounds__(kSchurDenseThreads, 3) k_schur_dense(Dev d) {
+// 128 registers: four 4-warp CTAs per SM (Final: 3 CTAs at 140 registers 3.25 ms, 4 CTAs 2.95 ms, 5 CTAs
+// with spills 3.86 ms)
+__global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
   // Warp per chunk of at most kSchurChunk pairs of one camera block (a long
   // block -- a diagonal one holds every observation of its camera -- is cut
   // into several, so no warp walks a whole camera's observations alone).
   // Lane = pair slot: each lane forms the whole 6x6 V_k V_l^T of its pairs
-  // (both 144-byte records reach its registers once: the LSU writeback of
-  // loaded bytes, not L1 or DRAM, bounds this kernel; ~168 registers, so
-  // 4-warp CTAs, 3 per SM), then a fixed
+  // (both 96-byte [Q | y] records reach its registers once: the LSU writeback of
+  // loaded bytes, not L1 or DRAM, bounds this kernel; 128 registers, so
+  // 4-warp CTAs, 4 per SM), then a fixed
   // reduce-scatter tree over the 32 slots leaves elements
   // 9 g .. 9 g + 8 of the chunk sum in lane group g = lane >> 3. A block of
   // one chunk is written at once; otherwise each chunk stores its 6x6
@@ -1122,7 +1129,7 @@ __global__ void __launch_bounds__(kSchurDenseThreads, 3) k_schur_dense(Dev d) {
 #pragma unroll 1
   for (int q = ch.y + lane; q < ch.z; q += 32) {
     const int2 pr = d.pairs[q];
-    // five 32-byte loads a record: each touches one whole sector (16-byte
+    // three 32-byte loads a record: each touches one whole sector (16-byte
     // loads touch every sector twice, and the L1 pays per sector touched)
     const double* wa = d.wstore + (long long)pr.x * kVStride;
     const double* wb = d.wstore + (long long)pr.y * kVStride;
@@ -1132,15 +1139,41 @@ __global__ void __launch_bounds__(kSchurDenseThreads, 3) k_schur_dense(Dev d) {
       ldg_v4(wa + 4 * j, a + 4 * j);
       ldg_v4(wb + 4 * j, b + 4 * j);
     }
+    // V_a V_b^T = [G, G Y_b^T; Y_a G, Y_a G Y_b^T] with G = Q_a Q_b^T and
+    // Y = [y]x: row i of G Y_b^T is y_b x (row i of G), column j of Y_a X
+    // is y_a x (column j of X)
+    const double ya[3] = {a[9], a[10], a[11]}, yb[3] = {b[9], b[10], b[11]};
+    double G[9], T[9];
 #pragma unroll
-    for (int m = 0; m < 6; ++m)
+    for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int n = 0; n < 6; ++n) {
-        double& c = acc[m * 6 + n];
-        c = fma(a[3 * m], b[3 * n], c);
-        c = fma(a[3 * m + 1], b[3 * n + 1], c);
-        c = fma(a[3 * m + 2], b[3 * n + 2], c);
+      for (int j = 0; j < 3; ++j) {
+        const double gij = a[3 * i] * b[3 * j] + a[3 * i + 1] * b[3 * j + 1] + a[3 * i + 2] * b[3 * j + 2];
+        G[i * 3 + j] = gij;
+        acc[i * 6 + j] += gij;
       }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+        const double tij = yb[j1] * G[i * 3 + j2] - yb[j2] * G[i * 3 + j1];
+        T[i * 3 + j] = tij;
+        acc[i * 6 + 3 + j] += tij;
+      }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double& bl = acc[(3 + i) * 6 + j];
+        bl = fma(ya[i1], G[i2 * 3 + j], bl);
+        bl = fma(-ya[i2], G[i1 * 3 + j], bl);
+        double& br = acc[(3 + i) * 6 + 3 + j];
+        br = fma(ya[i1], T[i2 * 3 + j], br);
+        br = fma(-ya[i2], T[i1 * 3 + j], br);
+      }
+    }
   }
   // reduce-scatter: xor 16 halves the 36 sums (bit 4 keeps [18 b4, +18)),
   // xor 8 halves again (bit 3 keeps the upper 9), xor 4/2/1 finish the 9

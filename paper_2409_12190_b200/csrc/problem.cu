@@ -1168,7 +1168,7 @@ void Problem::build_direct() {
     d_.schur_part = dalloc<double>(36 * chunks.size());
   }
   d_.nblk = static_cast<int>(bcam.size());
-  if (!d_.wstore) d_.wstore = dalloc<double>(20 * static_cast<std::size_t>(plan_.N));  // kVStride
+  if (!d_.wstore) d_.wstore = dalloc<double>(12 * static_cast<std::size_t>(plan_.N));  // kVStride
   if (!d_.lam) {
     d_.lam = dalloc<double>(1);
     lam_host_ = static_cast<double*>(pinned_take());
