@@ -45,7 +45,8 @@ struct TileCholPlan {
   std::vector<int> colptr;          // nt+1: L tiles of column j, diagonal first, rows ascending
   std::vector<int> rowidx;          // tile row of each stored tile (slot = position)
   std::vector<int> rptr;            // nt+1: row structure of column j: k < j with L(j,k) != 0
-  std::vector<int> rk, rslot;       // k ascending, slot of L(j,k)
+  std::vector<int> rk, rslot;       // k in (level(k), k) order, slot of L(j,k)
+  std::vector<int> level;           // per column: 1 + the highest level of its k (0: no updates)
   std::vector<int> uptr;            // per row-structure entry q: range of its tile updates
   std::vector<int> usrc, udst;      // update: C(udst) -= L(usrc) L(rslot[q])^T
   // per column, all its updates ordered by (k, target tile):
@@ -78,6 +79,7 @@ struct TileCholTasks {
   std::vector<int> tasks;            // 4 per task
   std::vector<unsigned> hmask;       // per column: bit s set when tile position s has a helper
   std::vector<int> bptr, bop;        // the owner's ops per column, then the helper ranges
+  std::vector<int> order;            // the columns in queue order (the backward takes it reversed)
   int helpers = 0;
 };
 // Only the queue's last `tail_tasks` tasks (the grid size) get helpers.
@@ -112,6 +114,7 @@ struct TileChol {
   unsigned* pflags;     // nnz: a helper's tile is pre-updated (or null without helpers)
   const int* tasks;     // 4 per task (plan_chol_tasks), or null: task i = column i, no helpers
   const unsigned* hmask;  // per column helper positions (with tasks)
+  const int* border;    // backward: column of the s-th claim (the queue's columns reversed), or null
   int ntask;
   unsigned* next;       // 3 words: work counters (factor, backward; CTAs claim columns in topological
                         // order) and the epoch, the flag value of the current solve

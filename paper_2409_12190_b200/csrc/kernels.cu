@@ -1103,8 +1103,53 @@ __device__ __forceinline__ void ldg_v4(const double* p, double* o) {
                : "l"(p));
 }
 constexpr int kSchurDenseThreads = 128;
+// acc += V_a V_b^T from two [Q | y] records
+__device__ __forceinline__ void schur_pair(const double (&a)[kVStride], const double (&b)[kVStride], double (&acc)[36]) {
+  // V_a V_b^T = [G, G Y_b^T; Y_a G, Y_a G Y_b^T] with G = Q_a Q_b^T and
+  // Y = [y]x: row i of G Y_b^T is y_b x (row i of G), column j of Y_a X
+  // is y_a x (column j of X)
+  const double ya[3] = {a[9], a[10], a[11]}, yb[3] = {b[9], b[10], b[11]};
+  double G[9], T[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double gij = a[3 * i] * b[3 * j] + a[3 * i + 1] * b[3 * j + 1] + a[3 * i + 2] * b[3 * j + 2];
+      G[i * 3 + j] = gij;
+      acc[i * 6 + j] += gij;
+    }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+      const double tij = yb[j1] * G[i * 3 + j2] - yb[j2] * G[i * 3 + j1];
+      T[i * 3 + j] = tij;
+      acc[i * 6 + 3 + j] += tij;
+    }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double& bl = acc[(3 + i) * 6 + j];
+      bl = fma(ya[i1], G[i2 * 3 + j], bl);
+      bl = fma(-ya[i2], G[i1 * 3 + j], bl);
+      double& br = acc[(3 + i) * 6 + 3 + j];
+      br = fma(ya[i1], T[i2 * 3 + j], br);
+      br = fma(-ya[i2], T[i1 * 3 + j], br);
+    }
+  }
+}
+__device__ __forceinline__ void ld_rec(const double* w, int r, double (&a)[kVStride]) {
+  // three 32-byte loads a record: each touches one whole sector (16-byte
+  // loads touch every sector twice, and the L1 pays per sector touched)
+  const double* p = w + (long long)r * kVStride;
+#pragma unroll
+  for (int j = 0; j < kVStride / 4; ++j) ldg_v4(p + 4 * j, a + 4 * j);
+}
 // 128 registers: four 4-warp CTAs per SM (Final: 3 CTAs at 140 registers 3.25 ms, 4 CTAs 2.95 ms, 5 CTAs
-// with spills 3.86 ms)
+// with spills 3.86 ms; 2.72 ms with the next pair's index loaded ahead)
 __global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
   // Warp per chunk of at most kSchurChunk pairs of one camera block (a long
   // block -- a diagonal one holds every observation of its camera -- is cut
@@ -1126,54 +1171,19 @@ __global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
   double acc[36];
 #pragma unroll
   for (int j = 0; j < 36; ++j) acc[j] = 0.0;
+  // the next pair's index is loaded before this pair's records (a fully
+  // prefetched next pair -- its records too -- needs 168 registers and three
+  // CTAs per SM: 3.80 vs 2.72 ms at Final)
+  int q = ch.y + lane;
+  int2 pr = q < ch.z ? d.pairs[q] : make_int2(0, 0);
 #pragma unroll 1
-  for (int q = ch.y + lane; q < ch.z; q += 32) {
-    const int2 pr = d.pairs[q];
-    // three 32-byte loads a record: each touches one whole sector (16-byte
-    // loads touch every sector twice, and the L1 pays per sector touched)
-    const double* wa = d.wstore + (long long)pr.x * kVStride;
-    const double* wb = d.wstore + (long long)pr.y * kVStride;
+  for (; q < ch.z; q += 32) {
+    const int2 pn = q + 32 < ch.z ? d.pairs[q + 32] : pr;
     double a[kVStride], b[kVStride];
-#pragma unroll
-    for (int j = 0; j < kVStride / 4; ++j) {
-      ldg_v4(wa + 4 * j, a + 4 * j);
-      ldg_v4(wb + 4 * j, b + 4 * j);
-    }
-    // V_a V_b^T = [G, G Y_b^T; Y_a G, Y_a G Y_b^T] with G = Q_a Q_b^T and
-    // Y = [y]x: row i of G Y_b^T is y_b x (row i of G), column j of Y_a X
-    // is y_a x (column j of X)
-    const double ya[3] = {a[9], a[10], a[11]}, yb[3] = {b[9], b[10], b[11]};
-    double G[9], T[9];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double gij = a[3 * i] * b[3 * j] + a[3 * i + 1] * b[3 * j + 1] + a[3 * i + 2] * b[3 * j + 2];
-        G[i * 3 + j] = gij;
-        acc[i * 6 + j] += gij;
-      }
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
-        const double tij = yb[j1] * G[i * 3 + j2] - yb[j2] * G[i * 3 + j1];
-        T[i * 3 + j] = tij;
-        acc[i * 6 + 3 + j] += tij;
-      }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        double& bl = acc[(3 + i) * 6 + j];
-        bl = fma(ya[i1], G[i2 * 3 + j], bl);
-        bl = fma(-ya[i2], G[i1 * 3 + j], bl);
-        double& br = acc[(3 + i) * 6 + 3 + j];
-        br = fma(ya[i1], T[i2 * 3 + j], br);
-        br = fma(-ya[i2], T[i1 * 3 + j], br);
-      }
-    }
+    ld_rec(d.wstore, pr.x, a);
+    ld_rec(d.wstore, pr.y, b);
+    schur_pair(a, b, acc);
+    pr = pn;
   }
   // reduce-scatter: xor 16 halves the 36 sums (bit 4 keeps [18 b4, +18)),
   // xor 8 halves again (bit 3 keeps the upper 9), xor 4/2/1 finish the 9

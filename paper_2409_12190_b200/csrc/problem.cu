@@ -1317,6 +1317,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.bop = upload(tk.bop);
   t.tasks = upload(tk.tasks);
   t.hmask = upload(tk.hmask);
+  t.border = upload(std::vector<int>(tk.order.rbegin(), tk.order.rend()));
   t.ntask = static_cast<int>(tk.tasks.size() / 4);
   chol_helpers_ = tk.helpers;
   t.tiles = d_.stiles;

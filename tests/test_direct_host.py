@@ -138,7 +138,7 @@ def test_chol_helper_tasks_partition_the_updates(min_ops, tail):
     """Update helpers: every update of the factorisation runs
     exactly once, a helper's updates are its tile's non-k_last updates in the
     owner's order, the queue is ordered so that every task only waits on
-    tasks before it (column order, a column's helpers before its owner), and
+    tasks before it (topological, a column's helpers before its owner), and
     only the queue's last `tail` tasks belong to columns with helpers."""
     C = 96
     order, gptr = nd_order(C, ring_edges(C, 6), 24)
@@ -152,12 +152,19 @@ def test_chol_helper_tasks_partition_the_updates(min_ops, tail):
     nt = at // 8
     pairs = sorted({(max(pos[a] // 8, pos[b] // 8), min(pos[a] // 8, pos[b] // 8)) for a, b in ring_edges(C, 6)})
     ob, oo, bp, op, tasks, hm = chol_tasks(nt, pairs, min_ops, tail)
+    colptr, _ = tile_symbolic(nt, [p for p in pairs if p[0] != p[1]])
+    slot_col = np.repeat(np.arange(nt), np.diff(colptr))  # the column of every stored tile slot
+
+    def mine_ops(ops, b, e):
+        return [tuple(x) for x in ops[b:e]]
+
     seen = []
-    last_col, owner_seen = -1, set()
+    owner_seen = set()
     for qi, (j, s, b, e) in enumerate(tasks):
-        assert j >= last_col  # column order
-        last_col = j
         orig = [tuple(x) for x in oo[ob[j]:ob[j + 1]]]
+        # topological: the owners of every column k whose tiles this task reads (L(j,k), L(i,k)) came before
+        deps = {slot_col[x[1]] for x in mine_ops(op, b, e)} | {slot_col[x[2]] for x in mine_ops(op, b, e)}
+        assert deps <= owner_seen, (j, deps - owner_seen)
         qlast = max((x[3] for x in orig), default=-1)
         mine = [tuple(x) for x in op[b:e]]
         if s == 0:
