@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <chrono>
 #include <mutex>
+#include <exception>
+#include <thread>
 #include <map>
 #include <climits>
 #include <cstddef>
@@ -215,6 +217,49 @@ void download_pageable(void* dst, const void* src, std::size_t bytes, cudaStream
     });
   }
 }
+// A large pageable upload on a helper thread and its own stream, so that it
+// overlaps host / device work of the caller (the device planner); wait_on()
+// joins and orders a consumer stream after the copy. The destructor joins on
+// every path (exceptions included).
+struct AsyncUpload {
+  std::thread th;
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev = nullptr;
+  std::exception_ptr err;
+  void* dst = nullptr;
+  void start(const void* src, std::size_t bytes, int device) {
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    ck(cudaMallocAsync(&dst, bytes, s), "cudaMallocAsync upload");
+    th = std::thread([this, src, bytes, device] {
+      try {
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        upload_pageable(dst, src, bytes, s, device);
+        ck(cudaEventRecord(ev, s), "event record");
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+  }
+  // the buffer passes to the caller (who frees it, stream-ordered, on `consumer`)
+  void* wait_on(cudaStream_t consumer) {
+    th.join();
+    if (err) std::rethrow_exception(err);
+    ck(cudaStreamWaitEvent(consumer, ev, 0), "stream wait");
+    void* p = dst;
+    dst = nullptr;
+    return p;
+  }
+  ~AsyncUpload() {
+    if (th.joinable()) th.join();
+    if (s) {
+      if (dst) cudaFreeAsync(dst, s);
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    if (ev) cudaEventDestroy(ev);
+  }
+};
 }  // namespace
 
 template <class T>
@@ -330,11 +375,15 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   std::vector<int> small_tiles, big_tiles;
   DevicePlan dp;
   int* dcam = nullptr;  // raw observation indices on the device (device plan)
+  AsyncUpload px_up;    // device plan: the pixels, uploaded beside the planner
   if (dev_plan) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&dcam), 2 * sizeof(int) * static_cast<std::size_t>(use_N), stream_),
        "cudaMallocAsync observation indices");
     upload_pageable(dcam, use_cam, sizeof(int) * use_N, stream_, opt.device);
     upload_pageable(dcam + use_N, use_pt, sizeof(int) * use_N, stream_, opt.device);
+    // the pixels travel while the planner runs (its kernels and host steps
+    // leave the copy engine idle); gathered into slot order below
+    px_up.start(px2, 2 * sizeof(double) * static_cast<std::size_t>(use_N), opt.device);
     try {
       build_plan_device(C, use_P, dcam, dcam + use_N, use_N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
                         kPipePts, kSliceLimit, [this](std::size_t n) { return static_cast<void*>(dalloc<char>(n)); },
@@ -494,9 +543,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     d.small_tiles = dp.small_tiles;
     d.big_tiles = dp.big_tiles;
     double* px = dalloc<double>(2 * static_cast<std::size_t>(use_N));
-    double* raw = nullptr;
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&raw), 2 * sizeof(double) * use_N, stream_), "cudaMallocAsync");
-    upload_pageable(raw, px2, 2 * sizeof(double) * use_N, stream_, opt.device);
+    double* raw = static_cast<double*>(px_up.wait_on(stream_));
     BAE_LAUNCHED(launch_gather_pixels(raw, d.obs_orig, px, use_N, stream_));
     ck(cudaFreeAsync(raw, stream_), "cudaFreeAsync");
     d.obs_px = px;
@@ -1206,8 +1253,10 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   keys.reserve(bcam.size());
   for (const int2& b : bcam)
     if (b.x != b.y) keys.push_back(static_cast<long long>(b.x) * C + b.y);
-  std::sort(keys.begin(), keys.end());
-  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  if (!std::is_sorted(keys.begin(), keys.end())) {  // the block list is already row by row, each pair once
+    std::sort(keys.begin(), keys.end());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  }
   if (comm_) {
     int* dcnt = nullptr;
     ck(cudaMalloc(&dcnt, sizeof(int)), "cudaMalloc");

@@ -184,3 +184,67 @@ def test_chol_helper_tasks_partition_the_updates(min_ops, tail):
         assert len(tasks) - first <= tail
     if min_ops == 0:
         assert not helped and len(tasks) == nt
+
+
+def _nd_serial(C, edges, leaf):
+    """Serial restatement of nd_camera_groups (chol.cu) for the threaded version's check."""
+    adj = [[] for _ in range(C)]
+    for a, b in edges:
+        adj[a].append(b)
+        adj[b].append(a)
+    groups = []
+
+    def bfs(root, inset):
+        level = {root: 0}
+        order = [root]
+        for v in order:
+            for w in adj[v]:
+                if w in inset and w not in level:
+                    level[w] = level[v] + 1
+                    order.append(w)
+        return order, level
+
+    def rec(nodes):
+        if not nodes:
+            return
+        nodes = sorted(nodes)
+        inset = set(nodes)
+        order, level = bfs(nodes[0], inset)
+        if len(order) != len(nodes):
+            rest = [v for v in nodes if v not in level]
+            rec(order)
+            rec(rest)
+            return
+        order, level = bfs(order[-1], inset)
+        nlev = level[order[-1]] + 1
+        if len(nodes) <= leaf or nlev < 3:
+            groups.append(order)
+            return
+        cnt = [0] * nlev
+        for v in nodes:
+            cnt[level[v]] += 1
+        m, acc = 0, 0
+        while m < nlev:
+            acc += cnt[m]
+            if 2 * acc >= len(nodes):
+                break
+            m += 1
+        m = min(max(m, 1), nlev - 2)
+        rec([v for v in order if level[v] < m])
+        rec([v for v in order if level[v] > m])
+        groups.append([v for v in order if level[v] == m])
+
+    rec(list(range(C)))
+    return groups
+
+
+def test_nd_order_threaded_equals_serial():
+    """The top levels of the nested dissection run on threads; the groups and
+    their order equal the serial recursion (a ring with a wide band and a
+    second component, big enough for the threaded levels)."""
+    C = 3000
+    edges = ring_edges(2600, 12) + [(a + 2600, b + 2600) for a, b in ring_edges(400, 3)]
+    order, gptr = nd_order(C, edges, 24)
+    ref = _nd_serial(C, edges, 24)
+    got = [list(order[gptr[g]:gptr[g + 1]]) for g in range(len(gptr) - 1)]
+    assert got == ref
