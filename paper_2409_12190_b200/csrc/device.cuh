@@ -151,6 +151,11 @@ constexpr int kSchurWarps = 4;
 // 234 vs 296 us).
 constexpr int kSchurMaxReg = 168;
 
+// Programmatic dependent launch: wait until the preceding kernel of the
+// stream has completed and its writes are visible (a no-op for a kernel not
+// launched with the programmatic attribute).
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }

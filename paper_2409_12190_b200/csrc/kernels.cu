@@ -720,6 +720,32 @@ __device__ __forceinline__ void cam_block_acc(const Dev& d, int c, double* red, 
 //   extra 2 (prep)          : [1 if a local point block was not SPD]
 // The W = 6 instance (PCG product) is skipped once the solve has finished,
 // like the other kernels of a PCG chunk.
+// Thread-strided sums over the per-tile [cost, gradient] pairs in the
+// thread's fixed order (tt, tt + blockDim, ...), eight loads in flight (a
+// one-block reduction over 316 k tiles waited on one load at a time: 145 us).
+template <bool kTwo>
+__device__ __forceinline__ void tile_pair_sums(const double* tr, int T, double& a, double& b) {
+  const int bd = blockDim.x;
+  int tt = threadIdx.x;
+  for (; tt + 7 * bd < T; tt += 8 * bd) {
+    double va[8], vb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      va[k] = tr[(tt + k * bd) * 2];
+      if (kTwo) vb[k] = tr[(tt + k * bd) * 2 + 1];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      a += va[k];
+      if (kTwo) b += vb[k];
+    }
+  }
+  for (; tt < T; tt += bd) {
+    a += tr[tt * 2];
+    if (kTwo) b += tr[tt * 2 + 1];
+  }
+}
+
 template <int W, int NT>
 __global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg_gated) {
   __shared__ double red[(32 / W) * (NT / 32) * W];
@@ -728,10 +754,7 @@ __global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg
   if (blockIdx.x == gridDim.x - 1) {
     if (extra == 1) {
       double a = 0.0, b = 0.0;
-      for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) {
-        a += d.tile_red[tt * 2];
-        b += d.tile_red[tt * 2 + 1];
-      }
+      tile_pair_sums<true>(d.tile_red, d.T, a, b);
       a = block_sum(a, red);
       __syncthreads();
       b = block_sum(b, red);
@@ -809,12 +832,7 @@ __global__ void __launch_bounds__(kCamNT) k_cam_lin_prep(Dev d, double clo, doub
 __global__ void __launch_bounds__(1024) k_lin_totals(Dev d) {
   __shared__ double red[32];
   double a = 0.0, b = 0.0, g = 0.0;
-  if (!d.cred) {
-    for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) {
-      a += d.tile_red[tt * 2];
-      b += d.tile_red[tt * 2 + 1];
-    }
-  }
+  if (!d.cred) tile_pair_sums<true>(d.tile_red, d.T, a, b);
   for (int c = threadIdx.x; c < d.C; c += blockDim.x) g += d.cam_dot[c];
   a = block_sum(a, red);
   __syncthreads();
@@ -834,8 +852,8 @@ __global__ void __launch_bounds__(1024) k_lin_totals(Dev d) {
 // Total of the per-tile costs, fixed order, one block.
 __global__ void k_sum_tiles(Dev d, int trial) {
   __shared__ double red[32];
-  double a = 0.0;
-  for (int tt = threadIdx.x; tt < d.T; tt += blockDim.x) a += d.tile_red[tt * 2];
+  double a = 0.0, unused = 0.0;
+  tile_pair_sums<false>(d.tile_red, d.T, a, unused);
   a = block_sum(a, red);
   if (d.cred) {  // sharded: [local cost, local trial failure] go to the cross-rank sum
     if (threadIdx.x == 0) {
@@ -1799,6 +1817,7 @@ __device__ __forceinline__ void sx_all_tiles(const Dev& d, const PcgDev& st, cha
 
 __global__ void __maxnreg__(kSchurMaxReg) k_schur_tiles(Dev d, int slice) {
   extern __shared__ __align__(128) char smem[];
+  grid_dep_wait();
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
   const int wpb = blockDim.x >> 5;
@@ -1812,6 +1831,7 @@ __global__ void __maxnreg__(kSchurMaxReg) k_schur_tiles(Dev d, int slice) {
 __global__ void __launch_bounds__(128) k_schur_cams(Dev d) {
   __shared__ double red[20 * 6];
   __shared__ double acc[6];
+  grid_dep_wait();
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
   const int c = blockIdx.x;
@@ -1843,6 +1863,7 @@ constexpr int kUpdNT = 256;
 __global__ void __launch_bounds__(kUpdNT) k_pcg_update(Dev d) {
   __shared__ double red[32];
   __shared__ double s_pap;
+  grid_dep_wait();
   const PcgDev st = *d.pcg;
   if (st.state >= kPcgDone) return;
   double alpha = 0.0;
@@ -2222,16 +2243,47 @@ int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, do
   k_prep_totals<<<1, 1024, 0, s>>>(d, tol, budget);
   return n;
 }
+// Programmatic dependent launch: the kernel may be scheduled while its
+// predecessor in the stream drains (its blocks wait in griddepcontrol.wait,
+// the first statement of every kernel launched this way), so kernel
+// boundaries cost no launch gap; in a captured graph the edge becomes a
+// programmatic one. BAE_PDL=0 turns it off.
+static bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("BAE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <class... K, class... A>
+static void launch_pdl(void (*k)(K...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   int n = 3;
-  k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
   if (comm) {  // the one exchange per PCG iteration: 6C doubles
+    k_schur_tiles<<<schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s>>>(d, sm.schur.slice);
     k_cam_entry_sums<6, 128><<<d.C + 1, 128, 0, s>>>(d, 0, 1);
     comm->allreduce_sum(d.cred, 6 * static_cast<std::size_t>(d.C), s);
-    ++n;
+    k_schur_cams<<<d.C, 128, 0, s>>>(d);
+    k_pcg_update<<<elt_blocks(d.C, kUpdNT), kUpdNT, 0, s>>>(d);
+    return n + 1;
   }
-  k_schur_cams<<<d.C, 128, 0, s>>>(d);
-  k_pcg_update<<<elt_blocks(d.C, kUpdNT), kUpdNT, 0, s>>>(d);
+  launch_pdl(k_schur_tiles, schur_grid(d, sm), 32 * sm.schur.wpb, sm.schur.wpb * sm.schur.slice, s, d,
+             sm.schur.slice);
+  launch_pdl(k_schur_cams, d.C, 128, 0, s, d);
+  launch_pdl(k_pcg_update, elt_blocks(d.C, kUpdNT), kUpdNT, 0, s, d);
   return n;
 }
 static int resident_grid(const void* fn, int threads, int smem) {
