@@ -258,6 +258,7 @@ __device__ __forceinline__ char* ws_base(const Dev& d, const TileGeom& g, char* 
 // ---------------------------------------------------------------------------
 __global__ void k_camrec(const double* __restrict__ pose, const double* __restrict__ intr, double* __restrict__ rec,
                          int C) {
+  grid_dep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   const double* s = pose + (long long)c * 7;
@@ -575,6 +576,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
 // 96 registers: two CTAs of up to 10 warps (5 pairs, the Final-13682 slice)
 // per SM; 98 (rounded to 104) left one.
 __global__ void __maxnreg__(96) k_lin_prep(Dev d, int slice, double clo, double chi, int pf) {
+  grid_dep_wait();
   extern __shared__ __align__(16) char smem[];
   const int t = group_tile_index<kLinThreads>();
   if (t >= d.T) return;
@@ -589,6 +591,7 @@ __global__ void __maxnreg__(96) k_lin_prep(Dev d, int slice, double clo, double 
 }
 
 __global__ void __launch_bounds__(256) k_linearize(Dev d, int slice, int write_jac, int pf) {
+  grid_dep_wait();
   extern __shared__ __align__(16) char smem[];
   const int t = group_tile_index<32>();
   if (t >= d.T) return;
@@ -638,6 +641,7 @@ __device__ __forceinline__ void cost_tile(const Dev& d, const TileGeom& g, char*
 }
 
 __global__ void __launch_bounds__(256) k_cost(Dev d, int slice) {
+  grid_dep_wait();
   extern __shared__ __align__(16) char smem[];
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
@@ -748,6 +752,7 @@ __device__ __forceinline__ void tile_pair_sums(const double* tr, int T, double& 
 
 template <int W, int NT>
 __global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg_gated) {
+  grid_dep_wait();
   __shared__ double red[(32 / W) * (NT / 32) * W];
   __shared__ double acc[W];
   if (pcg_gated && d.pcg->state >= kPcgDone) return;
@@ -780,6 +785,7 @@ __global__ void __launch_bounds__(NT) k_cam_entry_sums(Dev d, int extra, int pcg
 constexpr int kCamNT = 512;
 
 __global__ void __launch_bounds__(kCamNT) k_cam_linearize(Dev d) {
+  grid_dep_wait();
   __shared__ double red[16 * 27];
   __shared__ double acc[27];
   const int c = blockIdx.x;
@@ -800,6 +806,7 @@ __global__ void __launch_bounds__(kCamNT) k_cam_linearize(Dev d) {
 // k_cam_prep_direct's damped H~_cc and Schur RHS, with the same summation
 // orders as those two kernels.
 __global__ void __launch_bounds__(kCamNT) k_cam_lin_prep(Dev d, double clo, double chi) {
+  grid_dep_wait();
   __shared__ double red[80 * 6];  // >= 16 * 27
   __shared__ double acc[27];
   __shared__ double acc6[6];
@@ -830,6 +837,7 @@ __global__ void __launch_bounds__(kCamNT) k_cam_lin_prep(Dev d, double clo, doub
 // Cost and ||J^T r||^2 of the linearisation (one block, fixed order): tile
 // totals in tile order (sharded: already summed over ranks) + camera |g_c|^2.
 __global__ void __launch_bounds__(1024) k_lin_totals(Dev d) {
+  grid_dep_wait();
   __shared__ double red[32];
   double a = 0.0, b = 0.0, g = 0.0;
   if (!d.cred) tile_pair_sums<true>(d.tile_red, d.T, a, b);
@@ -851,6 +859,7 @@ __global__ void __launch_bounds__(1024) k_lin_totals(Dev d) {
 
 // Total of the per-tile costs, fixed order, one block.
 __global__ void k_sum_tiles(Dev d, int trial) {
+  grid_dep_wait();
   __shared__ double red[32];
   double a = 0.0, unused = 0.0;
   tile_pair_sums<false>(d.tile_red, d.T, a, unused);
@@ -872,6 +881,7 @@ __global__ void k_sum_tiles(Dev d, int trial) {
 
 // Sharded runs: the cost (or trial cost) from the rank-summed [cost, failure].
 __global__ void k_finish_cost(Dev d, int trial) {
+  grid_dep_wait();
   const double a = d.cred[0];
   const bool bad = d.cred[1] > 0.0;
   if (trial) {
@@ -983,6 +993,7 @@ __device__ __forceinline__ void prep_tile(const Dev& d, const TileGeom& g, char*
 
 template <bool kDirect>
 __global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, double clo, double chi, int pf) {
+  grid_dep_wait();
   extern __shared__ __align__(16) char smem[];
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
@@ -998,6 +1009,7 @@ __global__ void __launch_bounds__(256) k_prep(Dev d, int slice, double lambda, d
 // Camera side of the direct solver's prep (block per camera): damped H~_cc
 // and the Schur RHS b = -g_c + sum_k J_c^T J_p H~_pp^-1 g_p.
 __global__ void __launch_bounds__(kCamNT) k_cam_prep_direct(Dev d, double lambda, double clo, double chi) {
+  grid_dep_wait();
   lambda = *d.lam;
   __shared__ double red[80 * 6];
   __shared__ double acc[6];
@@ -1023,6 +1035,7 @@ __global__ void __launch_bounds__(kCamNT) k_cam_prep_direct(Dev d, double lambda
 // numerically SPD), Schur RHS, and PCG initialisation x = 0, r = b,
 // z = M^-1 r; per-camera r.r and r.z for the totals.
 __global__ void __launch_bounds__(256) k_cam_prep(Dev d, double lambda, double clo, double chi) {
+  grid_dep_wait();
   __shared__ double red[8 * 27];
   __shared__ double acc[27];
   const int c = blockIdx.x;
@@ -1070,6 +1083,7 @@ __global__ void __launch_bounds__(256) k_cam_prep(Dev d, double lambda, double c
 
 // PCG start state from the prep totals (one block, fixed order).
 __global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long long budget) {
+  grid_dep_wait();
   __shared__ double red[32];
   double rr = 0.0, rz = 0.0;
   for (int c = threadIdx.x; c < d.C; c += blockDim.x) {
@@ -1169,6 +1183,7 @@ __device__ __forceinline__ void ld_rec(const double* w, int r, double (&a)[kVStr
 // 128 registers: four 4-warp CTAs per SM (Final: 3 CTAs at 140 registers 3.25 ms, 4 CTAs 2.95 ms, 5 CTAs
 // with spills 3.86 ms; 2.72 ms with the next pair's index loaded ahead)
 __global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
+  grid_dep_wait();
   // Warp per chunk of at most kSchurChunk pairs of one camera block (a long
   // block -- a diagonal one holds every observation of its camera -- is cut
   // into several, so no warp walks a whole camera's observations alone).
@@ -1304,6 +1319,7 @@ __global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
 
 // Sharded direct solve: the damped camera blocks join the rank-summed S.
 __global__ void k_add_hccd(Dev d) {
+  grid_dep_wait();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= 36LL * d.C) return;
   const int c = (int)(idx / 36), r = (int)(idx % 36) / 6, col = (int)(idx % 6);
@@ -1989,6 +2005,7 @@ __global__ void __launch_bounds__(32 * kSchurWarps, 2) k_pcg_persistent(Dev d, i
 // buffers, then point back-substitution + trial cost in one tile pass.
 // ---------------------------------------------------------------------------
 __global__ void k_cam_retract(Dev d) {
+  grid_dep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d.C) return;
   const double* s = d.pose + (long long)c * 7;
@@ -2095,6 +2112,7 @@ __device__ __forceinline__ void trial_tile(const Dev& d, const TileGeom& g, char
 }
 
 __global__ void __launch_bounds__(256) k_backsub_trial(Dev d, int slice, int pf) {
+  grid_dep_wait();
   extern __shared__ __align__(16) char smem[];
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
@@ -2106,6 +2124,7 @@ __global__ void __launch_bounds__(256) k_backsub_trial(Dev d, int slice, int pf)
 
 // Accept: trial parameters become current (lm.hpp:183-189).
 __global__ void k_commit(Dev d) {
+  grid_dep_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < (long long)d.P * 3) d.pts[i] = d.pts_t[i];
   if (i < (long long)d.C * 7) d.pose[i] = d.pose_t[i];
@@ -2178,6 +2197,40 @@ int launch_gather_pixels(const double* raw, const int* orig, double* px, long lo
   return 1;
 }
 
+// Programmatic dependent launch: the kernel may be scheduled while its
+// predecessor in the stream drains (its blocks wait in griddepcontrol.wait,
+// the first statement of every kernel launched this way), so kernel
+// boundaries cost no launch gap; in a captured graph the edge becomes a
+// programmatic one. BAE_PDL=0 turns it off. Sharded runs keep plain
+// launches (their exchanges sit between the kernels).
+static bool pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("BAE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <class... K, class... A>
+static void launch_k(bool pdl, void (*k)(K...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+                     A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_on()) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
+template <class... K, class... A>
+static void launch_pdl(void (*k)(K...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, A&&... args) {
+  launch_k(true, k, grid, block, smem, s, std::forward<A>(args)...);
+}
+
 int launch_camrec(const Dev& d, bool trial, cudaStream_t s) {
   k_camrec<<<elt_blocks(d.C, 128), 128, 0, s>>>(trial ? d.pose_t : d.pose, d.intr, trial ? d.camrec_t : d.camrec, d.C);
   return 1;
@@ -2195,26 +2248,28 @@ static int reduce_cams27(const Dev& d, int extra, int nextra, Comm* comm, cudaSt
 }
 int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStream_t s, Comm* comm) {
   int n = 3;
-  k_linearize<<<tile_blocks(d.T, sm.lin), 32 * sm.lin.wpb, sm.lin.wpb * sm.lin.slice, s>>>(
-      d, sm.lin.slice, write_jac ? 1 : 0, prefetch_distance((const void*)k_linearize, sm.lin));
+  launch_k(!comm, k_linearize, tile_blocks(d.T, sm.lin), 32 * sm.lin.wpb, sm.lin.wpb * sm.lin.slice, s, d,
+           sm.lin.slice, write_jac ? 1 : 0, prefetch_distance((const void*)k_linearize, sm.lin));
   if (comm) {
     n += reduce_cams27(d, 1, 2, comm, s);
     comm->allreduce_min(&d.lm->err_obs, 1, s);
   }
-  k_cam_linearize<<<d.C, kCamNT, 0, s>>>(d);
-  k_lin_totals<<<1, 1024, 0, s>>>(d);
+  launch_k(!comm, k_cam_linearize, d.C, kCamNT, 0, s, d);
+  launch_k(!comm, k_lin_totals, 1, 1024, 0, s, d);
   return n;
 }
 int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
-  k_lin_prep<<<tile_blocks(d.T, sm.linprep), kLinThreads * sm.linprep.wpb, sm.linprep.wpb * sm.linprep.slice, s>>>(
-      d, sm.linprep.slice, clo, chi, prefetch_distance((const void*)k_lin_prep, sm.linprep, kLinThreads));
-  k_cam_lin_prep<<<d.C, kCamNT, 0, s>>>(d, clo, chi);
-  k_lin_totals<<<1, 1024, 0, s>>>(d);
+  launch_k(true, k_lin_prep, tile_blocks(d.T, sm.linprep), kLinThreads * sm.linprep.wpb,
+           sm.linprep.wpb * sm.linprep.slice, s, d, sm.linprep.slice, clo, chi,
+           prefetch_distance((const void*)k_lin_prep, sm.linprep, kLinThreads));
+  launch_k(true, k_cam_lin_prep, d.C, kCamNT, 0, s, d, clo, chi);
+  launch_k(true, k_lin_totals, 1, 1024, 0, s, d);
   return 3;
 }
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
-  k_cost<<<tile_blocks(d.T, sm.cost), 32 * sm.cost.wpb, sm.cost.wpb * sm.cost.slice, s>>>(d, sm.cost.slice);
-  k_sum_tiles<<<1, 1024, 0, s>>>(d, 0);
+  launch_k(!comm, k_cost, tile_blocks(d.T, sm.cost), 32 * sm.cost.wpb, sm.cost.wpb * sm.cost.slice, s, d,
+           sm.cost.slice);
+  launch_k(!comm, k_sum_tiles, 1, 1024, 0, s, d, 0);
   if (!comm) return 2;
   comm->allreduce_sum(d.cred, 2, s);
   comm->allreduce_min(&d.lm->err_obs, 1, s);
@@ -2224,52 +2279,25 @@ int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
 int launch_prep(const Dev& d, const SmemSizes& sm, double lambda, double clo, double chi, double tol,
                 long long budget, cudaStream_t s, Comm* comm, bool direct) {
   if (direct) {  // RHS, damped H_cc and the per-slot W / W H~^-1 only
-    k_prep<true><<<tile_blocks(d.T, sm.prepd), 32 * sm.prepd.wpb, sm.prepd.wpb * sm.prepd.slice, s>>>(
-        d, sm.prepd.slice, lambda, clo, chi, prefetch_distance((const void*)k_prep<true>, sm.prepd));
+    launch_k(!comm, (k_prep<true>), tile_blocks(d.T, sm.prepd), 32 * sm.prepd.wpb, sm.prepd.wpb * sm.prepd.slice, s,
+             d, sm.prepd.slice, lambda, clo, chi, prefetch_distance((const void*)k_prep<true>, sm.prepd));
     int n = 2;
     if (comm) {
       k_cam_entry_sums<6, kCamNT><<<d.C + 1, kCamNT, 0, s>>>(d, 2, 0);
       comm->allreduce_sum(d.cred, 6 * static_cast<std::size_t>(d.C) + 1, s);
       ++n;
     }
-    k_cam_prep_direct<<<d.C, kCamNT, 0, s>>>(d, lambda, clo, chi);
+    launch_k(!comm, k_cam_prep_direct, d.C, kCamNT, 0, s, d, lambda, clo, chi);
     return n;
   }
   int n = 3;
-  k_prep<false><<<tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s>>>(
-      d, sm.prep.slice, lambda, clo, chi, prefetch_distance((const void*)k_prep<false>, sm.prep));
+  launch_k(!comm, (k_prep<false>), tile_blocks(d.T, sm.prep), 32 * sm.prep.wpb, sm.prep.wpb * sm.prep.slice, s, d,
+           sm.prep.slice, lambda, clo, chi, prefetch_distance((const void*)k_prep<false>, sm.prep));
   if (comm) n += reduce_cams27(d, 2, 1, comm, s);
-  k_cam_prep<<<d.C, 256, 0, s>>>(d, lambda, clo, chi);
-  k_prep_totals<<<1, 1024, 0, s>>>(d, tol, budget);
+  launch_k(!comm, k_cam_prep, d.C, 256, 0, s, d, lambda, clo, chi);
+  launch_k(!comm, k_prep_totals, 1, 1024, 0, s, d, tol, budget);
   return n;
 }
-// Programmatic dependent launch: the kernel may be scheduled while its
-// predecessor in the stream drains (its blocks wait in griddepcontrol.wait,
-// the first statement of every kernel launched this way), so kernel
-// boundaries cost no launch gap; in a captured graph the edge becomes a
-// programmatic one. BAE_PDL=0 turns it off.
-static bool pdl_on() {
-  static const bool on = [] {
-    const char* e = std::getenv("BAE_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-template <class... K, class... A>
-static void launch_pdl(void (*k)(K...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, A&&... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
-}
-
 int launch_pcg_iteration(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   int n = 3;
   if (comm) {  // the one exchange per PCG iteration: 6C doubles
@@ -2315,10 +2343,10 @@ int launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s) {
   return 1;
 }
 int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
-  k_cam_retract<<<elt_blocks(d.C, 128), 128, 0, s>>>(d);
-  k_backsub_trial<<<tile_blocks(d.T, sm.trial), 32 * sm.trial.wpb, sm.trial.wpb * sm.trial.slice, s>>>(
-      d, sm.trial.slice, prefetch_distance((const void*)k_backsub_trial, sm.trial));
-  k_sum_tiles<<<1, 1024, 0, s>>>(d, 1);
+  launch_k(!comm, k_cam_retract, elt_blocks(d.C, 128), 128, 0, s, d);
+  launch_k(!comm, k_backsub_trial, tile_blocks(d.T, sm.trial), 32 * sm.trial.wpb, sm.trial.wpb * sm.trial.slice, s,
+           d, sm.trial.slice, prefetch_distance((const void*)k_backsub_trial, sm.trial));
+  launch_k(!comm, k_sum_tiles, 1, 1024, 0, s, d, 1);
   if (!comm) return 3;
   comm->allreduce_sum(d.cred, 2, s);
   k_finish_cost<<<1, 1, 0, s>>>(d, 1);
@@ -2347,7 +2375,7 @@ int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
 }
 int launch_commit(const Dev& d, cudaStream_t s) {
   const long long n = std::max<long long>((long long)d.P * 3, (long long)d.C * kCamRec);
-  k_commit<<<elt_blocks(n, 256), 256, 0, s>>>(d);
+  launch_k(true, k_commit, elt_blocks(n, 256), 256, 0, s, d);
   return 1;
 }
 
