@@ -101,6 +101,7 @@ struct Dev {
   const int* blk_ptr;      // nblk + 1
   const int2* blk_cam;     // (c1, c2), c1 >= c2
   int nblk;
+  int defer_hccd;           // k_schur_dense: diagonal blocks without H~_cc (added by k_add_hccd)
   double* schur;           // 6C x 6C, column-major (lower triangle used; cuSOLVER path)
   // tile-sparse storage of S (chol.cuh): per camera block the slot of the
   // 48 x 48 tile holding it (8 cameras per tile), column-major tiles

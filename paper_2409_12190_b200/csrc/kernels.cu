@@ -1289,7 +1289,8 @@ __global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
     ldr = 1;
     ldc = n;
   }
-  const bool diag = cc.x == cc.y && !d.cred;  // sharded: H~_cc is added after the rank sum
+  // sharded: H~_cc is added after the rank sum; deferred: after the camera pass
+  const bool diag = cc.x == cc.y && !d.cred && !d.defer_hccd;
   if (count == 1) {
     const int e = g9 + j8;
     double v = -own;
@@ -2258,13 +2259,19 @@ int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStre
   launch_k(!comm, k_lin_totals, 1, 1024, 0, s, d);
   return n;
 }
-int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
+int launch_lin_prep_tiles(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
   launch_k(true, k_lin_prep, tile_blocks(d.T, sm.linprep), kLinThreads * sm.linprep.wpb,
            sm.linprep.wpb * sm.linprep.slice, s, d, sm.linprep.slice, clo, chi,
            prefetch_distance((const void*)k_lin_prep, sm.linprep, kLinThreads));
+  return 1;
+}
+int launch_lin_prep_cams(const Dev& d, double clo, double chi, cudaStream_t s) {
   launch_k(true, k_cam_lin_prep, d.C, kCamNT, 0, s, d, clo, chi);
   launch_k(true, k_lin_totals, 1, 1024, 0, s, d);
-  return 3;
+  return 2;
+}
+int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s) {
+  return launch_lin_prep_tiles(d, sm, clo, chi, s) + launch_lin_prep_cams(d, clo, chi, s);
 }
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) {
   launch_k(!comm, k_cost, tile_blocks(d.T, sm.cost), 32 * sm.cost.wpb, sm.cost.wpb * sm.cost.slice, s, d,
@@ -2352,12 +2359,14 @@ int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm) 
   k_finish_cost<<<1, 1, 0, s>>>(d, 1);
   return 4;
 }
-int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
+int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm, bool defer_hccd) {
   int n = 0;
   if (d.nblk > 0) {
     cudaMemsetAsync(d.blk_ticket, 0, sizeof(unsigned) * d.nblk, s);
+    Dev dd = d;
+    dd.defer_hccd = defer_hccd ? 1 : 0;
     k_schur_dense<<<(d.nchunk + kSchurDenseThreads / 32 - 1) / (kSchurDenseThreads / 32), kSchurDenseThreads, 0, s>>>(
-        d);
+        dd);
     ++n;
   }
   if (comm) {  // the direct solve's exchange: the reduced matrix, once per LM iteration
@@ -2372,6 +2381,10 @@ int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm) {
     ++n;
   }
   return n;
+}
+int launch_add_hccd(const Dev& d, cudaStream_t s) {
+  k_add_hccd<<<elt_blocks(36LL * d.C, 256), 256, 0, s>>>(d);
+  return 1;
 }
 int launch_commit(const Dev& d, cudaStream_t s) {
   const long long n = std::max<long long>((long long)d.P * 3, (long long)d.C * kCamRec);

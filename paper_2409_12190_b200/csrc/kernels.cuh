@@ -33,6 +33,10 @@ int launch_linearize(const Dev& d, const SmemSizes& sm, bool write_jac, cudaStre
 // and the prep for the damping in d.lam in one pass (k_lin_prep,
 // k_cam_lin_prep, k_lin_totals). Needs d.pcg zeroed first.
 int launch_lin_prep(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s);
+// The two halves of launch_lin_prep: the tile pass, then the camera pass + totals
+// (on a second stream beside the Schur assembly, single rank).
+int launch_lin_prep_tiles(const Dev& d, const SmemSizes& sm, double clo, double chi, cudaStream_t s);
+int launch_lin_prep_cams(const Dev& d, double clo, double chi, cudaStream_t s);
 int launch_cost(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
 // direct = true: the direct solver's prep (RHS, damped H_cc, per-slot W and
 // W H~_pp^-1; no block-Jacobi preconditioner and no PCG start state).
@@ -46,6 +50,9 @@ int launch_schur_only(const Dev& d, const SmemSizes& sm, cudaStream_t s);
 int launch_trial(const Dev& d, const SmemSizes& sm, cudaStream_t s, Comm* comm);
 int launch_commit(const Dev& d, cudaStream_t s);
 constexpr int kSchurChunk = 128;  // pairs per k_schur_dense warp (at most)
-int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm);
+// defer_hccd: the diagonal blocks leave out H~_cc (launch_add_hccd adds it
+// once the camera pass that forms it has run).
+int launch_schur_dense(const Dev& d, cudaStream_t s, Comm* comm, bool defer_hccd = false);
+int launch_add_hccd(const Dev& d, cudaStream_t s);
 
 }  // namespace bae

@@ -631,6 +631,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   d.blk_ticket = nullptr;
   d.schur_part = nullptr;
   d.nblk = 0;
+  d.defer_hccd = 0;
   d.schur = nullptr;
   ht.mark("allocs");
   static_assert(sizeof(PcgDev) <= kPinnedWord && sizeof(LmDev) <= kPinnedWord, "pinned word");
@@ -651,6 +652,7 @@ Problem::~Problem() {
   cudaSetDevice(opt_.device);
   for (auto& e : ev_pool_) cudaEventDestroy(e);
   if (solver_) cusolverDnDestroy(solver_);
+  if (side_) cudaStreamSynchronize(side_);
   if (stream_) cudaStreamSynchronize(stream_);  // the chunks are reused by the next problem
   pinned_give(host_info_);
   if (pcg_graph_) cudaGraphExecDestroy(pcg_graph_);
@@ -661,6 +663,9 @@ Problem::~Problem() {
   pinned_give(lm_host_);
   pinned_give(lm_reset_host_);
   pinned_give(lam_host_);
+  if (side_) cudaStreamDestroy(side_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
   if (stream_) cudaStreamDestroy(stream_);
   comm_.reset();
 }
@@ -972,7 +977,16 @@ void Problem::linearize_prep_async(double lambda, const bae_lm_config& cfg) {
      "H2D lambda");
   ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
   phase_begin(kPhLinearize);
-  BAE_LAUNCHED(launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_));
+  if (side_) {  // the camera pass beside the assembly (joined in solve_direct)
+    BAE_LAUNCHED(launch_lin_prep_tiles(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_));
+    ck(cudaEventRecord(ev_fork_, stream_), "event record");
+    ck(cudaStreamWaitEvent(side_, ev_fork_, 0), "stream wait");
+    BAE_LAUNCHED(launch_lin_prep_cams(d_, cfg.clamp_min, cfg.clamp_max, side_));
+    ck(cudaEventRecord(ev_join_, side_), "event record");
+    join_pending_ = true;
+  } else {
+    BAE_LAUNCHED(launch_lin_prep(d_, sm_, cfg.clamp_min, cfg.clamp_max, stream_));
+  }
   phase_end();
   prep_fused_ = true;
 }
@@ -1221,6 +1235,14 @@ void Problem::build_direct() {
     lam_host_ = static_cast<double*>(pinned_take());
   }
   ht.mark("direct: pair list");
+  // single rank: a second stream for the camera pass of the fused
+  // linearise + prep, beside the Schur assembly (BAE_FORK=0: one stream)
+  const char* fk = std::getenv("BAE_FORK");
+  if (!comm_ && !side_ && !(fk && fk[0] == '0')) {
+    ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+  }
   if (use_tiles_) {
     build_tile_chol(bcam);
     ht.mark("direct: tile symbolic");
@@ -1411,7 +1433,12 @@ bool Problem::solve_direct(double lambda, const bae_lm_config& cfg, SolveInfo& i
     ck(cudaMemsetAsync(d_.stiles, 0, sizeof(double) * kTT * d_.stile_count, stream_), "memset S tiles");
   else
     ck(cudaMemsetAsync(d_.schur, 0, sizeof(double) * n * n, stream_), "memset S");
-  BAE_LAUNCHED(launch_schur_dense(d_, stream_, comm_.get()));
+  BAE_LAUNCHED(launch_schur_dense(d_, stream_, comm_.get(), join_pending_));
+  if (join_pending_) {  // the camera pass formed H~_cc and the right-hand side
+    ck(cudaStreamWaitEvent(stream_, ev_join_, 0), "stream wait");
+    join_pending_ = false;
+    BAE_LAUNCHED(launch_add_hccd(d_, stream_));
+  }
   phase_end();
   if (use_tiles_) {
     // tile-sparse Cholesky + both substitutions: x = S^-1 rhs straight into d_.x

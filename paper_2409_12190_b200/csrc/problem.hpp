@@ -177,6 +177,11 @@ class Problem {
   Dev d_{};
   SmemSizes sm_;
   cudaStream_t stream_ = nullptr;
+  // single-rank direct path: the camera pass of the fused linearise + prep
+  // runs on side_ beside the Schur assembly (fork ev_fork_, join ev_join_)
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  bool join_pending_ = false;
   cudaGraphExec_t pcg_graph_ = nullptr;
   std::vector<void*> allocs_;  // arena chunks
   std::vector<std::size_t> alloc_bytes_;
