@@ -684,17 +684,26 @@ __device__ __forceinline__ void block_entry_sum(const Dev& d, int c, double* red
   const int e = d.cam_ent_ptr[c + 1];
   double acc = 0.0;
   if (active) {
+    // entries q, q + S, ... in that order (the sum's order); eight partials
+    // in flight, and the next eight entry ids loaded while they land, so a
+    // group costs one dependent round trip instead of two
+    constexpr int U = 8;
     int q = d.cam_ent_ptr[c] + slot;
-    for (; q + 3 * S < e; q += 4 * S) {
-      const int e0 = d.cam_ent[q], e1 = d.cam_ent[q + S], e2 = d.cam_ent[q + 2 * S], e3 = d.cam_ent[q + 3 * S];
-      const double v0 = src[(long long)e0 * W + j], v1 = src[(long long)e1 * W + j];
-      const double v2 = src[(long long)e2 * W + j], v3 = src[(long long)e3 * W + j];
-      acc += v0;
-      acc += v1;
-      acc += v2;
-      acc += v3;
+    int id[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) id[k] = q + k * S < e ? d.cam_ent[q + k * S] : -1;
+    while (q < e) {
+      double v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) v[k] = id[k] >= 0 ? src[(long long)id[k] * W + j] : 0.0;
+      const int qn = q + U * S;
+#pragma unroll
+      for (int k = 0; k < U; ++k) id[k] = qn + k * S < e ? d.cam_ent[qn + k * S] : -1;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (q + k * S < e) acc += v[k];
+      q = qn;
     }
-    for (; q < e; q += S) acc += src[(long long)d.cam_ent[q] * W + j];
     red[slot * W + j] = acc;
   }
   __syncthreads();
