@@ -226,15 +226,20 @@ struct AsyncUpload {
   cudaStream_t s = nullptr;
   cudaEvent_t ev = nullptr;
   std::exception_ptr err;
-  void* dst = nullptr;
-  void start(const void* src, std::size_t bytes, int device) {
+  void* dst = nullptr;       // owned until wait_on() hands it over
+  void* borrowed = nullptr;  // start(..., into): the caller's buffer
+  void start(const void* src, std::size_t bytes, int device, void* into = nullptr) {
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-    ck(cudaMallocAsync(&dst, bytes, s), "cudaMallocAsync upload");
-    th = std::thread([this, src, bytes, device] {
+    if (into)
+      borrowed = into;  // a caller's buffer (not freed here)
+    else
+      ck(cudaMallocAsync(&dst, bytes, s), "cudaMallocAsync upload");
+    void* to = into ? into : dst;
+    th = std::thread([this, src, bytes, device, to] {
       try {
         ck(cudaSetDevice(device), "cudaSetDevice");
-        upload_pageable(dst, src, bytes, s, device);
+        upload_pageable(to, src, bytes, s, device);
         ck(cudaEventRecord(ev, s), "event record");
       } catch (...) {
         err = std::current_exception();
@@ -246,7 +251,7 @@ struct AsyncUpload {
     th.join();
     if (err) std::rethrow_exception(err);
     ck(cudaStreamWaitEvent(consumer, ev, 0), "stream wait");
-    void* p = dst;
+    void* p = borrowed ? borrowed : dst;
     dst = nullptr;
     return p;
   }
@@ -819,12 +824,14 @@ void Problem::phase_collect() {
 
 void Problem::sync() { ck(cudaStreamSynchronize(stream_), "kernel execution"); }
 
-void Problem::set_parameters(const double* poses7, const double* points3) {
+void Problem::set_parameters(const double* poses7, const double* points3, bool points_staged) {
   activate();
   const int C = d_.C, P = d_.P;
   if (poses7)
     ck(cudaMemcpyAsync(d_.pose, poses7, 7 * sizeof(double) * C, cudaMemcpyHostToDevice, stream_), "H2D poses");
-  if (points3 && !comm_) {  // caller order up, permuted into the internal order on the device
+  if (points_staged) {  // already in pts_user_ (caller order; the stream is ordered after the copy)
+    BAE_LAUNCHED(launch_points_permute(pts_user_, src_of_internal_, d_.pts, P, true, stream_));
+  } else if (points3 && !comm_) {  // caller order up, permuted into the internal order on the device
     ensure_point_staging();
     upload_pageable(pts_user_, points3, 3 * sizeof(double) * P, stream_, opt_.device);
     BAE_LAUNCHED(launch_points_permute(pts_user_, src_of_internal_, d_.pts, P, true, stream_));
@@ -1625,10 +1632,24 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   validate_config(cfg);
   if (cfg.solver != BAE_SOLVER_PCG && cfg.solver != BAE_SOLVER_CHOLESKY)
     throw Error(BAE_ERR_INVALID_ARGUMENT, "LmConfig: unknown solver");
+  // The first direct solve's symbolic phase (pair list, nested dissection,
+  // tile symbolic) is host-heavy: the initial points travel on a helper
+  // thread meanwhile (single rank, large problems)
+  AsyncUpload pts_up;
+  const std::size_t pts_bytes = 3 * sizeof(double) * static_cast<std::size_t>(d_.P);
+  if (cfg.solver == BAE_SOLVER_CHOLESKY && !direct_ready_ && points3 && !comm_ && pts_bytes >= (64u << 20)) {
+    ensure_point_staging();
+    pts_up.start(points3, pts_bytes, opt_.device, pts_user_);
+  }
   if (cfg.solver == BAE_SOLVER_CHOLESKY) build_direct();
   if (plan_.has_empty_camera || plan_.has_empty_point)
     throw Error(BAE_ERR_INVALID_ARGUMENT, "diagonal op: missing diagonal entry");  // csr.hpp:53
-  if (poses7 || points3) set_parameters(poses7, points3);
+  if (pts_up.s) {
+    pts_up.wait_on(stream_);
+    set_parameters(poses7, nullptr, /*points_staged=*/true);
+  } else if (poses7 || points3) {
+    set_parameters(poses7, points3);
+  }
   const double n_obs = static_cast<double>(N_global_);
 
   cudaEvent_t ev0, ev1;

@@ -85,7 +85,8 @@ class Problem {
   const Dev& dev() const { return d_; }
 
   void activate();
-  void set_parameters(const double* poses7, const double* points3);
+  // points_staged: the points are already in pts_user_ (an upload beside the symbolic phase)
+  void set_parameters(const double* poses7, const double* points3, bool points_staged = false);
   void get_parameters(double* poses7, double* points3);
   double evaluate(double* resid2);
   void jacobian(double* jpose, double* jpoint, double* resid2);
