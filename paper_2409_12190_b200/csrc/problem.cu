@@ -155,9 +155,20 @@ PinnedStage& pinned_stage(int device) {
   if (!p) p = new PinnedStage;
   return *p;
 }
-void upload_pageable(void* dst, const void* src, std::size_t bytes, cudaStream_t s, int device) {
-  if (bytes < kStageMin) {
-    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+// Several pageable host ranges through one staging pipeline (the first
+// host copy and the last DMA of a call are not overlapped, so consecutive
+// arrays share one pipeline instead of one each).
+struct UploadSeg {
+  void* dst;
+  const void* src;
+  std::size_t bytes;
+};
+void upload_pageable_segs(const UploadSeg* seg, int nseg, cudaStream_t s, int device) {
+  std::size_t total = 0;
+  for (int k = 0; k < nseg; ++k) total += seg[k].bytes;
+  if (total < kStageMin) {
+    for (int k = 0; k < nseg; ++k)
+      ck(cudaMemcpyAsync(seg[k].dst, seg[k].src, seg[k].bytes, cudaMemcpyHostToDevice, s), "H2D");
     return;
   }
   PinnedStage& st = pinned_stage(device);
@@ -168,19 +179,25 @@ void upload_pageable(void* dst, const void* src, std::size_t bytes, cudaStream_t
   }
   const int nth = host_threads();
   std::size_t i = 0;
-  for (std::size_t off = 0; off < bytes; off += kStageBytes, ++i) {
-    const int b = static_cast<int>(i & 1);
-    const std::size_t n = std::min(kStageBytes, bytes - off);
-    if (i >= 2) ck(cudaEventSynchronize(st.ev[b]), "staging reuse");
-    char* to = static_cast<char*>(st.buf[b]);
-    const char* from = static_cast<const char*>(src) + off;
-    parallel_chunks(static_cast<std::int64_t>(n), nth, [&](int, std::int64_t a, std::int64_t e) {
-      std::memcpy(to + a, from + a, static_cast<std::size_t>(e - a));
-    });
-    ck(cudaMemcpyAsync(static_cast<char*>(dst) + off, to, n, cudaMemcpyHostToDevice, s), "H2D staged");
-    ck(cudaEventRecord(st.ev[b], s), "event record");
+  for (int k = 0; k < nseg; ++k) {
+    for (std::size_t off = 0; off < seg[k].bytes; off += kStageBytes, ++i) {
+      const int b = static_cast<int>(i & 1);
+      const std::size_t n = std::min(kStageBytes, seg[k].bytes - off);
+      if (i >= 2) ck(cudaEventSynchronize(st.ev[b]), "staging reuse");
+      char* to = static_cast<char*>(st.buf[b]);
+      const char* from = static_cast<const char*>(seg[k].src) + off;
+      parallel_chunks(static_cast<std::int64_t>(n), nth, [&](int, std::int64_t a, std::int64_t e) {
+        std::memcpy(to + a, from + a, static_cast<std::size_t>(e - a));
+      });
+      ck(cudaMemcpyAsync(static_cast<char*>(seg[k].dst) + off, to, n, cudaMemcpyHostToDevice, s), "H2D staged");
+      ck(cudaEventRecord(st.ev[b], s), "event record");
+    }
   }
   for (int b = 0; b < 2; ++b) ck(cudaEventSynchronize(st.ev[b]), "staging");  // buffers free for the next caller
+}
+void upload_pageable(void* dst, const void* src, std::size_t bytes, cudaStream_t s, int device) {
+  const UploadSeg seg{dst, src, bytes};
+  upload_pageable_segs(&seg, 1, s, device);
 }
 // The reverse: DMA into the staging buffers, the host pool copies out
 // (synchronises s).
@@ -384,8 +401,10 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   if (dev_plan) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&dcam), 2 * sizeof(int) * static_cast<std::size_t>(use_N), stream_),
        "cudaMallocAsync observation indices");
-    upload_pageable(dcam, use_cam, sizeof(int) * use_N, stream_, opt.device);
-    upload_pageable(dcam + use_N, use_pt, sizeof(int) * use_N, stream_, opt.device);
+    const UploadSeg idx[2] = {{dcam, use_cam, sizeof(int) * static_cast<std::size_t>(use_N)},
+                              {dcam + use_N, use_pt, sizeof(int) * static_cast<std::size_t>(use_N)}};
+    upload_pageable_segs(idx, 2, stream_, opt.device);
+    ht.mark("index upload");
     // the pixels travel while the planner runs (its kernels and host steps
     // leave the copy engine idle); gathered into slot order below
     px_up.start(px2, 2 * sizeof(double) * static_cast<std::size_t>(use_N), opt.device);
