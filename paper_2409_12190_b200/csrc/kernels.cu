@@ -1144,7 +1144,10 @@ __device__ __forceinline__ void ldg_v4(const double* p, double* o) {
                : "l"(p));
 }
 constexpr int kSchurDenseThreads = 128;
-// acc += V_a V_b^T from two [Q | y] records
+// acc += V_a V_b^T from two [Q | y] records (kSame: a and b are one record,
+// G = Q Q^T is formed from its six distinct dot products -- x y == y x, so
+// the same bits as the general form)
+template <bool kSame>
 __device__ __forceinline__ void schur_pair(const double (&a)[kVStride], const double (&b)[kVStride], double (&acc)[36]) {
   // V_a V_b^T = [G, G Y_b^T; Y_a G, Y_a G Y_b^T] with G = Q_a Q_b^T and
   // Y = [y]x: row i of G Y_b^T is y_b x (row i of G), column j of Y_a X
@@ -1155,7 +1158,11 @@ __device__ __forceinline__ void schur_pair(const double (&a)[kVStride], const do
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const double gij = a[3 * i] * b[3 * j] + a[3 * i + 1] * b[3 * j + 1] + a[3 * i + 2] * b[3 * j + 2];
+      double gij;
+      if (kSame && j < i)
+        gij = G[j * 3 + i];
+      else
+        gij = a[3 * i] * b[3 * j] + a[3 * i + 1] * b[3 * j + 1] + a[3 * i + 2] * b[3 * j + 2];
       G[i * 3 + j] = gij;
       acc[i * 6 + j] += gij;
     }
@@ -1221,10 +1228,15 @@ __global__ void __launch_bounds__(kSchurDenseThreads, 4) k_schur_dense(Dev d) {
 #pragma unroll 1
   for (; q < ch.z; q += 32) {
     const int2 pn = q + 32 < ch.z ? d.pairs[q + 32] : pr;
-    double a[kVStride], b[kVStride];
+    double a[kVStride];
     ld_rec(d.wstore, pr.x, a);
-    ld_rec(d.wstore, pr.y, b);
-    schur_pair(a, b, acc);
+    if (pr.x == pr.y) {  // (k, k): a quarter of the pairs (the diagonal blocks), one record
+      schur_pair<true>(a, a, acc);
+    } else {
+      double b[kVStride];
+      ld_rec(d.wstore, pr.y, b);
+      schur_pair<false>(a, b, acc);
+    }
     pr = pn;
   }
   // reduce-scatter: xor 16 halves the 36 sums (bit 4 keeps [18 b4, +18)),
