@@ -1201,10 +1201,12 @@ void Problem::build_direct() {
        "cudaMallocAsync pair offsets");
     try {
       const long long np = count_pairs(d_, off, stream_);
+      ht.mark("direct: pair count");
       if (np >= (1LL << 31) - 1) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
       int2* pairs = dalloc<int2>(static_cast<std::size_t>(std::max(np, 1LL)));
       npairs_ = np;
       build_pairs(d_, off, np, pairs, bcam, bptr, stream_);
+      ht.mark("direct: pair generate + sort + blocks");
       d_.pairs = pairs;
     } catch (...) {
       cudaFreeAsync(off, stream_);
