@@ -1132,8 +1132,8 @@ __global__ void __launch_bounds__(1024) k_prep_totals(Dev d, double tol, long lo
 // F2: dense reduced camera system for the direct solver (the reference's
 // default SolverChoice::cholesky, lm.hpp:132-136). One warp per camera block
 // (c1 >= c2):  S[c1,c2] = delta(c1,c2) H~_cc - sum_{points} sum_{k in c1, l in c2}
-// V_k V_l^T with V = W L^-T (H~_pp = L L^T, so V_k V_l^T = W_k H~_pp^-1 W_l^T
-// from half the bytes of W and W H~^-1), pairs in (point, k, l) order, lanes
+// V_k V_l^T with V = W L^-T (H~_pp = L L^T, so V_k V_l^T = W_k H~_pp^-1 W_l^T),
+// each V from its compact [Q | y] record, pairs in (point, k, l) order, lanes
 // strided over the block's pairs, fixed xor tree; column-major lower
 // triangle for potrf.
 // ---------------------------------------------------------------------------
