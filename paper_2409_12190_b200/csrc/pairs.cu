@@ -30,8 +30,9 @@ __device__ __forceinline__ int slot_camera(const Dev& d, const TileGeom& g, int 
   return d.ent_cam[g.eb + static_cast<int>(d.obs_lcpt[slot] & 0xffffu)];
 }
 
-// One warp per tile, a lane per point: pairs of each internal point.
-__global__ void k_pair_count(Dev d, long long* cnt) {
+// One warp per tile, a lane per point: pairs of each internal point (and,
+// with `blocks`, a bit per camera block that has one).
+__global__ void k_pair_count(Dev d, long long* cnt, unsigned* blocks) {
   const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= d.T) return;
   const TileGeom g = tile_geom(d, t);
@@ -40,9 +41,39 @@ __global__ void k_pair_count(Dev d, long long* cnt) {
     long long n = 0;
     for (int a = 0; a < m; ++a) {
       const int ca = slot_camera(d, g, g.ob + d.ptobs[j0 + a]);
-      for (int b = 0; b < m; ++b) n += ca >= slot_camera(d, g, g.ob + d.ptobs[j0 + b]) ? 1 : 0;
+      for (int b = 0; b < m; ++b) {
+        const int cb = slot_camera(d, g, g.ob + d.ptobs[j0 + b]);
+        if (ca >= cb) {
+          ++n;
+          if (blocks) {
+            const unsigned long long key = static_cast<unsigned long long>(ca) * d.C + cb;
+            const unsigned bit = 1u << (key & 31u);
+            unsigned* w = blocks + (key >> 5);
+            if (!(*w & bit)) atomicOr(w, bit);  // most blocks are marked early: skip the atomic
+          }
+        }
+      }
     }
     cnt[i] = n;
+  }
+}
+
+// Marked blocks -> keys c1 * C + c2, ascending: per word its popcount, an
+// exclusive scan, then every word writes its keys at its offset.
+__global__ void k_bits_count(const unsigned* w, long long nw, int* cnt) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nw) cnt[i] = __popc(w[i]);
+}
+__global__ void k_bits_emit(const unsigned* w, long long nw, const int* off, int C, int2* out) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nw) return;
+  unsigned v = w[i];
+  int at = off[i];
+  while (v) {
+    const int b = __ffs(v) - 1;
+    v &= v - 1;
+    const unsigned long long key = static_cast<unsigned long long>(i) * 32 + b;
+    out[at++] = int2{static_cast<int>(key / C), static_cast<int>(key % C)};
   }
 }
 
@@ -140,10 +171,10 @@ void keep_pool() {
 
 void pairs_pool_setup() { keep_pool(); }
 
-long long count_pairs(const Dev& d, long long* off, cudaStream_t s) {
+long long count_pairs(const Dev& d, long long* off, cudaStream_t s, unsigned* blocks) {
   // off: P + 1 entries; counts per internal point, then an exclusive scan
   ck(cudaMemsetAsync(off, 0, (static_cast<std::size_t>(d.P) + 1) * sizeof(long long), s), "memset");
-  k_pair_count<<<(d.T + 7) / 8, 256, 0, s>>>(d, off);
+  k_pair_count<<<(d.T + 7) / 8, 256, 0, s>>>(d, off, blocks);
   ck(cudaGetLastError(), "pair count");
   void* tmp = nullptr;
   std::size_t tb = 0;
@@ -157,6 +188,38 @@ long long count_pairs(const Dev& d, long long* off, cudaStream_t s) {
   ck(e, "pair scan");
   ck(e2, "pair count");
   return np;
+}
+
+std::vector<int2> marked_blocks(const Dev& d, const unsigned* blocks, cudaStream_t s) {
+  const long long nw = (static_cast<long long>(d.C) * d.C + 31) / 32;
+  int* cnt = nullptr;
+  int2* keys = nullptr;
+  void* tmp = nullptr;
+  std::size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, cnt, nw + 1, s);
+  std::vector<int2> out;
+  try {
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&cnt), (nw + 1) * sizeof(int), s), "cudaMallocAsync");
+    ck(cudaMallocAsync(&tmp, tb, s), "cudaMallocAsync CUB scratch");
+    ck(cudaMemsetAsync(cnt + nw, 0, sizeof(int), s), "memset");
+    const unsigned nb = static_cast<unsigned>((nw + 255) / 256);
+    k_bits_count<<<nb, 256, 0, s>>>(blocks, nw, cnt);
+    ck(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, cnt, nw + 1, s), "block scan");
+    int n = 0;
+    ck(cudaMemcpyAsync(&n, cnt + nw, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "block count");
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&keys), std::max(n, 1) * sizeof(int2), s), "cudaMallocAsync");
+    k_bits_emit<<<nb, 256, 0, s>>>(blocks, nw, cnt, d.C, keys);
+    out.resize(static_cast<std::size_t>(n));
+    ck(cudaMemcpyAsync(out.data(), keys, n * sizeof(int2), cudaMemcpyDeviceToHost, s), "D2H blocks");
+    ck(cudaStreamSynchronize(s), "blocks");
+  } catch (...) {
+    for (void* q : {static_cast<void*>(cnt), tmp, static_cast<void*>(keys)})
+      if (q) cudaFreeAsync(q, s);
+    throw;
+  }
+  for (void* q : {static_cast<void*>(cnt), tmp, static_cast<void*>(keys)}) cudaFreeAsync(q, s);
+  return out;
 }
 
 void build_pairs(const Dev& d, const long long* off, long long np, int2* pairs, std::vector<int2>& bcam,

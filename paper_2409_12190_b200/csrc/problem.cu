@@ -1179,6 +1179,17 @@ bool Problem::solve(double lambda, const bae_lm_config& cfg, SolveInfo& info) {
 // Maximum reduced-system order for the dense direct solve (8.6 GB of FP64).
 constexpr long long kDirectMaxOrder = 32768;
 
+struct TileCholHost {
+  int nt = 0, n = 0, npos = 0, ngroups = 0;
+  std::vector<int> pos_cam;
+  TileCholPlan pl;
+  std::vector<int2> blk_tile;
+  std::vector<unsigned long long> padmask;
+  TileCholTasks tk;
+};
+static void tile_chol_host(int C, const std::vector<int2>& bcam, const std::vector<long long>& keys, int help_min,
+                           int tail, TileCholHost& h);
+
 // Pair list of the reduced camera system: for every point, every ordered pair
 // of its observations (k, l) with camera(k) >= camera(l), grouped by camera
 // block (two-pass stable counting sort), point-major inside a block.
@@ -1193,15 +1204,52 @@ void Problem::build_direct() {
   // the pair list on the device (pairs.cu): count, scan, generate, sort by block
   std::vector<int2> bcam;
   std::vector<int> bptr;
+  // Single rank: the camera blocks are marked while the pairs are counted,
+  // so the tile Cholesky's host symbolic phase (ordering, symbolic
+  // factorisation, slots, task queue: ~8 ms at Final-13682) runs on a second
+  // host thread while the device generates and sorts the pair list
+  // (BAE_SYMB_OVERLAP=0: one after the other)
+  const char* so_env = std::getenv("BAE_SYMB_OVERLAP");
+  const bool overlap = use_tiles_ && !comm_ && d_.C <= 32768 && !(so_env && so_env[0] == '0');
+  std::vector<int2> bcam_pre;
+  TileCholHost chol_host;
+  std::thread chol_thread;
+  std::exception_ptr chol_err;
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{chol_thread};
   {
     long long* off = nullptr;
+    unsigned* marks = nullptr;
     pairs_pool_setup();
     ck(cudaMallocAsync(reinterpret_cast<void**>(&off), (static_cast<std::size_t>(d_.P) + 1) * sizeof(long long),
                        stream_),
        "cudaMallocAsync pair offsets");
     try {
-      const long long np = count_pairs(d_, off, stream_);
+      if (overlap) {
+        const std::size_t words = (static_cast<std::size_t>(d_.C) * d_.C + 31) / 32;
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&marks), words * sizeof(unsigned), stream_), "cudaMallocAsync");
+        ck(cudaMemsetAsync(marks, 0, words * sizeof(unsigned), stream_), "memset");
+      }
+      const long long np = count_pairs(d_, off, stream_, marks);
       ht.mark("direct: pair count");
+      if (overlap) {
+        bcam_pre = marked_blocks(d_, marks, stream_);
+        cudaFreeAsync(marks, stream_);
+        marks = nullptr;
+        const int help = chol_help_min(), tail = chol_tail(), C = d_.C;
+        chol_thread = std::thread([&, help, tail, C, keys = camera_graph_keys(bcam_pre)] {
+          try {
+            tile_chol_host(C, bcam_pre, keys, help, tail, chol_host);
+          } catch (...) {
+            chol_err = std::current_exception();
+          }
+        });
+        ht.mark("direct: blocks marked");
+      }
       if (np >= (1LL << 31) - 1) throw Error(BAE_ERR_UNSUPPORTED, "reduced camera system: too many pairs");
       int2* pairs = dalloc<int2>(static_cast<std::size_t>(std::max(np, 1LL)));
       npairs_ = np;
@@ -1210,6 +1258,7 @@ void Problem::build_direct() {
       d_.pairs = pairs;
     } catch (...) {
       cudaFreeAsync(off, stream_);
+      if (marks) cudaFreeAsync(marks, stream_);
       throw;
     }
     cudaFreeAsync(off, stream_);
@@ -1272,7 +1321,19 @@ void Problem::build_direct() {
     ck(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
   }
   if (use_tiles_) {
-    build_tile_chol(bcam);
+    if (overlap) {
+      chol_thread.join();
+      if (chol_err) std::rethrow_exception(chol_err);
+      const bool same = bcam.size() == bcam_pre.size() &&
+                        std::equal(bcam.begin(), bcam.end(), bcam_pre.begin(),
+                                   [](const int2& a, const int2& b) { return a.x == b.x && a.y == b.y; });
+      if (same)
+        upload_tile_chol(chol_host);
+      else  // (the marked blocks are the pair list's blocks by construction)
+        build_tile_chol(bcam);
+    } else {
+      build_tile_chol(bcam);
+    }
     ht.mark("direct: tile symbolic");
     direct_ready_ = true;
     return;
@@ -1293,12 +1354,86 @@ void Problem::build_direct() {
 }
 
 // Tile pattern of S (camera blocks -> 48 x 48 tiles, the union over ranks on
-// sharded runs), its symbolic factorisation and the device structures.
-void Problem::build_tile_chol(const std::vector<int2>& bcam) {
+// sharded runs), its symbolic factorisation and the device structures. The
+// host part (tile_chol_host: ordering, symbolic, slots, task queue) touches
+// no device state, so a single-rank problem runs it on a second host thread
+// while the device sorts the pair list (build_direct).
+
+// keys: the camera graph's edges c1 * C + c2 (c1 > c2), ascending, unique
+static void tile_chol_host(int C, const std::vector<int2>& bcam, const std::vector<long long>& keys, int help_min,
+                           int tail, TileCholHost& h) {
   HostTimer ht;
+  std::vector<std::pair<int, int>> edges;
+  edges.reserve(keys.size());
+  for (long long k : keys) edges.emplace_back(static_cast<int>(k / C), static_cast<int>(k % C));
+  // elimination order: nested dissection (BAE_ORDER=natural: camera order)
+  std::vector<std::vector<int>> groups;
+  const char* ord = std::getenv("BAE_ORDER");
+  if (ord && std::string(ord) == "natural") {
+    groups.emplace_back(C);
+    for (int c = 0; c < C; ++c) groups[0][c] = c;
+  } else {
+    int leaf = 24;  // cameras per nested-dissection leaf (3 tiles)
+    if (const char* l = std::getenv("BAE_ND_LEAF")) leaf = std::max(1, std::atoi(l));
+    groups = nd_camera_groups(C, edges, leaf);
+  }
+  ht.mark("chol: nested dissection");
+  // positions: groups in order, each padded to whole tiles (8 cameras)
+  std::vector<int> pos(static_cast<std::size_t>(C), -1), pos_cam;
+  for (const auto& g : groups) {
+    for (int c : g) {
+      pos[c] = static_cast<int>(pos_cam.size());
+      pos_cam.push_back(c);
+    }
+    while (pos_cam.size() % 8) pos_cam.push_back(-1);
+  }
+  const int npos = static_cast<int>(pos_cam.size());
+  const int n = 6 * npos;
+  const int nt = npos / 8;
+  h.ngroups = static_cast<int>(groups.size());
+  std::vector<std::pair<int, int>> tp;
+  tp.reserve(edges.size());
+  for (const auto& e : edges) {
+    const int a = pos[e.first] / 8, b = pos[e.second] / 8;
+    tp.emplace_back(std::max(a, b), std::min(a, b));
+  }
+  TileCholPlan pl = plan_tile_chol(n, tp);
+  ht.mark("chol: symbolic");
+  auto slot_of = [&](int ti, int tj) {
+    const auto first = pl.rowidx.begin() + pl.colptr[tj], last = pl.rowidx.begin() + pl.colptr[tj + 1];
+    const auto it = std::lower_bound(first, last, ti);
+    if (it == last || *it != ti) throw Error(BAE_ERR_INVALID_ARGUMENT, "tile pattern misses a camera block");
+    return static_cast<int>(it - pl.rowidx.begin());
+  };
+  // per camera block: its tile slot and where it sits (transposed when the
+  // ordering puts camera(k) before camera(l)); then per camera its diagonal slot
+  std::vector<int2> blk_tile;
+  blk_tile.reserve(bcam.size() + static_cast<std::size_t>(C));
+  for (const int2& b : bcam) {
+    int p1 = pos[b.x], p2 = pos[b.y];
+    const int trans = p1 < p2 ? 1 : 0;
+    if (trans) std::swap(p1, p2);
+    blk_tile.push_back(int2{slot_of(p1 / 8, p2 / 8), 6 * (p1 % 8) | (6 * (p2 % 8)) << 8 | trans << 16});
+  }
+  for (int c = 0; c < C; ++c) blk_tile.push_back(int2{slot_of(pos[c] / 8, pos[c] / 8), 6 * (pos[c] % 8)});
+  std::vector<unsigned long long> padmask(static_cast<std::size_t>(nt), 0ull);
+  for (int q = 0; q < npos; ++q)
+    if (pos_cam[q] < 0) padmask[q / 8] |= 0x3full << (6 * (q % 8));
+  h.tk = plan_chol_tasks(pl, help_min, tail);
+  ht.mark("chol: task queue");
+  h.nt = nt;
+  h.n = n;
+  h.npos = npos;
+  h.pos_cam = std::move(pos_cam);
+  h.blk_tile = std::move(blk_tile);
+  h.padmask = std::move(padmask);
+  h.pl = std::move(pl);
+}
+
+// The camera graph's edges from the block list (the union over ranks on
+// sharded runs, so that every rank derives the same order)
+std::vector<long long> Problem::camera_graph_keys(const std::vector<int2>& bcam) {
   const int C = d_.C;
-  // camera graph: pairs of distinct cameras that share a point (the union
-  // over ranks on sharded runs, so that every rank derives the same order)
   std::vector<long long> keys;
   keys.reserve(bcam.size());
   for (const int2& b : bcam)
@@ -1334,64 +1469,35 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
     std::sort(keys.begin(), keys.end());
     keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
   }
-  ht.mark("chol: camera graph");
-  std::vector<std::pair<int, int>> edges;
-  edges.reserve(keys.size());
-  for (long long k : keys) edges.emplace_back(static_cast<int>(k / C), static_cast<int>(k % C));
-  // elimination order: nested dissection (BAE_ORDER=natural: camera order)
-  std::vector<std::vector<int>> groups;
-  const char* ord = std::getenv("BAE_ORDER");
-  if (ord && std::string(ord) == "natural") {
-    groups.emplace_back(C);
-    for (int c = 0; c < C; ++c) groups[0][c] = c;
-  } else {
-    int leaf = 24;  // cameras per nested-dissection leaf (3 tiles)
-    if (const char* l = std::getenv("BAE_ND_LEAF")) leaf = std::max(1, std::atoi(l));
-    groups = nd_camera_groups(C, edges, leaf);
-  }
-  ht.mark("chol: nested dissection");
-  // positions: groups in order, each padded to whole tiles (8 cameras)
-  std::vector<int> pos(static_cast<std::size_t>(C), -1), pos_cam;
-  for (const auto& g : groups) {
-    for (int c : g) {
-      pos[c] = static_cast<int>(pos_cam.size());
-      pos_cam.push_back(c);
-    }
-    while (pos_cam.size() % 8) pos_cam.push_back(-1);
-  }
-  const int npos = static_cast<int>(pos_cam.size());
-  const int n = 6 * npos;
-  const int nt = npos / 8;
-  chol_groups_ = static_cast<int>(groups.size());
-  std::vector<std::pair<int, int>> tp;
-  tp.reserve(edges.size());
-  for (const auto& e : edges) {
-    const int a = pos[e.first] / 8, b = pos[e.second] / 8;
-    tp.emplace_back(std::max(a, b), std::min(a, b));
-  }
-  const TileCholPlan pl = plan_tile_chol(n, tp);
-  ht.mark("chol: symbolic");
-  auto slot_of = [&](int ti, int tj) {
-    const auto first = pl.rowidx.begin() + pl.colptr[tj], last = pl.rowidx.begin() + pl.colptr[tj + 1];
-    const auto it = std::lower_bound(first, last, ti);
-    if (it == last || *it != ti) throw Error(BAE_ERR_INVALID_ARGUMENT, "tile pattern misses a camera block");
-    return static_cast<int>(it - pl.rowidx.begin());
-  };
-  // per camera block: its tile slot and where it sits (transposed when the
-  // ordering puts camera(k) before camera(l)); then per camera its diagonal slot
-  std::vector<int2> blk_tile;
-  blk_tile.reserve(bcam.size() + static_cast<std::size_t>(C));
-  for (const int2& b : bcam) {
-    int p1 = pos[b.x], p2 = pos[b.y];
-    const int trans = p1 < p2 ? 1 : 0;
-    if (trans) std::swap(p1, p2);
-    blk_tile.push_back(int2{slot_of(p1 / 8, p2 / 8), 6 * (p1 % 8) | (6 * (p2 % 8)) << 8 | trans << 16});
-  }
-  for (int c = 0; c < C; ++c) blk_tile.push_back(int2{slot_of(pos[c] / 8, pos[c] / 8), 6 * (pos[c] % 8)});
-  std::vector<unsigned long long> padmask(static_cast<std::size_t>(nt), 0ull);
-  for (int q = 0; q < npos; ++q)
-    if (pos_cam[q] < 0) padmask[q / 8] |= 0x3full << (6 * (q % 8));
-  d_.blk_tile = upload(blk_tile);
+  return keys;
+}
+
+void Problem::build_tile_chol(const std::vector<int2>& bcam) {
+  TileCholHost h;
+  tile_chol_host(d_.C, bcam, camera_graph_keys(bcam), chol_help_min(), chol_tail(), h);
+  upload_tile_chol(h);
+}
+
+int Problem::chol_help_min() const {
+  // update helpers for tiles with many updates (BAE_CHOL_HELP = minimum
+  // count, 0 = off): a separator column's tile updates spread over CTAs
+  int help_min = 2;
+  if (const char* e = std::getenv("BAE_CHOL_HELP")) help_min = std::max(0, std::atoi(e));
+  return help_min;
+}
+int Problem::chol_tail() const {
+  // helpers for the queue's last two grids of tasks (one grid: Venice factor
+  // 398 us, two: 388 us, all: Final +8 %); BAE_CHOL_TAIL=n overrides
+  int tail = 2 * tile_chol_grid(1 << 30);
+  if (const char* e = std::getenv("BAE_CHOL_TAIL")) tail = std::max(0, std::atoi(e));
+  return tail;
+}
+
+void Problem::upload_tile_chol(TileCholHost& h) {
+  const TileCholPlan& pl = h.pl;
+  const int nt = h.nt, n = h.n;
+  chol_groups_ = h.ngroups;
+  d_.blk_tile = upload(h.blk_tile);
   d_.stile_count = pl.nnz_tiles();
   d_.stiles = dalloc<double>(static_cast<std::size_t>(pl.nnz_tiles()) * kTT);
   TileChol& t = tchol_;
@@ -1405,17 +1511,7 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.uptr = upload(pl.uptr);
   t.usrc = upload(pl.usrc);
   t.udst = upload(pl.udst);
-  // update helpers for tiles with many updates (BAE_CHOL_HELP = minimum
-  // count, 0 = off): a separator column's tile updates spread over CTAs
-  int help_min = 2;
-  if (const char* h = std::getenv("BAE_CHOL_HELP")) help_min = std::max(0, std::atoi(h));
-  ht.mark("chol: tile slots + uploads");
-  // helpers for the queue's last two grids of tasks (one grid: Venice factor
-  // 398 us, two: 388 us, all: Final +8 %); BAE_CHOL_TAIL=n overrides
-  int tail = 2 * tile_chol_grid(1 << 30);
-  if (const char* e = std::getenv("BAE_CHOL_TAIL")) tail = std::max(0, std::atoi(e));
-  const TileCholTasks tk = plan_chol_tasks(pl, help_min, tail);
-  ht.mark("chol: task queue");
+  const TileCholTasks& tk = h.tk;
   t.bptr = upload(tk.bptr);
   t.bop = upload(tk.bop);
   t.tasks = upload(tk.tasks);
@@ -1427,8 +1523,8 @@ void Problem::build_tile_chol(const std::vector<int2>& bcam) {
   t.rhs = d_.rhs;
   t.y = dalloc<double>(static_cast<std::size_t>(nt) * kTB);
   t.x = d_.x;
-  t.pos_cam = upload(pos_cam);
-  t.padmask = upload(padmask);
+  t.pos_cam = upload(h.pos_cam);
+  t.padmask = upload(h.padmask);
   t.nnz = static_cast<int>(pl.nnz_tiles());
   t.flags = dalloc<unsigned>(2 * static_cast<std::size_t>(t.nnz) + nt);
   t.pflags = t.flags + t.nnz + nt;

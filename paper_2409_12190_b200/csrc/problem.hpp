@@ -17,6 +17,8 @@
 
 namespace bae {
 
+struct TileCholHost;  // problem.cu: the host half of the tile Cholesky's symbolic phase
+
 struct SolveInfo {
   long long iters = 0;
   bool converged = false;
@@ -132,6 +134,10 @@ class Problem {
   void build_direct();
   void build_pcg_graph();
   void build_tile_chol(const std::vector<int2>& bcam);
+  std::vector<long long> camera_graph_keys(const std::vector<int2>& bcam);
+  int chol_help_min() const;
+  int chol_tail() const;
+  void upload_tile_chol(TileCholHost& h);
   void require_single(const char* what) const;
   const char* cheirality_msg() const;
   void ensure_host_obs_orig();
