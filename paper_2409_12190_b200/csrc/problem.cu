@@ -1148,6 +1148,9 @@ bool Problem::build_lm_graphs(const bae_lm_config& cfg) {
     BAE_LAUNCHED(launch_trial(d_, sm_, stream_, nullptr));
     ck(cudaMemcpyAsync(lm_host_, d_.lm, sizeof(LmDev), cudaMemcpyDeviceToHost, stream_), "D2H lm");
   };
+  // the solve graph carries no prep: the first iteration's comes fused with
+  // the initial linearisation, a rejected step's is launched before the graph
+  prep_fused_ = true;
   const bool a = capture(solve_trial, lm_graph_solve_, graph_solve_launches_);
   const bool b = a && capture(
                           [&] {
@@ -1777,21 +1780,6 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   ck(cudaEventCreate(&ev0), "event");
   ck(cudaEventCreate(&ev1), "event");
   ck(cudaEventRecord(ev0, stream_), "event record");
-  // Initial evaluate (lm.hpp:217-220); the linearisation computes the cost
-  // together with the first step's normal-equation blocks.
-  linearize();
-  double cost = lm_host_->cost;
-  double grad = std::sqrt(lm_host_->grad_sq);
-  std::vector<double> history{cost};
-  double lambda = cfg.initial_damping;
-  traj.clear();
-  traj.push_back({0, 1, cost, cost / n_obs, lambda, 0.0, 0, grad, cost});
-  int iterations = 0, accepted_steps = 0, rejected_steps = 0;
-  long long total_pcg = 0;
-  bool need_lin = false;
-  rep = bae_lm_report{};
-  rep.reason = BAE_TERM_MAX_ITERS;
-  const auto t0 = std::chrono::steady_clock::now();
   // Direct solves leave the factorisation's failure word and the next
   // linearisation's cost / gradient in flight: the trial's read-back is the
   // one host synchronisation of an LM iteration (a failed factorisation
@@ -1807,6 +1795,37 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
   prep_fused_ = false;
   const bool graphs = defer_factor_check_ && use_tiles_ && fuse_lin_prep(cfg) && !std::getenv("BAE_CHOL_TRACE") &&
                       !(lg && lg[0] == '0') && build_lm_graphs(cfg);
+  // Initial evaluate (lm.hpp:217-220); the linearisation computes the cost
+  // together with the first step's normal-equation blocks -- with the graphs,
+  // fused with the first step's prep at the initial damping (the same bits as
+  // the separate passes), so the first solve graph needs no prep of its own.
+  bool first_fused = false;
+  const char* ff = std::getenv("BAE_FIRST_FUSED");
+  if (graphs && !(ff && ff[0] == '0')) {
+    linearize_prep_async(cfg.initial_damping, cfg);
+    if (join_pending_) {  // the cost and gradient come from the camera pass
+      ck(cudaStreamWaitEvent(stream_, ev_join_, 0), "stream wait");
+      join_pending_ = false;
+    }
+    read_lm();
+    if (lm_host_->err_obs != INT_MAX) throw Error(BAE_ERR_CHEIRALITY, cheirality_msg(), lm_host_->err_obs);
+    first_fused = true;
+    prep_fused_ = false;  // (the graph replays do not consult it; later host-side solves must prep)
+  } else {
+    linearize();
+  }
+  double cost = lm_host_->cost;
+  double grad = std::sqrt(lm_host_->grad_sq);
+  std::vector<double> history{cost};
+  double lambda = cfg.initial_damping;
+  traj.clear();
+  traj.push_back({0, 1, cost, cost / n_obs, lambda, 0.0, 0, grad, cost});
+  int iterations = 0, accepted_steps = 0, rejected_steps = 0;
+  long long total_pcg = 0;
+  bool need_lin = false;
+  rep = bae_lm_report{};
+  rep.reason = BAE_TERM_MAX_ITERS;
+  const auto t0 = std::chrono::steady_clock::now();
   bool lin_pending = false, commit_pending = false;
   while (iterations < cfg.max_iterations) {
     const double lambda_used = lambda;
@@ -1822,9 +1841,17 @@ void Problem::optimize(const double* poses7, const double* points3, const bae_lm
         lin_pending = true;
         need_lin = false;
       } else {
+        if (!first_fused) {  // a rejected step (or the first, unfused): the prep, then the solve graph
+          ck(cudaMemcpyAsync(const_cast<double*>(d_.lam), lam_host_, sizeof(double), cudaMemcpyHostToDevice, stream_),
+             "H2D lambda");
+          ck(cudaMemsetAsync(d_.pcg, 0, sizeof(PcgDev), stream_), "memset pcg");
+          BAE_LAUNCHED(launch_prep(d_, sm_, lambda_used, cfg.clamp_min, cfg.clamp_max, cfg.pcg_tol, 1, stream_,
+                                   nullptr, true));
+        }
         ck(cudaGraphLaunch(lm_graph_solve_, stream_), "graph launch");
         BAE_LAUNCHED(graph_solve_launches_);
       }
+      first_fused = false;
       sync();
       info.pending = true;
     } else {
