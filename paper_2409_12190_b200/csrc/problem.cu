@@ -398,6 +398,7 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   DevicePlan dp;
   int* dcam = nullptr;  // raw observation indices on the device (device plan)
   AsyncUpload px_up;    // device plan: the pixels, uploaded beside the planner
+  AsyncUpload pts_up;   // and the initial points after them
   if (dev_plan) {
     ck(cudaMallocAsync(reinterpret_cast<void**>(&dcam), 2 * sizeof(int) * static_cast<std::size_t>(use_N), stream_),
        "cudaMallocAsync observation indices");
@@ -408,6 +409,13 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
     // the pixels travel while the planner runs (its kernels and host steps
     // leave the copy engine idle); gathered into slot order below
     px_up.start(px2, 2 * sizeof(double) * static_cast<std::size_t>(use_N), opt.device);
+    // the initial points follow on their own helper (the staging lock puts
+    // them after the pixels), into the caller-order buffer set_parameters
+    // permutes from
+    if (points3 && 3 * sizeof(double) * static_cast<std::size_t>(use_P) >= (64u << 20)) {
+      pts_user_ = dalloc<double>(3 * static_cast<std::size_t>(use_P));
+      pts_up.start(points3, 3 * sizeof(double) * static_cast<std::size_t>(use_P), opt.device, pts_user_);
+    }
     try {
       build_plan_device(C, use_P, dcam, dcam + use_N, use_N, std::min(tile_obs, kPipeObs), std::min(tile_cams, kPipeCams),
                         kPipePts, kSliceLimit, [this](std::size_t n) { return static_cast<void*>(dalloc<char>(n)); },
@@ -664,7 +672,16 @@ Problem::Problem(const double* poses7, int C, const double* points3, int P, cons
   ck(cudaMemset(d.pcg, 0, sizeof(PcgDev)), "memset");
 
   ht.mark("device alloc+upload");
-  set_parameters(poses7, points3);
+  if (pts_up.s) {
+    pts_up.wait_on(stream_);
+    if (!src_of_internal_) {  // (the device plan leaves its own copy)
+      std::vector<int> src(plan_.pt_of_internal.begin(), plan_.pt_of_internal.end());
+      src_of_internal_ = upload(src);
+    }
+    set_parameters(poses7, nullptr, /*points_staged=*/true);
+  } else {
+    set_parameters(poses7, points3);
+  }
   ht.mark("set_parameters");
   // Eager forward at construction, as make_ba_problem's graph does
   // (trace.hpp:152,385): cheirality surfaces here with the observation id.
