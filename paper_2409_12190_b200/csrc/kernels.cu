@@ -519,8 +519,7 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
       pt_put<9>(ws, g.npts, lp, 3, spl + 3);
     }
   }
-  // tile totals: a warp pair adds warp 1's trees to warp 0's through
-  // tile_red (global; ordered by the pair barrier)
+  // tile totals (tile_red): a warp pair adds warp 1's trees to warp 0's
   const double ct = cost.warp_total(), gt = gsq.warp_total();
   if constexpr (NT == 32) {
     if (lane == 0) {
@@ -529,14 +528,18 @@ __device__ __forceinline__ void lin_tile(const Dev& d, const TileGeom& g, char* 
     }
   } else {
     static_assert(NT == 64, "warp or warp pair");
+    // warp 1's trees reach warp 0 through shared memory (a global round trip
+    // here stalled warp 0, and with it the pair's next barrier, ~500 cycles)
+    __shared__ double pair_red[8][2];  // at most eight pairs per CTA (TileLaunch::wpb)
+    double* pr = pair_red[(threadIdx.x / NT) & 7];
     if (wp == 1 && lane == 0) {
-      d.tile_red[t * 2] = ct;
-      d.tile_red[t * 2 + 1] = gt;
+      pr[0] = ct;
+      pr[1] = gt;
     }
     tile_sync<NT>();
     if (wp == 0 && lane == 0) {
-      d.tile_red[t * 2] = ct + d.tile_red[t * 2];
-      d.tile_red[t * 2 + 1] = gt + d.tile_red[t * 2 + 1];
+      d.tile_red[t * 2] = ct + pr[0];
+      d.tile_red[t * 2 + 1] = gt + pr[1];
     }
   }
   if (kPrep) {
