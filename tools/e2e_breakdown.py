@@ -10,7 +10,7 @@ import paper_2409_12190_b200 as bae  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "final-13682"
 C, P, N = bae.synthetic.CONFIGS[name]
 s = bae.synthetic.bal_shaped(C, P, N, seed=C)
-for rep in range(3):
+for rep in range(int(os.environ.get("E2E_REPS", "3"))):
     print(f"--- rep {rep}", file=sys.stderr, flush=True)
     t0 = time.perf_counter()
     g = bae.make_ba_problem(s.poses, s.points, s.intrinsics, s.observations)
